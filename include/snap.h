@@ -1,0 +1,194 @@
+/*
+ * snap.h — C ABI of the B200-native snapshot / dedup / restore / splice hot
+ * path (arXiv 2202.07848 "Singularity", reference = fleetsim C++ simulator).
+ *
+ * The reference has no FFI: its hot path is in-process C++ (SURVEY.md §8b).
+ * Each entry point below names the reference interface it replaces
+ * (path:line relative to the reference's proj/). A maintainer swaps the
+ * reference's std::vector "device" for this library by binding these symbols
+ * (INTEGRATION.md shows the adapter). Plain pointers and sizes only.
+ *
+ * Conventions
+ *  - One snap_ctx per (job, GPU), the analogue of proxy::ProxyServer
+ *    (proxy.hpp:32-122): it owns the device arena (one cudaMalloc reservation,
+ *    SPEC.md:232), the chunk grid, digest vectors, the dedup table, the staging
+ *    image and (optionally) an NCCL communicator.
+ *  - All device work is issued on the ctx's own CUDA stream, in call order.
+ *    Calls that return host data synchronise that stream once per call.
+ *  - Return codes (common.hpp:31-49 error conventions):
+ *      SNAP_OK        success
+ *      SNAP_EINVAL    bad argument / geometry          (ConfigError)
+ *      SNAP_ENOMEM    out of device/host memory         (alloc -> nullopt)
+ *      SNAP_EFAULT    modeled fault, e.g. digest verification failed,
+ *                     missing content                   (SimFault)
+ *      SNAP_ECUDA     CUDA / NCCL runtime error
+ *      SNAP_EINTERNAL invariant broken                  (InternalError)
+ *    snap_last_error(ctx) returns the message of the last failure.
+ *  - Addresses are byte offsets inside the ctx arena (vdev::MemRange::addr,
+ *    vdev.hpp:49-53). Buffers are 256-byte aligned and sized
+ *    (BidiAllocator::kAlign, alloc.hpp:28; alloc.cpp:64).
+ *  - There is NO CPU fallback: every compute entry point runs sm_100a kernels
+ *    and fails with SNAP_ECUDA when no B200 is present.
+ */
+#ifndef SNAP_H
+#define SNAP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SNAP_OK 0
+#define SNAP_EINVAL (-1)
+#define SNAP_ENOMEM (-2)
+#define SNAP_EFAULT (-3)
+#define SNAP_ECUDA (-4)
+#define SNAP_EINTERNAL (-5)
+
+typedef struct snap_ctx snap_ctx;
+
+/* A tracked allocation: splice::RankBuf (splice.hpp:26-34) and
+ * ckpt::WorkerSnapshot::DevRec (ckpt.hpp:64-71). Canonical order of a buffer
+ * list is the order build_manifest walks it: rank ascending, slot ascending
+ * (ckpt.cpp:104,147). */
+typedef struct {
+  uint32_t rank;
+  int32_t slot;
+  uint64_t addr;
+  uint64_t bytes;
+  int32_t cat; /* vdev::BufCat (vdev.hpp:17): 0 Param 1 OptState 2 Grad 3 Activation 4 Scratch */
+  uint32_t flags;
+} snap_buf;
+
+/* Chunk grid: page digest = digest_of_words(page) (sim.hpp:67-70 on the
+ * reference's 4 KiB page unit, ckpt.hpp:15); chunk digest = digest_of_words
+ * over its page digests, or the direct FNV-1a of the chunk when
+ * page_bytes == chunk_bytes; buffer digest = digest_of_words over its chunk
+ * digests (the ledger key that replaces Gpu::digest, vdev.cpp:118). */
+typedef struct {
+  uint32_t page_bytes;  /* power of two, >= 256; default 4096 */
+  uint32_t chunk_bytes; /* power of two, multiple of page_bytes, <= 32 pages */
+} snap_geom;
+
+/* ---------------------------------------------------------------- context */
+
+/* ProxyServer ctor (proxy.cpp:7-14) + Gpu(id, mem_bytes) (vdev.cpp:67-70):
+ * reserves `arena_bytes` of HBM on `device` (zero-filled). */
+int snap_open(int device, uint64_t arena_bytes, snap_ctx** out);
+int snap_close(snap_ctx* ctx);
+const char* snap_last_error(const snap_ctx* ctx);
+const char* snap_strerror(int code);
+int snap_arena(snap_ctx* ctx, void** dev_base, uint64_t* bytes);
+/* Number of kernels this ctx has launched so far (evidence counter). */
+uint64_t snap_launch_count(const snap_ctx* ctx);
+int snap_sync(snap_ctx* ctx);
+
+/* splice::DeviceLayout::carve (splice.cpp:7-19): host arithmetic only.
+ * out = {rank_region_end, scratch_base, scratch_bytes}. */
+int snap_layout_carve(uint64_t mem_bytes, uint64_t max_buffer_bytes, double slack_fraction,
+                      uint64_t out[3]);
+
+/* Gpu::write_words / Gpu::words (vdev.cpp:106-124): host <-> arena copies. */
+int snap_write(snap_ctx* ctx, uint64_t addr, const void* src, uint64_t bytes);
+int snap_read(snap_ctx* ctx, uint64_t addr, void* dst, uint64_t bytes);
+/* Device-side synthetic content: words[i] = mix64(seed ^ (base + i))
+ * (sim.hpp:37-41), i counted in u64 words from `addr`. */
+int snap_fill_mix64(snap_ctx* ctx, uint64_t addr, uint64_t bytes, uint64_t seed, uint64_t base);
+/* XOR `value` into the u64 word at each addrs[i] (dirty-chunk mutation). */
+int snap_xor_words(snap_ctx* ctx, const uint64_t* addrs, uint64_t n, uint64_t value);
+
+/* ------------------------------------------------------- K1: hash (digest) */
+
+/* Installs the buffer list (a consistent cut of the ledger, ckpt.cpp:147) and
+ * its chunk grid; returns the number of chunks. */
+int snap_set_buffers(snap_ctx* ctx, const snap_buf* bufs, uint64_t n, const snap_geom* geom,
+                     uint64_t* n_chunks);
+/* K1: digests every chunk of every installed buffer (replaces
+ * GpuLedger::refresh_digests, splice.cpp:150-159, and the hashing inside
+ * BlobStore::put, ckpt.cpp:17). Async on the ctx stream. */
+int snap_hash(snap_ctx* ctx);
+/* Copies digest vectors to the host (any pointer may be NULL).
+ * buf_digests triggers the per-buffer fold kernel. */
+int snap_get_digests(snap_ctx* ctx, uint64_t* chunk_digests, uint32_t* chunk_lens,
+                     uint64_t* buf_digests);
+/* Gpu::digest over a list of ranges (vdev.cpp:118), hierarchical digest per
+ * range; synchronous convenience used by the ledger adapters. */
+int snap_digest_ranges(snap_ctx* ctx, const snap_buf* bufs, uint64_t n, const snap_geom* geom,
+                       uint64_t* out_buf_digests);
+
+/* ----------------------------------------- K2: dedup + dirty (selection) */
+
+/* Known-digest set = the BlobStore's key set (ckpt.hpp:39): chunks whose
+ * digest is known are not staged again (BlobStore::put fresh test,
+ * ckpt.cpp:18-20). */
+int snap_known_clear(snap_ctx* ctx);
+int snap_known_add(snap_ctx* ctx, const uint64_t* digests, uint64_t n);
+/* Adds every digest of the current grid to the known set (after a snapshot
+ * has been persisted: the next one is incremental). */
+int snap_known_commit(snap_ctx* ctx);
+/* K2 (single GPU): first occurrence in canonical order and not known
+ * (build_manifest unique_device set, ckpt.cpp:97,157-166), staging offsets by
+ * a deterministic decoupled look-back scan. Async. */
+int snap_select(snap_ctx* ctx);
+/* Copies the selection to the host (any pointer may be NULL).
+ * sel[g] in {0,1}; owner[g] = first-occurrence chunk index or UINT64_MAX
+ * when known; offsets[g] = staging byte offset of the chunk's bytes
+ * (UINT64_MAX when known). */
+int snap_get_selection(snap_ctx* ctx, uint8_t* sel, uint64_t* owner, uint64_t* offsets,
+                       uint64_t* staged_bytes, uint64_t* staged_chunks);
+
+/* --------------------------------------------------- K3: stream compaction */
+
+/* K3: gathers the selected chunks into the ctx staging image, canonical
+ * order (replaces the content_of + BlobStore::put copies, ckpt.cpp:161-163,
+ * and host_cache_put, splice.cpp:79-82,266). Async. */
+int snap_compact(snap_ctx* ctx);
+/* One call = K1 + K2 + K3 (+ K2 exchange when a communicator is attached):
+ * the device section of build_manifest (ckpt.cpp:147-167). Async. */
+int snap_snapshot(snap_ctx* ctx);
+int snap_staging(snap_ctx* ctx, void** dev_ptr, uint64_t* bytes);
+int snap_read_staging(snap_ctx* ctx, uint64_t off, void* dst, uint64_t bytes);
+
+/* ------------------------------------------------ K4: scatter-restore */
+
+/* K4: restore_job materialization (ckpt.cpp:517-528): chunk g of the
+ * installed grid is written at its recorded address from
+ * image + src_off[g] (host array, n_chunks entries). `image` is a device
+ * pointer (staging of this or a peer ctx, or any device buffer). With
+ * verify != 0 the restored chunks are re-hashed against expect_digests
+ * (BlobStore::get digest verification, ckpt.cpp:26-27) and SNAP_EFAULT is
+ * returned on any mismatch. */
+int snap_restore(snap_ctx* ctx, const void* image, uint64_t image_bytes, const uint64_t* src_off,
+                 const uint64_t* expect_digests, int verify);
+/* Inverse of the last snap_snapshot from this ctx's own staging image. */
+int snap_restore_self(snap_ctx* ctx, int verify);
+
+/* --------------------------------------- K5: spliced gradient reduction */
+
+#define SNAP_U64 0
+#define SNAP_F32 1
+/* K5: dst[i] = sum_r src_r[i] over `nsrc` arena ranges, fixed ascending order
+ * (u64 modular: collectives.cpp:140-141; f32: ((s0+s1)+s2)+..., IEEE RN).
+ * With accumulate != 0, dst is the first addend. Async. */
+int snap_grad_sum(snap_ctx* ctx, int dtype, const uint64_t* src_addrs, uint32_t nsrc,
+                  uint64_t dst_addr, uint64_t elems, int accumulate);
+
+/* ------------------------------------------------ multi-GPU (NCCL/NVLink) */
+
+int snap_comm_unique_id(void* id128);
+int snap_comm_init(snap_ctx* ctx, int nranks, int rank, const void* id128);
+/* Device-level allreduce of a gradient range (after K5 local sum,
+ * collectives.cpp:147-154 local closer). Async. */
+int snap_allreduce(snap_ctx* ctx, int dtype, uint64_t addr, uint64_t elems);
+
+/* ---------------------------------------------------------- timing */
+
+int snap_timer_start(snap_ctx* ctx);
+int snap_timer_stop(snap_ctx* ctx, float* ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SNAP_H */

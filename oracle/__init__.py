@@ -1,0 +1,240 @@
+"""oracle — TEST INFRASTRUCTURE ONLY.
+
+ctypes bindings to
+  * liboracle.so            the CPU restatement (snap_oracle.c), and
+  * _ref/libfleetsim_ref.so the reference library itself, compiled from
+                            /root/reference/proj/src by oracle/Makefile.
+
+Only tests/, __graft_entry__.smoke() (as the checker) and bench.py's
+cpu_baseline / --impl reference legs may import this package. The product
+(paper_2202_07848_b200) never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+_lib = None
+_ref = None
+
+U64P = C.POINTER(C.c_uint64)
+
+
+class OrBuf(C.Structure):
+    """or_buf / snap_buf: RankBuf/DevRec (splice.hpp:26-34, ckpt.hpp:64-71)."""
+
+    _fields_ = [
+        ("rank", C.c_uint32),
+        ("slot", C.c_int32),
+        ("addr", C.c_uint64),
+        ("bytes", C.c_uint64),
+        ("cat", C.c_int32),
+        ("flags", C.c_uint32),
+    ]
+
+
+def build() -> None:
+    subprocess.run(["make", "-s", "-C", HERE, "-j8"], check=True)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        path = os.path.join(HERE, "liboracle.so")
+        if not os.path.exists(path):
+            build()
+        L = C.CDLL(path)
+        L.or_fnv1a.restype = C.c_uint64
+        L.or_fnv1a.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64]
+        L.or_digest_of_words.restype = C.c_uint64
+        L.or_digest_of_words.argtypes = [C.c_void_p, C.c_uint64]
+        L.or_mix64.restype = C.c_uint64
+        L.or_mix64.argtypes = [C.c_uint64]
+        L.or_fill_mix64.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64]
+        L.or_num_chunks.restype = C.c_uint64
+        L.or_num_chunks.argtypes = [C.c_void_p, C.c_uint64, C.c_uint32]
+        L.or_hash.restype = C.c_int
+        L.or_hash.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32,
+                              C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
+        L.or_select.restype = C.c_uint64
+        L.or_select.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64,
+                                C.c_void_p, C.c_void_p, C.c_void_p]
+        L.or_stripe.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p,
+                                C.c_void_p, C.c_void_p, C.c_void_p]
+        L.or_compact.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p,
+                                 C.c_void_p, C.c_void_p]
+        L.or_restore.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p,
+                                 C.c_void_p]
+        L.or_grad_sum_u64.argtypes = [C.c_void_p, C.c_uint32, C.c_uint64, C.c_void_p]
+        L.or_grad_sum_f32.argtypes = [C.c_void_p, C.c_uint32, C.c_uint64, C.c_void_p]
+        _lib = L
+    return _lib
+
+
+def ref():
+    """The reference library (None when it was never built here)."""
+    global _ref
+    if _ref is None:
+        path = os.path.join(HERE, "_ref", "libfleetsim_ref.so")
+        if not os.path.exists(path):
+            return None
+        L = C.CDLL(path)
+        L.ref_digest_of_words.restype = C.c_uint64
+        L.ref_digest_of_words.argtypes = [C.c_void_p, C.c_uint64]
+        L.ref_digest_of_bytes.restype = C.c_uint64
+        L.ref_digest_of_bytes.argtypes = [C.c_void_p, C.c_uint64]
+        L.ref_mix64.restype = C.c_uint64
+        L.ref_mix64.argtypes = [C.c_uint64]
+        L.ref_store_new.restype = C.c_void_p
+        L.ref_store_free.argtypes = [C.c_void_p]
+        L.ref_store_put.restype = C.c_int
+        L.ref_store_put.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, U64P]
+        L.ref_store_get.restype = C.c_int
+        L.ref_store_get.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64]
+        L.ref_store_total_bytes.restype = C.c_uint64
+        L.ref_store_total_bytes.argtypes = [C.c_void_p]
+        L.ref_store_count.restype = C.c_uint64
+        L.ref_store_count.argtypes = [C.c_void_p]
+        L.ref_alloc_new.restype = C.c_void_p
+        L.ref_alloc_new.argtypes = [C.c_uint64, C.c_uint64]
+        L.ref_alloc_free_obj.argtypes = [C.c_void_p]
+        L.ref_alloc_alloc.restype = C.c_int
+        L.ref_alloc_alloc.argtypes = [C.c_void_p, C.c_uint64, C.c_int, U64P]
+        L.ref_alloc_free.restype = C.c_int
+        L.ref_alloc_free.argtypes = [C.c_void_p, C.c_uint64]
+        L.ref_alloc_stable_digest.restype = C.c_uint64
+        L.ref_alloc_stable_digest.argtypes = [C.c_void_p]
+        L.ref_alloc_cursors.argtypes = [C.c_void_p, U64P, U64P, U64P]
+        L.ref_carve.restype = C.c_int
+        L.ref_carve.argtypes = [C.c_uint64, C.c_uint64, C.c_double, C.c_void_p]
+        L.ref_snapshot_chunks.restype = C.c_uint64
+        L.ref_snapshot_chunks.argtypes = [C.c_void_p, C.c_uint64, C.c_uint32, C.c_int, C.c_void_p]
+        L.ref_restore_chunks.restype = C.c_int
+        L.ref_restore_chunks.argtypes = [C.c_void_p, C.c_uint64, C.c_uint32, C.c_int, C.c_void_p]
+        L.ref_grad_sum_u64.argtypes = [C.c_void_p, C.c_uint32, C.c_uint64, C.c_void_p, C.c_int]
+        _ref = L
+    return _ref
+
+
+# ----------------------------------------------------------------- helpers
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def mix64(x: int) -> int:
+    return lib().or_mix64(x)
+
+
+def fill_mix64(nwords: int, seed: int = 0, base: int = 0) -> np.ndarray:
+    out = np.empty(nwords, dtype=np.uint64)
+    lib().or_fill_mix64(_p(out), nwords, seed, base)
+    return out
+
+
+def digest_of_words(words: np.ndarray) -> int:
+    w = np.ascontiguousarray(words, dtype=np.uint64)
+    return lib().or_digest_of_words(_p(w), w.size)
+
+
+def digest_of_bytes(b: bytes) -> int:
+    return lib().or_fnv1a(b, len(b), 14695981039346656037)
+
+
+def bufs_array(bufs):
+    """bufs: iterable of (rank, slot, addr, bytes, cat) tuples or dicts."""
+    arr = (OrBuf * max(1, len(bufs)))()
+    for i, b in enumerate(bufs):
+        if isinstance(b, dict):
+            b = (b.get("rank", 0), b.get("slot", i), b["addr"], b["bytes"], b.get("cat", 0))
+        arr[i] = OrBuf(b[0], b[1], b[2], b[3], b[4] if len(b) > 4 else 0, 0)
+    return arr
+
+
+def num_chunks(bufs, chunk_bytes: int) -> int:
+    return lib().or_num_chunks(bufs_array(bufs), len(bufs), chunk_bytes)
+
+
+def _arena_ptrs(arenas):
+    arenas = [np.ascontiguousarray(a).view(np.uint8) for a in arenas]
+    ptrs = (C.c_void_p * len(arenas))(*[a.ctypes.data for a in arenas])
+    return arenas, ptrs
+
+
+def hash_chunks(arenas, bufs, page_bytes=4096, chunk_bytes=65536, nthreads=8):
+    """Returns (chunk_digests u64[n], chunk_lens u32[n], buf_digests u64[nbufs])."""
+    keep, ptrs = _arena_ptrs(arenas)
+    n = num_chunks(bufs, chunk_bytes)
+    d = np.zeros(max(n, 1), dtype=np.uint64)
+    lens = np.zeros(max(n, 1), dtype=np.uint32)
+    bd = np.zeros(max(len(bufs), 1), dtype=np.uint64)
+    rc = lib().or_hash(ptrs, bufs_array(bufs), len(bufs), page_bytes, chunk_bytes, _p(d), _p(lens),
+                       _p(bd), nthreads)
+    assert rc == 0, "or_hash: bad page/chunk geometry"
+    del keep
+    return d[:n], lens[:n], bd[: len(bufs)]
+
+
+def select(digests, lens, known=None):
+    """Returns (sel u8[n], owner u64[n], offsets u64[n], total_bytes)."""
+    d = np.ascontiguousarray(digests, dtype=np.uint64)
+    ln = np.ascontiguousarray(lens, dtype=np.uint32)
+    kn = np.ascontiguousarray(known if known is not None else np.zeros(0), dtype=np.uint64)
+    n = d.size
+    sel = np.zeros(max(n, 1), dtype=np.uint8)
+    owner = np.zeros(max(n, 1), dtype=np.uint64)
+    off = np.zeros(max(n, 1), dtype=np.uint64)
+    total = lib().or_select(_p(d), _p(ln), n, _p(kn), kn.size, _p(sel), _p(owner), _p(off))
+    return sel[:n], owner[:n], off[:n], int(total)
+
+
+def stripe(digests, lens, n_per_rank, sel):
+    d = np.ascontiguousarray(digests, dtype=np.uint64)
+    ln = np.ascontiguousarray(lens, dtype=np.uint32)
+    npr = np.ascontiguousarray(n_per_rank, dtype=np.uint64)
+    s = np.ascontiguousarray(sel, dtype=np.uint8)
+    n = d.size
+    writer = np.zeros(max(n, 1), dtype=np.int32)
+    off = np.zeros(max(n, 1), dtype=np.uint64)
+    sb = np.zeros(len(npr), dtype=np.uint64)
+    lib().or_stripe(_p(d), _p(ln), _p(npr), len(npr), _p(s), _p(writer), _p(off), _p(sb))
+    return writer[:n], off[:n], sb
+
+
+def compact(arenas, bufs, chunk_bytes, sel, offsets, total):
+    keep, ptrs = _arena_ptrs(arenas)
+    staging = np.zeros(max(int(total), 1), dtype=np.uint8)
+    s = np.ascontiguousarray(sel, dtype=np.uint8)
+    o = np.ascontiguousarray(offsets, dtype=np.uint64)
+    lib().or_compact(ptrs, bufs_array(bufs), len(bufs), chunk_bytes, _p(s), _p(o), _p(staging))
+    del keep
+    return staging[: int(total)]
+
+
+def restore(arenas, bufs, chunk_bytes, image, src_off):
+    """Scatter image chunks into the (mutable numpy) arenas in place."""
+    arenas = [a.view(np.uint8) for a in arenas]
+    ptrs = (C.c_void_p * len(arenas))(*[a.ctypes.data for a in arenas])
+    img = np.ascontiguousarray(image, dtype=np.uint8)
+    so = np.ascontiguousarray(src_off, dtype=np.uint64)
+    lib().or_restore(ptrs, bufs_array(bufs), len(bufs), chunk_bytes, _p(img), _p(so))
+
+
+def grad_sum_u64(grads):
+    gs = [np.ascontiguousarray(g, dtype=np.uint64) for g in grads]
+    ptrs = (C.c_void_p * len(gs))(*[g.ctypes.data for g in gs])
+    out = np.empty_like(gs[0])
+    lib().or_grad_sum_u64(ptrs, len(gs), gs[0].size, _p(out))
+    return out
+
+
+def grad_sum_f32(grads):
+    gs = [np.ascontiguousarray(g, dtype=np.float32) for g in grads]
+    ptrs = (C.c_void_p * len(gs))(*[g.ctypes.data for g in gs])
+    out = np.empty_like(gs[0])
+    lib().or_grad_sum_f32(ptrs, len(gs), gs[0].size, _p(out))
+    return out

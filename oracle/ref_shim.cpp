@@ -1,0 +1,182 @@
+// ref_shim.cpp — extern "C" wrapper over the REFERENCE library (fleetsim_core),
+// compiled from /root/reference/proj/src by oracle/Makefile into oracle/_ref/.
+// TEST INFRASTRUCTURE ONLY: it lets the tests pin the CPU restatement
+// (oracle/snap_oracle.c) and the product against the reference's own code,
+// and lets bench.py time the reference's CPU path (`--impl reference`,
+// cpu_baseline kind "reference"). Nothing in the product links it.
+#include <atomic>
+#include <cstring>
+#include <memory>
+#include <thread>
+#include <vector>
+
+#include "fleetsim/alloc.hpp"
+#include "fleetsim/ckpt.hpp"
+#include "fleetsim/sim.hpp"
+#include "fleetsim/splice.hpp"
+#include "fleetsim/vdev.hpp"
+
+using namespace fleetsim;
+
+extern "C" {
+
+// sim.hpp:67-70
+uint64_t ref_digest_of_words(const uint64_t* w, uint64_t n) {
+  return sim::digest_of_words(std::span<const u64>(w, n)).value;
+}
+// sim.hpp:58-65
+uint64_t ref_digest_of_bytes(const uint8_t* p, uint64_t n) {
+  return sim::digest_of(std::span<const u8>(p, n)).value;
+}
+uint64_t ref_mix64(uint64_t x) { return sim::mix64(x); }
+
+// ---- ckpt::BlobStore (ckpt.cpp:16-52) ----
+void* ref_store_new() { return new ckpt::BlobStore(); }
+void ref_store_free(void* s) { delete static_cast<ckpt::BlobStore*>(s); }
+int ref_store_put(void* s, const uint64_t* w, uint64_t n, uint64_t* digest) {
+  auto r = static_cast<ckpt::BlobStore*>(s)->put(std::span<const u64>(w, n));
+  *digest = r.digest.value;
+  return r.fresh ? 1 : 0;
+}
+// 0 ok, -1 missing / verification failure (SimFault), -2 size mismatch
+int ref_store_get(void* s, uint64_t digest, uint64_t* out, uint64_t n) {
+  try {
+    const auto& v = static_cast<ckpt::BlobStore*>(s)->get(sim::Digest{digest});
+    if (v.size() != n) return -2;
+    std::memcpy(out, v.data(), n * 8);
+    return 0;
+  } catch (const SimFault&) {
+    return -1;
+  }
+}
+uint64_t ref_store_total_bytes(void* s) { return static_cast<ckpt::BlobStore*>(s)->total_bytes(); }
+uint64_t ref_store_count(void* s) { return static_cast<ckpt::BlobStore*>(s)->count(); }
+
+// ---- mem::BidiAllocator (alloc.cpp:62-155) ----
+void* ref_alloc_new(uint64_t low, uint64_t high) { return new mem::BidiAllocator(low, high); }
+void ref_alloc_free_obj(void* a) { delete static_cast<mem::BidiAllocator*>(a); }
+// 0 ok, 1 OOM (nullopt), -1 SimFault
+int ref_alloc_alloc(void* a, uint64_t bytes, int stable, uint64_t* addr) {
+  try {
+    auto r = static_cast<mem::BidiAllocator*>(a)->alloc(
+        bytes, stable ? mem::Stability::Stable : mem::Stability::Transient);
+    if (!r) return 1;
+    *addr = *r;
+    return 0;
+  } catch (const SimFault&) {
+    return -1;
+  }
+}
+int ref_alloc_free(void* a, uint64_t addr) {
+  try {
+    static_cast<mem::BidiAllocator*>(a)->free(addr);
+    return 0;
+  } catch (const SimFault&) {
+    return -1;
+  }
+}
+uint64_t ref_alloc_stable_digest(void* a) {
+  return static_cast<mem::BidiAllocator*>(a)->stable_state_digest().value;
+}
+void ref_alloc_cursors(void* a, uint64_t* tc, uint64_t* sc, uint64_t* live) {
+  auto* x = static_cast<mem::BidiAllocator*>(a);
+  *tc = x->transient_cursor();
+  *sc = x->stable_cursor();
+  *live = x->live_bytes();
+}
+
+// ---- splice::DeviceLayout::carve (splice.cpp:7-19) ----
+int ref_carve(uint64_t mem, uint64_t max_buf, double slack, uint64_t out[3]) {
+  try {
+    auto l = splice::DeviceLayout::carve(mem, max_buf, slack);
+    out[0] = l.rank_region_end;
+    out[1] = l.scratch_base;
+    out[2] = l.scratch_bytes;
+    return 0;
+  } catch (const InternalError&) {
+    return -1;
+  }
+}
+
+// ---- the reference's CPU snapshot path, timed as the baseline ----
+// Per 64 KiB chunk: BlobStore::put (digest_of_words + dedup map + copy),
+// exactly what build_manifest does per device buffer (ckpt.cpp:157-164), at
+// chunk granularity. One BlobStore per thread (the class is not thread-safe).
+// Returns store-fresh bytes; digests[g] receives the put digest.
+uint64_t ref_snapshot_chunks(const uint8_t* image, uint64_t bytes, uint32_t chunk_bytes,
+                             int nthreads, uint64_t* digests) {
+  uint64_t nchunks = (bytes + chunk_bytes - 1) / chunk_bytes;
+  if (nthreads < 1) nthreads = 1;
+  std::atomic<uint64_t> fresh{0};
+  auto work = [&](int t) {
+    ckpt::BlobStore store;
+    uint64_t f = 0;
+    for (uint64_t g = t; g < nchunks; g += nthreads) {
+      uint64_t off = g * chunk_bytes;
+      uint64_t len = std::min<uint64_t>(chunk_bytes, bytes - off);
+      auto r = store.put(std::span<const u64>(reinterpret_cast<const u64*>(image + off), len / 8));
+      if (digests) digests[g] = r.digest.value;
+      if (r.fresh) f += len;
+    }
+    fresh += f;
+  };
+  std::vector<std::thread> th;
+  for (int t = 1; t < nthreads; ++t) th.emplace_back(work, t);
+  work(0);
+  for (auto& x : th) x.join();
+  return fresh.load();
+}
+
+// Reference restore path: BlobStore::get (digest-verified, ckpt.cpp:23-29) +
+// Gpu::write_words at the recorded address (ckpt.cpp:522-523).
+// Returns 0, or -1 on a verification failure.
+int ref_restore_chunks(const uint8_t* image, uint64_t bytes, uint32_t chunk_bytes, int nthreads,
+                       uint8_t* out) {
+  uint64_t nchunks = (bytes + chunk_bytes - 1) / chunk_bytes;
+  if (nthreads < 1) nthreads = 1;
+  std::atomic<int> bad{0};
+  auto work = [&](int t) {
+    ckpt::BlobStore store;
+    std::vector<sim::Digest> ds;
+    for (uint64_t g = t; g < nchunks; g += nthreads) {
+      uint64_t off = g * chunk_bytes;
+      uint64_t len = std::min<uint64_t>(chunk_bytes, bytes - off);
+      ds.push_back(store.put(std::span<const u64>(reinterpret_cast<const u64*>(image + off), len / 8))
+                       .digest);
+    }
+    size_t i = 0;
+    for (uint64_t g = t; g < nchunks; g += nthreads, ++i) {
+      uint64_t off = g * chunk_bytes;
+      try {
+        const auto& v = store.get(ds[i]);
+        std::memcpy(out + off, v.data(), v.size() * 8);
+      } catch (const SimFault&) {
+        bad = 1;
+      }
+    }
+  };
+  std::vector<std::thread> th;
+  for (int t = 1; t < nthreads; ++t) th.emplace_back(work, t);
+  work(0);
+  for (auto& x : th) x.join();
+  return bad ? -1 : 0;
+}
+
+// Reference gradient sum (collectives.cpp:140-141) over nranks contributions.
+void ref_grad_sum_u64(const uint64_t* const* g, uint32_t nranks, uint64_t n, uint64_t* out,
+                      int nthreads) {
+  if (nthreads < 1) nthreads = 1;
+  auto work = [&](int t) {
+    uint64_t lo = n * t / nthreads, hi = n * (t + 1) / nthreads;
+    std::vector<u64> sum(hi - lo, 0);
+    for (uint32_t r = 0; r < nranks; ++r)
+      for (uint64_t i = lo; i < hi; ++i) sum[i - lo] += g[r][i];
+    std::memcpy(out + lo, sum.data(), (hi - lo) * 8);
+  };
+  std::vector<std::thread> th;
+  for (int t = 1; t < nthreads; ++t) th.emplace_back(work, t);
+  work(0);
+  for (auto& x : th) x.join();
+}
+
+}  // extern "C"

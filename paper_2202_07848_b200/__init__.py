@@ -1,0 +1,313 @@
+"""paper_2202_07848_b200 — B200-native snapshot / dedup / restore / splice hot path.
+
+Thin ctypes binding of the C ABI in include/snap.h (libsnap.so, built in-tree
+by `make -C paper_2202_07848_b200`). There is no CPU fallback: importing works
+anywhere, but every compute call goes through the sm_100a kernels and raises
+SnapError when the library or a B200 is missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsnap.so")
+
+SNAP_OK, SNAP_EINVAL, SNAP_ENOMEM, SNAP_EFAULT, SNAP_ECUDA, SNAP_EINTERNAL = 0, -1, -2, -3, -4, -5
+U64, F32 = 0, 1
+
+# vdev::BufCat (vdev.hpp:17)
+PARAM, OPTSTATE, GRAD, ACTIVATION, SCRATCH = range(5)
+
+
+class SnapError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{msg} (code {code})")
+        self.code = code
+
+
+class SnapFault(SnapError):
+    """SNAP_EFAULT: the reference's SimFault (common.hpp:31-35)."""
+
+
+class SnapBuf(C.Structure):
+    """snap_buf = RankBuf/DevRec (splice.hpp:26-34, ckpt.hpp:64-71)."""
+
+    _fields_ = [
+        ("rank", C.c_uint32),
+        ("slot", C.c_int32),
+        ("addr", C.c_uint64),
+        ("bytes", C.c_uint64),
+        ("cat", C.c_int32),
+        ("flags", C.c_uint32),
+    ]
+
+
+class SnapGeom(C.Structure):
+    _fields_ = [("page_bytes", C.c_uint32), ("chunk_bytes", C.c_uint32)]
+
+
+_lib = None
+
+_SIGS = {
+    "snap_open": (C.c_int, [C.c_int, C.c_uint64, C.POINTER(C.c_void_p)]),
+    "snap_close": (C.c_int, [C.c_void_p]),
+    "snap_last_error": (C.c_char_p, [C.c_void_p]),
+    "snap_strerror": (C.c_char_p, [C.c_int]),
+    "snap_arena": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)]),
+    "snap_launch_count": (C.c_uint64, [C.c_void_p]),
+    "snap_sync": (C.c_int, [C.c_void_p]),
+    "snap_layout_carve": (C.c_int, [C.c_uint64, C.c_uint64, C.c_double, C.c_void_p]),
+    "snap_write": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64]),
+    "snap_read": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64]),
+    "snap_fill_mix64": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64]),
+    "snap_xor_words": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64]),
+    "snap_set_buffers": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p,
+                                   C.POINTER(C.c_uint64)]),
+    "snap_hash": (C.c_int, [C.c_void_p]),
+    "snap_get_digests": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "snap_digest_ranges": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]),
+    "snap_known_clear": (C.c_int, [C.c_void_p]),
+    "snap_known_add": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
+    "snap_known_commit": (C.c_int, [C.c_void_p]),
+    "snap_select": (C.c_int, [C.c_void_p]),
+    "snap_get_selection": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                     C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "snap_compact": (C.c_int, [C.c_void_p]),
+    "snap_snapshot": (C.c_int, [C.c_void_p]),
+    "snap_staging": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)]),
+    "snap_read_staging": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64]),
+    "snap_restore": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_int]),
+    "snap_restore_self": (C.c_int, [C.c_void_p, C.c_int]),
+    "snap_grad_sum": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_uint32, C.c_uint64,
+                                C.c_uint64, C.c_int]),
+    "snap_comm_unique_id": (C.c_int, [C.c_void_p]),
+    "snap_comm_init": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
+    "snap_allreduce": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, C.c_uint64]),
+    "snap_timer_start": (C.c_int, [C.c_void_p]),
+    "snap_timer_stop": (C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
+}
+
+
+def build() -> None:
+    subprocess.run(["make", "-s", "-C", HERE, "-j8"], check=True)
+
+
+def lib():
+    """Loads libsnap.so; raises if it was never built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise SnapError(SNAP_ECUDA, f"{LIB_PATH} missing: run `make -C {HERE}` "
+                                        "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def exported_symbols():
+    return list(_SIGS)
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def bufs_array(bufs):
+    arr = (SnapBuf * max(1, len(bufs)))()
+    for i, b in enumerate(bufs):
+        if isinstance(b, dict):
+            b = (b.get("rank", 0), b.get("slot", i), b["addr"], b["bytes"], b.get("cat", 0))
+        arr[i] = SnapBuf(b[0], b[1], b[2], b[3], b[4] if len(b) > 4 else 0, 0)
+    return arr
+
+
+def layout_carve(mem_bytes, max_buffer_bytes, slack_fraction):
+    """splice::DeviceLayout::carve (splice.cpp:7-19) -> (rank_region_end, scratch_base, scratch_bytes)."""
+    out = (C.c_uint64 * 3)()
+    rc = lib().snap_layout_carve(mem_bytes, max_buffer_bytes, slack_fraction, out)
+    if rc != SNAP_OK:
+        raise SnapError(rc, "device too small for layout")
+    return tuple(out)
+
+
+class Ctx:
+    """One snap_ctx: the per-(job, GPU) device proxy (proxy.hpp:32-122)."""
+
+    def __init__(self, device: int = 0, arena_bytes: int = 1 << 28):
+        self._L = lib()
+        h = C.c_void_p()
+        rc = self._L.snap_open(device, arena_bytes, C.byref(h))
+        if rc != SNAP_OK:
+            raise SnapError(rc, f"snap_open(device={device}, arena={arena_bytes}): "
+                                f"{self._L.snap_strerror(rc).decode()}")
+        self.h = h
+        self.arena_bytes = arena_bytes
+        self.nchunks = 0
+        self.nbufs = 0
+
+    # -- plumbing
+    def close(self):
+        if self.h:
+            self._L.snap_close(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def _ck(self, rc, what):
+        if rc != SNAP_OK:
+            msg = f"{what}: {self._L.snap_last_error(self.h).decode()}"
+            raise (SnapFault if rc == SNAP_EFAULT else SnapError)(rc, msg)
+
+    @property
+    def launches(self) -> int:
+        return int(self._L.snap_launch_count(self.h))
+
+    def arena_ptr(self) -> int:
+        p = C.c_void_p()
+        self._ck(self._L.snap_arena(self.h, C.byref(p), None), "snap_arena")
+        return p.value
+
+    def sync(self):
+        self._ck(self._L.snap_sync(self.h), "snap_sync")
+
+    def write(self, addr: int, data: np.ndarray):
+        d = np.ascontiguousarray(data)
+        self._ck(self._L.snap_write(self.h, addr, _p(d), d.nbytes), "snap_write")
+
+    def read(self, addr: int, nbytes: int) -> np.ndarray:
+        out = np.empty(nbytes, dtype=np.uint8)
+        self._ck(self._L.snap_read(self.h, addr, _p(out), nbytes), "snap_read")
+        return out
+
+    def fill_mix64(self, addr: int, nbytes: int, seed: int = 0, base: int = 0):
+        self._ck(self._L.snap_fill_mix64(self.h, addr, nbytes, seed, base), "snap_fill_mix64")
+
+    def xor_words(self, addrs, value: int):
+        a = np.ascontiguousarray(addrs, dtype=np.uint64)
+        self._ck(self._L.snap_xor_words(self.h, _p(a), a.size, value), "snap_xor_words")
+
+    # -- K1
+    def set_buffers(self, bufs, page_bytes=4096, chunk_bytes=65536) -> int:
+        arr = bufs_array(bufs)
+        g = SnapGeom(page_bytes, chunk_bytes)
+        n = C.c_uint64()
+        self._ck(self._L.snap_set_buffers(self.h, arr, len(bufs), C.byref(g), C.byref(n)),
+                 "snap_set_buffers")
+        self.nchunks = n.value
+        self.nbufs = len(bufs)
+        return self.nchunks
+
+    def hash(self):
+        self._ck(self._L.snap_hash(self.h), "snap_hash")
+
+    def digests(self, buf_digests=False):
+        n = self.nchunks
+        d = np.zeros(max(n, 1), dtype=np.uint64)
+        lens = np.zeros(max(n, 1), dtype=np.uint32)
+        bd = np.zeros(max(self.nbufs, 1), dtype=np.uint64)
+        self._ck(self._L.snap_get_digests(self.h, _p(d), _p(lens), _p(bd) if buf_digests else None),
+                 "snap_get_digests")
+        if buf_digests:
+            return d[:n], lens[:n], bd[: self.nbufs]
+        return d[:n], lens[:n]
+
+    # -- K2
+    def known_clear(self):
+        self._ck(self._L.snap_known_clear(self.h), "snap_known_clear")
+
+    def known_add(self, digests):
+        d = np.ascontiguousarray(digests, dtype=np.uint64)
+        self._ck(self._L.snap_known_add(self.h, _p(d), d.size), "snap_known_add")
+
+    def known_commit(self):
+        self._ck(self._L.snap_known_commit(self.h), "snap_known_commit")
+
+    def select(self):
+        self._ck(self._L.snap_select(self.h), "snap_select")
+
+    def selection(self):
+        n = self.nchunks
+        sel = np.zeros(max(n, 1), dtype=np.uint8)
+        owner = np.zeros(max(n, 1), dtype=np.uint64)
+        off = np.zeros(max(n, 1), dtype=np.uint64)
+        sb, sc = C.c_uint64(), C.c_uint64()
+        self._ck(self._L.snap_get_selection(self.h, _p(sel), _p(owner), _p(off), C.byref(sb),
+                                            C.byref(sc)), "snap_get_selection")
+        return sel[:n], owner[:n], off[:n], sb.value, sc.value
+
+    # -- K3
+    def compact(self):
+        self._ck(self._L.snap_compact(self.h), "snap_compact")
+
+    def snapshot(self):
+        self._ck(self._L.snap_snapshot(self.h), "snap_snapshot")
+
+    def staging_ptr(self):
+        p, n = C.c_void_p(), C.c_uint64()
+        self._ck(self._L.snap_staging(self.h, C.byref(p), C.byref(n)), "snap_staging")
+        return p.value, n.value
+
+    def read_staging(self, off: int, nbytes: int) -> np.ndarray:
+        out = np.empty(nbytes, dtype=np.uint8)
+        self._ck(self._L.snap_read_staging(self.h, off, _p(out), nbytes), "snap_read_staging")
+        return out
+
+    # -- K4
+    def restore(self, image_ptr: int, image_bytes: int, src_off, expect=None, verify=True):
+        so = np.ascontiguousarray(src_off, dtype=np.uint64)
+        ex = None if expect is None else np.ascontiguousarray(expect, dtype=np.uint64)
+        self._ck(self._L.snap_restore(self.h, C.c_void_p(image_ptr), image_bytes, _p(so),
+                                      _p(ex) if ex is not None else None, 1 if verify else 0),
+                 "snap_restore")
+
+    def restore_self(self, verify=True):
+        self._ck(self._L.snap_restore_self(self.h, 1 if verify else 0), "snap_restore_self")
+
+    # -- K5
+    def grad_sum(self, dtype, src_addrs, dst_addr, elems, accumulate=False):
+        a = np.ascontiguousarray(src_addrs, dtype=np.uint64)
+        self._ck(self._L.snap_grad_sum(self.h, dtype, _p(a), a.size, dst_addr, elems,
+                                       1 if accumulate else 0), "snap_grad_sum")
+
+    # -- NCCL
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        rc = lib().snap_comm_unique_id(buf)
+        if rc != SNAP_OK:
+            raise SnapError(rc, "ncclGetUniqueId failed")
+        return bytes(buf)
+
+    def comm_init(self, nranks: int, rank: int, uid: bytes):
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        self._ck(self._L.snap_comm_init(self.h, nranks, rank, buf), "snap_comm_init")
+
+    def allreduce(self, dtype, addr, elems):
+        self._ck(self._L.snap_allreduce(self.h, dtype, addr, elems), "snap_allreduce")
+
+    # -- timing
+    def timer_start(self):
+        self._ck(self._L.snap_timer_start(self.h), "snap_timer_start")
+
+    def timer_stop(self) -> float:
+        ms = C.c_float()
+        self._ck(self._L.snap_timer_stop(self.h, C.byref(ms)), "snap_timer_stop")
+        return ms.value

@@ -1,0 +1,137 @@
+// k_copy.cu — K3 (stream compaction gather into the staging image) and K4
+// (inverse scatter-restore), plus the digest comparison used by verified
+// restores.
+//
+// K3 replaces the per-buffer copies of build_manifest's dump
+// (content_of + BlobStore::put, ckpt.cpp:161-163) and the swap-out copies of
+// execute_switch (host_cache_put, splice.cpp:79-82,266); K4 replaces
+// restore_job's Gpu::write_words at the recorded address (ckpt.cpp:522-523)
+// and the swap-in writes of execute_switch (splice.cpp:293-303).
+//
+// One warp moves one chunk: 32 lanes x 16 B per access, 8 independent
+// 16-byte loads in flight per lane (4 KiB per warp) before the stores, so a
+// persistent grid of 148 x 32 warps keeps ~19 MB of reads in flight. Loads
+// and stores use the streaming (.cs / evict-first) hints: neither side is
+// re-read soon.
+#include <cuda_runtime.h>
+
+#include "snap_internal.h"
+
+namespace snap {
+namespace {
+
+constexpr int kThreads = 512;
+constexpr int kUnroll = 8;
+
+__device__ __forceinline__ uint32_t find_buf(const GridDev& g, uint64_t gc) {
+  uint32_t lo = 0, hi = g.nbufs;
+  while (hi - lo > 1) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (__ldg(g.cstart + mid) <= gc) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ const uint8_t* chunk_ptr(const uint8_t* arena, const GridDev& g,
+                                                    uint64_t gc) {
+  const uint32_t b = find_buf(g, gc);
+  return arena + __ldg(g.addr + b) + ((gc - __ldg(g.cstart + b)) << g.chunk_shift);
+}
+
+// Warp copy of `len` bytes (multiple of 256, both pointers 256-B aligned).
+__device__ __forceinline__ void warp_copy(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src,
+                                          uint32_t len, int lane) {
+  const uint4* s = reinterpret_cast<const uint4*>(src);
+  uint4* d = reinterpret_cast<uint4*>(dst);
+  const uint32_t n16 = len >> 4;
+  uint32_t i = lane;
+  for (; i + (kUnroll - 1) * 32 < n16; i += kUnroll * 32) {
+    uint4 v[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) v[u] = __ldcs(s + i + u * 32);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) __stcs(d + i + u * 32, v[u]);
+  }
+  for (; i < n16; i += 32) __stcs(d + i, __ldcs(s + i));
+}
+
+__global__ void __launch_bounds__(kThreads)
+k_gather(const uint8_t* __restrict__ arena, GridDev g, const uint32_t* __restrict__ lens,
+         const uint32_t* __restrict__ sel_list, const uint64_t* __restrict__ totals,
+         const uint64_t* __restrict__ offsets, uint8_t* __restrict__ staging) {
+  const uint64_t nsel = totals[0];
+  const int lane = threadIdx.x & 31;
+  const uint64_t w0 = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * kThreads) >> 5;
+  for (uint64_t w = w0; w < nsel; w += nw) {
+    const uint32_t gc = sel_list[w];
+    warp_copy(staging + offsets[gc], chunk_ptr(arena, g, gc), lens[gc], lane);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+k_scatter(uint8_t* __restrict__ arena, GridDev g, const uint32_t* __restrict__ lens,
+          const uint8_t* __restrict__ image, const uint64_t* __restrict__ src_off) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t w0 = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * kThreads) >> 5;
+  for (uint64_t gc = w0; gc < g.nchunks; gc += nw) {
+    uint8_t* dst = const_cast<uint8_t*>(chunk_ptr(arena, g, gc));
+    warp_copy(dst, image + src_off[gc], lens[gc], lane);
+  }
+}
+
+__global__ void k_compare(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b,
+                          uint64_t n, unsigned long long* nbad) {
+  unsigned long long bad = 0;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    bad += a[i] != b[i];
+  for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  if ((threadIdx.x & 31) == 0 && bad) atomicAdd(nbad, bad);
+}
+
+unsigned copy_grid() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return unsigned(n) * 2;  // 2 CTAs x 16 warps per SM
+}
+
+}  // namespace
+
+int launch_gather(const uint8_t* arena, const GridDev& g, const uint32_t* lens,
+                  const uint32_t* sel_list, const uint64_t* totals, const uint64_t* offsets,
+                  uint8_t* staging, uint64_t max_sel, cudaStream_t s) {
+  if (max_sel == 0) return 0;
+  uint64_t blocks = (max_sel * 32 + kThreads - 1) / kThreads;
+  if (blocks > copy_grid()) blocks = copy_grid();
+  k_gather<<<unsigned(blocks), kThreads, 0, s>>>(arena, g, lens, sel_list, totals, offsets,
+                                                 staging);
+  return 1;
+}
+
+int launch_scatter(uint8_t* arena, const GridDev& g, const uint32_t* lens, const uint8_t* image,
+                   const uint64_t* src_off, cudaStream_t s) {
+  if (g.nchunks == 0) return 0;
+  uint64_t blocks = (g.nchunks * 32 + kThreads - 1) / kThreads;
+  if (blocks > copy_grid()) blocks = copy_grid();
+  k_scatter<<<unsigned(blocks), kThreads, 0, s>>>(arena, g, lens, image, src_off);
+  return 1;
+}
+
+int launch_compare(const uint64_t* a, const uint64_t* b, uint64_t n, unsigned long long* nbad,
+                   cudaStream_t s) {
+  cudaMemsetAsync(nbad, 0, sizeof(unsigned long long), s);
+  if (n == 0) return 0;
+  uint64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_compare<<<unsigned(blocks), 256, 0, s>>>(a, b, n, nbad);
+  return 1;
+}
+
+}  // namespace snap

@@ -1,0 +1,69 @@
+// snap_internal.h — shared declarations of the sm_100a kernels and the ctx.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "snap.h"
+
+namespace snap {
+
+constexpr uint64_t kFnvOffset = 14695981039346656037ull;  // sim.hpp:57
+constexpr uint32_t kFnvPrimeLo = 0x1b3u;                   // prime = 2^40 + 0x1b3 (sim.hpp:58)
+
+// Device-resident buffer table for one installed grid.
+struct GridDev {
+  const uint64_t* addr = nullptr;    // [nbufs]
+  const uint64_t* bytes = nullptr;   // [nbufs]
+  const uint64_t* cstart = nullptr;  // [nbufs + 1] chunk prefix
+  uint32_t nbufs = 0;
+  uint64_t nchunks = 0;
+  uint32_t page_shift = 12;
+  uint32_t chunk_shift = 16;
+};
+
+// Open-addressing digest table (dedup + known set), power-of-two capacity.
+struct TableDev {
+  unsigned long long* keys = nullptr;  // kEmptyKey = unused
+  unsigned long long* vals = nullptr;  // min chunk index
+  uint64_t mask = 0;
+};
+constexpr unsigned long long kEmptyKey = 0xffffffffffffffffull;
+
+// Launchers (each returns the number of kernels launched).
+int launch_hash(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig, cudaStream_t s);
+int launch_buf_fold(const GridDev& g, const uint64_t* chunk_dig, uint64_t* buf_dig, cudaStream_t s);
+int launch_fill_mix64(uint64_t* dst, uint64_t nwords, uint64_t seed, uint64_t base, cudaStream_t s);
+int launch_xor_words(uint8_t* arena, const uint64_t* addrs, uint64_t n, uint64_t value,
+                     cudaStream_t s);
+
+int launch_table_clear(TableDev t, cudaStream_t s);
+int launch_table_insert_min(TableDev t, const uint64_t* keys, uint64_t n, uint64_t index_base,
+                            cudaStream_t s);
+// sel/owner/offsets + compact index list; `scan_state` sized by scan_state_words(n)
+uint64_t scan_state_words(uint64_t n);
+int launch_select(TableDev dedup, TableDev known, bool use_known, const uint64_t* dig,
+                  const uint32_t* lens, uint64_t n, uint64_t* scan_state, uint8_t* sel,
+                  uint64_t* owner, uint64_t* offsets, uint32_t* sel_list, uint64_t* totals,
+                  cudaStream_t s);
+int launch_resolve_dups(const uint8_t* sel, const uint64_t* owner, uint64_t* offsets, uint64_t n,
+                        cudaStream_t s);
+
+// K3 / K4 chunk copies.
+int launch_gather(const uint8_t* arena, const GridDev& g, const uint32_t* lens,
+                  const uint32_t* sel_list, const uint64_t* totals, const uint64_t* offsets,
+                  uint8_t* staging, uint64_t max_sel, cudaStream_t s);
+int launch_scatter(uint8_t* arena, const GridDev& g, const uint32_t* lens, const uint8_t* image,
+                   const uint64_t* src_off, cudaStream_t s);
+int launch_compare(const uint64_t* a, const uint64_t* b, uint64_t n, unsigned long long* nbad,
+                   cudaStream_t s);
+
+// K5.
+int launch_grad_sum(int dtype, uint8_t* arena, const uint64_t* src_addrs_dev, uint32_t nsrc,
+                    uint64_t dst_addr, uint64_t elems, int accumulate, cudaStream_t s);
+
+}  // namespace snap
