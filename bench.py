@@ -1,0 +1,408 @@
+"""bench.py — snapshot hash+dedup+compact GB/s on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], "C2"): one data-parallel rank per GPU, each holding a
+2 GiB device image = 1.5 GiB replicated state (bf16 params + fp32 Adam m, v: 2:4:4 bytes per
+param, identical bytes at identical addresses on every rank) + 0.5 GiB per-rank state
+(gradients/activations), 64 KiB chunks of 16 x 4 KiB pages. One step = one snapshot of every
+rank's image: K1 hash -> (N>1: NCCL allgather of digest vectors) -> K2 dedup/select ->
+K3 striped stream compaction into the staging image. Weak scaling: each GPU owns one rank.
+
+value = total image bytes snapshotted by all ranks / step time (max over ranks, CUDA events).
+e2e   = the same through snap_snapshot_host(): the image starts in pinned host memory, the
+        H2D copy and the D2H of the staging shard + digests are inside the timed region.
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+GIB = 1 << 30
+CHUNK = 65536
+PAGE = 4096
+METRIC = "snapshot hash+dedup+compact GB/s (1/2/4/8 GPU, % HBM roofline); splice swap ms"
+
+
+# ------------------------------------------------------------------ workload
+
+def c2_layout():
+    """C2 per-rank image: replicated P (bf16) + m, v (fp32) then per-rank grads.
+    Returns (bufs, replicated_bytes, per_rank_bytes). Identical addresses on every rank
+    (the allocator's stable-address property, test_alloc.cpp:44-80)."""
+    nparams = 161_061_248  # 10 B/param -> 1.5 GiB - 256 B
+    bufs, addr, slot = [], 0, 0
+
+    def add(total, n, cat):
+        nonlocal addr, slot
+        per = (total // n) // 256 * 256
+        for i in range(n):
+            sz = per if i < n - 1 else total - per * (n - 1)
+            bufs.append((0, slot, addr, sz, cat))
+            addr += sz
+            slot += 1
+
+    add(2 * nparams, 96, 0)  # params, bf16
+    add(4 * nparams, 96, 1)  # Adam m
+    add(4 * nparams, 96, 1)  # Adam v
+    replicated = addr
+    add(512 << 20, 64, 2)  # per-rank grads/activations
+    return bufs, replicated, addr - replicated
+
+
+def fill_rank(ctx, rank, replicated, per_rank, seed=1):
+    ctx.fill_mix64(0, replicated, seed, 0)
+    ctx.fill_mix64(replicated, per_rank, seed ^ (rank << 40), replicated // 8)
+
+
+def host_image(rank, replicated, per_rank, seed=1):
+    import oracle as O
+    img = np.empty((replicated + per_rank) // 8, np.uint64)
+    O.lib().or_fill_mix64(img.ctypes.data, replicated // 8, seed, 0)
+    O.lib().or_fill_mix64(img[replicated // 8:].ctypes.data, per_rank // 8, seed ^ (rank << 40),
+                          replicated // 8)
+    return img
+
+
+# ------------------------------------------------------------------ plumbing
+
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch.distributed as td
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            td.init_process_group("gloo", rank=self.rank, world_size=self.world)
+            self.td = td
+
+    def barrier(self):
+        if self.world > 1:
+            self.td.barrier()
+
+    def max(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64)
+        self.td.all_reduce(t, op=self.td.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64)
+        self.td.all_reduce(t, op=self.td.ReduceOp.SUM)
+        return float(t.item())
+
+    def bcast_bytes(self, b: bytes | None, n: int) -> bytes:
+        if self.world == 1:
+            return b
+        import torch
+        t = torch.zeros(n, dtype=torch.uint8)
+        if self.rank == 0:
+            t[:] = torch.frombuffer(bytearray(b), dtype=torch.uint8)
+        self.td.broadcast(t, 0)
+        return bytes(t.numpy().tobytes())
+
+    def close(self):
+        if self.world > 1:
+            self.td.destroy_process_group()
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = self.rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i] == "Active"})
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(r[0]) for r in rows if num(r[0])]
+        load = [s for s, r in zip(sm, rows) if (num(r[2]) or 0) > 250] or sm
+        return {"sm_mhz": float(np.median(load)) if load else None,
+                "sm_max_mhz": num(rows[0][1]) if rows else None,
+                "samples": len(rows), "reasons": reasons}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def traffic_for(kernel: str):
+    """dram read+write bytes per launch of `kernel` from the committed ncu summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        return t.get(kernel, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def cpu_baseline(replicated, per_rank, seconds_cap=30.0):
+    """The reference's own CPU snapshot path (oracle/_ref: per-chunk BlobStore::put =
+    digest_of_words + dedup map + copy, ckpt.cpp:16-21), all host threads, on this
+    rank-0 image. Bounded sample: the first `sample` bytes of the rank image."""
+    import oracle as O
+    R = O.ref()
+    kind = "reference"
+    nthreads = os.cpu_count() or 1
+    img = host_image(0, replicated, per_rank)
+    sample = min(img.nbytes, 1 << 30)
+    if R is None:
+        return {"value": None, "unit": "GB/s", "cores": nthreads, "kind": "unavailable",
+                "sample": "reference library not built"}
+    t0 = time.perf_counter()
+    R.ref_snapshot_chunks(img.ctypes.data, sample, CHUNK, nthreads, None)
+    dt = time.perf_counter() - t0
+    # single-core figure on 128 MiB for context (the reference is single-threaded)
+    t1 = time.perf_counter()
+    R.ref_snapshot_chunks(img.ctypes.data, 128 << 20, CHUNK, 1, None)
+    dt1 = time.perf_counter() - t1
+    return {"value": round(sample / dt / 1e9, 3), "unit": "GB/s", "cores": nthreads, "kind": kind,
+            "sample": f"first {sample >> 20} MiB of the rank-0 C2 image, 64 KiB chunks, "
+                      f"BlobStore::put per chunk, {nthreads} threads x 1 store each",
+            "single_core_gbs": round((128 << 20) / dt1 / 1e9, 3)}
+
+
+# ------------------------------------------------------------------ arms
+
+def run_reference(args, dist):
+    """--impl reference: the reference's CPU implementation of the path (BlobStore::put per
+    chunk over the same rank image), all host threads, rank 0 only."""
+    if dist.rank != 0:
+        return
+    import oracle as O
+    R = O.ref()
+    bufs, replicated, per_rank = c2_layout()
+    cfg = {"workload": "C2 rank image: 1.5 GiB replicated bf16 P + fp32 Adam m,v + 0.5 GiB "
+                       "per-rank grads, 64 KiB chunks", "chunk_bytes": CHUNK,
+           "image_bytes_per_rank": replicated + per_rank}
+    if R is None:
+        print(json.dumps({"impl": "reference", "unavailable": "reference library (oracle/_ref) "
+                                                             "not built"}))
+        return
+    nthreads = os.cpu_count() or 1
+    img = host_image(0, replicated, per_rank)
+    sample = min(img.nbytes, 1 << 30)
+    for _ in range(args.warmup):
+        R.ref_snapshot_chunks(img.ctypes.data, sample, CHUNK, nthreads, None)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        R.ref_snapshot_chunks(img.ctypes.data, sample, CHUNK, nthreads, None)
+    dt = time.perf_counter() - t0
+    v = sample * args.steps / dt / 1e9
+    desc = (f"per step: first {sample >> 20} MiB of the rank-0 C2 image, BlobStore::put per "
+            f"64 KiB chunk, {nthreads} threads")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": cfg,
+        "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": nthreads,
+                         "kind": "reference", "sample": desc},
+        "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0}}))
+
+
+def run_ours(args, dist):
+    import paper_2202_07848_b200 as snap
+
+    bufs, replicated, per_rank = c2_layout()
+    image = replicated + per_rank
+    N = dist.world
+    ctx = snap.Ctx(dist.local, image + (16 << 20))
+    fill_rank(ctx, dist.rank, replicated, per_rank)
+    nchunks = ctx.set_buffers(bufs, PAGE, CHUNK)
+    if N > 1:
+        uid = snap.Ctx.unique_id() if dist.rank == 0 else None
+        uid = dist.bcast_bytes(uid, 128)
+        ctx.comm_init(N, dist.rank, uid)
+    ctx.sync()
+
+    def step():
+        ctx.snapshot()
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    ctx.sync()
+    # staged bytes of this rank (shard at N>1) -> W
+    if N > 1:
+        _, _, my_bytes, my_chunks = ctx.shard()
+        _, _, _, g_bytes, g_chunks = ctx.global_selection()
+    else:
+        _, _, _, my_bytes, my_chunks = ctx.selection()
+        g_bytes, g_chunks = my_bytes, my_chunks
+
+    clocks = ClockSampler(dist.local)
+    ctx.prof_enable(True)
+    l0 = ctx.launches
+    dist.barrier()
+    ctx.sync()
+    clocks.start()
+    ctx.timer_start()
+    for _ in range(args.steps):
+        step()
+    ms = ctx.timer_stop()
+    clk = clocks.stop()
+    launches = ctx.launches - l0
+    t_hash, n_hash = ctx.prof_read(snap.PROF_HASH)
+    t_sel, n_sel = ctx.prof_read(snap.PROF_SELECT)
+    t_cmp, n_cmp = ctx.prof_read(snap.PROF_COMPACT)
+    t_xch, n_xch = ctx.prof_read(snap.PROF_EXCHANGE)
+    ctx.prof_enable(False)
+    ms_max = dist.max(ms)
+    w_total = dist.sum(float(my_bytes))
+    step_s = ms_max / 1e3 / args.steps
+    value = N * image / step_s / 1e9
+    peak, peak_src = peaks()
+    hash_ms = t_hash / max(n_hash, 1)
+    cmp_ms = t_cmp / max(n_cmp, 1)
+    achieved = image / (hash_ms / 1e3) / 1e9
+
+    # ---- e2e through the host-buffer entry point (pinned host image and staging)
+    hostimg = snap.PinnedHost(image)
+    himg = host_image(dist.rank, replicated, per_rank)
+    hostimg.array[:] = himg.view(np.uint8)
+    del himg
+    hstage = snap.PinnedHost(image)
+    hdig = np.zeros(nchunks, np.uint64)
+    for _ in range(2):
+        ctx.snapshot_host(hostimg.ptr, 0, image, hstage.ptr, image, hdig)
+    e2e_steps = max(1, min(args.steps, 5))
+    dist.barrier()
+    t0 = time.perf_counter()
+    staged = 0
+    for _ in range(e2e_steps):
+        staged = ctx.snapshot_host(hostimg.ptr, 0, image, hstage.ptr, image, hdig)
+    e2e_s = dist.max(time.perf_counter() - t0) / e2e_steps
+    e2e = {"value": round(N * image / e2e_s / 1e9, 2), "unit": "GB/s",
+           "h2d_bytes_per_step": image, "d2h_bytes_per_step": int(staged + 8 * nchunks),
+           "api": "snap_snapshot_host (pinned host image -> arena -> K1-K3 -> staging shard + "
+                  "digests to pinned host)"}
+    # correctness self-check of the timed path at N=1: restore the staging image bit-exactly
+    check = None
+    if N == 1:
+        d_before, _ = ctx.digests()
+        ctx.write(0, np.zeros(1 << 20, np.uint8))
+        ctx.restore_self(verify=True)
+        d_after, _ = ctx.digests()
+        check = bool(np.array_equal(d_before, d_after))
+    hostimg.free()
+    hstage.free()
+
+    base = cpu_baseline(replicated, per_rank) if (dist.rank == 0 and N == 1) else None
+    if dist.rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": N,
+            "steps": args.steps, "warmup": max(args.warmup, 3),
+            "ms_per_step": round(step_s * 1e3, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": "C2: data-parallel image per rank = 1.5 GiB replicated "
+                                   "(bf16 params + fp32 Adam m,v; identical on all ranks) + "
+                                   "0.5 GiB per-rank grads; one rank per GPU; cross-rank dedup "
+                                   "+ striped compaction at N>1",
+                       "image_bytes_per_rank": image, "chunk_bytes": CHUNK, "page_bytes": PAGE,
+                       "chunks_per_rank": nchunks, "parallelism": f"dp{N} (1 rank/GPU)",
+                       "l2": "inputs 2 GiB/GPU > 126 MB L2 (no flush needed)",
+                       "staged_bytes_total": int(w_total), "unique_bytes_global": int(g_bytes)},
+            "roofline": {"bound": "hbm", "kernel": "k_hash (K1)",
+                         "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": image,
+                         "traffic": traffic_for("k_hash")},
+            "step_hbm": {"rw_bytes_per_gpu": int(image + my_bytes),
+                         "rw_gbs_per_gpu": round((image + my_bytes) / step_s / 1e9, 1),
+                         "frac": round((image + my_bytes) / step_s / 1e9 / peak, 4)},
+            "kernels_ms": {"hash": round(hash_ms, 4), "select": round(t_sel / max(n_sel, 1), 4),
+                           "compact": round(cmp_ms, 4),
+                           "exchange": round(t_xch / max(n_xch, 1), 4) if n_xch else 0.0,
+                           "compact_gbs": round(2 * my_bytes / (cmp_ms / 1e3) / 1e9, 1)
+                           if cmp_ms else None},
+            "gpu_launches": launches,
+            "clocks": clk,
+            "e2e": e2e,
+            "cpu_baseline": base,
+            "restore_check": check,
+        }
+        print(json.dumps(line))
+    ctx.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    args = ap.parse_args()
+    dist = Dist()
+    try:
+        if args.impl == "reference":
+            run_reference(args, dist)
+        else:
+            run_ours(args, dist)
+    finally:
+        dist.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -90,6 +90,11 @@ int snap_sync(snap_ctx* ctx);
 int snap_layout_carve(uint64_t mem_bytes, uint64_t max_buffer_bytes, double slack_fraction,
                       uint64_t out[3]);
 
+/* Pinned host memory for staging images / host-side inputs (page-locked so
+ * H2D/D2H run at PCIe DMA speed). */
+int snap_host_alloc(uint64_t bytes, void** out);
+int snap_host_free(void* p);
+
 /* Gpu::write_words / Gpu::words (vdev.cpp:106-124): host <-> arena copies. */
 int snap_write(snap_ctx* ctx, uint64_t addr, const void* src, uint64_t bytes);
 int snap_read(snap_ctx* ctx, uint64_t addr, void* dst, uint64_t bytes);
@@ -148,6 +153,14 @@ int snap_compact(snap_ctx* ctx);
 /* One call = K1 + K2 + K3 (+ K2 exchange when a communicator is attached):
  * the device section of build_manifest (ckpt.cpp:147-167). Async. */
 int snap_snapshot(snap_ctx* ctx);
+/* End-to-end from HOST memory, the call a checkpoint driver makes
+ * (CheckpointFlow -> build_manifest -> persist, ckpt.cpp:543-617): copies
+ * `bytes` from host_src into the arena at `addr`, runs snap_snapshot over the
+ * installed buffers, and copies the staging image (this rank's shard when a
+ * communicator is attached) and the chunk digests back to the host. */
+int snap_snapshot_host(snap_ctx* ctx, const void* host_src, uint64_t addr, uint64_t bytes,
+                       void* host_staging, uint64_t staging_cap, uint64_t* staged_bytes,
+                       uint64_t* host_digests);
 int snap_staging(snap_ctx* ctx, void** dev_ptr, uint64_t* bytes);
 int snap_read_staging(snap_ctx* ctx, uint64_t off, void* dst, uint64_t bytes);
 
@@ -179,6 +192,20 @@ int snap_grad_sum(snap_ctx* ctx, int dtype, const uint64_t* src_addrs, uint32_t 
 
 int snap_comm_unique_id(void* id128);
 int snap_comm_init(snap_ctx* ctx, int nranks, int rank, const void* id128);
+/* With a communicator attached, snap_select allgathers every rank's digest
+ * vector (padded to the largest rank, rank-major) and selects over the global
+ * canonical order; selection vectors then have n_global = nranks * max_per_rank
+ * entries. Physical copies of replicated chunks are striped over their holders
+ * (ranks with the same digest at the same local chunk index):
+ * writer = holders[local_index % |holders|]; each rank stages only its shard. */
+int snap_global_info(snap_ctx* ctx, uint64_t* n_global, uint64_t* max_per_rank);
+int snap_get_global_digests(snap_ctx* ctx, uint64_t* gdig, uint32_t* glens);
+/* writer[g] (-1 when not staged) and shard_off[g] (offset inside the writer's
+ * shard, UINT64_MAX when not staged) over the global vector; my_bytes /
+ * my_chunks = size of this rank's shard. Any pointer may be NULL. */
+int snap_get_shard(snap_ctx* ctx, int32_t* writer, uint64_t* shard_off, uint64_t* my_bytes,
+                   uint64_t* my_chunks);
+
 /* Device-level allreduce of a gradient range (after K5 local sum,
  * collectives.cpp:147-154 local closer). Async. */
 int snap_allreduce(snap_ctx* ctx, int dtype, uint64_t addr, uint64_t elems);
@@ -187,6 +214,16 @@ int snap_allreduce(snap_ctx* ctx, int dtype, uint64_t addr, uint64_t elems);
 
 int snap_timer_start(snap_ctx* ctx);
 int snap_timer_stop(snap_ctx* ctx, float* ms);
+/* Per-kernel-class CUDA events on the ctx stream (live roofline evidence):
+ * kind 0 hash, 1 select, 2 compact, 3 restore, 4 grad, 5 exchange. */
+#define SNAP_PROF_HASH 0
+#define SNAP_PROF_SELECT 1
+#define SNAP_PROF_COMPACT 2
+#define SNAP_PROF_RESTORE 3
+#define SNAP_PROF_GRAD 4
+#define SNAP_PROF_EXCHANGE 5
+int snap_prof_enable(snap_ctx* ctx, int on);
+int snap_prof_read(snap_ctx* ctx, int kind, float* total_ms, uint64_t* count);
 
 #ifdef __cplusplus
 }

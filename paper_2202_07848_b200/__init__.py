@@ -87,6 +87,17 @@ _SIGS = {
     "snap_comm_unique_id": (C.c_int, [C.c_void_p]),
     "snap_comm_init": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
     "snap_allreduce": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, C.c_uint64]),
+    "snap_host_alloc": (C.c_int, [C.c_uint64, C.POINTER(C.c_void_p)]),
+    "snap_host_free": (C.c_int, [C.c_void_p]),
+    "snap_snapshot_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p,
+                                     C.c_uint64, C.POINTER(C.c_uint64), C.c_void_p]),
+    "snap_global_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "snap_get_global_digests": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "snap_get_shard": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64),
+                                 C.POINTER(C.c_uint64)]),
+    "snap_prof_enable": (C.c_int, [C.c_void_p, C.c_int]),
+    "snap_prof_read": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_float),
+                                 C.POINTER(C.c_uint64)]),
     "snap_timer_start": (C.c_int, [C.c_void_p]),
     "snap_timer_stop": (C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
 }
@@ -136,6 +147,33 @@ def layout_carve(mem_bytes, max_buffer_bytes, slack_fraction):
     if rc != SNAP_OK:
         raise SnapError(rc, "device too small for layout")
     return tuple(out)
+
+
+PROF_HASH, PROF_SELECT, PROF_COMPACT, PROF_RESTORE, PROF_GRAD, PROF_EXCHANGE = range(6)
+
+
+class PinnedHost:
+    """Page-locked host buffer (snap_host_alloc) viewed as a numpy uint8 array."""
+
+    def __init__(self, nbytes: int):
+        p = C.c_void_p()
+        rc = lib().snap_host_alloc(nbytes, C.byref(p))
+        if rc != SNAP_OK:
+            raise SnapError(rc, f"snap_host_alloc({nbytes})")
+        self.ptr = p.value
+        self.nbytes = nbytes
+        self.array = np.ctypeslib.as_array((C.c_uint8 * max(nbytes, 1)).from_address(self.ptr))[:nbytes]
+
+    def free(self):
+        if self.ptr:
+            lib().snap_host_free(C.c_void_p(self.ptr))
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
 
 
 class Ctx:
@@ -269,6 +307,56 @@ class Ctx:
         out = np.empty(nbytes, dtype=np.uint8)
         self._ck(self._L.snap_read_staging(self.h, off, _p(out), nbytes), "snap_read_staging")
         return out
+
+    def snapshot_host(self, host_ptr: int, addr: int, nbytes: int, staging_ptr: int,
+                      staging_cap: int, digests_out=None) -> int:
+        sb = C.c_uint64()
+        d = None if digests_out is None else digests_out
+        self._ck(self._L.snap_snapshot_host(self.h, C.c_void_p(host_ptr), addr, nbytes,
+                                            C.c_void_p(staging_ptr), staging_cap, C.byref(sb),
+                                            _p(d) if d is not None else None),
+                 "snap_snapshot_host")
+        return sb.value
+
+    def global_info(self):
+        n, m = C.c_uint64(), C.c_uint64()
+        self._ck(self._L.snap_global_info(self.h, C.byref(n), C.byref(m)), "snap_global_info")
+        return n.value, m.value
+
+    def global_digests(self):
+        n, _ = self.global_info()
+        d = np.zeros(max(n, 1), np.uint64)
+        ln = np.zeros(max(n, 1), np.uint32)
+        self._ck(self._L.snap_get_global_digests(self.h, _p(d), _p(ln)), "snap_get_global_digests")
+        return d[:n], ln[:n]
+
+    def global_selection(self):
+        """Selection over the global (allgathered) vector: sel, owner, offsets, bytes, chunks."""
+        n, _ = self.global_info()
+        sel = np.zeros(max(n, 1), dtype=np.uint8)
+        owner = np.zeros(max(n, 1), dtype=np.uint64)
+        off = np.zeros(max(n, 1), dtype=np.uint64)
+        sb, sc = C.c_uint64(), C.c_uint64()
+        self._ck(self._L.snap_get_selection(self.h, _p(sel), _p(owner), _p(off), C.byref(sb),
+                                            C.byref(sc)), "snap_get_selection")
+        return sel[:n], owner[:n], off[:n], sb.value, sc.value
+
+    def shard(self):
+        n, _ = self.global_info()
+        w = np.zeros(max(n, 1), np.int32)
+        so = np.zeros(max(n, 1), np.uint64)
+        mb, mc = C.c_uint64(), C.c_uint64()
+        self._ck(self._L.snap_get_shard(self.h, _p(w), _p(so), C.byref(mb), C.byref(mc)),
+                 "snap_get_shard")
+        return w[:n], so[:n], mb.value, mc.value
+
+    def prof_enable(self, on=True):
+        self._ck(self._L.snap_prof_enable(self.h, 1 if on else 0), "snap_prof_enable")
+
+    def prof_read(self, kind):
+        ms, n = C.c_float(), C.c_uint64()
+        self._ck(self._L.snap_prof_read(self.h, kind, C.byref(ms), C.byref(n)), "snap_prof_read")
+        return ms.value, n.value
 
     # -- K4
     def restore(self, image_ptr: int, image_bytes: int, src_off, expect=None, verify=True):

@@ -1,7 +1,8 @@
 // capi.cpp — the C ABI (include/snap.h): one snap_ctx per (job, GPU), the
 // B200 analogue of proxy::ProxyServer (proxy.hpp:32-122) + vdev::Gpu memory
 // (vdev.hpp:65-122). Host code only; every byte of device work is one of the
-// sm_100a kernels in k_*.cu, issued on the ctx stream.
+// sm_100a kernels in k_*.cu, issued on the ctx stream (NCCL collectives on the
+// same stream for the cross-rank exchange).
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -23,8 +24,13 @@ struct DevMem {
   size_t cap = 0;
 };
 
-struct Status {
-  int code;
+// Per-kernel-class CUDA event pairs, recorded on the ctx stream when enabled
+// (bench.py reads the live duration of the dominant kernel from these).
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
 };
 
 }  // namespace
@@ -49,23 +55,32 @@ struct snap_ctx {
   bool hashed = false;
 
   // dedup table (per snapshot) and known set (store index)
-  DevMem dd_keys, dd_vals;
+  DevMem dd_keys, dd_vals, dd_slot;
   uint64_t dd_mask = 0;
   DevMem kn_keys, kn_vals, kn_list;
   uint64_t kn_mask = 0, kn_count = 0;
 
-  // selection
+  // selection over the (local or global) canonical chunk vector
   DevMem scan, sel, owner, offsets, sel_list, totals;
+  uint64_t sel_n = 0;  // entries of the selection vectors (nchunks, or nranks * maxn)
   bool selected = false;
   DevMem staging;
-  uint64_t staging_valid = 0;  // upper bound of staged bytes of the last compact
+  uint64_t staging_valid = 0;
+
+  // cross-rank exchange (NCCL allgather of digest vectors) and striping
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  bool exchanged = false;
+  uint64_t maxn = 0;
+  std::vector<uint64_t> counts;
+  bool glens_valid = false;
+  DevMem d_counts, d_gdig, d_glens, d_writer, d_shard_off, d_my_list, d_my_off, d_my_totals;
 
   // verify / restore scratch
   DevMem d_dig2, d_expect, d_nbad, d_srcoff;
 
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  ncclComm_t comm = nullptr;
-  int nranks = 1, rank = 0;
+  Prof prof;
 };
 
 namespace {
@@ -89,13 +104,19 @@ int fail(snap_ctx* c, int code, const std::string& msg) {
       return fail(ctx, SNAP_ECUDA, std::string(#call) + ": " + ncclGetErrorString(r_)); \
   } while (0)
 
-// Checks the last launch of the ctx stream (launch-configuration errors).
-#define CKL(n)                                                                           \
-  do {                                                                                   \
-    ctx->launches += (n);                                                                \
-    cudaError_t e_ = cudaGetLastError();                                                 \
-    if (e_ != cudaSuccess)                                                               \
+// Counts kernels of the last launcher call and checks launch-configuration errors.
+#define CKL(n)                                                                               \
+  do {                                                                                       \
+    ctx->launches += (n);                                                                    \
+    cudaError_t e_ = cudaGetLastError();                                                     \
+    if (e_ != cudaSuccess)                                                                   \
       return fail(ctx, SNAP_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define RC(x)             \
+  do {                    \
+    int rc_ = (x);        \
+    if (rc_) return rc_;  \
   } while (0)
 
 template <typename T>
@@ -145,6 +166,11 @@ int ensure_keep(snap_ctx* ctx, DevMem& m, size_t count, size_t keep, T** out) {
   return SNAP_OK;
 }
 
+template <typename T>
+T* P(DevMem& m) {
+  return static_cast<T*>(m.p);
+}
+
 void release(DevMem& m) {
   if (m.p) cudaFree(m.p);
   m.p = nullptr;
@@ -169,34 +195,168 @@ int check_range(snap_ctx* ctx, uint64_t addr, uint64_t bytes) {
   return SNAP_OK;
 }
 
+// ---- profiler ----
+enum { kProfHash = 0, kProfSelect, kProfCompact, kProfRestore, kProfGrad, kProfExchange, kProfN };
+
+cudaEvent_t prof_event(snap_ctx* ctx) {
+  Prof& p = ctx->prof;
+  if (p.used == p.pool.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    p.pool.push_back(e);
+  }
+  return p.pool[p.used++];
+}
+
+struct ProfScope {
+  snap_ctx* ctx;
+  int kind;
+  cudaEvent_t a = nullptr;
+  ProfScope(snap_ctx* c, int k) : ctx(c), kind(k) {
+    if (ctx->prof.on) {
+      a = prof_event(ctx);
+      if (a) cudaEventRecord(a, ctx->stream);
+    }
+  }
+  ~ProfScope() {
+    if (a) {
+      cudaEvent_t b = prof_event(ctx);
+      if (b) {
+        cudaEventRecord(b, ctx->stream);
+        ctx->prof.marks.push_back({kind, {a, b}});
+      }
+    }
+  }
+};
+
 int ensure_known(snap_ctx* ctx, uint64_t extra) {
   // grows (and rebuilds) the known-set table to keep load <= 1/2
   const uint64_t need = ctx->kn_count + extra;
   uint64_t* list;
-  if (int rc = ensure_keep(ctx, ctx->kn_list, need, ctx->kn_count * 8, &list)) return rc;
+  RC(ensure_keep(ctx, ctx->kn_list, need, ctx->kn_count * 8, &list));
   if (ctx->kn_mask && 2 * need <= ctx->kn_mask + 1) return SNAP_OK;
   const uint64_t cap = table_cap(need);
   unsigned long long *k, *v;
-  if (int rc = ensure(ctx, ctx->kn_keys, cap + 1, &k)) return rc;
-  if (int rc = ensure(ctx, ctx->kn_vals, cap + 1, &v)) return rc;
+  RC(ensure(ctx, ctx->kn_keys, cap + 1, &k));
+  RC(ensure(ctx, ctx->kn_vals, cap + 1, &v));
   ctx->kn_mask = cap - 1;
   TableDev t{k, v, ctx->kn_mask};
   CKL(snap::launch_table_clear(t, ctx->stream));
-  CKL(snap::launch_table_insert_min(t, static_cast<uint64_t*>(ctx->kn_list.p), ctx->kn_count, 0,
-                                    ctx->stream));
+  CKL(snap::launch_table_insert_min(t, P<uint64_t>(ctx->kn_list), ctx->kn_count, 0, ctx->stream));
   return SNAP_OK;
 }
 
 int known_insert_dev(snap_ctx* ctx, const uint64_t* dev_digests, uint64_t n) {
   if (n == 0) return SNAP_OK;
-  if (int rc = ensure_known(ctx, n)) return rc;
-  uint64_t* list = static_cast<uint64_t*>(ctx->kn_list.p);
+  RC(ensure_known(ctx, n));
+  uint64_t* list = P<uint64_t>(ctx->kn_list);
   CK(cudaMemcpyAsync(list + ctx->kn_count, dev_digests, n * 8, cudaMemcpyDeviceToDevice,
                      ctx->stream));
-  TableDev t{static_cast<unsigned long long*>(ctx->kn_keys.p),
-             static_cast<unsigned long long*>(ctx->kn_vals.p), ctx->kn_mask};
+  TableDev t{P<unsigned long long>(ctx->kn_keys), P<unsigned long long>(ctx->kn_vals), ctx->kn_mask};
   CKL(snap::launch_table_insert_min(t, list + ctx->kn_count, n, 0, ctx->stream));
   ctx->kn_count += n;
+  return SNAP_OK;
+}
+
+// Selection over a canonical vector (local grid or allgathered global one).
+int select_impl(snap_ctx* ctx, const uint64_t* dig, const uint32_t* lens, uint64_t n) {
+  const uint64_t cap = table_cap(n);
+  unsigned long long *k, *v;
+  uint64_t *slot, *scan, *owner, *offsets, *totals;
+  uint8_t* sel;
+  uint32_t* list;
+  RC(ensure(ctx, ctx->dd_keys, cap + 1, &k));
+  RC(ensure(ctx, ctx->dd_vals, cap + 1, &v));
+  RC(ensure(ctx, ctx->dd_slot, n, &slot));
+  RC(ensure(ctx, ctx->scan, snap::scan_state_words(n) + 1, &scan));
+  RC(ensure(ctx, ctx->sel, n, &sel));
+  RC(ensure(ctx, ctx->owner, n, &owner));
+  RC(ensure(ctx, ctx->offsets, n, &offsets));
+  RC(ensure(ctx, ctx->sel_list, n, &list));
+  RC(ensure(ctx, ctx->totals, 4, &totals));
+  ctx->dd_mask = cap - 1;
+  TableDev dd{k, v, ctx->dd_mask};
+  TableDev kn{P<unsigned long long>(ctx->kn_keys), P<unsigned long long>(ctx->kn_vals), ctx->kn_mask};
+  CKL(snap::launch_table_clear(dd, ctx->stream));
+  CKL(snap::launch_dedup_insert(dd, kn, ctx->kn_count > 0, dig, lens, n, slot, ctx->stream));
+  CKL(snap::launch_select(dd, slot, lens, n, scan, sel, owner, offsets, list, totals, ctx->stream));
+  CKL(snap::launch_resolve_dups(sel, owner, offsets, n, ctx->stream));
+  ctx->sel_n = n;
+  ctx->selected = true;
+  return SNAP_OK;
+}
+
+// NCCL allgather of the per-rank digest vectors (and chunk lengths once per
+// grid), padded to the largest rank: the only bytes that cross NVLink (8 B
+// per 64 KiB chunk).
+int exchange_impl(snap_ctx* ctx) {
+  const int R = ctx->nranks;
+  if (!ctx->glens_valid) {
+    uint64_t* dc;
+    RC(ensure(ctx, ctx->d_counts, 2 * R, &dc));
+    CK(cudaMemcpyAsync(dc + R, &ctx->nchunks, 8, cudaMemcpyHostToDevice, ctx->stream));
+    CKN(ncclAllGather(dc + R, dc, 1, ncclUint64, ctx->comm, ctx->stream));
+    ctx->counts.assign(R, 0);
+    CK(cudaMemcpyAsync(ctx->counts.data(), dc, 8 * R, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->maxn = *std::max_element(ctx->counts.begin(), ctx->counts.end());
+  }
+  const uint64_t maxn = ctx->maxn, n = uint64_t(R) * maxn;
+  uint64_t* gdig;
+  uint32_t* glens;
+  RC(ensure(ctx, ctx->d_gdig, n + maxn, &gdig));
+  RC(ensure(ctx, ctx->d_glens, n + maxn, &glens));
+  // send buffers live past the gathered region: [n, n + maxn)
+  uint64_t* sdig = gdig + n;
+  if (ctx->nchunks)
+    CK(cudaMemcpyAsync(sdig, P<uint64_t>(ctx->d_dig), ctx->nchunks * 8, cudaMemcpyDeviceToDevice,
+                       ctx->stream));
+  CKN(ncclAllGather(sdig, gdig, maxn, ncclUint64, ctx->comm, ctx->stream));
+  if (!ctx->glens_valid) {
+    uint32_t* slen = glens + n;
+    CK(cudaMemsetAsync(slen, 0, maxn * 4, ctx->stream));
+    if (ctx->nchunks)
+      CK(cudaMemcpyAsync(slen, P<uint32_t>(ctx->d_lens), ctx->nchunks * 4,
+                         cudaMemcpyDeviceToDevice, ctx->stream));
+    CKN(ncclAllGather(slen, glens, maxn, ncclUint32, ctx->comm, ctx->stream));
+    ctx->glens_valid = true;
+  }
+  ctx->exchanged = true;
+  return SNAP_OK;
+}
+
+int stripe_impl(snap_ctx* ctx) {
+  const uint64_t maxn = ctx->maxn, n = uint64_t(ctx->nranks) * maxn;
+  int32_t* writer;
+  uint64_t *shard_off, *my_off, *my_tot;
+  uint32_t* my_list;
+  RC(ensure(ctx, ctx->d_writer, n, &writer));
+  RC(ensure(ctx, ctx->d_shard_off, n, &shard_off));
+  RC(ensure(ctx, ctx->d_my_list, maxn, &my_list));
+  RC(ensure(ctx, ctx->d_my_off, maxn, &my_off));
+  RC(ensure(ctx, ctx->d_my_totals, 4, &my_tot));
+  CKL(snap::launch_stripe_writer(P<uint64_t>(ctx->d_gdig), P<uint32_t>(ctx->d_glens),
+                                 P<uint8_t>(ctx->sel), ctx->nranks, maxn, writer, ctx->stream));
+  CKL(snap::launch_shard_scan(writer, P<uint32_t>(ctx->d_glens), ctx->nranks, maxn, ctx->rank, true,
+                              P<uint64_t>(ctx->scan), shard_off, my_list, my_off, my_tot,
+                              ctx->stream));
+  return SNAP_OK;
+}
+
+int compact_impl(snap_ctx* ctx) {
+  uint8_t* st;
+  if (ctx->comm && ctx->exchanged) {
+    RC(ensure(ctx, ctx->staging, ctx->grid_bytes, &st));
+    CKL(snap::launch_gather(ctx->arena, ctx->grid, P<uint32_t>(ctx->d_lens), P<uint32_t>(ctx->d_my_list),
+                            P<uint64_t>(ctx->d_my_totals), P<uint64_t>(ctx->d_my_off), true, st,
+                            ctx->nchunks, ctx->stream));
+  } else {
+    RC(ensure(ctx, ctx->staging, ctx->grid_bytes, &st));
+    CKL(snap::launch_gather(ctx->arena, ctx->grid, P<uint32_t>(ctx->d_lens), P<uint32_t>(ctx->sel_list),
+                            P<uint64_t>(ctx->totals), P<uint64_t>(ctx->offsets), false, st,
+                            ctx->nchunks, ctx->stream));
+  }
+  ctx->staging_valid = ctx->grid_bytes;
   return SNAP_OK;
 }
 
@@ -219,7 +379,6 @@ const char* snap_strerror(int code) {
 const char* snap_last_error(const snap_ctx* ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
 
 int snap_open(int device, uint64_t arena_bytes, snap_ctx** out) {
-  snap_ctx* ctx = nullptr;
   if (!out || arena_bytes == 0 || arena_bytes % 256) return SNAP_EINVAL;
   *out = nullptr;
   int ndev = 0;
@@ -229,7 +388,7 @@ int snap_open(int device, uint64_t arena_bytes, snap_ctx** out) {
     return SNAP_ECUDA;
   }
   if (device < 0 || device >= ndev) return SNAP_EINVAL;
-  ctx = new snap_ctx();
+  snap_ctx* ctx = new snap_ctx();
   ctx->device = device;
   auto bail = [&](int code) {
     snap_close(ctx);
@@ -257,12 +416,15 @@ int snap_close(snap_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
-  for (DevMem* m : {&ctx->d_addr, &ctx->d_bytes, &ctx->d_cstart, &ctx->d_lens, &ctx->d_dig,
-                    &ctx->d_bufdig, &ctx->dd_keys, &ctx->dd_vals, &ctx->kn_keys, &ctx->kn_vals,
-                    &ctx->kn_list, &ctx->scan, &ctx->sel, &ctx->owner, &ctx->offsets,
-                    &ctx->sel_list, &ctx->totals, &ctx->staging, &ctx->d_dig2, &ctx->d_expect,
-                    &ctx->d_nbad, &ctx->d_srcoff})
+  for (DevMem* m :
+       {&ctx->d_addr, &ctx->d_bytes, &ctx->d_cstart, &ctx->d_lens, &ctx->d_dig, &ctx->d_bufdig,
+        &ctx->dd_keys, &ctx->dd_vals, &ctx->dd_slot, &ctx->kn_keys, &ctx->kn_vals, &ctx->kn_list,
+        &ctx->scan, &ctx->sel, &ctx->owner, &ctx->offsets, &ctx->sel_list, &ctx->totals,
+        &ctx->staging, &ctx->d_counts, &ctx->d_gdig, &ctx->d_glens, &ctx->d_writer,
+        &ctx->d_shard_off, &ctx->d_my_list, &ctx->d_my_off, &ctx->d_my_totals, &ctx->d_dig2,
+        &ctx->d_expect, &ctx->d_nbad, &ctx->d_srcoff})
     release(*m);
+  for (cudaEvent_t e : ctx->prof.pool) cudaEventDestroy(e);
   if (ctx->arena) cudaFree(ctx->arena);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
@@ -301,9 +463,28 @@ int snap_layout_carve(uint64_t mem_bytes, uint64_t max_buffer_bytes, double slac
   return SNAP_OK;
 }
 
+int snap_host_alloc(uint64_t bytes, void** out) {
+  if (!out) return SNAP_EINVAL;
+  *out = nullptr;
+  cudaError_t e = cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return e == cudaErrorMemoryAllocation ? SNAP_ENOMEM : SNAP_ECUDA;
+  }
+  return SNAP_OK;
+}
+
+int snap_host_free(void* p) {
+  if (p && cudaFreeHost(p) != cudaSuccess) {
+    cudaGetLastError();
+    return SNAP_ECUDA;
+  }
+  return SNAP_OK;
+}
+
 int snap_write(snap_ctx* ctx, uint64_t addr, const void* src, uint64_t bytes) {
   if (!ctx || (!src && bytes)) return SNAP_EINVAL;
-  if (int rc = check_range(ctx, addr, bytes)) return rc;
+  RC(check_range(ctx, addr, bytes));
   CK(cudaSetDevice(ctx->device));
   CK(cudaMemcpyAsync(ctx->arena + addr, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -312,7 +493,7 @@ int snap_write(snap_ctx* ctx, uint64_t addr, const void* src, uint64_t bytes) {
 
 int snap_read(snap_ctx* ctx, uint64_t addr, void* dst, uint64_t bytes) {
   if (!ctx || (!dst && bytes)) return SNAP_EINVAL;
-  if (int rc = check_range(ctx, addr, bytes)) return rc;
+  RC(check_range(ctx, addr, bytes));
   CK(cudaSetDevice(ctx->device));
   CK(cudaMemcpyAsync(dst, ctx->arena + addr, bytes, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -321,7 +502,7 @@ int snap_read(snap_ctx* ctx, uint64_t addr, void* dst, uint64_t bytes) {
 
 int snap_fill_mix64(snap_ctx* ctx, uint64_t addr, uint64_t bytes, uint64_t seed, uint64_t base) {
   if (!ctx || addr % 8 || bytes % 8) return fail(ctx, SNAP_EINVAL, "fill: unaligned range");
-  if (int rc = check_range(ctx, addr, bytes)) return rc;
+  RC(check_range(ctx, addr, bytes));
   CK(cudaSetDevice(ctx->device));
   CKL(snap::launch_fill_mix64(reinterpret_cast<uint64_t*>(ctx->arena + addr), bytes / 8, seed,
                               base, ctx->stream));
@@ -336,7 +517,7 @@ int snap_xor_words(snap_ctx* ctx, const uint64_t* addrs, uint64_t n, uint64_t va
   if (n == 0) return SNAP_OK;
   CK(cudaSetDevice(ctx->device));
   uint64_t* d;
-  if (int rc = ensure(ctx, ctx->d_srcoff, n, &d)) return rc;
+  RC(ensure(ctx, ctx->d_srcoff, n, &d));
   CK(cudaMemcpyAsync(d, addrs, n * 8, cudaMemcpyHostToDevice, ctx->stream));
   CKL(snap::launch_xor_words(ctx->arena, d, n, value, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -362,7 +543,7 @@ int snap_set_buffers(snap_ctx* ctx, const snap_buf* bufs, uint64_t n, const snap
     if (x.bytes == 0 || x.addr % 256 || x.bytes % 256)
       return fail(ctx, SNAP_EINVAL, "buffer " + std::to_string(b) +
                                         ": address and size must be non-zero multiples of 256");
-    if (int rc = check_range(ctx, x.addr, x.bytes)) return rc;
+    RC(check_range(ctx, x.addr, x.bytes));
     addr[b] = x.addr;
     bytes[b] = x.bytes;
     const uint64_t nc = (x.bytes + g.chunk_bytes - 1) / g.chunk_bytes;
@@ -371,15 +552,15 @@ int snap_set_buffers(snap_ctx* ctx, const snap_buf* bufs, uint64_t n, const snap
       lens.push_back(static_cast<uint32_t>(std::min<uint64_t>(g.chunk_bytes, x.bytes - k * g.chunk_bytes)));
     total += x.bytes;
   }
-  if (cstart[n] >= (1ull << 32)) return fail(ctx, SNAP_EINVAL, "too many chunks");
+  if (cstart[n] >= (1ull << 31)) return fail(ctx, SNAP_EINVAL, "too many chunks");
   CK(cudaSetDevice(ctx->device));
   uint64_t *da, *db, *dc, *dd;
   uint32_t* dl;
-  if (int rc = ensure(ctx, ctx->d_addr, n, &da)) return rc;
-  if (int rc = ensure(ctx, ctx->d_bytes, n, &db)) return rc;
-  if (int rc = ensure(ctx, ctx->d_cstart, n + 1, &dc)) return rc;
-  if (int rc = ensure(ctx, ctx->d_lens, cstart[n], &dl)) return rc;
-  if (int rc = ensure(ctx, ctx->d_dig, cstart[n], &dd)) return rc;
+  RC(ensure(ctx, ctx->d_addr, n, &da));
+  RC(ensure(ctx, ctx->d_bytes, n, &db));
+  RC(ensure(ctx, ctx->d_cstart, n + 1, &dc));
+  RC(ensure(ctx, ctx->d_lens, cstart[n], &dl));
+  RC(ensure(ctx, ctx->d_dig, cstart[n], &dd));
   CK(cudaMemcpyAsync(da, addr.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(db, bytes.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(dc, cstart.data(), (n + 1) * 8, cudaMemcpyHostToDevice, ctx->stream));
@@ -395,6 +576,8 @@ int snap_set_buffers(snap_ctx* ctx, const snap_buf* bufs, uint64_t n, const snap
                       log2u(g.chunk_bytes)};
   ctx->hashed = false;
   ctx->selected = false;
+  ctx->exchanged = false;
+  ctx->glens_valid = false;
   if (n_chunks) *n_chunks = ctx->nchunks;
   return SNAP_OK;
 }
@@ -402,9 +585,13 @@ int snap_set_buffers(snap_ctx* ctx, const snap_buf* bufs, uint64_t n, const snap
 int snap_hash(snap_ctx* ctx) {
   if (!ctx) return SNAP_EINVAL;
   CK(cudaSetDevice(ctx->device));
-  CKL(snap::launch_hash(ctx->arena, ctx->grid, static_cast<uint64_t*>(ctx->d_dig.p), ctx->stream));
+  {
+    ProfScope ps(ctx, kProfHash);
+    CKL(snap::launch_hash(ctx->arena, ctx->grid, P<uint64_t>(ctx->d_dig), ctx->stream));
+  }
   ctx->hashed = true;
   ctx->selected = false;
+  ctx->exchanged = false;
   return SNAP_OK;
 }
 
@@ -418,8 +605,8 @@ int snap_get_digests(snap_ctx* ctx, uint64_t* chunk_digests, uint32_t* chunk_len
                        ctx->stream));
   if (buf_digests && !ctx->bufs.empty()) {
     uint64_t* bd;
-    if (int rc = ensure(ctx, ctx->d_bufdig, ctx->bufs.size(), &bd)) return rc;
-    CKL(snap::launch_buf_fold(ctx->grid, static_cast<uint64_t*>(ctx->d_dig.p), bd, ctx->stream));
+    RC(ensure(ctx, ctx->d_bufdig, ctx->bufs.size(), &bd));
+    CKL(snap::launch_buf_fold(ctx->grid, P<uint64_t>(ctx->d_dig), bd, ctx->stream));
     CK(cudaMemcpyAsync(buf_digests, bd, ctx->bufs.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
   }
   CK(cudaStreamSynchronize(ctx->stream));
@@ -430,8 +617,8 @@ int snap_get_digests(snap_ctx* ctx, uint64_t* chunk_digests, uint32_t* chunk_len
 int snap_digest_ranges(snap_ctx* ctx, const snap_buf* bufs, uint64_t n, const snap_geom* geom,
                        uint64_t* out) {
   uint64_t nc = 0;
-  if (int rc = snap_set_buffers(ctx, bufs, n, geom, &nc)) return rc;
-  if (int rc = snap_hash(ctx)) return rc;
+  RC(snap_set_buffers(ctx, bufs, n, geom, &nc));
+  RC(snap_hash(ctx));
   return snap_get_digests(ctx, nullptr, nullptr, out);
 }
 
@@ -442,8 +629,8 @@ int snap_known_clear(snap_ctx* ctx) {
   ctx->kn_count = 0;
   if (ctx->kn_mask) {
     CK(cudaSetDevice(ctx->device));
-    TableDev t{static_cast<unsigned long long*>(ctx->kn_keys.p),
-               static_cast<unsigned long long*>(ctx->kn_vals.p), ctx->kn_mask};
+    TableDev t{P<unsigned long long>(ctx->kn_keys), P<unsigned long long>(ctx->kn_vals),
+               ctx->kn_mask};
     CKL(snap::launch_table_clear(t, ctx->stream));
   }
   return SNAP_OK;
@@ -454,9 +641,9 @@ int snap_known_add(snap_ctx* ctx, const uint64_t* digests, uint64_t n) {
   if (n == 0) return SNAP_OK;
   CK(cudaSetDevice(ctx->device));
   uint64_t* tmp;
-  if (int rc = ensure(ctx, ctx->d_dig2, n, &tmp)) return rc;
+  RC(ensure(ctx, ctx->d_dig2, n, &tmp));
   CK(cudaMemcpyAsync(tmp, digests, n * 8, cudaMemcpyHostToDevice, ctx->stream));
-  if (int rc = known_insert_dev(ctx, tmp, n)) return rc;
+  RC(known_insert_dev(ctx, tmp, n));
   CK(cudaStreamSynchronize(ctx->stream));
   return SNAP_OK;
 }
@@ -465,39 +652,37 @@ int snap_known_commit(snap_ctx* ctx) {
   if (!ctx) return SNAP_EINVAL;
   if (!ctx->hashed) return fail(ctx, SNAP_EINVAL, "known_commit before snap_hash");
   CK(cudaSetDevice(ctx->device));
-  return known_insert_dev(ctx, static_cast<uint64_t*>(ctx->d_dig.p), ctx->nchunks);
+  if (ctx->comm && ctx->exchanged) {
+    // the store is global: every rank's digests become known
+    const uint64_t n = uint64_t(ctx->nranks) * ctx->maxn;
+    std::vector<uint32_t> gl(n);
+    std::vector<uint64_t> gd(n), live;
+    CK(cudaMemcpyAsync(gl.data(), ctx->d_glens.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(gd.data(), ctx->d_gdig.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (uint64_t i = 0; i < n; ++i)
+      if (gl[i]) live.push_back(gd[i]);
+    return snap_known_add(ctx, live.data(), live.size());
+  }
+  return known_insert_dev(ctx, P<uint64_t>(ctx->d_dig), ctx->nchunks);
 }
 
 int snap_select(snap_ctx* ctx) {
   if (!ctx) return SNAP_EINVAL;
   if (!ctx->hashed) return fail(ctx, SNAP_EINVAL, "select before snap_hash");
   CK(cudaSetDevice(ctx->device));
-  const uint64_t n = ctx->nchunks;
-  const uint64_t cap = table_cap(n);
-  unsigned long long *k, *v;
-  uint64_t *scan, *owner, *offsets, *totals;
-  uint8_t* sel;
-  uint32_t* list;
-  if (int rc = ensure(ctx, ctx->dd_keys, cap + 1, &k)) return rc;
-  if (int rc = ensure(ctx, ctx->dd_vals, cap + 1, &v)) return rc;
-  if (int rc = ensure(ctx, ctx->scan, snap::scan_state_words(n) + 1, &scan)) return rc;
-  if (int rc = ensure(ctx, ctx->sel, n, &sel)) return rc;
-  if (int rc = ensure(ctx, ctx->owner, n, &owner)) return rc;
-  if (int rc = ensure(ctx, ctx->offsets, n, &offsets)) return rc;
-  if (int rc = ensure(ctx, ctx->sel_list, n, &list)) return rc;
-  if (int rc = ensure(ctx, ctx->totals, 4, &totals)) return rc;
-  ctx->dd_mask = cap - 1;
-  TableDev dd{k, v, ctx->dd_mask};
-  TableDev kn{static_cast<unsigned long long*>(ctx->kn_keys.p),
-              static_cast<unsigned long long*>(ctx->kn_vals.p), ctx->kn_mask};
-  const uint64_t* dig = static_cast<uint64_t*>(ctx->d_dig.p);
-  CKL(snap::launch_table_clear(dd, ctx->stream));
-  CKL(snap::launch_table_insert_min(dd, dig, n, 0, ctx->stream));
-  CKL(snap::launch_select(dd, kn, ctx->kn_count > 0, dig, static_cast<uint32_t*>(ctx->d_lens.p), n,
-                          scan, sel, owner, offsets, list, totals, ctx->stream));
-  CKL(snap::launch_resolve_dups(sel, owner, offsets, n, ctx->stream));
-  ctx->selected = true;
-  return SNAP_OK;
+  if (ctx->comm) {
+    {
+      ProfScope ps(ctx, kProfExchange);
+      RC(exchange_impl(ctx));
+    }
+    ProfScope ps(ctx, kProfSelect);
+    RC(select_impl(ctx, P<uint64_t>(ctx->d_gdig), P<uint32_t>(ctx->d_glens),
+                   uint64_t(ctx->nranks) * ctx->maxn));
+    return stripe_impl(ctx);
+  }
+  ProfScope ps(ctx, kProfSelect);
+  return select_impl(ctx, P<uint64_t>(ctx->d_dig), P<uint32_t>(ctx->d_lens), ctx->nchunks);
 }
 
 int snap_get_selection(snap_ctx* ctx, uint8_t* sel, uint64_t* owner, uint64_t* offsets,
@@ -505,7 +690,7 @@ int snap_get_selection(snap_ctx* ctx, uint8_t* sel, uint64_t* owner, uint64_t* o
   if (!ctx) return SNAP_EINVAL;
   if (!ctx->selected) return fail(ctx, SNAP_EINVAL, "get_selection before snap_select");
   CK(cudaSetDevice(ctx->device));
-  const uint64_t n = ctx->nchunks;
+  const uint64_t n = ctx->sel_n;
   uint64_t tot[2] = {0, 0};
   if (n) {
     if (sel) CK(cudaMemcpyAsync(sel, ctx->sel.p, n, cudaMemcpyDeviceToHost, ctx->stream));
@@ -520,26 +705,95 @@ int snap_get_selection(snap_ctx* ctx, uint8_t* sel, uint64_t* owner, uint64_t* o
   return SNAP_OK;
 }
 
+int snap_global_info(snap_ctx* ctx, uint64_t* n_global, uint64_t* max_per_rank) {
+  if (!ctx) return SNAP_EINVAL;
+  const bool g = ctx->comm && ctx->exchanged;
+  if (n_global) *n_global = g ? uint64_t(ctx->nranks) * ctx->maxn : ctx->nchunks;
+  if (max_per_rank) *max_per_rank = g ? ctx->maxn : ctx->nchunks;
+  return SNAP_OK;
+}
+
+int snap_get_global_digests(snap_ctx* ctx, uint64_t* gdig, uint32_t* glens) {
+  if (!ctx) return SNAP_EINVAL;
+  if (!(ctx->comm && ctx->exchanged)) return fail(ctx, SNAP_EINVAL, "no exchanged digests");
+  CK(cudaSetDevice(ctx->device));
+  const uint64_t n = uint64_t(ctx->nranks) * ctx->maxn;
+  if (gdig) CK(cudaMemcpyAsync(gdig, ctx->d_gdig.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (glens) CK(cudaMemcpyAsync(glens, ctx->d_glens.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return SNAP_OK;
+}
+
+int snap_get_shard(snap_ctx* ctx, int32_t* writer, uint64_t* shard_off, uint64_t* my_bytes,
+                   uint64_t* my_chunks) {
+  if (!ctx) return SNAP_EINVAL;
+  if (!(ctx->comm && ctx->exchanged && ctx->selected))
+    return fail(ctx, SNAP_EINVAL, "get_shard needs a multi-rank snap_select");
+  CK(cudaSetDevice(ctx->device));
+  const uint64_t n = uint64_t(ctx->nranks) * ctx->maxn;
+  uint64_t tot[2] = {0, 0};
+  CK(cudaMemcpyAsync(tot, ctx->d_my_totals.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
+  if (shard_off) {
+    // offsets inside every writer's shard: one shard scan per writer rank
+    uint64_t dummy_tot[2];
+    (void)dummy_tot;
+    uint64_t* tt;
+    RC(ensure(ctx, ctx->d_nbad, 4, &tt));
+    CK(cudaMemsetAsync(ctx->d_shard_off.p, 0xff, n * 8, ctx->stream));
+    for (int q = 0; q < ctx->nranks; ++q)
+      CKL(snap::launch_shard_scan(P<int32_t>(ctx->d_writer), P<uint32_t>(ctx->d_glens), ctx->nranks,
+                                  ctx->maxn, q, false, P<uint64_t>(ctx->scan),
+                                  P<uint64_t>(ctx->d_shard_off), nullptr, nullptr, tt, ctx->stream));
+    CK(cudaMemcpyAsync(shard_off, ctx->d_shard_off.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  if (writer) CK(cudaMemcpyAsync(writer, ctx->d_writer.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (my_chunks) *my_chunks = tot[0];
+  if (my_bytes) *my_bytes = tot[1];
+  return SNAP_OK;
+}
+
 // ---------------------------------------------------------------- K3
 
 int snap_compact(snap_ctx* ctx) {
   if (!ctx) return SNAP_EINVAL;
   if (!ctx->selected) return fail(ctx, SNAP_EINVAL, "compact before snap_select");
   CK(cudaSetDevice(ctx->device));
-  uint8_t* st;
-  if (int rc = ensure(ctx, ctx->staging, ctx->grid_bytes, &st)) return rc;
-  CKL(snap::launch_gather(ctx->arena, ctx->grid, static_cast<uint32_t*>(ctx->d_lens.p),
-                          static_cast<uint32_t*>(ctx->sel_list.p),
-                          static_cast<uint64_t*>(ctx->totals.p),
-                          static_cast<uint64_t*>(ctx->offsets.p), st, ctx->nchunks, ctx->stream));
-  ctx->staging_valid = ctx->grid_bytes;
-  return SNAP_OK;
+  ProfScope ps(ctx, kProfCompact);
+  return compact_impl(ctx);
 }
 
 int snap_snapshot(snap_ctx* ctx) {
-  if (int rc = snap_hash(ctx)) return rc;
-  if (int rc = snap_select(ctx)) return rc;
+  RC(snap_hash(ctx));
+  RC(snap_select(ctx));
   return snap_compact(ctx);
+}
+
+int snap_snapshot_host(snap_ctx* ctx, const void* host_src, uint64_t addr, uint64_t bytes,
+                       void* host_staging, uint64_t staging_cap, uint64_t* staged_bytes,
+                       uint64_t* host_digests) {
+  if (!ctx || (!host_src && bytes)) return SNAP_EINVAL;
+  RC(check_range(ctx, addr, bytes));
+  CK(cudaSetDevice(ctx->device));
+  if (bytes)
+    CK(cudaMemcpyAsync(ctx->arena + addr, host_src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  RC(snap_snapshot(ctx));
+  uint64_t tot[2] = {0, 0};
+  const bool shard = ctx->comm && ctx->exchanged;
+  CK(cudaMemcpyAsync(tot, shard ? ctx->d_my_totals.p : ctx->totals.p, 16, cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  if (host_digests && ctx->nchunks)
+    CK(cudaMemcpyAsync(host_digests, ctx->d_dig.p, ctx->nchunks * 8, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (tot[1] > staging_cap && host_staging)
+    return fail(ctx, SNAP_EINVAL, "snapshot_host: staging buffer too small");
+  if (host_staging && tot[1]) {
+    CK(cudaMemcpyAsync(host_staging, ctx->staging.p, tot[1], cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  if (staged_bytes) *staged_bytes = tot[1];
+  return SNAP_OK;
 }
 
 int snap_staging(snap_ctx* ctx, void** dev_ptr, uint64_t* bytes) {
@@ -565,8 +819,8 @@ int snap_read_staging(snap_ctx* ctx, uint64_t off, void* dst, uint64_t bytes) {
 static int verify_grid(snap_ctx* ctx, const uint64_t* expect_dev) {
   uint64_t* d2;
   unsigned long long* nbad;
-  if (int rc = ensure(ctx, ctx->d_dig2, ctx->nchunks, &d2)) return rc;
-  if (int rc = ensure(ctx, ctx->d_nbad, 1, &nbad)) return rc;
+  RC(ensure(ctx, ctx->d_dig2, ctx->nchunks, &d2));
+  RC(ensure(ctx, ctx->d_nbad, 4, &nbad));
   CKL(snap::launch_hash(ctx->arena, ctx->grid, d2, ctx->stream));
   CKL(snap::launch_compare(d2, expect_dev, ctx->nchunks, nbad, ctx->stream));
   unsigned long long bad = 0;
@@ -587,15 +841,18 @@ int snap_restore(snap_ctx* ctx, const void* image, uint64_t image_bytes, const u
                                         " has no source in the image (missing blob)");
   CK(cudaSetDevice(ctx->device));
   uint64_t* so;
-  if (int rc = ensure(ctx, ctx->d_srcoff, ctx->nchunks, &so)) return rc;
+  RC(ensure(ctx, ctx->d_srcoff, ctx->nchunks, &so));
   CK(cudaMemcpyAsync(so, src_off, ctx->nchunks * 8, cudaMemcpyHostToDevice, ctx->stream));
-  CKL(snap::launch_scatter(ctx->arena, ctx->grid, static_cast<uint32_t*>(ctx->d_lens.p),
-                           static_cast<const uint8_t*>(image), so, ctx->stream));
+  {
+    ProfScope ps(ctx, kProfRestore);
+    CKL(snap::launch_scatter(ctx->arena, ctx->grid, P<uint32_t>(ctx->d_lens),
+                             static_cast<const uint8_t*>(image), so, ctx->stream));
+  }
   if (!verify) return snap_sync(ctx);
-  const uint64_t* expect = static_cast<uint64_t*>(ctx->d_dig.p);
+  const uint64_t* expect = P<uint64_t>(ctx->d_dig);
   if (expect_digests) {
     uint64_t* e;
-    if (int rc = ensure(ctx, ctx->d_expect, ctx->nchunks, &e)) return rc;
+    RC(ensure(ctx, ctx->d_expect, ctx->nchunks, &e));
     CK(cudaMemcpyAsync(e, expect_digests, ctx->nchunks * 8, cudaMemcpyHostToDevice, ctx->stream));
     expect = e;
   } else if (!ctx->hashed) {
@@ -610,12 +867,18 @@ int snap_restore_self(snap_ctx* ctx, int verify) {
   if (ctx->kn_count)
     return fail(ctx, SNAP_EINVAL, "restore_self: incremental snapshot (known set) needs the "
                                   "older images; use snap_restore");
+  if (ctx->comm && ctx->exchanged)
+    return fail(ctx, SNAP_EINVAL, "restore_self: multi-rank snapshots restore from the shards "
+                                  "(snap_restore)");
   CK(cudaSetDevice(ctx->device));
-  CKL(snap::launch_scatter(ctx->arena, ctx->grid, static_cast<uint32_t*>(ctx->d_lens.p),
-                           static_cast<const uint8_t*>(ctx->staging.p),
-                           static_cast<uint64_t*>(ctx->offsets.p), ctx->stream));
+  {
+    ProfScope ps(ctx, kProfRestore);
+    CKL(snap::launch_scatter(ctx->arena, ctx->grid, P<uint32_t>(ctx->d_lens),
+                             static_cast<const uint8_t*>(ctx->staging.p), P<uint64_t>(ctx->offsets),
+                             ctx->stream));
+  }
   if (!verify) return SNAP_OK;
-  return verify_grid(ctx, static_cast<uint64_t*>(ctx->d_dig.p));
+  return verify_grid(ctx, P<uint64_t>(ctx->d_dig));
 }
 
 // ---------------------------------------------------------------- K5
@@ -628,11 +891,12 @@ int snap_grad_sum(snap_ctx* ctx, int dtype, const uint64_t* src_addrs, uint32_t 
   if (elems > ctx->arena_bytes / esz) return fail(ctx, SNAP_EINVAL, "grad_sum: size");
   for (uint32_t r = 0; r < nsrc; ++r) {
     if (src_addrs[r] % 16) return fail(ctx, SNAP_EINVAL, "grad_sum: sources must be 16-B aligned");
-    if (int rc = check_range(ctx, src_addrs[r], elems * esz)) return rc;
+    RC(check_range(ctx, src_addrs[r], elems * esz));
   }
   if (dst_addr % 16) return fail(ctx, SNAP_EINVAL, "grad_sum: dst must be 16-B aligned");
-  if (int rc = check_range(ctx, dst_addr, elems * esz)) return rc;
+  RC(check_range(ctx, dst_addr, elems * esz));
   CK(cudaSetDevice(ctx->device));
+  ProfScope ps(ctx, kProfGrad);
   CKL(snap::launch_grad_sum(dtype, ctx->arena, src_addrs, nsrc, dst_addr, elems, accumulate,
                             ctx->stream));
   return SNAP_OK;
@@ -659,13 +923,15 @@ int snap_comm_init(snap_ctx* ctx, int nranks, int rank, const void* id128) {
   CKN(ncclCommInitRank(&ctx->comm, nranks, id, rank));
   ctx->nranks = nranks;
   ctx->rank = rank;
+  ctx->glens_valid = false;
+  ctx->exchanged = false;
   return SNAP_OK;
 }
 
 int snap_allreduce(snap_ctx* ctx, int dtype, uint64_t addr, uint64_t elems) {
   if (!ctx || !ctx->comm) return fail(ctx, SNAP_EINVAL, "allreduce: no communicator");
   const uint64_t esz = dtype == SNAP_F32 ? 4 : 8;
-  if (int rc = check_range(ctx, addr, elems * esz)) return rc;
+  RC(check_range(ctx, addr, elems * esz));
   CK(cudaSetDevice(ctx->device));
   CKN(ncclAllReduce(ctx->arena + addr, ctx->arena + addr, elems,
                     dtype == SNAP_F32 ? ncclFloat32 : ncclUint64, ncclSum, ctx->comm, ctx->stream));
@@ -687,6 +953,34 @@ int snap_timer_stop(snap_ctx* ctx, float* ms) {
   CK(cudaEventRecord(ctx->ev1, ctx->stream));
   CK(cudaEventSynchronize(ctx->ev1));
   CK(cudaEventElapsedTime(ms, ctx->ev0, ctx->ev1));
+  return SNAP_OK;
+}
+
+int snap_prof_enable(snap_ctx* ctx, int on) {
+  if (!ctx) return SNAP_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->prof.on = on != 0;
+  ctx->prof.used = 0;
+  ctx->prof.marks.clear();
+  return SNAP_OK;
+}
+
+int snap_prof_read(snap_ctx* ctx, int kind, float* total_ms, uint64_t* count) {
+  if (!ctx || !total_ms || !count) return SNAP_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->stream));
+  float tot = 0;
+  uint64_t n = 0;
+  for (auto& m : ctx->prof.marks)
+    if (m.first == kind) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, m.second.first, m.second.second));
+      tot += ms;
+      ++n;
+    }
+  *total_ms = tot;
+  *count = n;
   return SNAP_OK;
 }
 

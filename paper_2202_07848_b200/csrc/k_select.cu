@@ -1,14 +1,22 @@
 // k_select.cu — K2: dedup table + dirty test + deterministic stream-compaction
-// offsets.
+// offsets, single GPU and cross-rank (after the NCCL allgather of digest
+// vectors).
 //
 // Reference semantics (build_manifest, ckpt.cpp:97,147-167; BlobStore::put,
 // ckpt.cpp:16-21): walking chunks in canonical (rank, slot, chunk) order, a
-// chunk is staged iff its digest was not seen earlier in this snapshot AND
-// is not already in the store (the "known" set). Order independence on the
-// GPU: the dedup table stores min(chunk index) per digest (atomicMin), so the
-// first occurrence is found without any ordering between threads; staging
-// offsets come from a single-pass decoupled look-back scan over canonical
-// chunk order, so the staging image is bit-identical run to run.
+// chunk is staged iff its digest was not seen earlier in this snapshot AND is
+// not already in the store (the "known" set). Order independence on the GPU:
+// the dedup table keeps min(canonical index) per digest (atomicMin), so the
+// first occurrence is found without ordering threads; staging offsets come
+// from a single-pass decoupled look-back scan over canonical chunk order, so
+// the staging image is bit-identical run to run.
+//
+// Cross-rank: every GPU builds the same global table from the
+// allgathered vectors; the logical owner is the first occurrence, but the
+// physical copy of a replicated chunk is striped over its holders (ranks whose
+// chunk at the same local index has the same digest): writer =
+// holders[local_index % |holders|]. Each GPU stages only the chunks it writes,
+// in canonical order (its shard of the global image).
 #include <cuda_runtime.h>
 
 #include "snap_internal.h"
@@ -63,10 +71,60 @@ __global__ void k_table_insert_min(TableDev t, const uint64_t* __restrict__ keys
   }
 }
 
-// ---- selection + decoupled look-back scan ---------------------------------
+// Insert every live chunk (len > 0; padding entries of the allgathered
+// vectors have len 0) with its canonical index; record its slot and whether
+// the known set holds it, so the scan needs one load per chunk.
+__global__ void k_dedup_insert(TableDev dedup, TableDev known, int use_known,
+                               const uint64_t* __restrict__ dig, const uint32_t* __restrict__ lens,
+                               uint64_t n, uint64_t* __restrict__ slot) {
+  for (uint64_t g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < n;
+       g += uint64_t(gridDim.x) * blockDim.x) {
+    uint64_t s = ~0ull;
+    if (lens[g] != 0) {
+      const unsigned long long d = dig[g];
+      const bool is_known = use_known && table_find(known, d) != ~0ull;
+      if (!is_known) {
+        s = table_find_or_insert(dedup, d);
+        atomicMin(dedup.vals + s, static_cast<unsigned long long>(g));
+      }
+    }
+    slot[g] = s;
+  }
+}
+
+// Stripe writer of every selected global chunk (rank-major, `maxn` per rank).
+__global__ void k_stripe_writer(const uint64_t* __restrict__ gdig, const uint32_t* __restrict__ glens,
+                                const uint8_t* __restrict__ sel, uint32_t nranks, uint64_t maxn,
+                                int32_t* __restrict__ writer) {
+  const uint64_t n = uint64_t(nranks) * maxn;
+  for (uint64_t g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < n;
+       g += uint64_t(gridDim.x) * blockDim.x) {
+    int32_t w = -1;
+    if (sel[g]) {
+      const uint64_t i = g % maxn;
+      const uint64_t d = gdig[g];
+      const uint32_t ln = glens[g];
+      uint32_t nh = 0;
+      for (uint32_t q = 0; q < nranks; ++q)
+        nh += (glens[q * maxn + i] == ln && gdig[q * maxn + i] == d);
+      uint32_t pick = static_cast<uint32_t>(i % nh), seen = 0;
+      for (uint32_t q = 0; q < nranks; ++q)
+        if (glens[q * maxn + i] == ln && gdig[q * maxn + i] == d) {
+          if (seen == pick) {
+            w = static_cast<int32_t>(q);
+            break;
+          }
+          ++seen;
+        }
+    }
+    writer[g] = w;
+  }
+}
+
+// ---- decoupled look-back scan -------------------------------------------
 // Status word per tile: flag (2 bits) | chunk count (26 bits) | 256-byte units (36 bits).
 constexpr int kThreads = 256;
-constexpr int kItems = 8;
+constexpr int kItems = 4;
 constexpr int kTile = kThreads * kItems;
 constexpr uint64_t kFlagAgg = 1ull << 62;
 constexpr uint64_t kFlagPre = 2ull << 62;
@@ -82,42 +140,14 @@ __device__ __forceinline__ uint64_t ld_status(const uint64_t* p) {
   return v;
 }
 
-__global__ void __launch_bounds__(kThreads)
-k_select_scan(TableDev dedup, TableDev known, int use_known, const uint64_t* __restrict__ dig,
-              const uint32_t* __restrict__ lens, uint64_t n, uint64_t* __restrict__ status,
-              unsigned int* __restrict__ tile_counter, uint8_t* __restrict__ sel,
-              uint64_t* __restrict__ owner, uint64_t* __restrict__ offsets,
-              uint32_t* __restrict__ sel_list, uint64_t* __restrict__ totals) {
-  __shared__ unsigned int s_tile;
+// Block-wide exclusive scan + tile prefix by decoupled look-back. Returns the
+// exclusive prefix of this thread's first item; publishes totals from the
+// last tile.
+__device__ uint64_t tile_scan(uint64_t local, uint64_t tile, uint64_t ntiles, uint64_t* status,
+                              uint64_t* totals) {
   __shared__ uint64_t s_warp[kThreads / 32];
   __shared__ uint64_t s_excl;
-  if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
-  __syncthreads();
-  const uint64_t tile = s_tile;
-  const uint64_t base = tile * kTile + uint64_t(threadIdx.x) * kItems;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-
-  uint64_t val[kItems];
-  uint64_t own[kItems];
-  uint64_t local = 0;
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const uint64_t g = base + j;
-    val[j] = 0;
-    own[j] = ~0ull;
-    if (g < n) {
-      const unsigned long long d = dig[g];
-      bool is_known = false;
-      if (use_known) is_known = table_find(known, d) != ~0ull;
-      if (!is_known) {
-        const uint64_t s = table_find(dedup, d);
-        own[j] = dedup.vals[s];
-        if (own[j] == g) val[j] = (1ull << kUnitBits) | (lens[g] >> 8);
-      }
-    }
-    local += val[j];
-  }
-  // block-wide exclusive scan of per-thread sums
   uint64_t incl = local;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -127,7 +157,7 @@ k_select_scan(TableDev dedup, TableDev known, int use_known, const uint64_t* __r
   if (lane == 31) s_warp[warp] = incl;
   __syncthreads();
   if (warp == 0) {
-    uint64_t w = lane < kThreads / 32 ? s_warp[lane] : 0;
+    const uint64_t w = lane < kThreads / 32 ? s_warp[lane] : 0;
     uint64_t wi = w;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -135,8 +165,7 @@ k_select_scan(TableDev dedup, TableDev known, int use_known, const uint64_t* __r
       if (lane >= o) wi += y;
     }
     const uint64_t agg = __shfl_sync(0xffffffffu, wi, kThreads / 32 - 1);
-    if (lane < kThreads / 32) s_warp[lane] = wi - w;  // exclusive per warp
-    // decoupled look-back over predecessor tiles
+    if (lane < kThreads / 32) s_warp[lane] = wi - w;
     uint64_t excl = 0;
     if (tile == 0) {
       if (lane == 0) st_status(status, kFlagPre | agg);
@@ -162,7 +191,7 @@ k_select_scan(TableDev dedup, TableDev known, int use_known, const uint64_t* __r
     }
     if (lane == 0) {
       s_excl = excl;
-      if ((tile + 1) * kTile >= n) {  // last tile publishes the totals
+      if (tile + 1 == ntiles) {
         const uint64_t tot = excl + agg;
         totals[0] = tot >> kUnitBits;
         totals[1] = (tot & ((1ull << kUnitBits) - 1)) << 8;
@@ -170,16 +199,82 @@ k_select_scan(TableDev dedup, TableDev known, int use_known, const uint64_t* __r
     }
   }
   __syncthreads();
-  uint64_t run = s_excl + s_warp[warp] + (incl - local);
+  return s_excl + s_warp[warp] + (incl - local);
+}
+
+__device__ __forceinline__ uint64_t next_tile(unsigned int* counter) {
+  __shared__ unsigned int s_tile;
+  if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
+  __syncthreads();
+  return s_tile;
+}
+
+__global__ void __launch_bounds__(kThreads)
+k_select_scan(TableDev dedup, const uint64_t* __restrict__ slot, const uint32_t* __restrict__ lens,
+              uint64_t n, uint64_t* __restrict__ status, unsigned int* __restrict__ tile_counter,
+              uint8_t* __restrict__ sel, uint64_t* __restrict__ owner,
+              uint64_t* __restrict__ offsets, uint32_t* __restrict__ sel_list,
+              uint64_t* __restrict__ totals) {
+  const uint64_t tile = next_tile(tile_counter);
+  const uint64_t ntiles = (n + kTile - 1) / kTile;
+  const uint64_t base = tile * kTile + uint64_t(threadIdx.x) * kItems;
+  uint64_t val[kItems], own[kItems], local = 0;
+  uint64_t s[kItems];
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) s[j] = base + j < n ? slot[base + j] : ~0ull;
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    own[j] = s[j] == ~0ull ? ~0ull : dedup.vals[s[j]];
+    val[j] = own[j] == base + j ? (1ull << kUnitBits) | (lens[base + j] >> 8) : 0;
+    local += val[j];
+  }
+  uint64_t run = tile_scan(local, tile, ntiles, status, totals);
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
     const uint64_t g = base + j;
     if (g < n) {
-      const bool s = val[j] != 0;
-      sel[g] = s;
+      const bool sl = val[j] != 0;
+      sel[g] = sl;
       owner[g] = own[j];
       offsets[g] = own[j] == ~0ull ? ~0ull : (run & ((1ull << kUnitBits) - 1)) << 8;
-      if (s) sel_list[run >> kUnitBits] = static_cast<uint32_t>(g);
+      if (sl) sel_list[run >> kUnitBits] = static_cast<uint32_t>(g);
+    }
+    run += val[j];
+  }
+}
+
+// Shard scan for writer `me`: offsets of the chunks `me` writes, in canonical
+// order (its shard of the global image); with write_list, my_list[k] = local
+// chunk index of the k-th chunk of the shard and my_off[k] its offset.
+__global__ void __launch_bounds__(kThreads)
+k_shard_scan(const int32_t* __restrict__ writer, const uint32_t* __restrict__ glens, uint64_t n,
+             uint64_t maxn, int32_t me, int write_list, uint64_t* __restrict__ status,
+             unsigned int* __restrict__ tile_counter, uint64_t* __restrict__ shard_off,
+             uint32_t* __restrict__ my_list, uint64_t* __restrict__ my_off,
+             uint64_t* __restrict__ totals) {
+  const uint64_t tile = next_tile(tile_counter);
+  const uint64_t ntiles = (n + kTile - 1) / kTile;
+  const uint64_t base = tile * kTile + uint64_t(threadIdx.x) * kItems;
+  uint64_t val[kItems], local = 0;
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const uint64_t g = base + j;
+    val[j] = (g < n && writer[g] == me) ? (1ull << kUnitBits) | (glens[g] >> 8) : 0;
+    local += val[j];
+  }
+  uint64_t run = tile_scan(local, tile, ntiles, status, totals);
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const uint64_t g = base + j;
+    if (g < n) {
+      const uint64_t off = (run & ((1ull << kUnitBits) - 1)) << 8;
+      if (val[j]) {
+        shard_off[g] = off;
+        if (write_list) {
+          my_list[run >> kUnitBits] = static_cast<uint32_t>(g % maxn);
+          my_off[run >> kUnitBits] = off;
+        }
+      }
     }
     run += val[j];
   }
@@ -217,20 +312,50 @@ int launch_table_insert_min(TableDev t, const uint64_t* keys, uint64_t n, uint64
   return 1;
 }
 
-int launch_select(TableDev dedup, TableDev known, bool use_known, const uint64_t* dig,
-                  const uint32_t* lens, uint64_t n, uint64_t* scan_state, uint8_t* sel,
-                  uint64_t* owner, uint64_t* offsets, uint32_t* sel_list, uint64_t* totals,
-                  cudaStream_t s) {
+int launch_dedup_insert(TableDev dedup, TableDev known, bool use_known, const uint64_t* dig,
+                        const uint32_t* lens, uint64_t n, uint64_t* slot, cudaStream_t s) {
+  if (n == 0) return 0;
+  k_dedup_insert<<<grid_for(n, 128, 148 * 32), 128, 0, s>>>(dedup, known, use_known ? 1 : 0, dig,
+                                                             lens, n, slot);
+  return 1;
+}
+
+int launch_select(TableDev dedup, const uint64_t* slot, const uint32_t* lens, uint64_t n,
+                  uint64_t* scan_state, uint8_t* sel, uint64_t* owner, uint64_t* offsets,
+                  uint32_t* sel_list, uint64_t* totals, cudaStream_t s) {
   const uint64_t tiles = (n + kTile - 1) / kTile;
-  // scan_state = [tiles] status words + 1 word of tile counter
   cudaMemsetAsync(scan_state, 0, (tiles + 1) * sizeof(uint64_t), s);
   if (n == 0) {
     cudaMemsetAsync(totals, 0, 2 * sizeof(uint64_t), s);
     return 0;
   }
   k_select_scan<<<unsigned(tiles), kThreads, 0, s>>>(
-      dedup, known, use_known ? 1 : 0, dig, lens, n, scan_state,
-      reinterpret_cast<unsigned int*>(scan_state + tiles), sel, owner, offsets, sel_list, totals);
+      dedup, slot, lens, n, scan_state, reinterpret_cast<unsigned int*>(scan_state + tiles), sel,
+      owner, offsets, sel_list, totals);
+  return 1;
+}
+
+int launch_stripe_writer(const uint64_t* gdig, const uint32_t* glens, const uint8_t* sel,
+                         uint32_t nranks, uint64_t maxn, int32_t* writer, cudaStream_t s) {
+  const uint64_t n = uint64_t(nranks) * maxn;
+  if (n == 0) return 0;
+  k_stripe_writer<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(gdig, glens, sel, nranks, maxn, writer);
+  return 1;
+}
+
+int launch_shard_scan(const int32_t* writer, const uint32_t* glens, uint32_t nranks, uint64_t maxn,
+                      int32_t q, bool write_list, uint64_t* scan_state, uint64_t* shard_off,
+                      uint32_t* my_list, uint64_t* my_off, uint64_t* totals, cudaStream_t s) {
+  const uint64_t n = uint64_t(nranks) * maxn;
+  const uint64_t tiles = (n + kTile - 1) / kTile;
+  cudaMemsetAsync(scan_state, 0, (tiles + 1) * sizeof(uint64_t), s);
+  if (n == 0) {
+    cudaMemsetAsync(totals, 0, 2 * sizeof(uint64_t), s);
+    return 0;
+  }
+  k_shard_scan<<<unsigned(tiles), kThreads, 0, s>>>(
+      writer, glens, n, maxn, q, write_list ? 1 : 0, scan_state,
+      reinterpret_cast<unsigned int*>(scan_state + tiles), shard_off, my_list, my_off, totals);
   return 1;
 }
 

@@ -44,19 +44,30 @@ int launch_xor_words(uint8_t* arena, const uint64_t* addrs, uint64_t n, uint64_t
 int launch_table_clear(TableDev t, cudaStream_t s);
 int launch_table_insert_min(TableDev t, const uint64_t* keys, uint64_t n, uint64_t index_base,
                             cudaStream_t s);
-// sel/owner/offsets + compact index list; `scan_state` sized by scan_state_words(n)
+// K2: insert (slot + known flag per chunk), then the selection scan:
+// sel/owner/offsets + compact index list; `scan_state` sized by scan_state_words(n).
 uint64_t scan_state_words(uint64_t n);
-int launch_select(TableDev dedup, TableDev known, bool use_known, const uint64_t* dig,
-                  const uint32_t* lens, uint64_t n, uint64_t* scan_state, uint8_t* sel,
-                  uint64_t* owner, uint64_t* offsets, uint32_t* sel_list, uint64_t* totals,
-                  cudaStream_t s);
+int launch_dedup_insert(TableDev dedup, TableDev known, bool use_known, const uint64_t* dig,
+                        const uint32_t* lens, uint64_t n, uint64_t* slot, cudaStream_t s);
+int launch_select(TableDev dedup, const uint64_t* slot, const uint32_t* lens, uint64_t n,
+                  uint64_t* scan_state, uint8_t* sel, uint64_t* owner, uint64_t* offsets,
+                  uint32_t* sel_list, uint64_t* totals, cudaStream_t s);
+// Cross-rank striping: writer per selected global chunk, then one shard scan
+// per writer q (write_list for q == this rank: local chunk list + offsets).
+int launch_stripe_writer(const uint64_t* gdig, const uint32_t* glens, const uint8_t* sel,
+                         uint32_t nranks, uint64_t maxn, int32_t* writer, cudaStream_t s);
+int launch_shard_scan(const int32_t* writer, const uint32_t* glens, uint32_t nranks, uint64_t maxn,
+                      int32_t q, bool write_list, uint64_t* scan_state, uint64_t* shard_off,
+                      uint32_t* my_list, uint64_t* my_off, uint64_t* totals, cudaStream_t s);
 int launch_resolve_dups(const uint8_t* sel, const uint64_t* owner, uint64_t* offsets, uint64_t n,
                         cudaStream_t s);
 
 // K3 / K4 chunk copies.
+// offsets_by_list: dst offset of list entry k is offsets[k] (shard lists) instead
+// of offsets[sel_list[k]] (single-GPU image).
 int launch_gather(const uint8_t* arena, const GridDev& g, const uint32_t* lens,
                   const uint32_t* sel_list, const uint64_t* totals, const uint64_t* offsets,
-                  uint8_t* staging, uint64_t max_sel, cudaStream_t s);
+                  bool offsets_by_list, uint8_t* staging, uint64_t max_sel, cudaStream_t s);
 int launch_scatter(uint8_t* arena, const GridDev& g, const uint32_t* lens, const uint8_t* image,
                    const uint64_t* src_off, cudaStream_t s);
 int launch_compare(const uint64_t* a, const uint64_t* b, uint64_t n, unsigned long long* nbad,
