@@ -59,8 +59,14 @@ typedef struct {
   uint64_t addr;
   uint64_t bytes;
   int32_t cat; /* vdev::BufCat (vdev.hpp:17): 0 Param 1 OptState 2 Grad 3 Activation 4 Scratch */
-  uint32_t flags;
+  uint32_t flags; /* SNAP_BUF_* layout hints (never affect results, only speed) */
 } snap_buf;
+
+/* Hint: the buffer holds identical bytes at the same address on every DP
+ * rank (default for cat Param/OptState, test_workload.cpp:210-218). Only used
+ * to predict the staging layout of the fused hash+compaction pass. */
+#define SNAP_BUF_REPLICATED 1u
+#define SNAP_BUF_PRIVATE 2u
 
 /* Chunk grid: page digest = digest_of_words(page) (sim.hpp:67-70 on the
  * reference's 4 KiB page unit, ckpt.hpp:15); chunk digest = digest_of_words

@@ -66,6 +66,12 @@ struct snap_ctx {
   bool selected = false;
   DevMem staging;
   uint64_t staging_valid = 0;
+  // speculative layout for the fused hash+compaction pass (double-buffered:
+  // the gather/fix-up writes the actual layout as the next prediction)
+  DevMem d_spec[2];
+  int spec_cur = 0;
+  bool spec_ready = false;
+  bool spec_used = false;
 
   // cross-rank exchange (NCCL allgather of digest vectors) and striping
   ncclComm_t comm = nullptr;
@@ -343,18 +349,97 @@ int stripe_impl(snap_ctx* ctx) {
   return SNAP_OK;
 }
 
+// Speculative staging layout before any digest is known:
+// single GPU: every chunk staged, canonical order (identity prefix);
+// multi-rank: chunks of buffers hinted replicated are predicted striped
+// (writer = local_index % nranks), others written by their own rank; shard
+// order follows the predicted global index (first holder's rank, local index).
+bool replicated_hint(const snap_buf& b) {
+  if (b.flags & SNAP_BUF_REPLICATED) return true;
+  if (b.flags & SNAP_BUF_PRIVATE) return false;
+  return b.cat == 0 || b.cat == 1;  // Param / OptState: identical across DP replicas
+}
+
+int init_spec(snap_ctx* ctx) {
+  const uint64_t n = ctx->nchunks;
+  std::vector<uint64_t> spec(n, ~0ull);
+  if (!ctx->comm || ctx->nranks == 1) {
+    uint64_t off = 0;
+    for (uint64_t g = 0; g < n; ++g) {
+      spec[g] = off;
+      off += ctx->h_lens[g];
+    }
+  } else {
+    std::vector<uint8_t> rep(n, 0);
+    for (size_t b = 0; b < ctx->bufs.size(); ++b)
+      for (uint64_t g = ctx->h_cstart[b]; g < ctx->h_cstart[b + 1]; ++g)
+        rep[g] = replicated_hint(ctx->bufs[b]);
+    const uint64_t N = ctx->nranks, me = ctx->rank;
+    uint64_t off = 0;
+    auto take = [&](uint64_t g) {
+      spec[g] = off;
+      off += ctx->h_lens[g];
+    };
+    if (me == 0) {
+      for (uint64_t g = 0; g < n; ++g)
+        if (!rep[g] || g % N == 0) take(g);
+    } else {
+      for (uint64_t g = 0; g < n; ++g)
+        if (rep[g] && g % N == me) take(g);
+      for (uint64_t g = 0; g < n; ++g)
+        if (!rep[g]) take(g);
+    }
+  }
+  uint64_t* d;
+  RC(ensure(ctx, ctx->d_spec[ctx->spec_cur], n, &d));
+  CK(cudaMemcpyAsync(d, spec.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->spec_ready = true;
+  return SNAP_OK;
+}
+
+// K1 with the fused speculative compaction (full snapshots); incremental
+// snapshots (known set non-empty) hash only and gather the few dirty chunks.
+int hash_fused(snap_ctx* ctx) {
+  if (ctx->kn_count > 0) {
+    CKL(snap::launch_hash(ctx->arena, ctx->grid, P<uint64_t>(ctx->d_dig), nullptr, nullptr,
+                          ctx->stream));
+    ctx->spec_used = false;
+    return SNAP_OK;
+  }
+  if (!ctx->spec_ready) RC(init_spec(ctx));
+  uint8_t* st;
+  RC(ensure(ctx, ctx->staging, ctx->grid_bytes, &st));
+  CKL(snap::launch_hash(ctx->arena, ctx->grid, P<uint64_t>(ctx->d_dig),
+                        P<uint64_t>(ctx->d_spec[ctx->spec_cur]), st, ctx->stream));
+  ctx->spec_used = true;
+  return SNAP_OK;
+}
+
 int compact_impl(snap_ctx* ctx) {
   uint8_t* st;
+  RC(ensure(ctx, ctx->staging, ctx->grid_bytes, &st));
+  const uint64_t* spec_cur = nullptr;
+  uint64_t* spec_next = nullptr;
+  if (ctx->spec_used) {
+    spec_cur = P<uint64_t>(ctx->d_spec[ctx->spec_cur]);
+    RC(ensure(ctx, ctx->d_spec[1 - ctx->spec_cur], ctx->nchunks, &spec_next));
+    CK(cudaMemsetAsync(spec_next, 0xff, ctx->nchunks * 8, ctx->stream));
+  }
   if (ctx->comm && ctx->exchanged) {
-    RC(ensure(ctx, ctx->staging, ctx->grid_bytes, &st));
-    CKL(snap::launch_gather(ctx->arena, ctx->grid, P<uint32_t>(ctx->d_lens), P<uint32_t>(ctx->d_my_list),
-                            P<uint64_t>(ctx->d_my_totals), P<uint64_t>(ctx->d_my_off), true, st,
+    CKL(snap::launch_gather(ctx->arena, ctx->grid, P<uint32_t>(ctx->d_lens),
+                            P<uint32_t>(ctx->d_my_list), P<uint64_t>(ctx->d_my_totals),
+                            P<uint64_t>(ctx->d_my_off), true, spec_cur, spec_next, st,
                             ctx->nchunks, ctx->stream));
   } else {
-    RC(ensure(ctx, ctx->staging, ctx->grid_bytes, &st));
-    CKL(snap::launch_gather(ctx->arena, ctx->grid, P<uint32_t>(ctx->d_lens), P<uint32_t>(ctx->sel_list),
-                            P<uint64_t>(ctx->totals), P<uint64_t>(ctx->offsets), false, st,
+    CKL(snap::launch_gather(ctx->arena, ctx->grid, P<uint32_t>(ctx->d_lens),
+                            P<uint32_t>(ctx->sel_list), P<uint64_t>(ctx->totals),
+                            P<uint64_t>(ctx->offsets), false, spec_cur, spec_next, st,
                             ctx->nchunks, ctx->stream));
+  }
+  if (ctx->spec_used) {
+    ctx->spec_cur = 1 - ctx->spec_cur;
+    ctx->spec_used = false;  // the image is final; a second compact re-gathers
   }
   ctx->staging_valid = ctx->grid_bytes;
   return SNAP_OK;
@@ -422,7 +507,7 @@ int snap_close(snap_ctx* ctx) {
         &ctx->scan, &ctx->sel, &ctx->owner, &ctx->offsets, &ctx->sel_list, &ctx->totals,
         &ctx->staging, &ctx->d_counts, &ctx->d_gdig, &ctx->d_glens, &ctx->d_writer,
         &ctx->d_shard_off, &ctx->d_my_list, &ctx->d_my_off, &ctx->d_my_totals, &ctx->d_dig2,
-        &ctx->d_expect, &ctx->d_nbad, &ctx->d_srcoff})
+        &ctx->d_expect, &ctx->d_nbad, &ctx->d_srcoff, &ctx->d_spec[0], &ctx->d_spec[1]})
     release(*m);
   for (cudaEvent_t e : ctx->prof.pool) cudaEventDestroy(e);
   if (ctx->arena) cudaFree(ctx->arena);
@@ -578,6 +663,8 @@ int snap_set_buffers(snap_ctx* ctx, const snap_buf* bufs, uint64_t n, const snap
   ctx->selected = false;
   ctx->exchanged = false;
   ctx->glens_valid = false;
+  ctx->spec_ready = false;
+  ctx->spec_used = false;
   if (n_chunks) *n_chunks = ctx->nchunks;
   return SNAP_OK;
 }
@@ -587,8 +674,10 @@ int snap_hash(snap_ctx* ctx) {
   CK(cudaSetDevice(ctx->device));
   {
     ProfScope ps(ctx, kProfHash);
-    CKL(snap::launch_hash(ctx->arena, ctx->grid, P<uint64_t>(ctx->d_dig), ctx->stream));
+    CKL(snap::launch_hash(ctx->arena, ctx->grid, P<uint64_t>(ctx->d_dig), nullptr, nullptr,
+                          ctx->stream));
   }
+  ctx->spec_used = false;
   ctx->hashed = true;
   ctx->selected = false;
   ctx->exchanged = false;
@@ -764,7 +853,15 @@ int snap_compact(snap_ctx* ctx) {
 }
 
 int snap_snapshot(snap_ctx* ctx) {
-  RC(snap_hash(ctx));
+  if (!ctx) return SNAP_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  {
+    ProfScope ps(ctx, kProfHash);
+    RC(hash_fused(ctx));
+  }
+  ctx->hashed = true;
+  ctx->selected = false;
+  ctx->exchanged = false;
   RC(snap_select(ctx));
   return snap_compact(ctx);
 }
@@ -821,7 +918,7 @@ static int verify_grid(snap_ctx* ctx, const uint64_t* expect_dev) {
   unsigned long long* nbad;
   RC(ensure(ctx, ctx->d_dig2, ctx->nchunks, &d2));
   RC(ensure(ctx, ctx->d_nbad, 4, &nbad));
-  CKL(snap::launch_hash(ctx->arena, ctx->grid, d2, ctx->stream));
+  CKL(snap::launch_hash(ctx->arena, ctx->grid, d2, nullptr, nullptr, ctx->stream));
   CKL(snap::launch_compare(d2, expect_dev, ctx->nchunks, nbad, ctx->stream));
   unsigned long long bad = 0;
   CK(cudaMemcpyAsync(&bad, nbad, 8, cudaMemcpyDeviceToHost, ctx->stream));
@@ -925,6 +1022,7 @@ int snap_comm_init(snap_ctx* ctx, int nranks, int rank, const void* id128) {
   ctx->rank = rank;
   ctx->glens_valid = false;
   ctx->exchanged = false;
+  ctx->spec_ready = false;
   return SNAP_OK;
 }
 

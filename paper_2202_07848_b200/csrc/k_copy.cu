@@ -55,17 +55,26 @@ __device__ __forceinline__ void warp_copy(uint8_t* __restrict__ dst, const uint8
   for (; i < n16; i += 32) __stcs(d + i, __ldcs(s + i));
 }
 
+// K3 gather / fix-up. For the k-th staged chunk gc = sel_list[k] with staging
+// offset `off`: when the fused hash pass already wrote it there
+// (spec_cur[gc] == off) nothing moves; otherwise the chunk is copied from the
+// arena (never from the speculative image, so there is no overlap hazard).
+// spec_next[gc] = off records the layout as the next snapshot's prediction.
 __global__ void __launch_bounds__(kThreads)
 k_gather(const uint8_t* __restrict__ arena, GridDev g, const uint32_t* __restrict__ lens,
          const uint32_t* __restrict__ sel_list, const uint64_t* __restrict__ totals,
-         const uint64_t* __restrict__ offsets, int by_list, uint8_t* __restrict__ staging) {
+         const uint64_t* __restrict__ offsets, int by_list, const uint64_t* __restrict__ spec_cur,
+         uint64_t* __restrict__ spec_next, uint8_t* __restrict__ staging) {
   const uint64_t nsel = totals[0];
   const int lane = threadIdx.x & 31;
   const uint64_t w0 = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
   const uint64_t nw = (uint64_t(gridDim.x) * kThreads) >> 5;
   for (uint64_t w = w0; w < nsel; w += nw) {
     const uint32_t gc = sel_list[w];
-    warp_copy(staging + offsets[by_list ? w : gc], chunk_ptr(arena, g, gc), lens[gc], lane);
+    const uint64_t off = offsets[by_list ? w : gc];
+    if (spec_next && lane == 0) spec_next[gc] = off;
+    if (spec_cur && spec_cur[gc] == off) continue;
+    warp_copy(staging + off, chunk_ptr(arena, g, gc), lens[gc], lane);
   }
 }
 
@@ -106,12 +115,14 @@ unsigned copy_grid() {
 
 int launch_gather(const uint8_t* arena, const GridDev& g, const uint32_t* lens,
                   const uint32_t* sel_list, const uint64_t* totals, const uint64_t* offsets,
-                  bool offsets_by_list, uint8_t* staging, uint64_t max_sel, cudaStream_t s) {
+                  bool offsets_by_list, const uint64_t* spec_cur, uint64_t* spec_next,
+                  uint8_t* staging, uint64_t max_sel, cudaStream_t s) {
   if (max_sel == 0) return 0;
   uint64_t blocks = (max_sel * 32 + kThreads - 1) / kThreads;
   if (blocks > copy_grid()) blocks = copy_grid();
   k_gather<<<unsigned(blocks), kThreads, 0, s>>>(arena, g, lens, sel_list, totals, offsets,
-                                                 offsets_by_list ? 1 : 0, staging);
+                                                 offsets_by_list ? 1 : 0, spec_cur, spec_next,
+                                                 staging);
   return 1;
 }
 

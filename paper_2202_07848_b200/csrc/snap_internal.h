@@ -35,7 +35,10 @@ struct TableDev {
 constexpr unsigned long long kEmptyKey = 0xffffffffffffffffull;
 
 // Launchers (each returns the number of kernels launched).
-int launch_hash(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig, cudaStream_t s);
+// K1; with spec_off != nullptr also the fused speculative K3 (TMA bulk stores
+// of every chunk whose spec_off[chunk] != ~0 to staging + spec_off[chunk]).
+int launch_hash(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
+                const uint64_t* spec_off, uint8_t* staging, cudaStream_t s);
 int launch_buf_fold(const GridDev& g, const uint64_t* chunk_dig, uint64_t* buf_dig, cudaStream_t s);
 int launch_fill_mix64(uint64_t* dst, uint64_t nwords, uint64_t seed, uint64_t base, cudaStream_t s);
 int launch_xor_words(uint8_t* arena, const uint64_t* addrs, uint64_t n, uint64_t value,
@@ -64,10 +67,13 @@ int launch_resolve_dups(const uint8_t* sel, const uint64_t* owner, uint64_t* off
 
 // K3 / K4 chunk copies.
 // offsets_by_list: dst offset of list entry k is offsets[k] (shard lists) instead
-// of offsets[sel_list[k]] (single-GPU image).
+// of offsets[sel_list[k]] (single-GPU image). spec_cur (nullable): chunks the
+// fused hash pass already wrote at the right offset are skipped; spec_next
+// (nullable) receives the actual layout (next prediction).
 int launch_gather(const uint8_t* arena, const GridDev& g, const uint32_t* lens,
                   const uint32_t* sel_list, const uint64_t* totals, const uint64_t* offsets,
-                  bool offsets_by_list, uint8_t* staging, uint64_t max_sel, cudaStream_t s);
+                  bool offsets_by_list, const uint64_t* spec_cur, uint64_t* spec_next,
+                  uint8_t* staging, uint64_t max_sel, cudaStream_t s);
 int launch_scatter(uint8_t* arena, const GridDev& g, const uint32_t* lens, const uint8_t* image,
                    const uint64_t* src_off, cudaStream_t s);
 int launch_compare(const uint64_t* a, const uint64_t* b, uint64_t n, unsigned long long* nbad,

@@ -200,3 +200,34 @@ def test_grad_sum(snap, ctx, dtype):
         ctx.grad_sum(code, [r * stride], dst, n, accumulate=True)
     got2 = np.frombuffer(ctx.read(dst, nb).tobytes(), dtype=gs[0].dtype)
     assert np.array_equal(got2.view(np.uint8), exp.view(np.uint8))
+
+
+def test_fused_speculation_learns_and_recovers(snap, ctx, golden):
+    """Fused hash+compaction: the first snapshot speculates the identity layout, later
+    ones reuse the last actual layout; every mispredicted chunk is fixed up from the
+    arena, so the staging image always equals the oracle's."""
+    arena, bufs = load_ragged(ctx, golden)
+    ctx.set_buffers(bufs, 4096, 65536)
+
+    def check(host):
+        ctx.snapshot()
+        d, lens = ctx.digests()
+        sel, owner, off, sbytes, _ = ctx.selection()
+        osel, oown, ooff, otot = O.select(d, lens)
+        assert np.array_equal(sel, osel) and np.array_equal(off, ooff) and sbytes == otot
+        assert np.array_equal(ctx.read_staging(0, sbytes),
+                              O.compact([host], bufs, 65536, osel, ooff, otot))
+
+    check(arena)          # identity speculation, fix-up after the duplicate buffer
+    check(arena)          # learned layout: no fix-up
+    # break the duplicate (buffer 3 becomes unique) -> prediction too small, fix-up again
+    src, dst, n = golden["ragged"]["dup"]
+    ctx.xor_words([dst + 4096], 0x5A5A)
+    host = ctx.read(0, golden["ragged"]["arena_bytes"])
+    check(host)
+    check(host)
+    # make buffer 0 a copy of buffer 5's first 256 B -> new duplicate: holes, fix-up
+    b0 = bufs[0]
+    ctx.write(b0[2], host[bufs[5][2]:bufs[5][2] + b0[3]])
+    host = ctx.read(0, golden["ragged"]["arena_bytes"])
+    check(host)
