@@ -1,0 +1,32 @@
+"""Multi-GPU parity (needs >= 2 B200s: gpurun --gpus 2|4): cross-rank dedup over NCCL
+allgather + striped shards vs the oracle. Skips on a 1-GPU box."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+pytestmark = pytest.mark.gpu
+
+
+def ngpus():
+    try:
+        out = subprocess.run(["nvidia-smi", "-L"], capture_output=True, text=True, timeout=30)
+        return len([x for x in out.stdout.splitlines() if x.startswith("GPU")])
+    except Exception:
+        return 0
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_dist_snapshot_parity(world):
+    if ngpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr=127.0.0.1", "--master-port=29533",
+           os.path.join(ROOT, "tests", "dist_snapshot_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    print(r.stdout[-3000:], r.stderr[-3000:])
+    assert r.returncode == 0
+    assert "DIST PARITY OK" in r.stdout

@@ -1,0 +1,82 @@
+// Raw FNV-1a throughput ceiling on B200: data synthesized in registers (no
+// memory traffic), CH independent chains per thread, several step variants.
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ void stepA(uint32_t& lo, uint32_t& hi, uint32_t b) {
+  const uint32_t x = lo ^ (b & 0xffu);
+  const uint64_t t = (uint64_t)x * 0x1b3u;
+  uint32_t y;
+  asm("{\n\t.reg .u32 s;\n\tshl.b32 s, %1, 8;\n\tadd.u32 %0, s, %2;\n\t}" : "=r"(y) : "r"(x), "r"((uint32_t)(t >> 32)));
+  hi = hi * 0x1b3u + y;
+  lo = (uint32_t)t;
+}
+// lo via IMAD.LO and carry via IMAD.HI (no IMAD.WIDE)
+__device__ __forceinline__ void stepB(uint32_t& lo, uint32_t& hi, uint32_t b) {
+  const uint32_t x = lo ^ (b & 0xffu);
+  uint32_t y;
+  asm("mad.hi.u32 %0, %1, 435, %2;" : "=r"(y) : "r"(x), "r"(x << 8));
+  hi = hi * 0x1b3u + y;
+  lo = x * 0x1b3u;
+}
+// 64-bit mul by the full prime (compiler's own lowering)
+__device__ __forceinline__ void stepC(uint32_t& lo, uint32_t& hi, uint32_t b) {
+  uint64_t h = ((uint64_t)hi << 32) | lo;
+  h ^= (b & 0xff);
+  h *= 1099511628211ull;
+  lo = (uint32_t)h; hi = (uint32_t)(h >> 32);
+}
+
+template <int V, int CH>
+__global__ void __launch_bounds__(512) k(uint64_t* out, int iters) {
+  uint32_t lo[CH], hi[CH];
+  for (int c = 0; c < CH; ++c) { lo[c] = 0x84222325u + c; hi[c] = 0xcbf29ce4u; }
+  uint32_t w = threadIdx.x * 2654435761u;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      w = w * 1664525u + 1013904223u;  // one LCG per 4 words x CH chains
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        uint32_t ww = w ^ c;
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) {
+          if (V == 0) stepA(lo[c], hi[c], ww >> (8 * bb));
+          if (V == 1) stepB(lo[c], hi[c], ww >> (8 * bb));
+          if (V == 2) stepC(lo[c], hi[c], ww >> (8 * bb));
+        }
+      }
+    }
+  }
+  uint64_t r = 0;
+  for (int c = 0; c < CH; ++c) r ^= ((uint64_t)hi[c] << 32) | lo[c];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = r;
+}
+
+template <int V, int CH>
+void run(const char* name, int threads, int blocksPerSM) {
+  uint64_t* d;
+  cudaMalloc(&d, 148 * 4 * 1024 * 8);
+  int iters = 2048;
+  int blocks = 148 * blocksPerSM;
+  k<V, CH><<<blocks, threads>>>(d, 16);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a); cudaEventCreate(&b);
+  cudaEventRecord(a);
+  k<V, CH><<<blocks, threads>>>(d, iters);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms; cudaEventElapsedTime(&ms, a, b);
+  double bytes = double(blocks) * threads * CH * iters * 16.0;
+  printf("%-8s CH=%d threads/SM=%4d : %8.1f GB/s-equivalent\n", name, CH, threads * blocksPerSM,
+         bytes / ms / 1e6);
+  cudaFree(d);
+}
+
+int main() {
+  run<0, 1>("A", 512, 1); run<0, 2>("A", 512, 1); run<0, 4>("A", 256, 1); run<0, 1>("A", 1024, 1); run<0, 2>("A", 1024, 1);
+  run<1, 1>("B-hi", 512, 1); run<1, 2>("B-hi", 512, 1); run<1, 2>("B-hi", 1024, 1);
+  run<2, 1>("C-64", 512, 1); run<2, 2>("C-64", 512, 1); run<2, 2>("C-64", 1024, 1);
+  return 0;
+}
