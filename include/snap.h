@@ -96,6 +96,26 @@ int snap_sync(snap_ctx* ctx);
 int snap_layout_carve(uint64_t mem_bytes, uint64_t max_buffer_bytes, double slack_fraction,
                       uint64_t out[3]);
 
+/* ------------------------------------------- device-proxy memory tracker */
+
+/* mem::BidiAllocator (alloc.hpp:17-62, alloc.cpp:62-155): stable requests
+ * top-down, transient bottom-up over [low, high), 256-byte rounding, free
+ * lists with coalescing. Host metadata only; one tracker per rank over the
+ * ctx rank region (proxy.cpp:100-108).
+ * snap_alloc_alloc: SNAP_OK, SNAP_ENOMEM (cursors would cross = nullopt),
+ * SNAP_EFAULT (zero size). snap_alloc_free: SNAP_EFAULT for an unknown
+ * address (SimFault, alloc.cpp:88). Snapshot = u64 words, exact state
+ * (BidiAllocator::snapshot/restore, alloc.cpp:116-140). */
+int snap_alloc_create(uint64_t low, uint64_t high, void** out);
+int snap_alloc_destroy(void* a);
+int snap_alloc_alloc(void* a, uint64_t bytes, int stable, uint64_t* addr);
+int snap_alloc_free(void* a, uint64_t addr);
+uint64_t snap_alloc_stable_digest(void* a);
+int snap_alloc_cursors(void* a, uint64_t* transient_cursor, uint64_t* stable_cursor,
+                       uint64_t* live_bytes);
+int snap_alloc_snapshot(void* a, uint64_t* words, uint64_t cap, uint64_t* n);
+int snap_alloc_restore(void* a, const uint64_t* words, uint64_t n);
+
 /* Pinned host memory for staging images / host-side inputs (page-locked so
  * H2D/D2H run at PCIe DMA speed). */
 int snap_host_alloc(uint64_t bytes, void** out);

@@ -98,6 +98,16 @@ _SIGS = {
     "snap_prof_enable": (C.c_int, [C.c_void_p, C.c_int]),
     "snap_prof_read": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_float),
                                  C.POINTER(C.c_uint64)]),
+    "snap_alloc_create": (C.c_int, [C.c_uint64, C.c_uint64, C.POINTER(C.c_void_p)]),
+    "snap_alloc_destroy": (C.c_int, [C.c_void_p]),
+    "snap_alloc_alloc": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int, C.POINTER(C.c_uint64)]),
+    "snap_alloc_free": (C.c_int, [C.c_void_p, C.c_uint64]),
+    "snap_alloc_stable_digest": (C.c_uint64, [C.c_void_p]),
+    "snap_alloc_cursors": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                     C.POINTER(C.c_uint64)]),
+    "snap_alloc_snapshot": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64,
+                                      C.POINTER(C.c_uint64)]),
+    "snap_alloc_restore": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
     "snap_timer_start": (C.c_int, [C.c_void_p]),
     "snap_timer_stop": (C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
 }
@@ -150,6 +160,71 @@ def layout_carve(mem_bytes, max_buffer_bytes, slack_fraction):
 
 
 PROF_HASH, PROF_SELECT, PROF_COMPACT, PROF_RESTORE, PROF_GRAD, PROF_EXCHANGE = range(6)
+
+
+class BidiAllocator:
+    """mem::BidiAllocator (alloc.hpp:17-62): same method names and error behaviour —
+    alloc() returns None on OOM (std::nullopt) and raises SnapFault on a zero size,
+    free() raises SnapFault on an unknown address."""
+
+    STABLE, TRANSIENT = 1, 0
+
+    def __init__(self, low: int, high: int):
+        self._L = lib()
+        h = C.c_void_p()
+        rc = self._L.snap_alloc_create(low, high, C.byref(h))
+        if rc != SNAP_OK:
+            raise SnapError(rc, "allocator region must be aligned and non-empty")
+        self.h = h
+
+    def __del__(self):
+        try:
+            if self.h:
+                self._L.snap_alloc_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def alloc(self, nbytes: int, stable: bool):
+        a = C.c_uint64()
+        rc = self._L.snap_alloc_alloc(self.h, nbytes, 1 if stable else 0, C.byref(a))
+        if rc == SNAP_ENOMEM:
+            return None
+        if rc == SNAP_EFAULT:
+            raise SnapFault(rc, "alloc: zero size")
+        if rc != SNAP_OK:
+            raise SnapError(rc, "alloc")
+        return a.value
+
+    def free(self, addr: int):
+        rc = self._L.snap_alloc_free(self.h, addr)
+        if rc == SNAP_EFAULT:
+            raise SnapFault(rc, "free: unknown allocation")
+        if rc != SNAP_OK:
+            raise SnapError(rc, "free")
+
+    def stable_state_digest(self) -> int:
+        return int(self._L.snap_alloc_stable_digest(self.h))
+
+    def cursors(self):
+        t, s, l = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        self._L.snap_alloc_cursors(self.h, C.byref(t), C.byref(s), C.byref(l))
+        return t.value, s.value, l.value
+
+    def snapshot(self) -> np.ndarray:
+        n = C.c_uint64()
+        self._L.snap_alloc_snapshot(self.h, None, 0, C.byref(n))
+        w = np.zeros(max(n.value, 1), np.uint64)
+        rc = self._L.snap_alloc_snapshot(self.h, _p(w), w.size, C.byref(n))
+        if rc != SNAP_OK:
+            raise SnapError(rc, "snapshot")
+        return w[: n.value]
+
+    def restore(self, words: np.ndarray):
+        w = np.ascontiguousarray(words, dtype=np.uint64)
+        rc = self._L.snap_alloc_restore(self.h, _p(w), w.size)
+        if rc != SNAP_OK:
+            raise SnapError(rc, "restore: malformed snapshot")
 
 
 class PinnedHost:
