@@ -67,6 +67,9 @@ typedef struct {
  * to predict the staging layout of the fused hash+compaction pass. */
 #define SNAP_BUF_REPLICATED 1u
 #define SNAP_BUF_PRIVATE 2u
+/* RankBuf::pending_result (splice.hpp:33): a gradient whose collective result
+ * is pending; skipped by splice switches (consumed by K5 accumulation). */
+#define SNAP_BUF_PENDING 4u
 
 /* Chunk grid: page digest = digest_of_words(page) (sim.hpp:67-70 on the
  * reference's 4 KiB page unit, ckpt.hpp:15); chunk digest = digest_of_words
@@ -213,6 +216,25 @@ int snap_restore_self(snap_ctx* ctx, int verify);
  * With accumulate != 0, dst is the first addend. Async. */
 int snap_grad_sum(snap_ctx* ctx, int dtype, const uint64_t* src_addrs, uint32_t nsrc,
                   uint64_t dst_addr, uint64_t elems, int accumulate);
+
+/* ------------------------------------------------- replica splicing */
+
+/* Context switch between time-sliced ranks sharing this GPU
+ * (GpuLedger::plan_switch + execute_switch, splice.cpp:167-306, called by
+ * JobRuntime::switch_to, job.cpp:146-198). The reference's host cache becomes a
+ * digest-indexed chunk cache of `cache_bytes` in HBM. */
+typedef struct {
+  uint64_t hashed_bytes;   /* live bytes of the outgoing rank digested (K1) */
+  uint64_t swap_out_bytes; /* bytes newly saved to the chunk cache (K3) */
+  uint64_t swap_in_bytes;  /* bytes restored from the chunk cache (K4) */
+  uint64_t resident_bytes; /* incoming bytes already in place (same range, same digest) */
+  uint64_t cache_bytes;    /* chunk cache occupancy after the switch */
+} snap_switch_stats;
+int snap_splice_init(snap_ctx* ctx, uint64_t cache_bytes);
+int snap_splice_set_rank(snap_ctx* ctx, int rank, const snap_buf* bufs, uint64_t n,
+                         const snap_geom* geom);
+int snap_splice_switch(snap_ctx* ctx, int from, int to, snap_switch_stats* stats);
+int snap_splice_recorded(snap_ctx* ctx, int rank, uint64_t* digests, uint64_t* n);
 
 /* ------------------------------------------------ multi-GPU (NCCL/NVLink) */
 

@@ -116,6 +116,16 @@ def ref():
         L.ref_restore_chunks.restype = C.c_int
         L.ref_restore_chunks.argtypes = [C.c_void_p, C.c_uint64, C.c_uint32, C.c_int, C.c_void_p]
         L.ref_grad_sum_u64.argtypes = [C.c_void_p, C.c_uint32, C.c_uint64, C.c_void_p, C.c_int]
+        L.ref_splice_new.restype = C.c_void_p
+        L.ref_splice_new.argtypes = [C.c_uint64, C.c_uint64]
+        L.ref_splice_free.argtypes = [C.c_void_p]
+        L.ref_splice_alloc.restype = C.c_int
+        L.ref_splice_alloc.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_uint64, C.c_uint64,
+                                       C.c_int, C.c_int]
+        L.ref_splice_write.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64]
+        L.ref_splice_read.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64]
+        L.ref_splice_switch.restype = C.c_int
+        L.ref_splice_switch.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p]
         _ref = L
     return _ref
 

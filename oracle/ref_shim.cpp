@@ -179,4 +179,71 @@ void ref_grad_sum_u64(const uint64_t* const* g, uint32_t nranks, uint64_t n, uin
   for (auto& x : th) x.join();
 }
 
+// ---- splice::GpuLedger + vdev::Gpu (splice.cpp:150-354, vdev.cpp:72-124) ----
+// Scripted driver for the splice parity test. Before every plan the outgoing
+// rank's digests are refreshed (refresh_digests also updates the ledger
+// entries), which is the one-line fix of SURVEY App. A-1 (stale Entry::digest).
+struct RefSplice {
+  std::unique_ptr<vdev::Gpu> gpu;
+  std::unique_ptr<splice::GpuLedger> led;
+};
+
+void* ref_splice_new(uint64_t mem_bytes, uint64_t max_buf) {
+  auto* s = new RefSplice();
+  s->gpu = std::make_unique<vdev::Gpu>(0, mem_bytes);
+  s->led = std::make_unique<splice::GpuLedger>(*s->gpu,
+                                               splice::DeviceLayout::carve(mem_bytes, max_buf, 0.0));
+  return s;
+}
+void ref_splice_free(void* s) { delete static_cast<RefSplice*>(s); }
+
+// the active rank allocates a buffer (worker.cpp:145-148): ledger + registry
+int ref_splice_alloc(void* p, int rank, int slot, uint64_t addr, uint64_t bytes, int cat,
+                     int pending) {
+  auto* s = static_cast<RefSplice*>(p);
+  try {
+    s->led->on_alloc(rank, slot, addr, bytes, static_cast<vdev::BufCat>(cat));
+    s->gpu->register_buffer({addr, bytes}, static_cast<vdev::BufCat>(cat));
+    if (pending) s->led->mark_pending_result(rank, slot);
+    return 0;
+  } catch (const SimFault&) {
+    return -1;
+  } catch (const InternalError&) {
+    return -2;
+  }
+}
+
+int ref_splice_write(void* p, uint64_t addr, const uint64_t* words, uint64_t n) {
+  auto* s = static_cast<RefSplice*>(p);
+  s->gpu->write_words({addr, n * 8}, std::span<const u64>(words, n));
+  return 0;
+}
+
+int ref_splice_read(void* p, uint64_t addr, uint64_t* words, uint64_t n) {
+  auto* s = static_cast<RefSplice*>(p);
+  auto sp = s->gpu->words({addr, n * 8});
+  std::memcpy(words, sp.data(), n * 8);
+  return 0;
+}
+
+// out = {swap_out_bytes, swap_in_bytes, d2d_bytes, moves, host_cache_bytes}
+int ref_splice_switch(void* p, int from, int to, uint64_t* out) {
+  auto* s = static_cast<RefSplice*>(p);
+  try {
+    if (from >= 0) s->led->refresh_digests(from);
+    auto plan = s->led->plan_switch(from < 0 ? kNoRank : from, to < 0 ? kNoRank : to);
+    s->led->execute_switch(from < 0 ? kNoRank : from, to < 0 ? kNoRank : to, plan);
+    out[0] = plan.swap_out_bytes;
+    out[1] = plan.swap_in_bytes;
+    out[2] = plan.d2d_bytes;
+    out[3] = plan.moves.size();
+    out[4] = s->led->host_cache_bytes();
+    return 0;
+  } catch (const SimFault&) {
+    return -1;
+  } catch (const InternalError&) {
+    return -2;
+  }
+}
+
 }  // extern "C"

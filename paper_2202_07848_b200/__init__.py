@@ -46,6 +46,20 @@ class SnapBuf(C.Structure):
     ]
 
 
+class SwitchStats(C.Structure):
+    """snap_switch_stats: the switch_report trace fields (job.cpp:181-195)."""
+
+    _fields_ = [("hashed_bytes", C.c_uint64), ("swap_out_bytes", C.c_uint64),
+                ("swap_in_bytes", C.c_uint64), ("resident_bytes", C.c_uint64),
+                ("cache_bytes", C.c_uint64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+BUF_REPLICATED, BUF_PRIVATE, BUF_PENDING = 1, 2, 4
+
+
 class SnapGeom(C.Structure):
     _fields_ = [("page_bytes", C.c_uint32), ("chunk_bytes", C.c_uint32)]
 
@@ -108,6 +122,10 @@ _SIGS = {
     "snap_alloc_snapshot": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64,
                                       C.POINTER(C.c_uint64)]),
     "snap_alloc_restore": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
+    "snap_splice_init": (C.c_int, [C.c_void_p, C.c_uint64]),
+    "snap_splice_set_rank": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_uint64, C.c_void_p]),
+    "snap_splice_switch": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
+    "snap_splice_recorded": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.POINTER(C.c_uint64)]),
     "snap_timer_start": (C.c_int, [C.c_void_p]),
     "snap_timer_stop": (C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
 }
@@ -443,6 +461,24 @@ class Ctx:
 
     def restore_self(self, verify=True):
         self._ck(self._L.snap_restore_self(self.h, 1 if verify else 0), "snap_restore_self")
+
+    # -- splice (GpuLedger::plan_switch/execute_switch)
+    def splice_init(self, cache_bytes: int):
+        self._ck(self._L.snap_splice_init(self.h, cache_bytes), "snap_splice_init")
+
+    def splice_set_rank(self, rank: int, bufs, page_bytes=4096, chunk_bytes=65536):
+        arr = bufs_array([b[:5] for b in bufs])
+        for i, b in enumerate(bufs):
+            if len(b) > 5:
+                arr[i].flags = b[5]
+        g = SnapGeom(page_bytes, chunk_bytes)
+        self._ck(self._L.snap_splice_set_rank(self.h, rank, arr, len(bufs), C.byref(g)),
+                 "snap_splice_set_rank")
+
+    def splice_switch(self, frm: int, to: int) -> dict:
+        st = SwitchStats()
+        self._ck(self._L.snap_splice_switch(self.h, frm, to, C.byref(st)), "snap_splice_switch")
+        return st.as_dict()
 
     # -- K5
     def grad_sum(self, dtype, src_addrs, dst_addr, elems, accumulate=False):

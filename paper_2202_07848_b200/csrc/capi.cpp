@@ -3,203 +3,11 @@
 // (vdev.hpp:65-122). Host code only; every byte of device work is one of the
 // sm_100a kernels in k_*.cu, issued on the ctx stream (NCCL collectives on the
 // same stream for the cross-rank exchange).
-#include <cuda_runtime.h>
-#include <nccl.h>
+#include "ctx.h"
 
-#include <algorithm>
-#include <cstdio>
-#include <cstring>
-#include <string>
-#include <vector>
-
-#include "snap_internal.h"
-
-using snap::GridDev;
-using snap::TableDev;
+void splice_release(snap_ctx* ctx);
 
 namespace {
-
-struct DevMem {
-  void* p = nullptr;
-  size_t cap = 0;
-};
-
-// Per-kernel-class CUDA event pairs, recorded on the ctx stream when enabled
-// (bench.py reads the live duration of the dominant kernel from these).
-struct Prof {
-  bool on = false;
-  std::vector<cudaEvent_t> pool;
-  size_t used = 0;
-  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
-};
-
-}  // namespace
-
-struct snap_ctx {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  uint8_t* arena = nullptr;
-  uint64_t arena_bytes = 0;
-  std::string err;
-  uint64_t launches = 0;
-
-  // installed grid
-  std::vector<snap_buf> bufs;
-  snap_geom geom{4096, 65536};
-  uint64_t nchunks = 0;
-  uint64_t grid_bytes = 0;
-  std::vector<uint64_t> h_cstart;
-  std::vector<uint32_t> h_lens;
-  DevMem d_addr, d_bytes, d_cstart, d_lens, d_dig, d_bufdig;
-  GridDev grid;
-  bool hashed = false;
-
-  // dedup table (per snapshot) and known set (store index)
-  DevMem dd_keys, dd_vals, dd_slot;
-  uint64_t dd_mask = 0;
-  DevMem kn_keys, kn_vals, kn_list;
-  uint64_t kn_mask = 0, kn_count = 0;
-
-  // selection over the (local or global) canonical chunk vector
-  DevMem scan, sel, owner, offsets, sel_list, totals;
-  uint64_t sel_n = 0;  // entries of the selection vectors (nchunks, or nranks * maxn)
-  bool selected = false;
-  DevMem staging;
-  uint64_t staging_valid = 0;
-  // speculative layout for the fused hash+compaction pass (double-buffered:
-  // the gather/fix-up writes the actual layout as the next prediction)
-  DevMem d_spec[2];
-  int spec_cur = 0;
-  bool spec_ready = false;
-  bool spec_used = false;
-
-  // cross-rank exchange (NCCL allgather of digest vectors) and striping
-  ncclComm_t comm = nullptr;
-  int nranks = 1, rank = 0;
-  bool exchanged = false;
-  uint64_t maxn = 0;
-  std::vector<uint64_t> counts;
-  bool glens_valid = false;
-  DevMem d_counts, d_gdig, d_glens, d_writer, d_shard_off, d_my_list, d_my_off, d_my_totals;
-
-  // verify / restore scratch
-  DevMem d_dig2, d_expect, d_nbad, d_srcoff;
-
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  Prof prof;
-};
-
-namespace {
-
-int fail(snap_ctx* c, int code, const std::string& msg) {
-  if (c) c->err = msg;
-  return code;
-}
-
-#define CK(call)                                                                        \
-  do {                                                                                  \
-    cudaError_t e_ = (call);                                                            \
-    if (e_ != cudaSuccess)                                                              \
-      return fail(ctx, SNAP_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
-  } while (0)
-
-#define CKN(call)                                                                        \
-  do {                                                                                   \
-    ncclResult_t r_ = (call);                                                            \
-    if (r_ != ncclSuccess)                                                               \
-      return fail(ctx, SNAP_ECUDA, std::string(#call) + ": " + ncclGetErrorString(r_)); \
-  } while (0)
-
-// Counts kernels of the last launcher call and checks launch-configuration errors.
-#define CKL(n)                                                                               \
-  do {                                                                                       \
-    ctx->launches += (n);                                                                    \
-    cudaError_t e_ = cudaGetLastError();                                                     \
-    if (e_ != cudaSuccess)                                                                   \
-      return fail(ctx, SNAP_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
-  } while (0)
-
-#define RC(x)             \
-  do {                    \
-    int rc_ = (x);        \
-    if (rc_) return rc_;  \
-  } while (0)
-
-template <typename T>
-int ensure(snap_ctx* ctx, DevMem& m, size_t count, T** out) {
-  size_t bytes = std::max<size_t>(count * sizeof(T), 256);
-  if (bytes > m.cap) {
-    if (m.p) {
-      cudaStreamSynchronize(ctx->stream);
-      cudaFree(m.p);
-      m.p = nullptr;
-      m.cap = 0;
-    }
-    cudaError_t e = cudaMalloc(&m.p, bytes);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      return fail(ctx, e == cudaErrorMemoryAllocation ? SNAP_ENOMEM : SNAP_ECUDA,
-                  std::string("cudaMalloc: ") + cudaGetErrorString(e));
-    }
-    m.cap = bytes;
-  }
-  *out = static_cast<T*>(m.p);
-  return SNAP_OK;
-}
-
-// Like ensure(), but keeps the first `keep` bytes when it has to grow.
-template <typename T>
-int ensure_keep(snap_ctx* ctx, DevMem& m, size_t count, size_t keep, T** out) {
-  size_t bytes = std::max<size_t>(count * sizeof(T), 256);
-  if (bytes > m.cap) {
-    bytes = std::max(bytes, 2 * m.cap);
-    void* p = nullptr;
-    cudaError_t e = cudaMalloc(&p, bytes);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      return fail(ctx, e == cudaErrorMemoryAllocation ? SNAP_ENOMEM : SNAP_ECUDA,
-                  std::string("cudaMalloc: ") + cudaGetErrorString(e));
-    }
-    if (m.p) {
-      if (keep) cudaMemcpyAsync(p, m.p, keep, cudaMemcpyDeviceToDevice, ctx->stream);
-      cudaStreamSynchronize(ctx->stream);
-      cudaFree(m.p);
-    }
-    m.p = p;
-    m.cap = bytes;
-  }
-  *out = static_cast<T*>(m.p);
-  return SNAP_OK;
-}
-
-template <typename T>
-T* P(DevMem& m) {
-  return static_cast<T*>(m.p);
-}
-
-void release(DevMem& m) {
-  if (m.p) cudaFree(m.p);
-  m.p = nullptr;
-  m.cap = 0;
-}
-
-bool pow2(uint64_t x) { return x && !(x & (x - 1)); }
-uint32_t log2u(uint64_t x) {
-  uint32_t s = 0;
-  while ((1ull << s) < x) ++s;
-  return s;
-}
-uint64_t table_cap(uint64_t n) {
-  uint64_t c = 1024;
-  while (c < 2 * n) c <<= 1;
-  return c;
-}
-
-int check_range(snap_ctx* ctx, uint64_t addr, uint64_t bytes) {
-  if (addr > ctx->arena_bytes || bytes > ctx->arena_bytes - addr)
-    return fail(ctx, SNAP_EINVAL, "range outside the arena");
-  return SNAP_OK;
-}
 
 // ---- profiler ----
 enum { kProfHash = 0, kProfSelect, kProfCompact, kProfRestore, kProfGrad, kProfExchange, kProfN };
@@ -264,8 +72,12 @@ int known_insert_dev(snap_ctx* ctx, const uint64_t* dev_digests, uint64_t n) {
   return SNAP_OK;
 }
 
-// Selection over a canonical vector (local grid or allgathered global one).
-int select_impl(snap_ctx* ctx, const uint64_t* dig, const uint32_t* lens, uint64_t n) {
+}  // namespace
+
+// Selection over a canonical vector against an explicit known table (the
+// splice chunk cache uses its own index as the known set).
+int select_with_known(snap_ctx* ctx, const uint64_t* dig, const uint32_t* lens, uint64_t n,
+                      TableDev kn, bool use_known) {
   const uint64_t cap = table_cap(n);
   unsigned long long *k, *v;
   uint64_t *slot, *scan, *owner, *offsets, *totals;
@@ -282,12 +94,20 @@ int select_impl(snap_ctx* ctx, const uint64_t* dig, const uint32_t* lens, uint64
   RC(ensure(ctx, ctx->totals, 4, &totals));
   ctx->dd_mask = cap - 1;
   TableDev dd{k, v, ctx->dd_mask};
-  TableDev kn{P<unsigned long long>(ctx->kn_keys), P<unsigned long long>(ctx->kn_vals), ctx->kn_mask};
   CKL(snap::launch_table_clear(dd, ctx->stream));
-  CKL(snap::launch_dedup_insert(dd, kn, ctx->kn_count > 0, dig, lens, n, slot, ctx->stream));
+  CKL(snap::launch_dedup_insert(dd, kn, use_known, dig, lens, n, slot, ctx->stream));
   CKL(snap::launch_select(dd, slot, lens, n, scan, sel, owner, offsets, list, totals, ctx->stream));
   CKL(snap::launch_resolve_dups(sel, owner, offsets, n, ctx->stream));
   ctx->sel_n = n;
+  return SNAP_OK;
+}
+
+namespace {
+
+// Selection over a canonical vector (local grid or allgathered global one).
+int select_impl(snap_ctx* ctx, const uint64_t* dig, const uint32_t* lens, uint64_t n) {
+  TableDev kn{P<unsigned long long>(ctx->kn_keys), P<unsigned long long>(ctx->kn_vals), ctx->kn_mask};
+  RC(select_with_known(ctx, dig, lens, n, kn, ctx->kn_count > 0));
   ctx->selected = true;
   return SNAP_OK;
 }
@@ -501,6 +321,7 @@ int snap_close(snap_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
+  splice_release(ctx);
   for (DevMem* m :
        {&ctx->d_addr, &ctx->d_bytes, &ctx->d_cstart, &ctx->d_lens, &ctx->d_dig, &ctx->d_bufdig,
         &ctx->dd_keys, &ctx->dd_vals, &ctx->dd_slot, &ctx->kn_keys, &ctx->kn_vals, &ctx->kn_list,

@@ -1,0 +1,203 @@
+// ctx.h — the snap_ctx definition and host helpers shared by the C-ABI
+// translation units (capi.cpp, splice_host.cpp).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "snap_internal.h"
+
+using snap::GridDev;
+using snap::TableDev;
+
+struct SpliceState;
+
+struct DevMem {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
+// Per-kernel-class CUDA event pairs, recorded on the ctx stream when enabled
+// (bench.py reads the live duration of the dominant kernel from these).
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
+};
+
+struct snap_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint8_t* arena = nullptr;
+  uint64_t arena_bytes = 0;
+  std::string err;
+  uint64_t launches = 0;
+
+  // installed grid
+  std::vector<snap_buf> bufs;
+  snap_geom geom{4096, 65536};
+  uint64_t nchunks = 0;
+  uint64_t grid_bytes = 0;
+  std::vector<uint64_t> h_cstart;
+  std::vector<uint32_t> h_lens;
+  DevMem d_addr, d_bytes, d_cstart, d_lens, d_dig, d_bufdig;
+  GridDev grid;
+  bool hashed = false;
+
+  // dedup table (per snapshot) and known set (store index)
+  DevMem dd_keys, dd_vals, dd_slot;
+  uint64_t dd_mask = 0;
+  DevMem kn_keys, kn_vals, kn_list;
+  uint64_t kn_mask = 0, kn_count = 0;
+
+  // selection over the (local or global) canonical chunk vector
+  DevMem scan, sel, owner, offsets, sel_list, totals;
+  uint64_t sel_n = 0;  // entries of the selection vectors (nchunks, or nranks * maxn)
+  bool selected = false;
+  DevMem staging;
+  uint64_t staging_valid = 0;
+  // speculative layout for the fused hash+compaction pass (double-buffered:
+  // the gather/fix-up writes the actual layout as the next prediction)
+  DevMem d_spec[2];
+  int spec_cur = 0;
+  bool spec_ready = false;
+  bool spec_used = false;
+
+  // cross-rank exchange (NCCL allgather of digest vectors) and striping
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  bool exchanged = false;
+  uint64_t maxn = 0;
+  std::vector<uint64_t> counts;
+  bool glens_valid = false;
+  DevMem d_counts, d_gdig, d_glens, d_writer, d_shard_off, d_my_list, d_my_off, d_my_totals;
+
+  // verify / restore scratch
+  DevMem d_dig2, d_expect, d_nbad, d_srcoff;
+
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  Prof prof;
+  SpliceState* splice = nullptr;
+};
+
+inline int fail(snap_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(ctx, SNAP_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define CKN(call)                                                                        \
+  do {                                                                                   \
+    ncclResult_t r_ = (call);                                                            \
+    if (r_ != ncclSuccess)                                                               \
+      return fail(ctx, SNAP_ECUDA, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+// Counts kernels of the last launcher call and checks launch-configuration errors.
+#define CKL(n)                                                                               \
+  do {                                                                                       \
+    ctx->launches += (n);                                                                    \
+    cudaError_t e_ = cudaGetLastError();                                                     \
+    if (e_ != cudaSuccess)                                                                   \
+      return fail(ctx, SNAP_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define RC(x)             \
+  do {                    \
+    int rc_ = (x);        \
+    if (rc_) return rc_;  \
+  } while (0)
+
+template <typename T>
+inline int ensure(snap_ctx* ctx, DevMem& m, size_t count, T** out) {
+  size_t bytes = std::max<size_t>(count * sizeof(T), 256);
+  if (bytes > m.cap) {
+    if (m.p) {
+      cudaStreamSynchronize(ctx->stream);
+      cudaFree(m.p);
+      m.p = nullptr;
+      m.cap = 0;
+    }
+    cudaError_t e = cudaMalloc(&m.p, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(ctx, e == cudaErrorMemoryAllocation ? SNAP_ENOMEM : SNAP_ECUDA,
+                  std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    m.cap = bytes;
+  }
+  *out = static_cast<T*>(m.p);
+  return SNAP_OK;
+}
+
+// Like ensure(), but keeps the first `keep` bytes when it has to grow.
+template <typename T>
+inline int ensure_keep(snap_ctx* ctx, DevMem& m, size_t count, size_t keep, T** out) {
+  size_t bytes = std::max<size_t>(count * sizeof(T), 256);
+  if (bytes > m.cap) {
+    bytes = std::max(bytes, 2 * m.cap);
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(ctx, e == cudaErrorMemoryAllocation ? SNAP_ENOMEM : SNAP_ECUDA,
+                  std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    if (m.p) {
+      if (keep) cudaMemcpyAsync(p, m.p, keep, cudaMemcpyDeviceToDevice, ctx->stream);
+      cudaStreamSynchronize(ctx->stream);
+      cudaFree(m.p);
+    }
+    m.p = p;
+    m.cap = bytes;
+  }
+  *out = static_cast<T*>(m.p);
+  return SNAP_OK;
+}
+
+template <typename T>
+inline T* P(DevMem& m) {
+  return static_cast<T*>(m.p);
+}
+
+inline void release(DevMem& m) {
+  if (m.p) cudaFree(m.p);
+  m.p = nullptr;
+  m.cap = 0;
+}
+
+inline bool pow2(uint64_t x) { return x && !(x & (x - 1)); }
+inline uint32_t log2u(uint64_t x) {
+  uint32_t s = 0;
+  while ((1ull << s) < x) ++s;
+  return s;
+}
+inline uint64_t table_cap(uint64_t n) {
+  uint64_t c = 1024;
+  while (c < 2 * n) c <<= 1;
+  return c;
+}
+
+int select_with_known(snap_ctx* ctx, const uint64_t* dig, const uint32_t* lens, uint64_t n,
+                      TableDev kn, bool use_known);
+
+inline int check_range(snap_ctx* ctx, uint64_t addr, uint64_t bytes) {
+  if (addr > ctx->arena_bytes || bytes > ctx->arena_bytes - addr)
+    return fail(ctx, SNAP_EINVAL, "range outside the arena");
+  return SNAP_OK;
+}
+

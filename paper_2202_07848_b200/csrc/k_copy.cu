@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include "snap_internal.h"
+#include "table.cuh"
 
 namespace snap {
 namespace {
@@ -100,6 +101,61 @@ __global__ void k_compare(const uint64_t* __restrict__ a, const uint64_t* __rest
   if ((threadIdx.x & 31) == 0 && bad) atomicAdd(nbad, bad);
 }
 
+// Splice swap-out bookkeeping: index the chunks just gathered into the chunk
+// cache (digest -> cache offset), the B200 replacement of host_cache_put's
+// digest-keyed std::map (splice.cpp:79-82).
+__global__ void k_cache_insert(TableDev cache, const uint64_t* __restrict__ dig,
+                               const uint32_t* __restrict__ sel_list,
+                               const uint64_t* __restrict__ totals,
+                               const uint64_t* __restrict__ offsets, uint64_t base) {
+  const uint64_t n = totals[0];
+  for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
+       k += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t g = sel_list[k];
+    const uint64_t s = table_find_or_insert(cache, dig[g]);
+    cache.vals[s] = base + offsets[g];
+  }
+}
+
+// Splice swap-in (plan_switch swap-in phase + execute_switch, splice.cpp:186-226,
+// 293-303, with the stale-digest fix of SURVEY App. A-1): chunk g of the
+// incoming rank is already resident when the outgoing rank's fresh digest of
+// the same address range equals the incoming rank's recorded digest;
+// otherwise its bytes come from the device chunk cache by digest. A digest
+// missing from the cache is counted (content lost -> SimFault on the host).
+__global__ void __launch_bounds__(kThreads)
+k_splice_in(uint8_t* __restrict__ arena, GridDev to, const uint32_t* __restrict__ lens,
+            const uint64_t* __restrict__ want, const int64_t* __restrict__ match,
+            const uint64_t* __restrict__ dig_from, TableDev cache,
+            const uint8_t* __restrict__ cache_base, unsigned long long* __restrict__ counters) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t w0 = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * kThreads) >> 5;
+  unsigned long long swapped = 0, resident = 0, missing = 0;
+  for (uint64_t g = w0; g < to.nchunks; g += nw) {
+    const uint64_t d = want[g];
+    const uint32_t len = lens[g];
+    const int64_t m = match ? match[g] : -1;
+    if (m >= 0 && dig_from[m] == d) {
+      resident += len;
+      continue;
+    }
+    const uint64_t s = table_find(cache, d);
+    if (s == ~0ull) {
+      missing += 1;
+      continue;
+    }
+    uint8_t* dst = const_cast<uint8_t*>(chunk_ptr(arena, to, g));
+    warp_copy(dst, cache_base + cache.vals[s], len, lane);
+    swapped += len;
+  }
+  if (lane == 0) {
+    if (swapped) atomicAdd(counters + 0, swapped);
+    if (resident) atomicAdd(counters + 1, resident);
+    if (missing) atomicAdd(counters + 2, missing);
+  }
+}
+
 unsigned copy_grid() {
   static int n = 0;
   if (n == 0) {
@@ -132,6 +188,28 @@ int launch_scatter(uint8_t* arena, const GridDev& g, const uint32_t* lens, const
   uint64_t blocks = (g.nchunks * 32 + kThreads - 1) / kThreads;
   if (blocks > copy_grid()) blocks = copy_grid();
   k_scatter<<<unsigned(blocks), kThreads, 0, s>>>(arena, g, lens, image, src_off);
+  return 1;
+}
+
+int launch_cache_insert(TableDev cache, const uint64_t* dig, const uint32_t* sel_list,
+                        const uint64_t* totals, const uint64_t* offsets, uint64_t base,
+                        uint64_t max_n, cudaStream_t s) {
+  if (max_n == 0) return 0;
+  uint64_t blocks = (max_n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_cache_insert<<<unsigned(blocks), 256, 0, s>>>(cache, dig, sel_list, totals, offsets, base);
+  return 1;
+}
+
+int launch_splice_in(uint8_t* arena, const GridDev& to, const uint32_t* lens, const uint64_t* want,
+                     const int64_t* match, const uint64_t* dig_from, TableDev cache,
+                     const uint8_t* cache_base, unsigned long long* counters, cudaStream_t s) {
+  cudaMemsetAsync(counters, 0, 3 * sizeof(unsigned long long), s);
+  if (to.nchunks == 0) return 0;
+  uint64_t blocks = (to.nchunks * 32 + kThreads - 1) / kThreads;
+  if (blocks > copy_grid()) blocks = copy_grid();
+  k_splice_in<<<unsigned(blocks), kThreads, 0, s>>>(arena, to, lens, want, match, dig_from, cache,
+                                                    cache_base, counters);
   return 1;
 }
 

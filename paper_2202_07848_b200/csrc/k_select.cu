@@ -20,38 +20,10 @@
 #include <cuda_runtime.h>
 
 #include "snap_internal.h"
+#include "table.cuh"
 
 namespace snap {
 namespace {
-
-__device__ __forceinline__ uint64_t mix64(uint64_t x) {
-  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
-  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
-  return x ^ (x >> 31);
-}
-
-// Slot of key k; the digest value equal to kEmptyKey lives in the extra slot
-// at index mask + 1 so every 64-bit digest is representable exactly.
-__device__ __forceinline__ uint64_t table_find_or_insert(TableDev t, unsigned long long k) {
-  if (k == kEmptyKey) return t.mask + 1;
-  uint64_t h = mix64(k) & t.mask;
-  for (;;) {
-    const unsigned long long prev = atomicCAS(t.keys + h, kEmptyKey, k);
-    if (prev == kEmptyKey || prev == k) return h;
-    h = (h + 1) & t.mask;
-  }
-}
-// Returns slot or UINT64_MAX when absent.
-__device__ __forceinline__ uint64_t table_find(TableDev t, unsigned long long k) {
-  if (k == kEmptyKey) return t.vals[t.mask + 1] != ~0ull ? t.mask + 1 : ~0ull;
-  uint64_t h = mix64(k) & t.mask;
-  for (;;) {
-    const unsigned long long cur = t.keys[h];
-    if (cur == k) return h;
-    if (cur == kEmptyKey) return ~0ull;
-    h = (h + 1) & t.mask;
-  }
-}
 
 __global__ void k_table_clear(TableDev t) {
   const uint64_t n = t.mask + 2;

@@ -79,6 +79,14 @@ int launch_scatter(uint8_t* arena, const GridDev& g, const uint32_t* lens, const
 int launch_compare(const uint64_t* a, const uint64_t* b, uint64_t n, unsigned long long* nbad,
                    cudaStream_t s);
 
+// Splice: chunk-cache index insert and the swap-in pass.
+int launch_cache_insert(TableDev cache, const uint64_t* dig, const uint32_t* sel_list,
+                        const uint64_t* totals, const uint64_t* offsets, uint64_t base,
+                        uint64_t max_n, cudaStream_t s);
+int launch_splice_in(uint8_t* arena, const GridDev& to, const uint32_t* lens, const uint64_t* want,
+                     const int64_t* match, const uint64_t* dig_from, TableDev cache,
+                     const uint8_t* cache_base, unsigned long long* counters, cudaStream_t s);
+
 // K5.
 int launch_grad_sum(int dtype, uint8_t* arena, const uint64_t* src_addrs_dev, uint32_t nsrc,
                     uint64_t dst_addr, uint64_t elems, int accumulate, cudaStream_t s);

@@ -1,0 +1,40 @@
+// table.cuh — open-addressing digest tables shared by the K2 (dedup / known
+// set) and splice (chunk cache index) kernels. Power-of-two capacity, linear
+// probing, key kEmptyKey = free; the digest value equal to kEmptyKey lives in
+// the extra slot mask + 1, so every 64-bit digest is representable exactly.
+#pragma once
+
+#include "snap_internal.h"
+
+namespace snap {
+
+__device__ __forceinline__ uint64_t tmix64(uint64_t x) {
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+
+__device__ __forceinline__ uint64_t table_find_or_insert(TableDev t, unsigned long long k) {
+  if (k == kEmptyKey) return t.mask + 1;
+  uint64_t h = tmix64(k) & t.mask;
+  for (;;) {
+    const unsigned long long prev = atomicCAS(t.keys + h, kEmptyKey, k);
+    if (prev == kEmptyKey || prev == k) return h;
+    h = (h + 1) & t.mask;
+  }
+}
+
+// Slot of k, or UINT64_MAX when absent (the kEmptyKey slot counts as present
+// once its value was set).
+__device__ __forceinline__ uint64_t table_find(TableDev t, unsigned long long k) {
+  if (k == kEmptyKey) return t.vals[t.mask + 1] != ~0ull ? t.mask + 1 : ~0ull;
+  uint64_t h = tmix64(k) & t.mask;
+  for (;;) {
+    const unsigned long long cur = t.keys[h];
+    if (cur == k) return h;
+    if (cur == kEmptyKey) return ~0ull;
+    h = (h + 1) & t.mask;
+  }
+}
+
+}  // namespace snap
