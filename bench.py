@@ -222,6 +222,141 @@ def cpu_baseline(replicated, per_rank, seconds_cap=30.0):
             "single_core_gbs": round((128 << 20) / dt1 / 1e9, 3)}
 
 
+# ------------------------------------------------------------------ C3: replica splicing
+
+def gpt2_medium_params():
+    """GPT-2-medium tensor sizes (354 823 168 params, 292 tensors)."""
+    t = [50257 * 1024, 1024 * 1024]
+    for _ in range(24):
+        t += [1024, 1024, 1024 * 3072, 3072, 1024 * 1024, 1024, 1024, 1024, 1024 * 4096, 4096,
+              4096 * 1024, 1024]
+    t += [1024, 1024]
+    assert sum(t) == 354_823_168 and len(t) == 292
+    return t
+
+
+def c3_layout(scale=1):
+    """Stable fp32 P, m, v per tensor (identical addresses on every replica) followed by one
+    fp32 gradient region per rank (pending during a switch). `scale` divides sizes."""
+    stable, addr, slot = [], 0, 0
+    sizes = [max(256, (4 * n // scale + 255) // 256 * 256) for n in gpt2_medium_params()]
+    for kind in range(3):  # P, m, v
+        for sz in sizes:
+            stable.append((0, slot, addr, sz, 0 if kind == 0 else 1, 0))
+            addr += sz
+            slot += 1
+    stable_bytes = addr
+    gbytes = sum(sizes)
+    return stable, stable_bytes, sizes, gbytes
+
+
+def splice_bench(snap, device, nranks=4):
+    """C3 on one GPU: 4 time-sliced ranks, GPT-2-medium fp32 P/m/v + per-rank G.
+    Returns switch ms (identical replicas, and with a fraction f of P/O chunks differing
+    per rank) and the K5 on-GPU gradient sum throughput."""
+    stable, sbytes, sizes, gbytes = c3_layout()
+    gregion = sbytes
+    arena = sbytes + (nranks + 1) * gbytes + (1 << 20)
+    out = {"workload": f"C3: {nranks} time-sliced DP ranks on 1 GPU, GPT-2-medium fp32 P+m+v "
+                       f"({sbytes / 1e9:.3f} GB/replica, identical addresses) + per-rank fp32 "
+                       f"G ({gbytes / 1e9:.3f} GB, pending at switch); chunk cache in HBM"}
+    with snap.Ctx(device, arena) as c:
+        c.splice_init(3 * sbytes)
+        goffs = np.cumsum([0] + sizes[:-1]).tolist()
+        for r in range(nranks):
+            g = [(0, 10000 + i, gregion + r * gbytes + off, sz, 2, snap.BUF_PENDING)
+                 for i, (off, sz) in enumerate(zip(goffs, sizes))]
+            c.splice_set_rank(r, stable + g)
+            c.fill_mix64(gregion + r * gbytes, gbytes, 77 + r, 0)
+        c.fill_mix64(0, sbytes, 5, 0)
+        for r in range(nranks):  # first activation of every rank
+            c.splice_switch(r, (r + 1) % nranks)
+
+        def timed_switch(frm, to):
+            c.sync()
+            c.timer_start()
+            t0 = time.perf_counter()
+            st = c.splice_switch(frm, to)
+            wall = (time.perf_counter() - t0) * 1e3
+            return c.timer_stop(), wall, st
+
+        res = [timed_switch(r % nranks, (r + 1) % nranks) for r in range(8)]
+        out["swap_ms_identical"] = round(float(np.median([x[0] for x in res])), 4)
+        out["swap_wall_ms_identical"] = round(float(np.median([x[1] for x in res])), 4)
+        st = res[-1][2]
+        out["identical_switch"] = {k: int(v) for k, v in st.items()}
+        out["digest_gbs"] = round(st["hashed_bytes"] / (out["swap_ms_identical"] / 1e3) / 1e9, 1)
+        # non-identical replicas: fraction f of the outgoing rank's P/O chunks changed
+        nck = sbytes // 65536
+        rng = np.random.default_rng(0)
+        sweep = {}
+        active = 0
+        for f in (0.05, 0.25):
+            ms_list, sts = [], []
+            for k in range(3):
+                chunks = rng.choice(nck, size=int(f * nck), replace=False)
+                c.xor_words(chunks.astype(np.uint64) * 65536, 0x51 + k + int(f * 1000))
+                ms, wall, st = timed_switch(active, (active + 1) % nranks)
+                active = (active + 1) % nranks
+                ms_list.append(ms)
+                sts.append(st)
+            sweep[str(f)] = {"swap_ms": round(float(np.median(ms_list)), 4),
+                             "swap_out_bytes": int(sts[-1]["swap_out_bytes"]),
+                             "swap_in_bytes": int(sts[-1]["swap_in_bytes"])}
+        out["swap_ms_divergent"] = sweep
+        # K5: fixed-order fp32 sum of the 4 ranks' gradients into the accumulator
+        n = gbytes // 4
+        srcs = [gregion + r * gbytes for r in range(nranks)]
+        acc = gregion + nranks * gbytes
+        c.grad_sum(snap.F32, srcs, acc, n)
+        c.sync()
+        c.timer_start()
+        reps = 5
+        for _ in range(reps):
+            c.grad_sum(snap.F32, srcs, acc, n)
+        ms = c.timer_stop() / reps
+        out["grad_sum_ms"] = round(ms, 4)
+        out["grad_sum_gbs"] = round((nranks + 1) * gbytes / (ms / 1e3) / 1e9, 1)
+        out["grad_sum"] = "K5 f32, 4 sources -> accumulator, fixed ascending dp order"
+    return out
+
+
+def ref_splice_bench(scale=8, nranks=4, switches=3):
+    """The reference's GpuLedger plan_switch + execute_switch (with the App. A-1 refresh)
+    on the C3 layout at 1/`scale` size, identical replicas; ms per switch x scale."""
+    import oracle as O
+    R = O.ref()
+    if R is None:
+        return None
+    stable, sbytes, sizes, gbytes = c3_layout(scale)
+    mem = sbytes + gbytes + (1 << 22)
+    s = R.ref_splice_new(mem, 1 << 20)
+    img = O.fill_mix64(sbytes // 8, 5, 0)
+    out = np.zeros(5, np.uint64)
+    gaddr = sbytes
+    for r in range(nranks):
+        for (_, slot, a, n, cat, _f) in stable:
+            R.ref_splice_alloc(s, r, slot, a, n, cat, 0)
+        off = 0
+        for i, sz in enumerate(sizes):
+            R.ref_splice_alloc(s, r, 10000 + i, gaddr + off, sz, 2, 1)
+            off += sz
+        R.ref_splice_write(s, 0, img.ctypes.data, img.size)
+        R.ref_splice_switch(s, r, (r + 1) % nranks if r + 1 < nranks else 0, out.ctypes.data)
+    times = []
+    for k in range(switches):
+        t0 = time.perf_counter()
+        rc = R.ref_splice_switch(s, k % nranks, (k + 1) % nranks, out.ctypes.data)
+        times.append(time.perf_counter() - t0)
+        if rc != 0:
+            break
+    R.ref_splice_free(s)
+    ms = float(np.median(times)) * 1e3
+    return {"swap_ms_identical_scaled": round(ms * scale, 1), "measured_ms": round(ms, 1),
+            "scale": f"1/{scale} of C3 (P/m/v {sbytes / 1e9:.3f} GB), 1 core, x{scale}",
+            "kind": "reference"}
+
+
 # ------------------------------------------------------------------ arms
 
 def run_reference(args, dist):
@@ -260,7 +395,8 @@ def run_reference(args, dist):
         "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": nthreads,
                          "kind": "reference", "sample": desc},
         "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0}}))
+                "d2h_bytes_per_step": 0},
+        "splice": ref_splice_bench()}))
 
 
 def run_ours(args, dist):
@@ -352,7 +488,13 @@ def run_ours(args, dist):
     hostimg.free()
     hstage.free()
 
+    ctx.close()
     base = cpu_baseline(replicated, per_rank) if (dist.rank == 0 and N == 1) else None
+    splice = None
+    if dist.rank == 0 and N == 1 and not args.no_splice:
+        splice = splice_bench(snap, dist.local)
+        if base is not None:
+            base["splice"] = ref_splice_bench()
     if dist.rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": N,
@@ -386,9 +528,9 @@ def run_ours(args, dist):
             "e2e": e2e,
             "cpu_baseline": base,
             "restore_check": check,
+            "splice": splice,
         }
         print(json.dumps(line))
-    ctx.close()
 
 
 def main():
@@ -397,6 +539,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-splice", action="store_true", help="skip the C3 splice section")
     args = ap.parse_args()
     dist = Dist()
     try:

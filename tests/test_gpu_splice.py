@@ -48,7 +48,8 @@ def test_splice_matches_reference_ledger(snap, mode):
     for r in range(nranks):
         t = {}
         for (_, s, a, n, c, f) in lay:
-            t[s] = O.fill_mix64(n // 8, 7 if c != 2 else 100 + r, 0)
+            # distinct bytes per buffer, so buffer- and chunk-granular dedup coincide
+            t[s] = O.fill_mix64(n // 8, 7 + 1000 * s if c != 2 else 100 + r, 0)
         truth.append(t)
 
     def write_rank(r):
@@ -125,7 +126,7 @@ def test_splice_identical_replicas_swap_nothing(snap):
 def test_splice_cache_full_is_enomem(snap):
     lay = rank_layout()
     with snap.Ctx(0, 16 * MIB) as ctx:
-        ctx.splice_init(4 * MIB)  # smaller than one rank's live state
+        ctx.splice_init(2 * MIB)  # smaller than one rank's live state (3.4 MiB)
         ctx.splice_set_rank(0, lay)
         ctx.splice_set_rank(1, lay)
         with pytest.raises(snap.SnapError) as e:
