@@ -150,18 +150,23 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) == 7:
-                self.rows.append(parts)
+                self.rows.append((time.perf_counter(), parts))
+
+    def window(self, t0, t1):
+        """Marks the timed region [t0, t1] (perf_counter); only samples inside it count."""
+        self.t0, self.t1 = t0, t1
 
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.12)
+        time.sleep(0.06)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=2)
         except subprocess.TimeoutExpired:
             self.proc.kill()
-        rows = self.rows
+        t0, t1 = getattr(self, "t0", 0.0), getattr(self, "t1", float("inf"))
+        rows = [r for (t, r) in self.rows if t0 <= t <= t1 + 0.03]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i] == "Active"})
 
@@ -429,15 +434,19 @@ def run_ours(args, dist):
         g_bytes, g_chunks = my_bytes, my_chunks
 
     clocks = ClockSampler(dist.local)
+    clocks.start()
+    for _ in range(20):  # keep the GPU busy while nvidia-smi starts sampling
+        step()
     ctx.prof_enable(True)
     l0 = ctx.launches
     dist.barrier()
     ctx.sync()
-    clocks.start()
+    tw0 = time.perf_counter()
     ctx.timer_start()
     for _ in range(args.steps):
         step()
     ms = ctx.timer_stop()
+    clocks.window(tw0, time.perf_counter())
     clk = clocks.stop()
     launches = ctx.launches - l0
     t_hash, n_hash = ctx.prof_read(snap.PROF_HASH)
