@@ -215,28 +215,34 @@ int init_spec(snap_ctx* ctx) {
   CK(cudaMemcpyAsync(d, spec.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->spec_ready = true;
+  ctx->h_spec = std::move(spec);
+  ctx->h_spec_valid = true;
   return SNAP_OK;
 }
 
 // K1 with the fused speculative compaction (full snapshots); incremental
 // snapshots (known set non-empty) hash only and gather the few dirty chunks.
-int hash_fused(snap_ctx* ctx) {
+// Chunks [c0, c1) only (c1 == 0: all), so the host-buffer path can hash each
+// slab as soon as it lands.
+int hash_fused(snap_ctx* ctx, uint64_t c0 = 0, uint64_t c1 = 0) {
+  GridDev g = ctx->grid;
+  g.c_begin = c0;
+  g.c_end = c1;
   if (ctx->kn_count > 0) {
-    CKL(snap::launch_hash(ctx->arena, ctx->grid, P<uint64_t>(ctx->d_dig), nullptr, nullptr,
-                          ctx->stream));
+    CKL(snap::launch_hash(ctx->arena, g, P<uint64_t>(ctx->d_dig), nullptr, nullptr, ctx->stream));
     ctx->spec_used = false;
     return SNAP_OK;
   }
   if (!ctx->spec_ready) RC(init_spec(ctx));
   uint8_t* st;
   RC(ensure(ctx, ctx->staging, ctx->grid_bytes, &st));
-  CKL(snap::launch_hash(ctx->arena, ctx->grid, P<uint64_t>(ctx->d_dig),
+  CKL(snap::launch_hash(ctx->arena, g, P<uint64_t>(ctx->d_dig),
                         P<uint64_t>(ctx->d_spec[ctx->spec_cur]), st, ctx->stream));
   ctx->spec_used = true;
   return SNAP_OK;
 }
 
-int compact_impl(snap_ctx* ctx) {
+int compact_impl(snap_ctx* ctx, uint32_t* moved = nullptr, unsigned int* nmoved = nullptr) {
   uint8_t* st;
   RC(ensure(ctx, ctx->staging, ctx->grid_bytes, &st));
   const uint64_t* spec_cur = nullptr;
@@ -246,20 +252,22 @@ int compact_impl(snap_ctx* ctx) {
     RC(ensure(ctx, ctx->d_spec[1 - ctx->spec_cur], ctx->nchunks, &spec_next));
     CK(cudaMemsetAsync(spec_next, 0xff, ctx->nchunks * 8, ctx->stream));
   }
+  if (nmoved) CK(cudaMemsetAsync(nmoved, 0, 4, ctx->stream));
   if (ctx->comm && ctx->exchanged) {
     CKL(snap::launch_gather(ctx->arena, ctx->grid, P<uint32_t>(ctx->d_lens),
                             P<uint32_t>(ctx->d_my_list), P<uint64_t>(ctx->d_my_totals),
                             P<uint64_t>(ctx->d_my_off), true, spec_cur, spec_next, st,
-                            ctx->nchunks, ctx->stream));
+                            ctx->nchunks, ctx->stream, moved, nmoved));
   } else {
     CKL(snap::launch_gather(ctx->arena, ctx->grid, P<uint32_t>(ctx->d_lens),
                             P<uint32_t>(ctx->sel_list), P<uint64_t>(ctx->totals),
                             P<uint64_t>(ctx->offsets), false, spec_cur, spec_next, st,
-                            ctx->nchunks, ctx->stream));
+                            ctx->nchunks, ctx->stream, moved, nmoved));
   }
   if (ctx->spec_used) {
     ctx->spec_cur = 1 - ctx->spec_cur;
     ctx->spec_used = false;  // the image is final; a second compact re-gathers
+    ctx->h_spec_valid = false;
   }
   ctx->staging_valid = ctx->grid_bytes;
   return SNAP_OK;
@@ -334,6 +342,10 @@ int snap_close(snap_ctx* ctx) {
   if (ctx->arena) cudaFree(ctx->arena);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  for (cudaEvent_t e : ctx->pipe_ev) cudaEventDestroy(e);
+  release(ctx->d_moved);
+  if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
+  if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return SNAP_OK;
@@ -687,12 +699,157 @@ int snap_snapshot(snap_ctx* ctx) {
   return snap_compact(ctx);
 }
 
+}  // extern "C"
+
+namespace {
+
+// Pipelined host-buffer snapshot: the image is copied in slabs on an H2D
+// stream, each slab's complete chunks are hashed (+ speculatively staged) on
+// the compute stream as soon as they land, and their staging bytes go back on
+// a D2H stream while later slabs are still copying in, so PCIe runs both
+// directions concurrently with the kernels. After selection, chunks the fix-up
+// moved are copied again (ordered after the speculative copies).
+int snapshot_host_pipelined(snap_ctx* ctx, const uint8_t* host_src, uint64_t addr,
+                            uint64_t bytes, uint8_t* host_staging, uint64_t cap,
+                            uint64_t* staged_bytes, uint64_t* host_digests) {
+  const uint64_t n = ctx->nchunks;
+  const uint64_t slab = 64ull << 20;
+  const uint64_t nslab = (bytes + slab - 1) / slab;
+  if (!ctx->h2d) CK(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
+  if (!ctx->d2h) CK(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
+  while (ctx->pipe_ev.size() < 2 * nslab + 2) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->pipe_ev.push_back(e);
+  }
+  const bool spec = ctx->kn_count == 0;
+  if (spec) {
+    if (!ctx->spec_ready) RC(init_spec(ctx));
+    if (!ctx->h_spec_valid) {
+      ctx->h_spec.resize(n);
+      CK(cudaMemcpyAsync(ctx->h_spec.data(), ctx->d_spec[ctx->spec_cur].p, n * 8,
+                         cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      ctx->h_spec_valid = true;
+    }
+  }
+  uint8_t* st;
+  RC(ensure(ctx, ctx->staging, ctx->grid_bytes, &st));
+  uint32_t* moved;
+  RC(ensure(ctx, ctx->d_moved, n + 1, &moved));
+  // chunk end addresses (canonical order, increasing: checked by the caller)
+  uint64_t next = 0, b = 0;
+  auto chunk_end = [&](uint64_t g) {
+    while (ctx->h_cstart[b + 1] <= g) ++b;
+    const uint64_t k = g - ctx->h_cstart[b];
+    return ctx->bufs[b].addr + (k << log2u(ctx->geom.chunk_bytes)) + ctx->h_lens[g];
+  };
+  {
+    ProfScope ps(ctx, kProfHash);
+    for (uint64_t k = 0; k < nslab; ++k) {
+      const uint64_t s0 = k * slab, s1 = std::min(bytes, s0 + slab);
+      CK(cudaMemcpyAsync(ctx->arena + addr + s0, host_src + s0, s1 - s0, cudaMemcpyHostToDevice,
+                         ctx->h2d));
+      CK(cudaEventRecord(ctx->pipe_ev[2 * k], ctx->h2d));
+      uint64_t hi = next;
+      while (hi < n && chunk_end(hi) <= addr + s1) ++hi;
+      if (hi == next) continue;
+      CK(cudaStreamWaitEvent(ctx->stream, ctx->pipe_ev[2 * k], 0));
+      RC(hash_fused(ctx, next, hi));
+      if (spec && host_staging) {
+        uint64_t lo = ~0ull, top = 0;
+        for (uint64_t g = next; g < hi; ++g)
+          if (ctx->h_spec[g] != ~0ull) {
+            lo = std::min(lo, ctx->h_spec[g]);
+            top = std::max(top, ctx->h_spec[g] + ctx->h_lens[g]);
+          }
+        top = std::min(top, cap);
+        if (lo < top) {
+          CK(cudaEventRecord(ctx->pipe_ev[2 * k + 1], ctx->stream));
+          CK(cudaStreamWaitEvent(ctx->d2h, ctx->pipe_ev[2 * k + 1], 0));
+          CK(cudaMemcpyAsync(host_staging + lo, st + lo, top - lo, cudaMemcpyDeviceToHost,
+                             ctx->d2h));
+        }
+      }
+      next = hi;
+    }
+  }
+  if (next != n) return fail(ctx, SNAP_EINTERNAL, "snapshot_host: chunks outside the image");
+  ctx->hashed = true;
+  ctx->selected = false;
+  ctx->exchanged = false;
+  RC(snap_select(ctx));
+  {
+    ProfScope ps(ctx, kProfCompact);
+    RC(compact_impl(ctx, moved, reinterpret_cast<unsigned int*>(moved + n)));
+  }
+  ctx->h_spec_valid = false;  // the fix-up wrote the next layout on the device
+  const bool shard = ctx->comm && ctx->exchanged;
+  uint64_t tot[2] = {0, 0};
+  uint32_t nmv = 0;
+  CK(cudaMemcpyAsync(tot, shard ? ctx->d_my_totals.p : ctx->totals.p, 16, cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaMemcpyAsync(&nmv, moved + n, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  if (host_digests && n)
+    CK(cudaMemcpyAsync(host_digests, ctx->d_dig.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (host_staging && tot[1] > cap)
+    return fail(ctx, SNAP_EINVAL, "snapshot_host: staging buffer too small");
+  if (host_staging) {
+    CK(cudaEventRecord(ctx->pipe_ev[2 * nslab], ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->d2h, ctx->pipe_ev[2 * nslab], 0));
+    if (!spec) {
+      if (tot[1])
+        CK(cudaMemcpyAsync(host_staging, st, tot[1], cudaMemcpyDeviceToHost, ctx->d2h));
+    } else if (nmv) {
+      // chunks the fix-up rewrote: copy their final bytes (after the speculative copies)
+      std::vector<uint32_t> idx(nmv), list;
+      CK(cudaMemcpy(idx.data(), moved, nmv * 4ull, cudaMemcpyDeviceToHost));
+      std::vector<uint64_t> off(shard ? ctx->maxn : n);
+      std::vector<uint32_t> lst(shard ? ctx->maxn : n);
+      CK(cudaMemcpy(off.data(), shard ? ctx->d_my_off.p : ctx->offsets.p, off.size() * 8,
+                    cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(lst.data(), shard ? ctx->d_my_list.p : ctx->sel_list.p, lst.size() * 4,
+                    cudaMemcpyDeviceToHost));
+      for (uint32_t w : idx) {
+        const uint32_t gc = lst[w];
+        const uint64_t o = shard ? off[w] : off[gc];
+        CK(cudaMemcpyAsync(host_staging + o, st + o, ctx->h_lens[gc], cudaMemcpyDeviceToHost,
+                           ctx->d2h));
+      }
+    }
+    CK(cudaStreamSynchronize(ctx->d2h));
+  }
+  ctx->staging_valid = ctx->grid_bytes;
+  if (staged_bytes) *staged_bytes = tot[1];
+  return SNAP_OK;
+}
+
+// The pipelined path needs the grid's chunks in increasing address order
+// inside [addr, addr + bytes).
+bool pipelinable(const snap_ctx* ctx, uint64_t addr, uint64_t bytes) {
+  uint64_t last = addr;
+  for (const snap_buf& b : ctx->bufs) {
+    if (b.addr < last || b.addr + b.bytes > addr + bytes) return false;
+    last = b.addr + b.bytes;
+  }
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
 int snap_snapshot_host(snap_ctx* ctx, const void* host_src, uint64_t addr, uint64_t bytes,
                        void* host_staging, uint64_t staging_cap, uint64_t* staged_bytes,
                        uint64_t* host_digests) {
   if (!ctx || (!host_src && bytes)) return SNAP_EINVAL;
   RC(check_range(ctx, addr, bytes));
   CK(cudaSetDevice(ctx->device));
+  if (bytes && ctx->nchunks && pipelinable(ctx, addr, bytes))
+    return snapshot_host_pipelined(ctx, static_cast<const uint8_t*>(host_src), addr, bytes,
+                                   static_cast<uint8_t*>(host_staging), staging_cap,
+                                   staged_bytes, host_digests);
   if (bytes)
     CK(cudaMemcpyAsync(ctx->arena + addr, host_src, bytes, cudaMemcpyHostToDevice, ctx->stream));
   RC(snap_snapshot(ctx));

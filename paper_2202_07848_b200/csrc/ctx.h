@@ -86,6 +86,14 @@ struct snap_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   Prof prof;
   SpliceState* splice = nullptr;
+
+  // host-buffer pipeline (snap_snapshot_host): copy streams, events, host
+  // mirror of the speculative layout, fix-up list
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  std::vector<cudaEvent_t> pipe_ev;
+  std::vector<uint64_t> h_spec;
+  bool h_spec_valid = false;
+  DevMem d_moved;
 };
 
 inline int fail(snap_ctx* c, int code, const std::string& msg) {

@@ -65,7 +65,8 @@ __global__ void __launch_bounds__(kThreads)
 k_gather(const uint8_t* __restrict__ arena, GridDev g, const uint32_t* __restrict__ lens,
          const uint32_t* __restrict__ sel_list, const uint64_t* __restrict__ totals,
          const uint64_t* __restrict__ offsets, int by_list, const uint64_t* __restrict__ spec_cur,
-         uint64_t* __restrict__ spec_next, uint8_t* __restrict__ staging) {
+         uint64_t* __restrict__ spec_next, uint8_t* __restrict__ staging,
+         uint32_t* __restrict__ moved, unsigned int* __restrict__ nmoved) {
   const uint64_t nsel = totals[0];
   const int lane = threadIdx.x & 31;
   const uint64_t w0 = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
@@ -76,6 +77,7 @@ k_gather(const uint8_t* __restrict__ arena, GridDev g, const uint32_t* __restric
     if (spec_next && lane == 0) spec_next[gc] = off;
     if (spec_cur && spec_cur[gc] == off) continue;
     warp_copy(staging + off, chunk_ptr(arena, g, gc), lens[gc], lane);
+    if (moved && lane == 0) moved[atomicAdd(nmoved, 1u)] = static_cast<uint32_t>(w);
   }
 }
 
@@ -172,13 +174,14 @@ unsigned copy_grid() {
 int launch_gather(const uint8_t* arena, const GridDev& g, const uint32_t* lens,
                   const uint32_t* sel_list, const uint64_t* totals, const uint64_t* offsets,
                   bool offsets_by_list, const uint64_t* spec_cur, uint64_t* spec_next,
-                  uint8_t* staging, uint64_t max_sel, cudaStream_t s) {
+                  uint8_t* staging, uint64_t max_sel, cudaStream_t s, uint32_t* moved,
+                  unsigned int* nmoved) {
   if (max_sel == 0) return 0;
   uint64_t blocks = (max_sel * 32 + kThreads - 1) / kThreads;
   if (blocks > copy_grid()) blocks = copy_grid();
   k_gather<<<unsigned(blocks), kThreads, 0, s>>>(arena, g, lens, sel_list, totals, offsets,
                                                  offsets_by_list ? 1 : 0, spec_cur, spec_next,
-                                                 staging);
+                                                 staging, moved, nmoved);
   return 1;
 }
 

@@ -132,7 +132,9 @@ k_hash(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ chun
   const uint32_t ns_shift = g.page_shift - slab_shift;  // steps per page (log2)
   const uint32_t ns = 1u << ns_shift;
   const uint64_t pb = 1ull << g.page_shift;
-  const uint64_t nslots = g.nchunks << ppc_shift;
+  const uint64_t c_end = g.c_end ? g.c_end : g.nchunks;
+  const uint64_t slot_base = g.c_begin << ppc_shift;
+  const uint64_t nslots = (c_end - g.c_begin) << ppc_shift;
   const uint64_t ntasks = (nslots + NP - 1) / NP;
   const uint64_t gw = uint64_t(blockIdx.x) * C::kWarps + warp;
   const uint64_t nw = uint64_t(gridDim.x) * C::kWarps;
@@ -158,12 +160,12 @@ k_hash(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ chun
 #pragma unroll
         for (int c = 0; c < CH; ++c) {
           const int j = c * 32 + lane;
-          const uint64_t slot = (gw + i * nw) * NP + j;
+          const uint64_t slot = slot_base + (gw + i * nw) * NP + j;
           const uint64_t gc = slot >> ppc_shift;
           const uint8_t* src = nullptr;
           uint8_t* dst = nullptr;
           uint32_t len = 0;
-          if (gc < g.nchunks) {
+          if (gc < c_end) {
             const uint32_t b = find_buf(g, gc);
             const uint64_t k = gc - __ldg(g.cstart + b);
             const uint64_t in_chunk = (slot & ((1u << ppc_shift) - 1)) << g.page_shift;
@@ -296,7 +298,7 @@ k_hash(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ chun
     __syncwarp();
     if (s == ns - 1) {
       // Task complete: each lane holds CH page digests (or nothing).
-      const uint64_t slot0 = (gw + i * nw) * NP;
+      const uint64_t slot0 = slot_base + (gw + i * nw) * NP;
 #pragma unroll
       for (int c = 0; c < CH; ++c) {
         const uint64_t myslot = slot0 + c * 32 + lane;
@@ -395,7 +397,10 @@ int launch_hash_cfg(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
     cudaFuncSetAttribute(k_hash<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem));
     attr = true;
   }
-  const uint64_t ntasks = ((g.nchunks << (g.chunk_shift - g.page_shift)) + C::kPages - 1) / C::kPages;
+  const uint64_t c_end = g.c_end ? g.c_end : g.nchunks;
+  if (c_end <= g.c_begin) return 0;
+  const uint64_t ntasks =
+      (((c_end - g.c_begin) << (g.chunk_shift - g.page_shift)) + C::kPages - 1) / C::kPages;
   uint64_t blocks = (ntasks + C::kWarps - 1) / C::kWarps;
   const uint64_t cap = uint64_t(sm_count());
   if (blocks > cap) blocks = cap;

@@ -24,6 +24,10 @@ struct GridDev {
   uint64_t nchunks = 0;
   uint32_t page_shift = 12;
   uint32_t chunk_shift = 16;
+  // K1 hashes chunks [c_begin, c_end) (c_end == 0: all); lets the host-buffer
+  // snapshot hash each slab as soon as its H2D copy lands
+  uint64_t c_begin = 0;
+  uint64_t c_end = 0;
 };
 
 // Open-addressing digest table (dedup + known set), power-of-two capacity.
@@ -69,11 +73,14 @@ int launch_resolve_dups(const uint8_t* sel, const uint64_t* owner, uint64_t* off
 // offsets_by_list: dst offset of list entry k is offsets[k] (shard lists) instead
 // of offsets[sel_list[k]] (single-GPU image). spec_cur (nullable): chunks the
 // fused hash pass already wrote at the right offset are skipped; spec_next
-// (nullable) receives the actual layout (next prediction).
+// (nullable) receives the actual layout (next prediction). moved (nullable)
+// receives the list index of every chunk actually copied (count in *nmoved,
+// zeroed by the caller).
 int launch_gather(const uint8_t* arena, const GridDev& g, const uint32_t* lens,
                   const uint32_t* sel_list, const uint64_t* totals, const uint64_t* offsets,
                   bool offsets_by_list, const uint64_t* spec_cur, uint64_t* spec_next,
-                  uint8_t* staging, uint64_t max_sel, cudaStream_t s);
+                  uint8_t* staging, uint64_t max_sel, cudaStream_t s, uint32_t* moved = nullptr,
+                  unsigned int* nmoved = nullptr);
 int launch_scatter(uint8_t* arena, const GridDev& g, const uint32_t* lens, const uint8_t* image,
                    const uint64_t* src_off, cudaStream_t s);
 int launch_compare(const uint64_t* a, const uint64_t* b, uint64_t n, unsigned long long* nbad,
