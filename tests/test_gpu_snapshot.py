@@ -231,3 +231,52 @@ def test_fused_speculation_learns_and_recovers(snap, ctx, golden):
     ctx.write(b0[2], host[bufs[5][2]:bufs[5][2] + b0[3]])
     host = ctx.read(0, golden["ragged"]["arena_bytes"])
     check(host)
+
+
+def test_snapshot_host_pipelined(snap):
+    """snap_snapshot_host (pinned host image -> arena -> K1..K3 -> staging to host), slab
+    pipelined: staging image == oracle compaction, through mispredicted, learned and
+    incremental layouts, and through the non-pipelined fallback (unsorted buffers)."""
+    nbytes = 160 << 20
+    img = O.fill_mix64(nbytes // 8, 21, 0)
+    # buffers spanning several 64 MiB slabs, a duplicate (mispredicted speculation)
+    bufs = [(0, 0, 0, 48 << 20, 0), (0, 1, 48 << 20, (40 << 20) + 768, 1),
+            (0, 2, 100 << 20, 20 << 20, 2), (0, 3, 128 << 20, 8 << 20, 1),
+            (0, 4, 150 << 20, 256, 4)]
+    img[(128 << 20) // 8:(136 << 20) // 8] = img[(56 << 20) // 8:(64 << 20) // 8]
+    pin = snap.PinnedHost(nbytes)
+    pin.array[:] = img.view(np.uint8)
+    out = snap.PinnedHost(nbytes)
+    with snap.Ctx(0, nbytes) as c:
+        c.set_buffers(bufs)
+        dig = np.zeros(c.nchunks, np.uint64)
+        od, olens, _ = O.hash_chunks([img], bufs)
+        osel, oown, ooff, otot = O.select(od, olens)
+        exp = O.compact([img], bufs, 65536, osel, ooff, otot)
+        for it in range(2):
+            staged = c.snapshot_host(pin.ptr, 0, nbytes, out.ptr, nbytes, dig)
+            assert staged == otot and np.array_equal(dig, od), it
+            assert np.array_equal(out.array[:staged], exp), it
+        # incremental: 3 dirty chunks against the committed store
+        c.known_commit()
+        host2 = img.copy()
+        host2[[3 * 8192, 700 * 8192, 1900 * 8192]] ^= np.uint64(0xABCD)
+        pin.array[:] = host2.view(np.uint8)
+        staged = c.snapshot_host(pin.ptr, 0, nbytes, out.ptr, nbytes, dig)
+        d2, l2, _ = O.hash_chunks([host2], bufs)
+        s2, _, o2, t2 = O.select(d2, l2, known=od)
+        assert staged == t2 == 3 * 65536
+        assert np.array_equal(out.array[:staged], O.compact([host2], bufs, 65536, s2, o2, t2))
+    # unsorted buffer order -> sequential fallback, same result
+    bufs_u = [bufs[1], bufs[0], bufs[2]]
+    with snap.Ctx(0, nbytes) as c:
+        pin.array[:] = img.view(np.uint8)
+        c.set_buffers(bufs_u)
+        dig = np.zeros(c.nchunks, np.uint64)
+        staged = c.snapshot_host(pin.ptr, 0, nbytes, out.ptr, nbytes, dig)
+        od, olens, _ = O.hash_chunks([img], bufs_u)
+        osel, oown, ooff, otot = O.select(od, olens)
+        assert staged == otot
+        assert np.array_equal(out.array[:staged], O.compact([img], bufs_u, 65536, osel, ooff, otot))
+    pin.free()
+    out.free()
