@@ -328,6 +328,294 @@ k_hash(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ chun
   cp_wait<0>();
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialized K1: HW hash warps only hash (LDS + FNV), CW copy warps own
+// all memory traffic — the coalesced cp.async fill of every hash warp's slab
+// ring (completion signalled straight to a per-stage mbarrier with
+// cp.async.mbarrier.arrive.noinc) and the speculative staging stores. The
+// hash warps' instruction stream is then pure FNV (no address math, no
+// cp.async bookkeeping), and memory latency never sits on their critical
+// path. Copy warp c serves hash warps c, c + CW, ... round-robin, running
+// ST - 1 steps ahead of them; a slab is refilled only after its hash warp
+// released it (empty barrier) and after the copy warp stored it.
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive(uint32_t bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+template <int HW, int CW, int ST>
+struct WsCfg {
+  static constexpr int kHW = HW, kCW = CW, kST = ST;
+  static constexpr int kSlab = 128;
+  static constexpr int kStageBytes = 32 * kSlab;
+  static constexpr int kPer = HW / CW;  // hash warps per copy warp
+  static_assert(HW % CW == 0, "copy warps must divide hash warps");
+  // smem: slabs [HW][ST][32][128] | full/empty mbarriers [HW][ST] x2 |
+  // copy-side descriptors [HW][2 parities][32] x (src, dst) | lens [HW][2][32]
+  static constexpr size_t kSlabBytes = size_t(HW) * ST * kStageBytes;
+  static constexpr size_t kBarBytes = size_t(HW) * ST * 2 * 8;
+  static constexpr size_t kDescBytes = size_t(HW) * 2 * 32 * 16;
+  static constexpr size_t kLenBytes = size_t(HW) * 2 * 32 * 4;
+  static constexpr size_t kStateBytes = size_t(HW) * 2 * 32;  // {src0, dst0, flags}
+  static constexpr size_t kSmem = kSlabBytes + kBarBytes + kDescBytes + kLenBytes + kStateBytes;
+};
+
+// copy-side task state of one (hash warp, task parity), warp-uniform
+struct WsTask {
+  const uint8_t* src0;
+  uint8_t* dst0;
+  uint32_t regular;
+  uint32_t writes;
+};
+static_assert(sizeof(WsTask) <= 32, "WsTask slot");
+
+template <class C>
+__global__ void __launch_bounds__((C::kHW + C::kCW) * 32, 1)
+k_hash_ws(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ chunk_dig,
+          const uint64_t* __restrict__ spec_off, uint8_t* __restrict__ staging) {
+  constexpr int HW = C::kHW, CW = C::kCW, ST = C::kST, SLAB = C::kSlab;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* slabs = smem;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kSlabBytes);  // full[h*ST+s], empty after
+  uint64_t* desc = reinterpret_cast<uint64_t*>(smem + C::kSlabBytes + C::kBarBytes);
+  uint32_t* lens = reinterpret_cast<uint32_t*>(smem + C::kSlabBytes + C::kBarBytes + C::kDescBytes);
+  uint8_t* tstate = smem + C::kSlabBytes + C::kBarBytes + C::kDescBytes + C::kLenBytes;
+  auto task_state = [&](int h, int par) -> WsTask& {
+    return *reinterpret_cast<WsTask*>(tstate + (h * 2 + par) * 32);
+  };
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // page length of slot `slot` (0 when outside the grid / past its buffer)
+  auto page_len = [&](uint64_t slot) -> uint32_t {
+    const uint64_t gc = slot >> (g.chunk_shift - g.page_shift);
+    if (gc >= (g.c_end ? g.c_end : g.nchunks)) return 0;
+    const uint32_t b = find_buf(g, gc);
+    const uint64_t kk = gc - __ldg(g.cstart + b);
+    const uint64_t off = (kk << g.chunk_shift) +
+                         ((slot & ((1u << (g.chunk_shift - g.page_shift)) - 1)) << g.page_shift);
+    const uint64_t bytes = __ldg(g.bytes + b);
+    if (off >= bytes) return 0;
+    const uint64_t rem = bytes - off, pg = 1ull << g.page_shift;
+    return static_cast<uint32_t>(rem < pg ? rem : pg);
+  };
+
+  const uint32_t ppc_shift = g.chunk_shift - g.page_shift;
+  const uint32_t ns_shift = g.page_shift - 7;
+  const uint32_t ns = 1u << ns_shift;
+  const uint64_t pb = 1ull << g.page_shift;
+  const uint64_t c_end = g.c_end ? g.c_end : g.nchunks;
+  const uint64_t slot_base = g.c_begin << ppc_shift;
+  const uint64_t nslots = (c_end - g.c_begin) << ppc_shift;
+  const uint64_t ntasks = (nslots + 31) >> 5;
+  const uint64_t nw = uint64_t(gridDim.x) * HW;
+  auto steps_of = [&](int h) -> uint64_t {
+    const uint64_t gw = uint64_t(blockIdx.x) * HW + h;
+    return gw >= ntasks ? 0 : ((ntasks - gw + nw - 1) / nw) << ns_shift;
+  };
+  auto full_bar = [&](int h, int s) { return smem_u32(bars + h * ST + s); };
+  auto empty_bar = [&](int h, int s) { return smem_u32(bars + HW * ST + h * ST + s); };
+
+  if (threadIdx.x == 0) {
+    for (int h = 0; h < HW; ++h)
+      for (int s = 0; s < ST; ++s) {
+        mbar_init(full_bar(h, s), 32);   // one cp.async arrival per copy lane
+        mbar_init(empty_bar(h, s), 32);  // every hash lane releases the slab
+      }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp < HW) {
+    // ------------------------------------------------------------ hash warp
+    const int h = warp;
+    const uint64_t gw = uint64_t(blockIdx.x) * HW + h;
+    const uint64_t nsteps = steps_of(h);
+    uint8_t* ring = slabs + size_t(h) * ST * C::kStageBytes;
+    uint32_t lo = 0, hi = 0, mylen = 0;
+    for (uint64_t t = 0; t < nsteps; ++t) {
+      const uint32_t s = static_cast<uint32_t>(t) & (ns - 1);
+      const uint64_t i = t >> ns_shift;
+      const int st = static_cast<int>(t % ST);
+      mbar_wait(full_bar(h, st), static_cast<uint32_t>((t / ST) & 1));
+      if (s == 0) {
+        mylen = page_len(slot_base + (gw + i * nw) * 32 + lane);
+        lo = static_cast<uint32_t>(kFnvOffset);
+        hi = static_cast<uint32_t>(kFnvOffset >> 32);
+      }
+      if (s * SLAB < mylen) {
+        const uint8_t* slab = ring + st * C::kStageBytes + lane * SLAB;
+#pragma unroll
+        for (int uu = 0; uu < 8; ++uu) {
+          const uint4 v = *reinterpret_cast<const uint4*>(slab + ((uu ^ (lane & 7)) << 4));
+          fnv_word(lo, hi, v.x);
+          fnv_word(lo, hi, v.y);
+          fnv_word(lo, hi, v.z);
+          fnv_word(lo, hi, v.w);
+        }
+      }
+      mbar_arrive(empty_bar(h, st));
+      if (s == ns - 1) {
+        const uint64_t slot0 = slot_base + (gw + i * nw) * 32;
+        if (ppc_shift == 0) {
+          if (mylen > 0) chunk_dig[slot0 + lane] = (uint64_t(hi) << 32) | lo;
+        } else {
+          const uint32_t ppc = 1u << ppc_shift;
+          const int base = lane & ~static_cast<int>(ppc - 1);
+          uint32_t flo = static_cast<uint32_t>(kFnvOffset);
+          uint32_t fhi = static_cast<uint32_t>(kFnvOffset >> 32);
+          for (uint32_t qq = 0; qq < ppc; ++qq) {
+            const uint32_t plo = __shfl_sync(kFull, lo, base + qq);
+            const uint32_t phi = __shfl_sync(kFull, hi, base + qq);
+            const uint32_t pl = __shfl_sync(kFull, mylen, base + qq);
+            if (pl > 0) {
+              fnv_word(flo, fhi, plo);
+              fnv_word(flo, fhi, phi);
+            }
+          }
+          if (lane == base && mylen > 0) chunk_dig[(slot0 + lane) >> ppc_shift] = (uint64_t(fhi) << 32) | flo;
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ copy warp
+    const int c = warp - HW;
+    const uint32_t u = lane & 7, q = lane >> 3;
+    // steps of every served hash warp (copy warp c serves c, c + CW, ...)
+    uint64_t nst[C::kPer];
+    uint64_t maxsteps = 0;
+#pragma unroll
+    for (int k = 0; k < C::kPer; ++k) {
+      nst[k] = steps_of(c + k * CW);
+      maxsteps = nst[k] > maxsteps ? nst[k] : maxsteps;
+    }
+    // fill step p of served warp k
+    auto fill = [&](int k, uint64_t p) {
+      const int h = c + k * CW;
+      const uint64_t gw = uint64_t(blockIdx.x) * HW + h;
+      const uint64_t i = p >> ns_shift;
+      const uint32_t s = static_cast<uint32_t>(p) & (ns - 1);
+      const int par = static_cast<int>(i & 1);
+      const int st = static_cast<int>(p % ST);
+      mbar_wait(empty_bar(h, st), static_cast<uint32_t>(((p / ST) & 1) ^ 1));
+      uint64_t* dsc = desc + (h * 2 + par) * 32 * 2;
+      if (s == 0) {
+        const uint64_t slot = slot_base + (gw + i * nw) * 32 + lane;
+        const uint64_t gc = slot >> ppc_shift;
+        const uint8_t* src = nullptr;
+        uint8_t* dst = nullptr;
+        uint32_t len = 0;
+        if (gc < c_end) {
+          const uint32_t b = find_buf(g, gc);
+          const uint64_t kk = gc - __ldg(g.cstart + b);
+          const uint64_t in_chunk = (slot & ((1u << ppc_shift) - 1)) << g.page_shift;
+          const uint64_t off = (kk << g.chunk_shift) + in_chunk;
+          const uint64_t bytes = __ldg(g.bytes + b);
+          if (off < bytes) {
+            const uint64_t rem = bytes - off;
+            len = static_cast<uint32_t>(rem < pb ? rem : pb);
+            src = arena + __ldg(g.addr + b) + off;
+            if (spec_off) {
+              const uint64_t so = __ldg(spec_off + gc);
+              if (so != ~0ull) dst = staging + so + in_chunk;
+            }
+          }
+        }
+        dsc[lane * 2] = reinterpret_cast<uint64_t>(src);
+        dsc[lane * 2 + 1] = reinterpret_cast<uint64_t>(dst);
+        lens[(h * 2 + par) * 32 + lane] = len;
+        const uint8_t* s0 = reinterpret_cast<const uint8_t*>(
+            __shfl_sync(kFull, reinterpret_cast<uint64_t>(src), 0));
+        uint8_t* d0 = reinterpret_cast<uint8_t*>(__shfl_sync(kFull, reinterpret_cast<uint64_t>(dst), 0));
+        const bool w = __any_sync(kFull, dst != nullptr);
+        const bool r = __all_sync(kFull, len == pb && src == s0 + lane * pb) &&
+                       (!w || __all_sync(kFull, d0 != nullptr && dst == d0 + lane * pb));
+        if (lane == 0) task_state(h, par) = WsTask{s0, d0, r ? 1u : 0u, w ? 1u : 0u};
+        __syncwarp();
+      }
+      const WsTask ts = task_state(h, par);
+      const uint32_t sbase = smem_u32(slabs + (size_t(h) * ST + st) * C::kStageBytes);
+      const uint32_t soff = s * SLAB + u * 16;
+      if (ts.regular) {
+        const uint8_t* src = ts.src0 + q * pb + soff;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const int j = kk * 4 + q;
+          cp_async16(sbase + j * SLAB + ((u ^ (j & 7)) << 4), src);
+          src += 4 * pb;
+        }
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const int j = kk * 4 + q;
+          const uint32_t len = lens[(h * 2 + par) * 32 + j];
+          if (soff < len)
+            cp_async16(sbase + j * SLAB + ((u ^ (j & 7)) << 4),
+                       reinterpret_cast<const uint8_t*>(dsc[j * 2]) + soff);
+        }
+      }
+      cp_async_arrive(full_bar(h, st));
+    };
+    // speculative store of step t of served warp k (data must have landed)
+    auto store = [&](int k, uint64_t t) {
+      const int h = c + k * CW;
+      const uint64_t i = t >> ns_shift;
+      const int par = static_cast<int>(i & 1);
+      const WsTask ts = task_state(h, par);
+      if (!ts.writes) return;
+      const uint32_t s = static_cast<uint32_t>(t) & (ns - 1);
+      const int st = static_cast<int>(t % ST);
+      mbar_wait(full_bar(h, st), static_cast<uint32_t>((t / ST) & 1));
+      const uint8_t* sb = slabs + (size_t(h) * ST + st) * C::kStageBytes;
+      const uint32_t soff = s * SLAB + u * 16;
+      const uint64_t* dsc = desc + (h * 2 + par) * 32 * 2;
+      if (ts.regular) {
+        uint8_t* dst = ts.dst0 + q * pb + soff;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const int j = kk * 4 + q;
+          st_stream16(dst, *reinterpret_cast<const uint4*>(sb + j * SLAB + ((u ^ (j & 7)) << 4)));
+          dst += 4 * pb;
+        }
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const int j = kk * 4 + q;
+          uint8_t* dst = reinterpret_cast<uint8_t*>(dsc[j * 2 + 1]);
+          if (dst && soff < lens[(h * 2 + par) * 32 + j])
+            st_stream16(dst + soff,
+                        *reinterpret_cast<const uint4*>(sb + j * SLAB + ((u ^ (j & 7)) << 4)));
+        }
+      }
+    };
+    // prologue: ST - 1 steps ahead for every served warp
+    for (int p = 0; p < ST - 1; ++p)
+#pragma unroll
+      for (int k = 0; k < C::kPer; ++k)
+        if (uint64_t(p) < nst[k]) fill(k, p);
+    for (uint64_t t = 0; t < maxsteps; ++t) {
+#pragma unroll
+      for (int k = 0; k < C::kPer; ++k) {
+        if (t + ST - 1 < nst[k]) fill(k, t + ST - 1);
+        if (t < nst[k]) store(k, t);
+      }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  }
+}
+
 // Buffer digest = digest_of_words(chunk digests of the buffer); one thread
 // per buffer (digest vectors are 1/8192 of the data).
 __global__ void k_buf_fold(GridDev g, const uint64_t* __restrict__ chunk_dig,
@@ -388,6 +676,28 @@ using CfgA = HashCfg<1, 128, 3, 16>;  // 512 chains/SM, 128-B slabs
 using CfgB = HashCfg<2, 64, 2, 16>;   // 1024 chains/SM, 64-B slabs
 using CfgC = HashCfg<2, 64, 3, 12>;   // 768 chains/SM, deeper ring
 using CfgD = HashCfg<2, 128, 2, 12>;  // 768 chains/SM, 128-B slabs
+using WsA = WsCfg<16, 4, 3>;          // warp-specialized: 16 hash + 4 copy warps
+using WsB = WsCfg<16, 2, 3>;          // 16 hash + 2 copy warps
+using WsC = WsCfg<12, 4, 4>;          // 12 hash + 4 copy warps, deeper ring
+
+template <class C>
+int launch_hash_ws(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
+                   const uint64_t* spec_off, uint8_t* staging, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_hash_ws<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem));
+    attr = true;
+  }
+  const uint64_t c_end = g.c_end ? g.c_end : g.nchunks;
+  if (c_end <= g.c_begin) return 0;
+  const uint64_t ntasks = (((c_end - g.c_begin) << (g.chunk_shift - g.page_shift)) + 31) / 32;
+  uint64_t blocks = (ntasks + C::kHW - 1) / C::kHW;
+  const uint64_t cap = uint64_t(sm_count());
+  if (blocks > cap) blocks = cap;
+  k_hash_ws<C><<<unsigned(blocks), (C::kHW + C::kCW) * 32, C::kSmem, s>>>(arena, g, chunk_dig,
+                                                                         spec_off, staging);
+  return 1;
+}
 
 template <class C>
 int launch_hash_cfg(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
@@ -425,6 +735,9 @@ int launch_hash(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
     case 1: return launch_hash_cfg<CfgB>(arena, g, chunk_dig, spec_off, staging, s);
     case 2: return launch_hash_cfg<CfgC>(arena, g, chunk_dig, spec_off, staging, s);
     case 3: return launch_hash_cfg<CfgD>(arena, g, chunk_dig, spec_off, staging, s);
+    case 4: return launch_hash_ws<WsA>(arena, g, chunk_dig, spec_off, staging, s);
+    case 5: return launch_hash_ws<WsB>(arena, g, chunk_dig, spec_off, staging, s);
+    case 6: return launch_hash_ws<WsC>(arena, g, chunk_dig, spec_off, staging, s);
     default: return launch_hash_cfg<CfgA>(arena, g, chunk_dig, spec_off, staging, s);
   }
 }
