@@ -254,6 +254,18 @@ int snap_get_global_digests(snap_ctx* ctx, uint64_t* gdig, uint32_t* glens);
 int snap_get_shard(snap_ctx* ctx, int32_t* writer, uint64_t* shard_off, uint64_t* my_bytes,
                    uint64_t* my_chunks);
 
+/* Resize / reshard (Scheduler::resize -> restore_job, sched.cpp:385-427,
+ * ckpt.cpp:407-538): every rank exports its staging shard as a 64-byte CUDA
+ * IPC handle, the handles are exchanged out of band (all ranks, rank order),
+ * and a target GPU then rebuilds rank `src_rank`'s device state (the
+ * installed grid must be that rank's layout) straight from the shards —
+ * peer shards are read over NVLink by the same kernel that scatters the
+ * chunks to their recorded addresses. verify != 0 re-hashes (K1) against the
+ * snapshot's digests (BlobStore::get verification, ckpt.cpp:26-27). */
+int snap_ipc_export(snap_ctx* ctx, void* handle64);
+int snap_ipc_import(snap_ctx* ctx, int nranks, const void* handles);
+int snap_restore_shards(snap_ctx* ctx, int src_rank, int verify);
+
 /* Device-level allreduce of a gradient range (after K5 local sum,
  * collectives.cpp:147-154 local closer). Async. */
 int snap_allreduce(snap_ctx* ctx, int dtype, uint64_t addr, uint64_t elems);

@@ -126,6 +126,9 @@ _SIGS = {
     "snap_splice_set_rank": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_uint64, C.c_void_p]),
     "snap_splice_switch": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
     "snap_splice_recorded": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.POINTER(C.c_uint64)]),
+    "snap_ipc_export": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "snap_ipc_import": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
+    "snap_restore_shards": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
     "snap_timer_start": (C.c_int, [C.c_void_p]),
     "snap_timer_stop": (C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
 }
@@ -442,6 +445,20 @@ class Ctx:
         self._ck(self._L.snap_get_shard(self.h, _p(w), _p(so), C.byref(mb), C.byref(mc)),
                  "snap_get_shard")
         return w[:n], so[:n], mb.value, mc.value
+
+    # -- resize / reshard
+    def ipc_export(self) -> bytes:
+        buf = (C.c_uint8 * 64)()
+        self._ck(self._L.snap_ipc_export(self.h, buf), "snap_ipc_export")
+        return bytes(buf)
+
+    def ipc_import(self, handles: bytes, nranks: int):
+        buf = (C.c_uint8 * len(handles)).from_buffer_copy(handles)
+        self._ck(self._L.snap_ipc_import(self.h, nranks, buf), "snap_ipc_import")
+
+    def restore_shards(self, src_rank: int, verify=True):
+        self._ck(self._L.snap_restore_shards(self.h, src_rank, 1 if verify else 0),
+                 "snap_restore_shards")
 
     def prof_enable(self, on=True):
         self._ck(self._L.snap_prof_enable(self.h, 1 if on else 0), "snap_prof_enable")

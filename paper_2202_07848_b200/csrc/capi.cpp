@@ -161,6 +161,7 @@ int stripe_impl(snap_ctx* ctx) {
   RC(ensure(ctx, ctx->d_my_list, maxn, &my_list));
   RC(ensure(ctx, ctx->d_my_off, maxn, &my_off));
   RC(ensure(ctx, ctx->d_my_totals, 4, &my_tot));
+  ctx->shard_offsets_all = false;
   CKL(snap::launch_stripe_writer(P<uint64_t>(ctx->d_gdig), P<uint32_t>(ctx->d_glens),
                                  P<uint8_t>(ctx->sel), ctx->nranks, maxn, writer, ctx->stream));
   CKL(snap::launch_shard_scan(writer, P<uint32_t>(ctx->d_glens), ctx->nranks, maxn, ctx->rank, true,
@@ -342,6 +343,9 @@ int snap_close(snap_ctx* ctx) {
   if (ctx->arena) cudaFree(ctx->arena);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  for (size_t r = 0; r < ctx->peer_staging.size(); ++r)
+    if (int(r) != ctx->rank && ctx->peer_staging[r]) cudaIpcCloseMemHandle(ctx->peer_staging[r]);
+  release(ctx->d_peers);
   for (cudaEvent_t e : ctx->pipe_ev) cudaEventDestroy(e);
   release(ctx->d_moved);
   if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
@@ -670,9 +674,91 @@ int snap_get_shard(snap_ctx* ctx, int32_t* writer, uint64_t* shard_off, uint64_t
   }
   if (writer) CK(cudaMemcpyAsync(writer, ctx->d_writer.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  if (shard_off) ctx->shard_offsets_all = true;
   if (my_chunks) *my_chunks = tot[0];
   if (my_bytes) *my_bytes = tot[1];
   return SNAP_OK;
+}
+
+// ------------------------------------------------- resize / reshard (C5)
+
+static int verify_grid(snap_ctx* ctx, const uint64_t* expect_dev);
+
+int snap_ipc_export(snap_ctx* ctx, void* handle64) {
+  if (!ctx || !handle64) return SNAP_EINVAL;
+  if (!ctx->staging.p) return fail(ctx, SNAP_EINVAL, "ipc_export: no staging image yet");
+  CK(cudaSetDevice(ctx->device));
+  cudaIpcMemHandle_t h;
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t size");
+  CK(cudaIpcGetMemHandle(&h, ctx->staging.p));
+  std::memcpy(handle64, &h, 64);
+  return SNAP_OK;
+}
+
+int snap_ipc_import(snap_ctx* ctx, int nranks, const void* handles) {
+  if (!ctx || !handles || nranks != ctx->nranks) return SNAP_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  for (size_t r = 0; r < ctx->peer_staging.size(); ++r)
+    if (int(r) != ctx->rank && ctx->peer_staging[r]) cudaIpcCloseMemHandle(ctx->peer_staging[r]);
+  ctx->peer_staging.assign(nranks, nullptr);
+  for (int r = 0; r < nranks; ++r) {
+    if (r == ctx->rank) {
+      ctx->peer_staging[r] = ctx->staging.p;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const uint8_t*>(handles) + 64 * r, 64);
+    CK(cudaIpcOpenMemHandle(&ctx->peer_staging[r], h, cudaIpcMemLazyEnablePeerAccess));
+  }
+  void** dp;
+  RC(ensure(ctx, ctx->d_peers, nranks, &dp));
+  CK(cudaMemcpyAsync(dp, ctx->peer_staging.data(), nranks * sizeof(void*), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return SNAP_OK;
+}
+
+// restore_job materialization after a resize (ckpt.cpp:504-533): rank
+// `src_rank`'s layout (= the installed grid) is rebuilt from the striped
+// shards of the last multi-rank snapshot, reading peer shards over NVLink.
+int snap_restore_shards(snap_ctx* ctx, int src_rank, int verify) {
+  if (!ctx || !ctx->comm || !ctx->exchanged || !ctx->selected || src_rank < 0 ||
+      src_rank >= ctx->nranks)
+    return fail(ctx, SNAP_EINVAL, "restore_shards needs a multi-rank snapshot");
+  if (int(ctx->peer_staging.size()) != ctx->nranks)
+    return fail(ctx, SNAP_EINVAL, "restore_shards: peers not imported (snap_ipc_import)");
+  if (ctx->counts[src_rank] != ctx->nchunks)
+    return fail(ctx, SNAP_EINVAL, "restore_shards: installed grid is not src_rank's layout");
+  CK(cudaSetDevice(ctx->device));
+  if (!ctx->shard_offsets_all) {
+    uint64_t* tt;
+    RC(ensure(ctx, ctx->d_nbad, 4, &tt));
+    const uint64_t n = uint64_t(ctx->nranks) * ctx->maxn;
+    CK(cudaMemsetAsync(ctx->d_shard_off.p, 0xff, n * 8, ctx->stream));
+    for (int q = 0; q < ctx->nranks; ++q)
+      CKL(snap::launch_shard_scan(P<int32_t>(ctx->d_writer), P<uint32_t>(ctx->d_glens), ctx->nranks,
+                                  ctx->maxn, q, false, P<uint64_t>(ctx->scan),
+                                  P<uint64_t>(ctx->d_shard_off), nullptr, nullptr, tt, ctx->stream));
+    ctx->shard_offsets_all = true;
+  }
+  unsigned long long* miss;
+  RC(ensure(ctx, ctx->d_nbad, 4, &miss));
+  {
+    ProfScope ps(ctx, kProfRestore);
+    CKL(snap::launch_scatter_shards(ctx->arena, ctx->grid, P<uint32_t>(ctx->d_lens),
+                                    uint64_t(src_rank) * ctx->maxn, P<uint64_t>(ctx->owner),
+                                    P<int32_t>(ctx->d_writer), P<uint64_t>(ctx->d_shard_off),
+                                    P<const uint8_t*>(ctx->d_peers), miss + 1, ctx->stream));
+  }
+  unsigned long long missing = 0;
+  CK(cudaMemcpyAsync(&missing, miss + 1, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (missing)
+    return fail(ctx, SNAP_EFAULT, "restore_shards: " + std::to_string(missing) +
+                                      " chunk(s) have no source (known/older blobs)");
+  if (!verify) return SNAP_OK;
+  // expected digests: src_rank's row of the allgathered vector
+  return verify_grid(ctx, P<uint64_t>(ctx->d_gdig) + uint64_t(src_rank) * ctx->maxn);
 }
 
 // ---------------------------------------------------------------- K3

@@ -94,6 +94,11 @@ struct snap_ctx {
   std::vector<uint64_t> h_spec;
   bool h_spec_valid = false;
   DevMem d_moved;
+
+  // resize / reshard: peer ranks' staging shards mapped over CUDA IPC
+  std::vector<void*> peer_staging;  // [nranks]; own rank = local staging
+  DevMem d_peers;
+  bool shard_offsets_all = false;   // d_shard_off valid for every writer
 };
 
 inline int fail(snap_ctx* c, int code, const std::string& msg) {

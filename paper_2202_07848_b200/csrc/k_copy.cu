@@ -93,6 +93,33 @@ k_scatter(uint8_t* __restrict__ arena, GridDev g, const uint32_t* __restrict__ l
   }
 }
 
+// K4 across GPUs (restore_job materialization after a resize, ckpt.cpp:517-528):
+// chunk g of rank `src_rank`'s layout is read from the shard of the rank that
+// wrote its first occurrence — over NVLink when that shard lives on a peer GPU
+// (CUDA-IPC-mapped staging pointers) — and written at its recorded address.
+// One pass: no intermediate gathered image in HBM.
+__global__ void __launch_bounds__(kThreads)
+k_scatter_shards(uint8_t* __restrict__ arena, GridDev g, const uint32_t* __restrict__ lens,
+                 uint64_t row, const uint64_t* __restrict__ owner,
+                 const int32_t* __restrict__ writer, const uint64_t* __restrict__ shard_off,
+                 const uint8_t* const* __restrict__ shards, unsigned long long* __restrict__ missing) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t w0 = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * kThreads) >> 5;
+  unsigned long long miss = 0;
+  for (uint64_t gc = w0; gc < g.nchunks; gc += nw) {
+    const uint64_t o = owner[row + gc];
+    const int32_t w = o == ~0ull ? -1 : writer[o];
+    if (w < 0) {
+      miss += 1;
+      continue;
+    }
+    uint8_t* dst = const_cast<uint8_t*>(chunk_ptr(arena, g, gc));
+    warp_copy(dst, shards[w] + shard_off[o], lens[gc], lane);
+  }
+  if (lane == 0 && miss) atomicAdd(missing, miss);
+}
+
 __global__ void k_compare(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b,
                           uint64_t n, unsigned long long* nbad) {
   unsigned long long bad = 0;
@@ -213,6 +240,19 @@ int launch_splice_in(uint8_t* arena, const GridDev& to, const uint32_t* lens, co
   if (blocks > copy_grid()) blocks = copy_grid();
   k_splice_in<<<unsigned(blocks), kThreads, 0, s>>>(arena, to, lens, want, match, dig_from, cache,
                                                     cache_base, counters);
+  return 1;
+}
+
+int launch_scatter_shards(uint8_t* arena, const GridDev& g, const uint32_t* lens, uint64_t row,
+                         const uint64_t* owner, const int32_t* writer, const uint64_t* shard_off,
+                         const uint8_t* const* shards, unsigned long long* missing,
+                         cudaStream_t s) {
+  cudaMemsetAsync(missing, 0, sizeof(unsigned long long), s);
+  if (g.nchunks == 0) return 0;
+  uint64_t blocks = (g.nchunks * 32 + kThreads - 1) / kThreads;
+  if (blocks > copy_grid()) blocks = copy_grid();
+  k_scatter_shards<<<unsigned(blocks), kThreads, 0, s>>>(arena, g, lens, row, owner, writer,
+                                                         shard_off, shards, missing);
   return 1;
 }
 

@@ -83,6 +83,11 @@ int launch_gather(const uint8_t* arena, const GridDev& g, const uint32_t* lens,
                   unsigned int* nmoved = nullptr);
 int launch_scatter(uint8_t* arena, const GridDev& g, const uint32_t* lens, const uint8_t* image,
                    const uint64_t* src_off, cudaStream_t s);
+// K4 from striped shards (peer staging pointers): chunk g of global row `row`.
+int launch_scatter_shards(uint8_t* arena, const GridDev& g, const uint32_t* lens, uint64_t row,
+                          const uint64_t* owner, const int32_t* writer, const uint64_t* shard_off,
+                          const uint8_t* const* shards, unsigned long long* missing,
+                          cudaStream_t s);
 int launch_compare(const uint64_t* a, const uint64_t* b, uint64_t n, unsigned long long* nbad,
                    cudaStream_t s);
 

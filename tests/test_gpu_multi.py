@@ -30,3 +30,18 @@ def test_dist_snapshot_parity(world):
     print(r.stdout[-3000:], r.stderr[-3000:])
     assert r.returncode == 0
     assert "DIST PARITY OK" in r.stdout
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_dist_resize_reshard(world):
+    """C5 shape: snapshot on N, restore on N/2 from NVLink-mapped shards, reshard on N/2,
+    restore on N/4 — bit-exact and digest-verified at every stage."""
+    if ngpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr=127.0.0.1", "--master-port=29534",
+           os.path.join(ROOT, "tests", "dist_resize_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    print(r.stdout[-3000:], r.stderr[-3000:])
+    assert r.returncode == 0
+    assert "RESIZE PARITY OK" in r.stdout
