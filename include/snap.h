@@ -240,6 +240,9 @@ int snap_splice_recorded(snap_ctx* ctx, int rank, uint64_t* digests, uint64_t* n
 
 int snap_comm_unique_id(void* id128);
 int snap_comm_init(snap_ctx* ctx, int nranks, int rank, const void* id128);
+/* Collective over the current communicator's ranks (call before re-forming a
+ * smaller/larger device-level world on resize, collectives.cpp:37-59). */
+int snap_comm_destroy(snap_ctx* ctx);
 /* With a communicator attached, snap_select allgathers every rank's digest
  * vector (padded to the largest rank, rank-major) and selects over the global
  * canonical order; selection vectors then have n_global = nranks * max_per_rank

@@ -100,6 +100,7 @@ _SIGS = {
                                 C.c_uint64, C.c_int]),
     "snap_comm_unique_id": (C.c_int, [C.c_void_p]),
     "snap_comm_init": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
+    "snap_comm_destroy": (C.c_int, [C.c_void_p]),
     "snap_allreduce": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, C.c_uint64]),
     "snap_host_alloc": (C.c_int, [C.c_uint64, C.POINTER(C.c_void_p)]),
     "snap_host_free": (C.c_int, [C.c_void_p]),
@@ -515,6 +516,9 @@ class Ctx:
     def comm_init(self, nranks: int, rank: int, uid: bytes):
         buf = (C.c_uint8 * 128).from_buffer_copy(uid)
         self._ck(self._L.snap_comm_init(self.h, nranks, rank, buf), "snap_comm_init")
+
+    def comm_destroy(self):
+        self._ck(self._L.snap_comm_destroy(self.h), "snap_comm_destroy")
 
     def allreduce(self, dtype, addr, elems):
         self._ck(self._L.snap_allreduce(self.h, dtype, addr, elems), "snap_allreduce")

@@ -1079,13 +1079,34 @@ int snap_comm_init(snap_ctx* ctx, int nranks, int rank, const void* id128) {
   CK(cudaSetDevice(ctx->device));
   ncclUniqueId id;
   std::memcpy(&id, id128, 128);
-  if (ctx->comm) ncclCommDestroy(ctx->comm);
-  ctx->comm = nullptr;
+  if (ctx->comm) return fail(ctx, SNAP_EINVAL, "comm_init: destroy the current communicator "
+                                               "first (snap_comm_destroy, collective)");
   CKN(ncclCommInitRank(&ctx->comm, nranks, id, rank));
   ctx->nranks = nranks;
   ctx->rank = rank;
   ctx->glens_valid = false;
   ctx->exchanged = false;
+  ctx->spec_ready = false;
+  return SNAP_OK;
+}
+
+// Collective over the communicator's ranks (the rendezvous of a resize,
+// collectives.cpp:37-59, rebuilds the device-level world afterwards).
+int snap_comm_destroy(snap_ctx* ctx) {
+  if (!ctx) return SNAP_EINVAL;
+  if (!ctx->comm) return SNAP_OK;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (size_t r = 0; r < ctx->peer_staging.size(); ++r)
+    if (int(r) != ctx->rank && ctx->peer_staging[r]) cudaIpcCloseMemHandle(ctx->peer_staging[r]);
+  ctx->peer_staging.clear();
+  CKN(ncclCommDestroy(ctx->comm));
+  ctx->comm = nullptr;
+  ctx->nranks = 1;
+  ctx->rank = 0;
+  ctx->glens_valid = false;
+  ctx->exchanged = false;
+  ctx->selected = false;
   ctx->spec_ready = false;
   return SNAP_OK;
 }

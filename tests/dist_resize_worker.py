@@ -47,6 +47,7 @@ def main():
     ok = True
 
     def new_comm(members):
+        ctx.comm_destroy()  # collective over the previous world (every rank that had one)
         uid = torch.zeros(128, dtype=torch.uint8)
         if rank == members[0]:
             uid[:] = torch.frombuffer(bytearray(snap.Ctx.unique_id()), dtype=torch.uint8)

@@ -26,7 +26,7 @@ def test_dist_snapshot_parity(world):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={world}", "--master-addr=127.0.0.1", "--master-port=29533",
            os.path.join(ROOT, "tests", "dist_snapshot_worker.py")]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=ROOT)
     print(r.stdout[-3000:], r.stderr[-3000:])
     assert r.returncode == 0
     assert "DIST PARITY OK" in r.stdout
@@ -41,7 +41,7 @@ def test_dist_resize_reshard(world):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={world}", "--master-addr=127.0.0.1", "--master-port=29534",
            os.path.join(ROOT, "tests", "dist_resize_worker.py")]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=ROOT)
     print(r.stdout[-3000:], r.stderr[-3000:])
     assert r.returncode == 0
     assert "RESIZE PARITY OK" in r.stdout
