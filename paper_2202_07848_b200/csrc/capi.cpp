@@ -175,6 +175,24 @@ int stripe_impl(snap_ctx* ctx) {
 // multi-rank: chunks of buffers hinted replicated are predicted striped
 // (writer = local_index % nranks), others written by their own rank; shard
 // order follows the predicted global index (first holder's rank, local index).
+// Staging capacity: a whole image on one GPU (every chunk may be staged); for a
+// multi-rank shard the predicted shard size + margin. keep = preserve the
+// speculative bytes already written when growing.
+int staging_reserve(snap_ctx* ctx, uint64_t bytes, bool keep, uint8_t** out) {
+  bytes = std::min<uint64_t>(std::max<uint64_t>(bytes, 256), std::max<uint64_t>(ctx->grid_bytes, 256));
+  if (bytes <= ctx->staging.cap) {
+    *out = static_cast<uint8_t*>(ctx->staging.p);
+    return SNAP_OK;
+  }
+  if (ctx->d2h) CK(cudaStreamSynchronize(ctx->d2h));  // in-flight D2H reads of the old image
+  return ensure_keep(ctx, ctx->staging, bytes, keep ? ctx->staging.cap : 0, out);
+}
+
+uint64_t staging_target(const snap_ctx* ctx) {
+  if (!ctx->comm || ctx->nranks == 1 || ctx->spec_bytes == 0) return ctx->grid_bytes;
+  return ctx->spec_bytes + ctx->spec_bytes / 16 + (64ull << 20);
+}
+
 bool replicated_hint(const snap_buf& b) {
   if (b.flags & SNAP_BUF_REPLICATED) return true;
   if (b.flags & SNAP_BUF_PRIVATE) return false;
@@ -216,6 +234,10 @@ int init_spec(snap_ctx* ctx) {
   CK(cudaMemcpyAsync(d, spec.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->spec_ready = true;
+  uint64_t top = 0;
+  for (uint64_t g = 0; g < n; ++g)
+    if (spec[g] != ~0ull) top = std::max<uint64_t>(top, spec[g] + ctx->h_lens[g]);
+  ctx->spec_bytes = top;
   ctx->h_spec = std::move(spec);
   ctx->h_spec_valid = true;
   return SNAP_OK;
@@ -236,7 +258,7 @@ int hash_fused(snap_ctx* ctx, uint64_t c0 = 0, uint64_t c1 = 0) {
   }
   if (!ctx->spec_ready) RC(init_spec(ctx));
   uint8_t* st;
-  RC(ensure(ctx, ctx->staging, ctx->grid_bytes, &st));
+  RC(staging_reserve(ctx, staging_target(ctx), true, &st));
   CKL(snap::launch_hash(ctx->arena, g, P<uint64_t>(ctx->d_dig),
                         P<uint64_t>(ctx->d_spec[ctx->spec_cur]), st, ctx->stream));
   ctx->spec_used = true;
@@ -245,7 +267,18 @@ int hash_fused(snap_ctx* ctx, uint64_t c0 = 0, uint64_t c1 = 0) {
 
 int compact_impl(snap_ctx* ctx, uint32_t* moved = nullptr, unsigned int* nmoved = nullptr) {
   uint8_t* st;
-  RC(ensure(ctx, ctx->staging, ctx->grid_bytes, &st));
+  const bool shard = ctx->comm && ctx->exchanged;
+  if (shard && staging_target(ctx) < ctx->grid_bytes) {
+    // shard-sized staging: learn the actual shard size, grow (keeping the
+    // speculative bytes) before the fix-up writes beyond the prediction
+    uint64_t tot[2] = {0, 0};
+    CK(cudaMemcpyAsync(tot, ctx->d_my_totals.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    RC(staging_reserve(ctx, tot[1], true, &st));
+    ctx->spec_bytes = std::max<uint64_t>(tot[1], 1);
+  } else {
+    RC(staging_reserve(ctx, ctx->grid_bytes, true, &st));
+  }
   const uint64_t* spec_cur = nullptr;
   uint64_t* spec_next = nullptr;
   if (ctx->spec_used) {
@@ -270,7 +303,7 @@ int compact_impl(snap_ctx* ctx, uint32_t* moved = nullptr, unsigned int* nmoved 
     ctx->spec_used = false;  // the image is final; a second compact re-gathers
     ctx->h_spec_valid = false;
   }
-  ctx->staging_valid = ctx->grid_bytes;
+  ctx->staging_valid = ctx->staging.cap;
   return SNAP_OK;
 }
 
@@ -820,7 +853,7 @@ int snapshot_host_pipelined(snap_ctx* ctx, const uint8_t* host_src, uint64_t add
     }
   }
   uint8_t* st;
-  RC(ensure(ctx, ctx->staging, ctx->grid_bytes, &st));
+  RC(staging_reserve(ctx, staging_target(ctx), true, &st));
   uint32_t* moved;
   RC(ensure(ctx, ctx->d_moved, n + 1, &moved));
   // chunk end addresses (canonical order, increasing: checked by the caller)
@@ -869,6 +902,7 @@ int snapshot_host_pipelined(snap_ctx* ctx, const uint8_t* host_src, uint64_t add
     ProfScope ps(ctx, kProfCompact);
     RC(compact_impl(ctx, moved, reinterpret_cast<unsigned int*>(moved + n)));
   }
+  st = static_cast<uint8_t*>(ctx->staging.p);  // the fix-up may have grown the image
   ctx->h_spec_valid = false;  // the fix-up wrote the next layout on the device
   const bool shard = ctx->comm && ctx->exchanged;
   uint64_t tot[2] = {0, 0};
@@ -906,7 +940,7 @@ int snapshot_host_pipelined(snap_ctx* ctx, const uint8_t* host_src, uint64_t add
     }
     CK(cudaStreamSynchronize(ctx->d2h));
   }
-  ctx->staging_valid = ctx->grid_bytes;
+  ctx->staging_valid = ctx->staging.cap;
   if (staged_bytes) *staged_bytes = tot[1];
   return SNAP_OK;
 }

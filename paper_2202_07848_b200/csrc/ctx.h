@@ -99,6 +99,9 @@ struct snap_ctx {
   std::vector<void*> peer_staging;  // [nranks]; own rank = local staging
   DevMem d_peers;
   bool shard_offsets_all = false;   // d_shard_off valid for every writer
+  // predicted staging bytes (multi-rank shards are sized to the prediction and
+  // grown on demand instead of reserving a whole image per GPU)
+  uint64_t spec_bytes = 0;
 };
 
 inline int fail(snap_ctx* c, int code, const std::string& msg) {
