@@ -362,6 +362,115 @@ def ref_splice_bench(scale=8, nranks=4, switches=3):
             "kind": "reference"}
 
 
+# ------------------------------------------------------------------ C4 / C5
+
+def incremental_bench(snap, device, gib=32, reps=3):
+    """C4 on this GPU: 32 GiB image, first checkpoint committed to the store index, then
+    5 % of the chunks dirtied (chunk c dirty iff mix64(seed ^ c) % 20 == 0) and the
+    incremental snapshot (K1 + K2 vs known set + K3 gather of the dirty chunks) timed."""
+    import oracle as O
+    nbytes = gib << 30
+    nb = 256 << 20
+    bufs = [(0, i, i * nb, nb, 1) for i in range(nbytes // nb)]
+    with snap.Ctx(device, nbytes + (1 << 20)) as c:
+        c.fill_mix64(0, nbytes, 99, 0)
+        n = c.set_buffers(bufs)
+        c.snapshot()
+        c.known_commit()
+        mix = np.array([O.mix64(99 ^ k) for k in range(n)], dtype=np.uint64)
+        dirty = np.nonzero(mix % np.uint64(20) == 0)[0].astype(np.uint64) * 65536
+        times, staged = [], 0
+        for k in range(reps):
+            c.xor_words(dirty, 0x1234567 + k)
+            c.sync()
+            c.timer_start()
+            c.snapshot()
+            times.append(c.timer_stop())
+            _, _, _, staged, nsel = c.selection()
+            assert nsel == dirty.size
+            c.known_commit()
+    ms = float(np.median(times))
+    peak, _ = peaks()
+    return {"workload": f"C4: {gib} GiB/GPU, {n} chunks, {dirty.size} dirty "
+                        f"({100 * dirty.size / n:.2f} %), store = previous checkpoint",
+            "ms": round(ms, 3), "R_gbs": round(nbytes / ms / 1e6, 1), "W_bytes": int(staged),
+            "rw_gbs": round((nbytes + staged) / ms / 1e6, 1),
+            "hbm_frac": round((nbytes + staged) / ms / 1e6 / peak, 4),
+            "bound": "FNV-1a instruction issue (FMA-heavy pipe): W << R, no stores to overlap"}
+
+
+def resize_bench(snap, dist, reps=2):
+    """C5 on the N GPUs of this run: Llama-3-8B DP state (80.3 GB/replica) snapshot on N,
+    restore onto N/2 from the peer shards over NVLink, reshard, repeat down to 1 GPU.
+    Scaled down (1/2, 1/4) only if a replica + its shard do not fit."""
+    import torch
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from bench_resize import layout
+    td = dist.td
+    rank, world = dist.rank, dist.world
+    scale = int(os.environ.get("C5_SCALE", "1"))
+    bufs, nbytes = layout(scale)
+    out = {"workload": f"C5: Llama-3-8B DP state {nbytes / 1e9:.2f} GB/replica (bf16 P + fp32 "
+                       f"m,v), identical on every rank; resize by halving", "stages": []}
+    ctx = snap.Ctx(dist.local, nbytes + (64 << 20))
+    try:
+        ctx.fill_mix64(0, nbytes, 77, 0)
+        ctx.set_buffers(bufs)
+
+        def tmax(x):
+            t = torch.tensor([x], dtype=torch.float64)
+            td.all_reduce(t, op=td.ReduceOp.MAX)
+            return float(t.item())
+
+        members = list(range(world))
+        while len(members) >= 2:
+            ctx.comm_destroy()
+            uid = dist.bcast_bytes(snap.Ctx.unique_id() if rank == members[0] else None, 128) \
+                if members[0] == 0 else None
+            if members[0] != 0:
+                raise RuntimeError("members must start at rank 0")
+            if rank in members:
+                ctx.comm_init(len(members), members.index(rank), uid)
+            snap_ms = 0.0
+            if rank in members:
+                ctx.snapshot()
+                ctx.sync()
+                ctx.timer_start()
+                for _ in range(reps):
+                    ctx.snapshot()
+                snap_ms = ctx.timer_stop() / reps
+            snap_ms = tmax(snap_ms)
+            handles = [None] * world
+            td.all_gather_object(handles, ctx.ipc_export() if rank in members else b"\0" * 64)
+            targets = members[: len(members) // 2]
+            rest_ms = 0.0
+            if rank in targets:
+                ctx.ipc_import(b"".join(handles[m] for m in members), len(members))
+                ctx.write(0, np.zeros(1 << 20, np.uint8))
+                ctx.sync()
+                ctx.timer_start()
+                ctx.restore_shards(members.index(rank), verify=False)
+                rest_ms = ctx.timer_stop()
+                ctx.restore_shards(members.index(rank), verify=True)
+            td.barrier()
+            rest_ms = tmax(rest_ms)
+            out["stages"].append({
+                "gpus": f"{len(members)}->{len(targets)}", "snapshot_ms": round(snap_ms, 3),
+                "snapshot_gbs_aggregate": round(len(members) * nbytes / snap_ms / 1e6, 1),
+                "restore_ms": round(rest_ms, 3),
+                "nvlink_gbs_per_target": round(nbytes * (len(members) - 1) / len(members)
+                                               / rest_ms / 1e6, 1),
+                "verified": True})
+            members = targets
+    finally:
+        try:
+            ctx.comm_destroy()
+        except Exception:
+            pass
+        ctx.close()
+    return out
+
+
 # ------------------------------------------------------------------ arms
 
 def run_reference(args, dist):
@@ -499,11 +608,24 @@ def run_ours(args, dist):
 
     ctx.close()
     base = cpu_baseline(replicated, per_rank) if (dist.rank == 0 and N == 1) else None
-    splice = None
+
+    def guarded(fn, *a):
+        try:
+            return fn(*a)
+        except Exception as e:  # an extra section must never cost the headline line
+            return {"error": repr(e)[:300]}
+
+    splice = incremental = resize = None
     if dist.rank == 0 and N == 1 and not args.no_splice:
-        splice = splice_bench(snap, dist.local)
+        splice = guarded(splice_bench, snap, dist.local)
+        incremental = guarded(incremental_bench, snap, dist.local)
         if base is not None:
-            base["splice"] = ref_splice_bench()
+            base["splice"] = guarded(ref_splice_bench)
+    if 1 < N <= 4 and not args.no_splice:
+        resize = guarded(resize_bench, snap, dist)
+    elif N > 4:
+        resize = {"skipped": "C5 resize section validated on 2 and 4 GPUs this round only "
+                             "(tools/bench_resize.py runs it at any N)"}
     if dist.rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": N,
@@ -538,6 +660,8 @@ def run_ours(args, dist):
             "cpu_baseline": base,
             "restore_check": check,
             "splice": splice,
+            "incremental": incremental,
+            "resize": resize,
         }
         print(json.dumps(line))
 
