@@ -26,6 +26,13 @@ namespace snap {
 namespace {
 
 constexpr uint32_t kFull = 0xffffffffu;
+__device__ __forceinline__ uint4 ld_shared16(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr));
+  return v;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -113,25 +120,29 @@ struct HashCfg {
 // also written to staging + offset with coalesced 16-byte streaming stores
 // read back from shared memory, so the image is read from HBM once for hash
 // and compaction together.
-template <class C>
+template <class C, int PS>
 __global__ void __launch_bounds__(C::kWarps * 32, 1)
 k_hash(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ chunk_dig,
        const uint64_t* __restrict__ spec_off, uint8_t* __restrict__ staging) {
   constexpr int CH = C::kCh, SLAB = C::kSlab, ST = C::kStages, NP = C::kPages;
-  constexpr int NU = C::kUnits;
+  constexpr int NU = C::kUnits, PPI = C::kPagesPerInstr;
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   uint8_t* wbuf = smem + warp * C::kWarpBytes;
+  const uint32_t wbuf_u = smem_u32(wbuf);
   uint8_t* dsm = smem + C::kWarps * C::kWarpBytes + warp * C::kDescBytes;
   uint64_t* dptr = reinterpret_cast<uint64_t*>(dsm);               // [2][NP][2] src,dst
   uint32_t* dlen = reinterpret_cast<uint32_t*>(dsm + 2 * NP * 16);  // [2][NP]
 
-  const uint32_t ppc_shift = g.chunk_shift - g.page_shift;
-  const uint32_t slab_shift = __ffs(SLAB) - 1;
-  const uint32_t ns_shift = g.page_shift - slab_shift;  // steps per page (log2)
+  // PS != 0: page size known at compile time (4 KiB), so every page stride
+  // below is an immediate offset
+  const uint32_t page_shift = PS ? PS : g.page_shift;
+  const uint32_t ppc_shift = g.chunk_shift - page_shift;
+  constexpr uint32_t slab_shift = SLAB == 256 ? 8 : (SLAB == 128 ? 7 : (SLAB == 64 ? 6 : 5));
+  const uint32_t ns_shift = page_shift - slab_shift;  // steps per page (log2)
   const uint32_t ns = 1u << ns_shift;
-  const uint64_t pb = 1ull << g.page_shift;
+  const uint64_t pb = 1ull << page_shift;
   const uint64_t c_end = g.c_end ? g.c_end : g.nchunks;
   const uint64_t slot_base = g.c_begin << ppc_shift;
   const uint64_t nslots = (c_end - g.c_begin) << ppc_shift;
@@ -142,12 +153,25 @@ k_hash(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ chun
   const uint64_t my_tasks = (ntasks - gw + nw - 1) / nw;
   const uint64_t nsteps = my_tasks << ns_shift;
   const uint32_t u = lane % NU, q = lane / NU;  // copy role: unit u of page q + k*PPI
+  // shared-memory byte offset of (page q + k*PPI, unit u) inside a stage:
+  // (q + k*PPI)*SLAB + ((u ^ sw(q + k*PPI)) << 4); sw only depends on k
+  // through (k*PPI) & 7, so two bases (even/odd k) + immediates cover all k
+  auto copy_off = [&](int k) -> uint32_t {
+    const int j = k * PPI + q;
+    return uint32_t(j) * SLAB + ((u ^ C::sw(j)) << 4);
+  };
+  // per-lane hash read address (stage 0): slab `lane` with its swizzle bits;
+  // unit uu is at (hbase ^ (uu << 4)) + stage * kStageBytes + c * 32 * SLAB
+  const uint32_t hbase = wbuf_u + lane * SLAB + (C::sw(lane) << 4);
 
   bool reg0 = false, reg1 = false, wr0 = false, wr1 = false;
   const uint8_t *rsrc0 = nullptr, *rsrc1 = nullptr;
   uint8_t *rdst0 = nullptr, *rdst1 = nullptr;
+  uint32_t ist = 0, cst = 0;  // stage of the next issue / of the step being consumed
 
   auto issue = [&](uint64_t p) {
+    const uint32_t st = ist;
+    ist = ist + 1 == ST ? 0 : ist + 1;
     if (p < nsteps) {
       const uint64_t i = p >> ns_shift;
       const uint32_t s = static_cast<uint32_t>(p) & (ns - 1);
@@ -168,7 +192,7 @@ k_hash(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ chun
           if (gc < c_end) {
             const uint32_t b = find_buf(g, gc);
             const uint64_t k = gc - __ldg(g.cstart + b);
-            const uint64_t in_chunk = (slot & ((1u << ppc_shift) - 1)) << g.page_shift;
+            const uint64_t in_chunk = (slot & ((1u << ppc_shift) - 1)) << page_shift;
             const uint64_t off = (k << g.chunk_shift) + in_chunk;
             const uint64_t bytes = __ldg(g.bytes + b);
             if (off < bytes) {
@@ -201,23 +225,20 @@ k_hash(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ chun
         }
         __syncwarp();
       }
-      const uint32_t sbase = smem_u32(wbuf + (p % ST) * C::kStageBytes);
+      const uint32_t sbase = wbuf_u + st * C::kStageBytes;
       const uint32_t soff = s * SLAB + u * 16;
       if (par ? reg1 : reg0) {
         const uint8_t* src = (par ? rsrc1 : rsrc0) + q * pb + soff;
 #pragma unroll
-        for (int k = 0; k < C::kCopyInstr; ++k) {
-          const int j = k * C::kPagesPerInstr + q;
-          cp_async16(sbase + j * SLAB + ((u ^ C::sw(j)) << 4), src);
-          src += C::kPagesPerInstr * pb;
-        }
+        for (int k = 0; k < C::kCopyInstr; ++k)
+          cp_async16(sbase + copy_off(k), src + uint64_t(k) * PPI * pb);
       } else {
 #pragma unroll
         for (int k = 0; k < C::kCopyInstr; ++k) {
-          const int j = k * C::kPagesPerInstr + q;
+          const int j = k * PPI + q;
           const uint32_t len = dlen[par * NP + j];
           if (soff < len)
-            cp_async16(sbase + j * SLAB + ((u ^ C::sw(j)) << 4),
+            cp_async16(sbase + copy_off(k),
                        reinterpret_cast<const uint8_t*>(dptr[(par * NP + j) * 2]) + soff);
         }
       }
@@ -225,30 +246,27 @@ k_hash(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ chun
     cp_commit();
   };
 
-  // Speculative compaction of step t: coalesced 16-byte stores (kUnits lanes
-  // per slab) read back from the swizzled stage buffer.
-  auto store = [&](uint64_t t) {
+  // Speculative compaction of the consumed step: coalesced 16-byte streaming
+  // stores (kUnits lanes per slab) read back from the swizzled stage buffer.
+  auto store = [&](uint64_t t, uint32_t st) {
     const uint64_t i = t >> ns_shift;
     const uint32_t par = static_cast<uint32_t>(i & 1);
     if (!(par ? wr1 : wr0)) return;
     const uint32_t s = static_cast<uint32_t>(t) & (ns - 1);
-    const uint8_t* sb = wbuf + (t % ST) * C::kStageBytes;
+    const uint8_t* sb = wbuf + st * C::kStageBytes;
     const uint32_t soff = s * SLAB + u * 16;
     if (par ? reg1 : reg0) {
       uint8_t* dst = (par ? rdst1 : rdst0) + q * pb + soff;
 #pragma unroll
-      for (int k = 0; k < C::kCopyInstr; ++k) {
-        const int j = k * C::kPagesPerInstr + q;
-        st_stream16(dst, *reinterpret_cast<const uint4*>(sb + j * SLAB + ((u ^ C::sw(j)) << 4)));
-        dst += C::kPagesPerInstr * pb;
-      }
+      for (int k = 0; k < C::kCopyInstr; ++k)
+        st_stream16(dst + uint64_t(k) * PPI * pb, *reinterpret_cast<const uint4*>(sb + copy_off(k)));
     } else {
 #pragma unroll
       for (int k = 0; k < C::kCopyInstr; ++k) {
-        const int j = k * C::kPagesPerInstr + q;
+        const int j = k * PPI + q;
         uint8_t* dst = reinterpret_cast<uint8_t*>(dptr[(par * NP + j) * 2 + 1]);
         if (dst && soff < dlen[par * NP + j])
-          st_stream16(dst + soff, *reinterpret_cast<const uint4*>(sb + j * SLAB + ((u ^ C::sw(j)) << 4)));
+          st_stream16(dst + soff, *reinterpret_cast<const uint4*>(sb + copy_off(k)));
       }
     }
   };
@@ -274,17 +292,17 @@ k_hash(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ chun
         hi[c] = static_cast<uint32_t>(kFnvOffset >> 32);
       }
     }
-    store(t);
-    const uint8_t* stage = wbuf + (t % ST) * C::kStageBytes;
+    const uint32_t st = cst;
+    cst = cst + 1 == ST ? 0 : cst + 1;
+    store(t, st);
+    const uint32_t sadd = st * C::kStageBytes;
 #pragma unroll
     for (int uu = 0; uu < NU; ++uu) {
       // CH independent chains interleaved unit by unit
       uint4 v[CH];
 #pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        const uint32_t j = c * 32 + lane;
-        v[c] = *reinterpret_cast<const uint4*>(stage + j * SLAB + ((uu ^ C::sw(j)) << 4));
-      }
+      for (int c = 0; c < CH; ++c)
+        v[c] = ld_shared16((hbase ^ (uu << 4)) + sadd + c * 32 * SLAB);
 #pragma unroll
       for (int c = 0; c < CH; ++c) {
         if (s * SLAB < mylen[c]) {
@@ -669,13 +687,15 @@ int sm_count() {
 
 }  // namespace
 
-// Variant selection (SNAP_HASH_VARIANT env, default 0 = CfgA, the fastest fused
-// hash+compaction on B200: 2.32 vs 2.14-2.28 TB/s of image for B/C/D); all compute
+// Variant selection (SNAP_HASH_VARIANT env; default: CfgE for fused launches,
+// CfgA for hash-only launches — the fastest of the measured geometries); all compute
 // identical digests, they only differ in latency hiding.
 using CfgA = HashCfg<1, 128, 3, 16>;  // 512 chains/SM, 128-B slabs
 using CfgB = HashCfg<2, 64, 2, 16>;   // 1024 chains/SM, 64-B slabs
 using CfgC = HashCfg<2, 64, 3, 12>;   // 768 chains/SM, deeper ring
 using CfgD = HashCfg<2, 128, 2, 12>;  // 768 chains/SM, 128-B slabs
+using CfgE = HashCfg<1, 256, 2, 12>;  // 256-B slabs: DRAM-friendly write segments
+using CfgF = HashCfg<1, 256, 2, 13>;
 using WsA = WsCfg<16, 4, 3>;          // warp-specialized: 16 hash + 4 copy warps
 using WsB = WsCfg<16, 2, 3>;          // 16 hash + 2 copy warps
 using WsC = WsCfg<12, 4, 4>;          // 12 hash + 4 copy warps, deeper ring
@@ -704,7 +724,8 @@ int launch_hash_cfg(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
                     const uint64_t* spec_off, uint8_t* staging, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_hash<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem));
+    cudaFuncSetAttribute(k_hash<C, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem));
+    cudaFuncSetAttribute(k_hash<C, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem));
     attr = true;
   }
   const uint64_t c_end = g.c_end ? g.c_end : g.nchunks;
@@ -714,15 +735,22 @@ int launch_hash_cfg(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
   uint64_t blocks = (ntasks + C::kWarps - 1) / C::kWarps;
   const uint64_t cap = uint64_t(sm_count());
   if (blocks > cap) blocks = cap;
-  k_hash<C><<<unsigned(blocks), C::kWarps * 32, C::kSmem, s>>>(arena, g, chunk_dig, spec_off, staging);
+  if (g.page_shift == 12)  // the reference's 4 KiB page: strides become immediates
+    k_hash<C, 12><<<unsigned(blocks), C::kWarps * 32, C::kSmem, s>>>(arena, g, chunk_dig, spec_off,
+                                                                     staging);
+  else
+    k_hash<C, 0><<<unsigned(blocks), C::kWarps * 32, C::kSmem, s>>>(arena, g, chunk_dig, spec_off,
+                                                                    staging);
   return 1;
 }
 
 int hash_variant() {
   static int v = -1;
   if (v < 0) {
+
     const char* e = getenv("SNAP_HASH_VARIANT");
-    v = e ? atoi(e) : 0;
+    v = e ? atoi(e) : -1;
+    if (v < 0) v = 99;  // default policy
   }
   return v;
 }
@@ -738,7 +766,15 @@ int launch_hash(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
     case 4: return launch_hash_ws<WsA>(arena, g, chunk_dig, spec_off, staging, s);
     case 5: return launch_hash_ws<WsB>(arena, g, chunk_dig, spec_off, staging, s);
     case 6: return launch_hash_ws<WsC>(arena, g, chunk_dig, spec_off, staging, s);
-    default: return launch_hash_cfg<CfgA>(arena, g, chunk_dig, spec_off, staging, s);
+    case 7: return launch_hash_cfg<CfgE>(arena, g, chunk_dig, spec_off, staging, s);
+    case 8: return launch_hash_cfg<CfgF>(arena, g, chunk_dig, spec_off, staging, s);
+    default:
+      // fused hash + speculative stores: 256-B slabs (contiguous 256-B write
+      // segments per page keep mixed read/write DRAM traffic at ~6 TB/s;
+      // 128-B segments cap it at ~5.2, tools/micro/pattern_bw2.cu);
+      // hash only: 128-B slabs and 16 warps hide the FNV chain latency better
+      if (spec_off) return launch_hash_cfg<CfgE>(arena, g, chunk_dig, spec_off, staging, s);
+      return launch_hash_cfg<CfgA>(arena, g, chunk_dig, spec_off, staging, s);
   }
 }
 
