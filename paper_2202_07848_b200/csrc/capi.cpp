@@ -370,7 +370,8 @@ int snap_close(snap_ctx* ctx) {
         &ctx->scan, &ctx->sel, &ctx->owner, &ctx->offsets, &ctx->sel_list, &ctx->totals,
         &ctx->staging, &ctx->d_counts, &ctx->d_gdig, &ctx->d_glens, &ctx->d_writer,
         &ctx->d_shard_off, &ctx->d_my_list, &ctx->d_my_off, &ctx->d_my_totals, &ctx->d_dig2,
-        &ctx->d_expect, &ctx->d_nbad, &ctx->d_srcoff, &ctx->d_spec[0], &ctx->d_spec[1]})
+        &ctx->d_expect, &ctx->d_nbad, &ctx->d_srcoff, &ctx->d_spec[0], &ctx->d_spec[1],
+        &ctx->d_tmaps})
     release(*m);
   for (cudaEvent_t e : ctx->prof.pool) cudaEventDestroy(e);
   if (ctx->arena) cudaFree(ctx->arena);
@@ -529,6 +530,7 @@ int snap_set_buffers(snap_ctx* ctx, const snap_buf* bufs, uint64_t n, const snap
   ctx->h_lens = std::move(lens);
   ctx->grid = GridDev{da, db, dc, static_cast<uint32_t>(n), ctx->nchunks, log2u(g.page_bytes),
                       log2u(g.chunk_bytes)};
+  build_tmaps(ctx, ctx->d_tmaps, addr.data(), bytes.data(), static_cast<uint32_t>(n), ctx->grid);
   ctx->hashed = false;
   ctx->selected = false;
   ctx->exchanged = false;

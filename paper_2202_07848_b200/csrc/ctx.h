@@ -99,6 +99,7 @@ struct snap_ctx {
   std::vector<void*> peer_staging;  // [nranks]; own rank = local staging
   DevMem d_peers;
   bool shard_offsets_all = false;   // d_shard_off valid for every writer
+  DevMem d_tmaps;  // per-buffer TMA tensor maps of the installed grid
   // predicted staging bytes (multi-rank shards are sized to the prediction and
   // grown on demand instead of reserving a whole image per GPU)
   uint64_t spec_bytes = 0;
@@ -210,6 +211,24 @@ inline uint64_t table_cap(uint64_t n) {
 
 int select_with_known(snap_ctx* ctx, const uint64_t* dig, const uint32_t* lens, uint64_t n,
                       TableDev kn, bool use_known);
+
+// Per-buffer TMA tensor maps for the hash-only TMA K1 variant (4 KiB pages; only
+// built when that variant is selected). On any
+// encode failure the grid simply keeps the cp.async kernel (tmaps = nullptr).
+inline void build_tmaps(snap_ctx* ctx, DevMem& m, const uint64_t* addr, const uint64_t* bytes,
+                        uint32_t n, GridDev& g) {
+  g.tmaps = nullptr;
+  if (!snap::hash_tma_selected() || g.page_shift != 12 || n == 0) return;
+  std::vector<uint8_t> host(size_t(n) * 128);
+  if (snap::encode_tensor_maps(ctx->arena, addr, bytes, n, host.data()) != 0) return;
+  uint8_t* d;
+  if (ensure(ctx, m, host.size(), &d) != SNAP_OK) return;
+  if (cudaMemcpyAsync(d, host.data(), host.size(), cudaMemcpyHostToDevice, ctx->stream) !=
+          cudaSuccess ||
+      cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+    return;
+  g.tmaps = d;
+}
 
 inline int check_range(snap_ctx* ctx, uint64_t addr, uint64_t bytes) {
   if (addr > ctx->arena_bytes || bytes > ctx->arena_bytes - addr)

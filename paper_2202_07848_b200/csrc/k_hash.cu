@@ -688,8 +688,9 @@ int sm_count() {
 }  // namespace
 
 // Variant selection (SNAP_HASH_VARIANT env; default: CfgE for fused launches,
-// CfgA for hash-only launches — the fastest of the measured geometries); all compute
-// identical digests, they only differ in latency hiding.
+// CfgA for hash-only launches — the fastest of the measured geometries; 10 = the
+// TMA tensor-load hash-only kernel, k_hash_tma.cu); all compute identical digests,
+// they only differ in how the bytes reach shared memory and in latency hiding.
 using CfgA = HashCfg<1, 128, 3, 16>;  // 512 chains/SM, 128-B slabs
 using CfgB = HashCfg<2, 64, 2, 16>;   // 1024 chains/SM, 64-B slabs
 using CfgC = HashCfg<2, 64, 3, 12>;   // 768 chains/SM, deeper ring
@@ -747,13 +748,14 @@ int launch_hash_cfg(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
 int hash_variant() {
   static int v = -1;
   if (v < 0) {
-
     const char* e = getenv("SNAP_HASH_VARIANT");
     v = e ? atoi(e) : -1;
     if (v < 0) v = 99;  // default policy
   }
   return v;
 }
+
+bool hash_tma_selected() { return hash_variant() == 10; }
 
 int launch_hash(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
                 const uint64_t* spec_off, uint8_t* staging, cudaStream_t s) {
@@ -768,11 +770,17 @@ int launch_hash(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
     case 6: return launch_hash_ws<WsC>(arena, g, chunk_dig, spec_off, staging, s);
     case 7: return launch_hash_cfg<CfgE>(arena, g, chunk_dig, spec_off, staging, s);
     case 8: return launch_hash_cfg<CfgF>(arena, g, chunk_dig, spec_off, staging, s);
+    case 9: return launch_hash_cfg<CfgA>(arena, g, chunk_dig, spec_off, staging, s);
+    case 10:
+      if (!spec_off && hash_tma_ok(g)) return launch_hash_tma(arena, g, chunk_dig, s);
+      [[fallthrough]];
     default:
       // fused hash + speculative stores: 256-B slabs (contiguous 256-B write
       // segments per page keep mixed read/write DRAM traffic at ~6 TB/s;
       // 128-B segments cap it at ~5.2, tools/micro/pattern_bw2.cu);
       // hash only: 128-B slabs and 16 warps hide the FNV chain latency better
+      // (the TMA variant measured 3.66 TB/s vs 3.73: the kernel is bound by the
+      // FMA-heavy pipe, not by the copy instructions TMA removes)
       if (spec_off) return launch_hash_cfg<CfgE>(arena, g, chunk_dig, spec_off, staging, s);
       return launch_hash_cfg<CfgA>(arena, g, chunk_dig, spec_off, staging, s);
   }

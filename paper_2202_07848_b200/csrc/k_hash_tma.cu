@@ -1,0 +1,313 @@
+// k_hash_tma.cu — K1 hash-only with TMA tensor loads (used when no
+// speculative stores are needed: incremental snapshots, splice swap-out
+// digests, restore verification).
+//
+// Same lane = page-chain scheme as k_hash.cu, but a warp's stage fill is ONE
+// instruction: for a "regular" task (32 full, contiguous 4 KiB pages of one
+// buffer) an elected lane issues cp.async.bulk.tensor.2d with a box of
+// 32 pages x 128 B from the buffer's tensor map (rows = pages, pitch 4 KiB);
+// the hardware SWIZZLE_128B layout is exactly the XOR layout the hash lanes
+// read (16-B unit u of page j at u ^ (j & 7)), and completion is counted in
+// bytes on one mbarrier per stage. Irregular tasks (buffer edges, tail pages)
+// use one 1D bulk copy per valid page slab (unswizzled layout) on the same
+// barrier. This removes the per-lane cp.async address math that costs ~1.2
+// instructions per hashed byte in the cp.async kernel.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstring>
+
+#include "snap_internal.h"
+
+namespace snap {
+namespace {
+
+constexpr uint32_t kFull = 0xffffffffu;
+constexpr int kSlab = 128;
+constexpr int kStageBytes = 32 * kSlab;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint4 ld_shared16(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tx)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, int x, int y,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(tmap), "r"(x), "r"(y), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes,
+                                          uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+// FNV-1a byte step (see k_hash.cu for the instruction-level derivation)
+__device__ __forceinline__ void fnv_step(uint32_t& lo, uint32_t& hi, uint32_t b) {
+  const uint32_t x = lo ^ (b & 0xffu);
+  const uint64_t t = static_cast<uint64_t>(x) * kFnvPrimeLo;
+  uint32_t y;
+  asm("{\n\t.reg .u32 s;\n\tshl.b32 s, %1, 8;\n\tadd.u32 %0, s, %2;\n\t}"
+      : "=r"(y)
+      : "r"(x), "r"(static_cast<uint32_t>(t >> 32)));
+  hi = hi * kFnvPrimeLo + y;
+  lo = static_cast<uint32_t>(t);
+}
+__device__ __forceinline__ void fnv_word(uint32_t& lo, uint32_t& hi, uint32_t w) {
+  fnv_step(lo, hi, w);
+  fnv_step(lo, hi, w >> 8);
+  fnv_step(lo, hi, w >> 16);
+  fnv_step(lo, hi, w >> 24);
+}
+__device__ __forceinline__ uint32_t find_buf(const GridDev& g, uint64_t gc) {
+  uint32_t lo = 0, hi = g.nbufs;
+  while (hi - lo > 1) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (__ldg(g.cstart + mid) <= gc) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// 4 KiB pages (PS = 12) only: the tensor maps describe a buffer as rows of 4 KiB.
+template <int WARPS, int ST>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+k_hash_tma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ chunk_dig) {
+  constexpr uint32_t page_shift = 12, ns_shift = page_shift - 7, ns = 1u << ns_shift;
+  constexpr uint64_t pb = 1ull << page_shift;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1 KiB alignment: the 128B-swizzle atom is 8 rows x 128 B
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* wbuf = smem + warp * ST * kStageBytes;
+  const uint32_t wbuf_u = smem_u32(wbuf);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * ST * kStageBytes) + warp * ST;
+  const uint32_t bar0 = smem_u32(bars);
+  const CUtensorMap* maps = static_cast<const CUtensorMap*>(g.tmaps);
+
+  const uint32_t ppc_shift = g.chunk_shift - page_shift;
+  const uint64_t c_end = g.c_end ? g.c_end : g.nchunks;
+  const uint64_t slot_base = g.c_begin << ppc_shift;
+  const uint64_t nslots = (c_end - g.c_begin) << ppc_shift;
+  const uint64_t ntasks = (nslots + 31) >> 5;
+  const uint64_t gw = uint64_t(blockIdx.x) * WARPS + warp;
+  const uint64_t nw = uint64_t(gridDim.x) * WARPS;
+  if (gw >= ntasks) return;
+  const uint64_t nsteps = ((ntasks - gw + nw - 1) / nw) << ns_shift;
+
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < ST; ++s) mbar_init(bar0 + 8 * s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+
+  // producer-side state of the task being loaded (warp-uniform except p_src/p_len)
+  bool p_reg = false;
+  uint32_t p_map = 0, p_row = 0;
+  const uint8_t* p_src = nullptr;
+  uint32_t p_len = 0;
+  uint32_t reg_bits = 0;  // bit (i & 1): task i was loaded through the tensor path
+  uint32_t ist = 0, cst = 0;
+
+  auto issue = [&](uint64_t p) {
+    const uint32_t st = ist;
+    ist = ist + 1 == ST ? 0 : ist + 1;
+    if (p >= nsteps) return;
+    const uint64_t i = p >> ns_shift;
+    const uint32_t s = static_cast<uint32_t>(p) & (ns - 1);
+    if (s == 0) {
+      const uint64_t slot = slot_base + (gw + i * nw) * 32 + lane;
+      const uint64_t gc = slot >> ppc_shift;
+      uint32_t b = 0xffffffffu, row = 0;
+      p_src = nullptr;
+      p_len = 0;
+      if (gc < c_end) {
+        b = find_buf(g, gc);
+        const uint64_t k = gc - __ldg(g.cstart + b);
+        const uint64_t off = (k << g.chunk_shift) + ((slot & ((1u << ppc_shift) - 1)) << page_shift);
+        const uint64_t bytes = __ldg(g.bytes + b);
+        if (off < bytes) {
+          const uint64_t rem = bytes - off;
+          p_len = static_cast<uint32_t>(rem < pb ? rem : pb);
+          p_src = arena + __ldg(g.addr + b) + off;
+          row = static_cast<uint32_t>(off >> page_shift);
+        }
+      }
+      const uint32_t b0 = __shfl_sync(kFull, b, 0);
+      const uint32_t r0 = __shfl_sync(kFull, row, 0);
+      p_reg = __all_sync(kFull, b == b0 && p_len == pb && row == r0 + lane);
+      p_map = b0;
+      p_row = r0;
+      if (p_reg) reg_bits |= 1u << (i & 1); else reg_bits &= ~(1u << (i & 1));
+    }
+    const uint32_t bar = bar0 + 8 * st;
+    const uint32_t dst = wbuf_u + st * kStageBytes;
+    if (p_reg) {
+      if (lane == 0) {
+        mbar_arrive_tx(bar, kStageBytes);
+        tma_load_2d(dst, maps + p_map, static_cast<int>(s * kSlab), static_cast<int>(p_row), bar);
+      }
+    } else {
+      const bool valid = s * kSlab < p_len;
+      const uint32_t nvalid = __popc(__ballot_sync(kFull, valid));
+      if (lane == 0) mbar_arrive_tx(bar, nvalid * kSlab);
+      __syncwarp();
+      if (valid) bulk_load(dst + lane * kSlab, p_src + s * kSlab, kSlab, bar);
+    }
+  };
+
+#pragma unroll
+  for (int p = 0; p < ST - 1; ++p) issue(p);
+
+  uint32_t lo = 0, hi = 0, mylen = 0;
+  const uint32_t hswz = wbuf_u + lane * kSlab;  // + ((uu ^ (lane & 7)) << 4) when swizzled
+  for (uint64_t t = 0; t < nsteps; ++t) {
+    issue(t + ST - 1);
+    const uint32_t st = cst;
+    cst = cst + 1 == ST ? 0 : cst + 1;
+    const uint64_t i = t >> ns_shift;
+    const uint32_t s = static_cast<uint32_t>(t) & (ns - 1);
+    if (s == 0) {
+      // own page length of task i (recomputed: the producer may already be ahead)
+      const uint64_t slot = slot_base + (gw + i * nw) * 32 + lane;
+      const uint64_t gc = slot >> ppc_shift;
+      mylen = 0;
+      if (gc < c_end) {
+        const uint32_t b = find_buf(g, gc);
+        const uint64_t k = gc - __ldg(g.cstart + b);
+        const uint64_t off = (k << g.chunk_shift) + ((slot & ((1u << ppc_shift) - 1)) << page_shift);
+        const uint64_t bytes = __ldg(g.bytes + b);
+        if (off < bytes) mylen = static_cast<uint32_t>(bytes - off < pb ? bytes - off : pb);
+      }
+      lo = static_cast<uint32_t>(kFnvOffset);
+      hi = static_cast<uint32_t>(kFnvOffset >> 32);
+    }
+    mbar_wait(bar0 + 8 * st, static_cast<uint32_t>((t / ST) & 1));
+    const uint32_t sw = (reg_bits >> (i & 1)) & 1 ? static_cast<uint32_t>(lane & 7) << 4 : 0u;
+    const uint32_t a = (hswz + st * kStageBytes) | sw;
+    if (s * kSlab < mylen) {
+#pragma unroll
+      for (int uu = 0; uu < 8; ++uu) {
+        const uint4 v = ld_shared16(a ^ (uu << 4));
+        fnv_word(lo, hi, v.x);
+        fnv_word(lo, hi, v.y);
+        fnv_word(lo, hi, v.z);
+        fnv_word(lo, hi, v.w);
+      }
+    }
+    __syncwarp();  // the slot is refilled ST - 1 steps later by this warp's lane 0
+    if (s == ns - 1) {
+      const uint64_t slot0 = slot_base + (gw + i * nw) * 32;
+      if (ppc_shift == 0) {
+        if (mylen > 0) chunk_dig[slot0 + lane] = (uint64_t(hi) << 32) | lo;
+      } else {
+        const uint32_t ppc = 1u << ppc_shift;
+        const int base = lane & ~static_cast<int>(ppc - 1);
+        uint32_t flo = static_cast<uint32_t>(kFnvOffset);
+        uint32_t fhi = static_cast<uint32_t>(kFnvOffset >> 32);
+        for (uint32_t qq = 0; qq < ppc; ++qq) {
+          const uint32_t plo = __shfl_sync(kFull, lo, base + qq);
+          const uint32_t phi = __shfl_sync(kFull, hi, base + qq);
+          const uint32_t pl = __shfl_sync(kFull, mylen, base + qq);
+          if (pl > 0) {
+            fnv_word(flo, fhi, plo);
+            fnv_word(flo, fhi, phi);
+          }
+        }
+        if (lane == base && mylen > 0) chunk_dig[(slot0 + lane) >> ppc_shift] = (uint64_t(fhi) << 32) | flo;
+      }
+    }
+  }
+}
+
+constexpr int kTmaWarps = 16, kTmaStages = 3;
+constexpr size_t kTmaSmem = size_t(kTmaWarps) * kTmaStages * kStageBytes +
+                            size_t(kTmaWarps) * kTmaStages * 8 + 1024;
+
+}  // namespace
+
+bool hash_tma_ok(const GridDev& g) { return g.tmaps != nullptr && g.page_shift == 12; }
+
+int launch_hash_tma(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_hash_tma<kTmaWarps, kTmaStages>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTmaSmem));
+    attr = true;
+  }
+  const uint64_t c_end = g.c_end ? g.c_end : g.nchunks;
+  if (c_end <= g.c_begin) return 0;
+  const uint64_t ntasks = (((c_end - g.c_begin) << (g.chunk_shift - g.page_shift)) + 31) / 32;
+  uint64_t blocks = (ntasks + kTmaWarps - 1) / kTmaWarps;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (blocks > uint64_t(sms)) blocks = uint64_t(sms);
+  k_hash_tma<kTmaWarps, kTmaStages><<<unsigned(blocks), kTmaWarps * 32, kTmaSmem, s>>>(arena, g,
+                                                                                     chunk_dig);
+  return 1;
+}
+
+// Host: one 2D tensor map per buffer (rows = its full 4 KiB pages, pitch 4 KiB,
+// box 32 rows x 128 B, 128B swizzle). Buffers with no full page get an unused
+// zeroed entry (their tasks are irregular).
+int encode_tensor_maps(const uint8_t* arena, const uint64_t* addr, const uint64_t* bytes,
+                       uint32_t nbufs, void* host_maps /* nbufs x 128 B */) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return -1;
+    encode = reinterpret_cast<EncodeFn>(fn);
+  }
+  CUtensorMap* maps = static_cast<CUtensorMap*>(host_maps);
+  for (uint32_t b = 0; b < nbufs; ++b) {
+    std::memset(&maps[b], 0, sizeof(CUtensorMap));
+    const cuuint64_t rows = bytes[b] >> 12;
+    if (rows == 0) continue;
+    const cuuint64_t dims[2] = {4096, rows};
+    const cuuint64_t strides[1] = {4096};
+    const cuuint32_t box[2] = {128, 32};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode(&maps[b], CU_TENSOR_MAP_DATA_TYPE_UINT8, 2,
+                        const_cast<uint8_t*>(arena + addr[b]), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return -2;
+  }
+  return 0;
+}
+
+}  // namespace snap

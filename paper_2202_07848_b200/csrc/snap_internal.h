@@ -28,6 +28,8 @@ struct GridDev {
   // snapshot hash each slab as soon as its H2D copy lands
   uint64_t c_begin = 0;
   uint64_t c_end = 0;
+  // per-buffer CUtensorMap array in device memory (4 KiB pages), or nullptr
+  const void* tmaps = nullptr;
 };
 
 // Open-addressing digest table (dedup + known set), power-of-two capacity.
@@ -43,6 +45,13 @@ constexpr unsigned long long kEmptyKey = 0xffffffffffffffffull;
 // of every chunk whose spec_off[chunk] != ~0 to staging + spec_off[chunk]).
 int launch_hash(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
                 const uint64_t* spec_off, uint8_t* staging, cudaStream_t s);
+// K1 hash-only through TMA tensor loads (needs grid tensor maps, 4 KiB pages).
+bool hash_tma_ok(const GridDev& g);
+bool hash_tma_selected();  // SNAP_HASH_VARIANT=10: tensor maps are built for the grid
+int launch_hash_tma(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig, cudaStream_t s);
+// host: one 128-byte CUtensorMap per buffer into host_maps; 0 on success
+int encode_tensor_maps(const uint8_t* arena, const uint64_t* addr, const uint64_t* bytes,
+                       uint32_t nbufs, void* host_maps);
 int launch_buf_fold(const GridDev& g, const uint64_t* chunk_dig, uint64_t* buf_dig, cudaStream_t s);
 int launch_fill_mix64(uint64_t* dst, uint64_t nwords, uint64_t seed, uint64_t base, cudaStream_t s);
 int launch_xor_words(uint8_t* arena, const uint64_t* addrs, uint64_t n, uint64_t value,

@@ -21,7 +21,7 @@ struct RankGrid {
   std::vector<uint32_t> lens;
   std::vector<uint64_t> chunk_addr;
   uint64_t nchunks = 0, bytes = 0;
-  DevMem d_addr, d_bytes, d_cstart, d_lens, d_rec;
+  DevMem d_addr, d_bytes, d_cstart, d_lens, d_rec, d_tmaps;
   GridDev grid;
   bool recorded = false;
 };
@@ -39,7 +39,8 @@ void splice_release(snap_ctx* ctx) {
   SpliceState* S = ctx->splice;
   if (!S) return;
   for (auto& [r, g] : S->ranks)
-    for (DevMem* m : {&g.d_addr, &g.d_bytes, &g.d_cstart, &g.d_lens, &g.d_rec}) release(*m);
+    for (DevMem* m : {&g.d_addr, &g.d_bytes, &g.d_cstart, &g.d_lens, &g.d_rec, &g.d_tmaps})
+      release(*m);
   for (auto& [k, m] : S->match) release(m);
   for (DevMem* m : {&S->cache, &S->ck, &S->cv, &S->counters}) release(*m);
   delete S;
@@ -119,6 +120,7 @@ int snap_splice_set_rank(snap_ctx* ctx, int rank, const snap_buf* bufs, uint64_t
   CK(cudaMemcpyAsync(dl, R.lens.data(), R.nchunks * 4, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   R.grid = GridDev{da, db, dc, uint32_t(nb), R.nchunks, log2u(g.page_bytes), log2u(g.chunk_bytes)};
+  build_tmaps(ctx, R.d_tmaps, addr.data(), bytes.data(), uint32_t(nb), R.grid);
   R.recorded = false;
   for (auto it = S->match.begin(); it != S->match.end();) {
     if (it->first.first == rank || it->first.second == rank) {

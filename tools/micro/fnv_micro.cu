@@ -28,8 +28,50 @@ __device__ __forceinline__ void stepC(uint32_t& lo, uint32_t& hi, uint32_t b) {
   lo = (uint32_t)h; hi = (uint32_t)(h >> 32);
 }
 
+
+// hi folded into the wide multiply's 64-bit addend: Y = hi*P + (x<<8) (shift via PRMT on the
+// ALU pipe), {lo,hi} = x*P + (Y<<32): one IMAD + one IMAD.WIDE per byte, no add
+__device__ __forceinline__ void stepD(uint32_t& lo, uint32_t& hi, uint32_t b, uint32_t z) {
+  const uint32_t x = lo ^ (b & 0xffu);
+  uint32_t s;
+  asm("prmt.b32 %0, %1, 0, 0x2104;" : "=r"(s) : "r"(x));
+  const uint32_t y = hi * 0x1b3u + s;
+  uint64_t t;
+  asm("{\n\t.reg .u64 c;\n\tmov.b64 c, {%2, %3};\n\tmad.wide.u32 %0, %1, 435, c;\n\t}"
+      : "=l"(t) : "r"(x), "r"(z), "r"(y));
+  lo = (uint32_t)t;
+  hi = (uint32_t)(t >> 32);
+}
+// same with a plain shift (ptxas picks the unit)
+__device__ __forceinline__ void stepE(uint32_t& lo, uint32_t& hi, uint32_t b) {
+  const uint32_t x = lo ^ (b & 0xffu);
+  const uint32_t y = hi * 0x1b3u + (x << 8);
+  const uint64_t t = (uint64_t)x * 0x1b3u + ((uint64_t)y << 32);
+  lo = (uint32_t)t;
+  hi = (uint32_t)(t >> 32);
+}
+
+// shift via PRMT (ALU only), then a plain add
+__device__ __forceinline__ void stepF(uint32_t& lo, uint32_t& hi, uint32_t b) {
+  const uint32_t x = lo ^ (b & 0xffu);
+  uint32_t s;
+  asm("prmt.b32 %0, %1, 0, 0x2104;" : "=r"(s) : "r"(x));
+  const uint64_t t = (uint64_t)x * 0x1b3u;
+  hi = hi * 0x1b3u + (uint32_t)(t >> 32) + s;
+  lo = (uint32_t)t;
+}
+// lo by IMAD, carry + shifted x by IMAD.HI with the PRMT'd shift as addend
+__device__ __forceinline__ void stepH(uint32_t& lo, uint32_t& hi, uint32_t b) {
+  const uint32_t x = lo ^ (b & 0xffu);
+  uint32_t s, y;
+  asm("prmt.b32 %0, %1, 0, 0x2104;" : "=r"(s) : "r"(x));
+  asm("mad.hi.u32 %0, %1, 435, %2;" : "=r"(y) : "r"(x), "r"(s));
+  hi = hi * 0x1b3u + y;
+  lo = x * 0x1b3u;
+}
+
 template <int V, int CH>
-__global__ void __launch_bounds__(512) k(uint64_t* out, int iters) {
+__global__ void __launch_bounds__(512) k(uint64_t* out, int iters, uint32_t z) {
   uint32_t lo[CH], hi[CH];
   for (int c = 0; c < CH; ++c) { lo[c] = 0x84222325u + c; hi[c] = 0xcbf29ce4u; }
   uint32_t w = threadIdx.x * 2654435761u;
@@ -45,6 +87,10 @@ __global__ void __launch_bounds__(512) k(uint64_t* out, int iters) {
           if (V == 0) stepA(lo[c], hi[c], ww >> (8 * bb));
           if (V == 1) stepB(lo[c], hi[c], ww >> (8 * bb));
           if (V == 2) stepC(lo[c], hi[c], ww >> (8 * bb));
+          if (V == 3) stepD(lo[c], hi[c], ww >> (8 * bb), z);
+          if (V == 4) stepE(lo[c], hi[c], ww >> (8 * bb));
+          if (V == 5) stepF(lo[c], hi[c], ww >> (8 * bb));
+          if (V == 6) stepH(lo[c], hi[c], ww >> (8 * bb));
         }
       }
     }
@@ -60,11 +106,11 @@ void run(const char* name, int threads, int blocksPerSM) {
   cudaMalloc(&d, 148 * 4 * 1024 * 8);
   int iters = 2048;
   int blocks = 148 * blocksPerSM;
-  k<V, CH><<<blocks, threads>>>(d, 16);
+  k<V, CH><<<blocks, threads>>>(d, 16, 0u);
   cudaEvent_t a, b;
   cudaEventCreate(&a); cudaEventCreate(&b);
   cudaEventRecord(a);
-  k<V, CH><<<blocks, threads>>>(d, iters);
+  k<V, CH><<<blocks, threads>>>(d, iters, 0u);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   float ms; cudaEventElapsedTime(&ms, a, b);
@@ -78,5 +124,9 @@ int main() {
   run<0, 1>("A", 512, 1); run<0, 2>("A", 512, 1); run<0, 4>("A", 256, 1); run<0, 1>("A", 1024, 1); run<0, 2>("A", 1024, 1);
   run<1, 1>("B-hi", 512, 1); run<1, 2>("B-hi", 512, 1); run<1, 2>("B-hi", 1024, 1);
   run<2, 1>("C-64", 512, 1); run<2, 2>("C-64", 512, 1); run<2, 2>("C-64", 1024, 1);
+  run<3, 1>("D-prmt", 512, 1); run<3, 2>("D-prmt", 512, 1); run<3, 4>("D-prmt", 256, 1); run<3, 2>("D-prmt", 1024, 1);
+  run<4, 1>("E-wide", 512, 1); run<4, 2>("E-wide", 512, 1); run<4, 2>("E-wide", 1024, 1);
+  run<5, 1>("F-prmt+", 512, 1); run<5, 2>("F-prmt+", 512, 1); run<5, 2>("F-prmt+", 1024, 1);
+  run<6, 1>("H-hi", 512, 1); run<6, 2>("H-hi", 512, 1); run<6, 2>("H-hi", 1024, 1);
   return 0;
 }
