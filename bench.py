@@ -399,6 +399,63 @@ def incremental_bench(snap, device, gib=32, reps=3):
             "bound": "FNV-1a instruction issue (FMA-heavy pipe): W << R, no stores to overlap"}
 
 
+def persist_bench(snap, device, mib=256):
+    """§8f row 2, the on-disk format: C1's 256 MiB image (4096 unique 64 KiB chunks)
+    snapshotted, persisted as blobs/<2hex>/<16hex> files straight from the device staging
+    (pinned slabs + writer threads), then loaded into a fresh context (reader threads ->
+    H2D -> K4 scatter -> K1 verification). Wall clock of each host call; files land in the
+    page cache (no fsync, same for the reference arm). Reference arm: BlobStore::put of
+    every chunk + BlobStore::persist (ckpt.cpp:16-52), single thread as written."""
+    import shutil
+    import tempfile
+    import oracle as O
+    nbytes = mib << 20
+    root = tempfile.mkdtemp(prefix="snap_persist_bench_")
+    try:
+        with snap.Ctx(device, nbytes + (1 << 20)) as c:
+            c.fill_mix64(0, nbytes, 1, 0)
+            c.set_buffers([(0, 0, 0, nbytes, 0)])
+            c.snapshot()
+            c.sync()
+            t = time.perf_counter()
+            c.persist(os.path.join(root, "first"))  # first call: allocates the pinned slabs
+            t_first = time.perf_counter() - t
+            t = time.perf_counter()
+            st = c.persist(os.path.join(root, "ours"))  # steady state: every file new
+            tp = time.perf_counter() - t
+            c.fill_mix64(0, nbytes, 2, 0)  # scramble, then restore from the directory
+            c.sync()
+            t = time.perf_counter()
+            ls = c.load(os.path.join(root, "ours"), verify=True)
+            tl = time.perf_counter() - t
+        out = {"workload": f"C1 {mib} MiB image, {st['blobs']} x 64 KiB blobs "
+                           "(page cache, no fsync)",
+               "persist_ms": round(tp * 1e3, 2), "persist_gbs": round(nbytes / tp / 1e9, 2),
+               "persist_first_call_ms": round(t_first * 1e3, 2),
+               "load_verify_ms": round(tl * 1e3, 2), "load_gbs": round(nbytes / tl / 1e9, 2),
+               "files": int(st["written"]), "loaded_blobs": int(ls["blobs"]),
+               "threads": min(os.cpu_count() or 1, 16)}
+        R = O.ref()
+        if R is not None:
+            import ctypes as C
+            img = O.fill_mix64(nbytes // 8, 1, 0)
+            store = R.ref_store_new()
+            d = C.c_uint64()
+            t = time.perf_counter()
+            for k in range(0, nbytes // 8, 8192):
+                R.ref_store_put(store, img[k:].ctypes.data_as(C.c_void_p), 8192, C.byref(d))
+            t_put = time.perf_counter()
+            R.ref_store_persist(store, os.path.join(root, "ref").encode())
+            tr = time.perf_counter() - t
+            R.ref_store_free(store)
+            out["reference_put_persist_ms"] = round(tr * 1e3, 1)
+            out["reference_persist_only_ms"] = round((t + tr - t_put) * 1e3, 1)
+            out["reference_gbs"] = round(nbytes / tr / 1e9, 3)
+        return out
+    finally:
+        shutil.rmtree(root, ignore_errors=True)
+
+
 def resize_bench(snap, dist, reps=2):
     """C5 on the N GPUs of this run: Llama-3-8B DP state (80.3 GB/replica) snapshot on N,
     restore onto N/2 from the peer shards over NVLink, reshard, repeat down to 1 GPU.
@@ -615,10 +672,11 @@ def run_ours(args, dist):
         except Exception as e:  # an extra section must never cost the headline line
             return {"error": repr(e)[:300]}
 
-    splice = incremental = resize = None
+    splice = incremental = resize = persist = None
     if dist.rank == 0 and N == 1 and not args.no_splice:
         splice = guarded(splice_bench, snap, dist.local)
         incremental = guarded(incremental_bench, snap, dist.local)
+        persist = guarded(persist_bench, snap, dist.local)
         if base is not None:
             base["splice"] = guarded(ref_splice_bench)
     if 1 < N <= 4 and not args.no_splice:
@@ -662,6 +720,7 @@ def run_ours(args, dist):
             "splice": splice,
             "incremental": incremental,
             "resize": resize,
+            "persist": persist,
         }
         print(json.dumps(line))
 

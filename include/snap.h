@@ -273,6 +273,46 @@ int snap_restore_shards(snap_ctx* ctx, int src_rank, int verify);
  * collectives.cpp:147-154 local closer). Async. */
 int snap_allreduce(snap_ctx* ctx, int dtype, uint64_t addr, uint64_t elems);
 
+/* ------------------------------------- on-disk format (persist / load) */
+
+/* BlobStore::blob_rel_path (ckpt.cpp:35-40): "blobs/<2hex>/<16hex>" of the
+ * digest, NUL-terminated into out (cap >= 32). Host only, no context. */
+int snap_blob_rel_path(uint64_t digest, char* out, uint64_t cap);
+
+typedef struct {
+  uint64_t blobs;         /* blobs this rank staged (its files to write / files read) */
+  uint64_t written;       /* files created by this call */
+  uint64_t present;       /* already in the directory: content-addressed, skipped */
+  uint64_t bytes;         /* bytes written (upload_bytes) or read */
+  uint64_t layout_chunks; /* chunks of the rank's layout */
+  uint64_t layout_blobs;  /* distinct blobs the layout references */
+  uint64_t layout_bytes;  /* their bytes (total_blob_bytes) */
+  uint64_t layout_bufs;   /* buffer records of the layout (installed by snap_load) */
+} snap_persist_stats;
+
+/* BlobStore::persist (ckpt.cpp:42-52) for the last snapshot plus the
+ * manifest's device section (ckpt.cpp:194-262): every chunk this rank staged
+ * (its shard when a communicator is attached) becomes
+ * <dir>/blobs/<2hex>/<16hex> holding the chunk's bytes (tmp + rename; blobs
+ * already present are skipped, like a non-fresh BlobStore::put). The rank's
+ * layout (buffer records + chunk digests) goes to <dir>/layout.<rank>.snapl
+ * (read by snap_load) and <dir>/manifest.dev.<rank>.json. Blob names are the
+ * chunk digests of the installed geometry; with page_bytes == chunk_bytes the
+ * name is digest_of_words(content) and the files are byte-identical to what
+ * the reference's BlobStore writes for those chunks. host_image (optional) is
+ * this rank's staging image already on the host (snap_snapshot_host output);
+ * otherwise the device staging is streamed out through pinned slabs.
+ * nthreads <= 0: one writer thread per core, at most 16. */
+int snap_persist(snap_ctx* ctx, const char* dir, const void* host_image, uint64_t host_bytes,
+                 int nthreads, snap_persist_stats* stats);
+/* restore_job materialization from a directory (ckpt.cpp:504-533): installs
+ * rank `rank`'s layout, streams every referenced blob through pinned slabs to
+ * the device and scatters the chunks to their recorded addresses (K4).
+ * verify != 0 re-hashes the restored grid (BlobStore::get verification,
+ * ckpt.cpp:26-27): SNAP_EFAULT on a corrupt, truncated or missing blob. */
+int snap_load(snap_ctx* ctx, const char* dir, int rank, int verify, int nthreads,
+              snap_persist_stats* stats);
+
 /* ---------------------------------------------------------- timing */
 
 int snap_timer_start(snap_ctx* ctx);

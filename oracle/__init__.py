@@ -99,6 +99,10 @@ def ref():
         L.ref_store_total_bytes.argtypes = [C.c_void_p]
         L.ref_store_count.restype = C.c_uint64
         L.ref_store_count.argtypes = [C.c_void_p]
+        L.ref_store_persist.restype = C.c_int
+        L.ref_store_persist.argtypes = [C.c_void_p, C.c_char_p]
+        L.ref_blob_rel_path.restype = C.c_int
+        L.ref_blob_rel_path.argtypes = [C.c_uint64, C.c_char_p, C.c_uint64]
         L.ref_alloc_new.restype = C.c_void_p
         L.ref_alloc_new.argtypes = [C.c_uint64, C.c_uint64]
         L.ref_alloc_free_obj.argtypes = [C.c_void_p]
@@ -153,6 +157,19 @@ def digest_of_words(words: np.ndarray) -> int:
 
 def digest_of_bytes(b: bytes) -> int:
     return lib().or_fnv1a(b, len(b), 14695981039346656037)
+
+
+def blob_rel_path(digest: int) -> str:
+    """BlobStore::blob_rel_path (ckpt.cpp:35-40): "blobs/" + first two hex digits of the
+    zero-padded 16-digit lowercase hex digest + "/" + the 16 digits."""
+    h = f"{digest:016x}"
+    return f"blobs/{h[:2]}/{h}"
+
+
+def persisted_tree(blobs):
+    """BlobStore::persist (ckpt.cpp:42-52) of a set of blobs {digest: bytes}: the expected
+    {relative path: content} of the directory (content = the blob's words, little endian)."""
+    return {blob_rel_path(d): bytes(b) for d, b in blobs.items()}
 
 
 def bufs_array(bufs):

@@ -51,6 +51,21 @@ int ref_store_get(void* s, uint64_t digest, uint64_t* out, uint64_t n) {
 }
 uint64_t ref_store_total_bytes(void* s) { return static_cast<ckpt::BlobStore*>(s)->total_bytes(); }
 uint64_t ref_store_count(void* s) { return static_cast<ckpt::BlobStore*>(s)->count(); }
+// BlobStore::persist / blob_rel_path (ckpt.cpp:35-52); 0 ok, -1 on any exception
+int ref_store_persist(void* s, const char* dir) {
+  try {
+    static_cast<ckpt::BlobStore*>(s)->persist(dir);
+    return 0;
+  } catch (...) {
+    return -1;
+  }
+}
+int ref_blob_rel_path(uint64_t digest, char* out, uint64_t cap) {
+  const std::string p = ckpt::BlobStore::blob_rel_path(sim::Digest{digest});
+  if (p.size() + 1 > cap) return -1;
+  std::memcpy(out, p.c_str(), p.size() + 1);
+  return 0;
+}
 
 // ---- mem::BidiAllocator (alloc.cpp:62-155) ----
 void* ref_alloc_new(uint64_t low, uint64_t high) { return new mem::BidiAllocator(low, high); }

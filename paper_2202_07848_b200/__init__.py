@@ -66,6 +66,19 @@ class SnapGeom(C.Structure):
 
 _lib = None
 
+class PersistStats(C.Structure):
+    """snap_persist_stats: blob files of one persist/load call and the rank layout's sizes
+    (Manifest sizes: upload_bytes, total_blob_bytes; ckpt.hpp:102-107)."""
+
+    _fields_ = [("blobs", C.c_uint64), ("written", C.c_uint64), ("present", C.c_uint64),
+                ("bytes", C.c_uint64), ("layout_chunks", C.c_uint64),
+                ("layout_blobs", C.c_uint64), ("layout_bytes", C.c_uint64),
+                ("layout_bufs", C.c_uint64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 _SIGS = {
     "snap_open": (C.c_int, [C.c_int, C.c_uint64, C.POINTER(C.c_void_p)]),
     "snap_close": (C.c_int, [C.c_void_p]),
@@ -106,6 +119,11 @@ _SIGS = {
     "snap_host_free": (C.c_int, [C.c_void_p]),
     "snap_snapshot_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p,
                                      C.c_uint64, C.POINTER(C.c_uint64), C.c_void_p]),
+    "snap_blob_rel_path": (C.c_int, [C.c_uint64, C.c_char_p, C.c_uint64]),
+    "snap_persist": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_uint64, C.c_int,
+                               C.POINTER(PersistStats)]),
+    "snap_load": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int, C.c_int, C.c_int,
+                            C.POINTER(PersistStats)]),
     "snap_global_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "snap_get_global_digests": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "snap_get_shard": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64),
@@ -157,6 +175,15 @@ def lib():
 
 def exported_symbols():
     return list(_SIGS)
+
+
+def blob_rel_path(digest: int) -> str:
+    """BlobStore::blob_rel_path (ckpt.cpp:35-40) as the product library computes it."""
+    b = C.create_string_buffer(40)
+    rc = lib().snap_blob_rel_path(C.c_uint64(digest), b, 40)
+    if rc:
+        raise SnapError(rc, "snap_blob_rel_path")
+    return b.value.decode()
 
 
 def _p(a):
@@ -414,6 +441,27 @@ class Ctx:
                                             _p(d) if d is not None else None),
                  "snap_snapshot_host")
         return sb.value
+
+    # -- on-disk format (BlobStore::persist, ckpt.cpp:42-52; restore_job, ckpt.cpp:504-533)
+    def persist(self, directory, host_ptr: int = 0, host_bytes: int = 0, threads: int = 0):
+        """Writes the last snapshot's staged chunks as blobs/<2hex>/<16hex> plus this
+        rank's layout + manifest under `directory`; returns the stats dict."""
+        st = PersistStats()
+        self._ck(self._L.snap_persist(self.h, os.fsencode(directory),
+                                      C.c_void_p(host_ptr) if host_ptr else None, host_bytes,
+                                      threads, C.byref(st)), "snap_persist")
+        return st.as_dict()
+
+    def load(self, directory, rank: int = 0, verify: bool = True, threads: int = 0):
+        """Installs rank `rank`'s persisted layout and restores its bytes from the blob files
+        (digest-verified when verify); returns the stats dict."""
+        st = PersistStats()
+        rc = self._L.snap_load(self.h, os.fsencode(directory), rank, 1 if verify else 0, threads,
+                               C.byref(st))
+        if st.layout_chunks or rc == SNAP_OK:  # the layout was installed (even if verify failed)
+            self.nchunks, self.nbufs = st.layout_chunks, st.layout_bufs
+        self._ck(rc, "snap_load")
+        return st.as_dict()
 
     def global_info(self):
         n, m = C.c_uint64(), C.c_uint64()

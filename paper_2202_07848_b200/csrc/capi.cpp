@@ -382,6 +382,8 @@ int snap_close(snap_ctx* ctx) {
   release(ctx->d_peers);
   for (cudaEvent_t e : ctx->pipe_ev) cudaEventDestroy(e);
   release(ctx->d_moved);
+  for (uint8_t* q : ctx->io_pin)
+    if (q) cudaFreeHost(q);
   if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
   if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);

@@ -103,6 +103,9 @@ struct snap_ctx {
   // predicted staging bytes (multi-rank shards are sized to the prediction and
   // grown on demand instead of reserving a whole image per GPU)
   uint64_t spec_bytes = 0;
+  // pinned slabs of the persist/load file path (allocated once, reused)
+  uint8_t* io_pin[2] = {nullptr, nullptr};
+  uint64_t io_pin_cap = 0;
 };
 
 inline int fail(snap_ctx* c, int code, const std::string& msg) {

@@ -36,3 +36,17 @@ def ctx(snap):
     c = snap.Ctx(0, 64 << 20)
     yield c
     c.close()
+
+
+@pytest.fixture(scope="session")
+def oracle_mod():
+    import oracle
+    return oracle
+
+
+@pytest.fixture(scope="session")
+def ref_lib(oracle_mod):
+    R = oracle_mod.ref()
+    if R is None:
+        pytest.skip("reference library (oracle/_ref) not built here")
+    return R

@@ -151,11 +151,56 @@ def main():
                     ok = False
         print("DIST PARITY", "OK" if ok else "FAIL", "world", world, "chunks", npr,
               "unique", int(osel.sum()))
+    ok = persist_stage(ctx, rank, world, objs, ok) and ok
     flag = torch.tensor([1 if ok else 0])
     td.broadcast(flag, 0)
     ctx.close()
     td.destroy_process_group()
     sys.exit(0 if int(flag.item()) == 1 else 1)
+
+
+def persist_stage(ctx, rank, world, objs, ok):
+    """On-disk format across ranks: every rank persists its shard of the (last) snapshot into
+    one shared directory (content-addressed, no coordination), then restores the NEXT rank's
+    layout from the directory alone into a fresh context and compares it with that rank's
+    image. Rank 0 checks that the directory holds exactly the globally unique chunks."""
+    import tempfile
+    import torch.distributed as td
+    paths = [None] * world
+    td.all_gather_object(paths, tempfile.mkdtemp(prefix="snap_persist_") if rank == 0 else None)
+    root = paths[0]
+    st = ctx.persist(root)
+    sts = [None] * world
+    td.all_gather_object(sts, st)
+    td.barrier()
+    good = True
+    peer = (rank + 1) % world
+    o = [x for x in objs if x["rank"] == peer][0]
+    bufs = [b[:5] for b in o["bufs"]]
+    nbytes = max(a + n for (_, _, a, n, _) in bufs)
+    with snap.Ctx(int(os.environ.get("LOCAL_RANK", rank)), nbytes + MIB) as c2:
+        c2.load(root, rank=peer)
+        got = c2.read(0, nbytes).view(np.uint64)
+        for (_, _, a, n, _) in bufs:
+            if not np.array_equal(got[a // 8:(a + n) // 8], o["host"][a // 8:(a + n) // 8]):
+                print(f"FAIL persist/load rank {rank} <- layout {peer}")
+                good = False
+    if rank == 0:
+        nfiles = sum(len(fs) for dp, _, fs in os.walk(os.path.join(root, "blobs")))
+        uniq = len(set(np.concatenate([O.hash_chunks([x["host"]], [b[:5] for b in x["bufs"]])[0]
+                                       for x in objs]).tolist()))
+        if nfiles != uniq or sum(s["written"] for s in sts) != uniq:
+            print(f"FAIL persist files {nfiles} written {[s['written'] for s in sts]} "
+                  f"unique {uniq}")
+            good = False
+        print("PERSIST", "OK" if good else "FAIL", "files", nfiles)
+    flags = [None] * world
+    td.all_gather_object(flags, good)
+    td.barrier()
+    if rank == 0:
+        import shutil
+        shutil.rmtree(root, ignore_errors=True)
+    return all(flags)
 
 
 def C_set_buffers(ctx, sb, n):

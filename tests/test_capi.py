@@ -48,3 +48,36 @@ def test_strerror(snap):
     L = snap.lib()
     assert L.snap_strerror(snap.SNAP_EFAULT) == b"fault (content/digest)"
     assert L.snap_strerror(0) == b"ok"
+
+
+def test_blob_rel_path_matches_reference(snap, oracle_mod, ref_lib):
+    # BlobStore::blob_rel_path (ckpt.cpp:35-40): product, oracle and the reference agree
+    import ctypes as C
+    import numpy as np
+    rng = np.random.default_rng(5)
+    ds = [0, 1, 0xff, 0xcbf29ce484222325, 2**64 - 1] + [int(x) for x in
+                                                          rng.integers(0, 2**63, 200)]
+    for d in ds:
+        b = C.create_string_buffer(64)
+        assert ref_lib.ref_blob_rel_path(C.c_uint64(d), b, 64) == 0
+        assert snap.blob_rel_path(d) == b.value.decode() == oracle_mod.blob_rel_path(d)
+
+
+def test_persisted_tree_oracle_matches_reference_store(oracle_mod, ref_lib, tmp_path):
+    # the oracle's expected directory == what the reference BlobStore::persist writes
+    import ctypes as C
+    import numpy as np
+    st = ref_lib.ref_store_new()
+    try:
+        blobs = {}
+        for i in range(40):
+            w = oracle_mod.fill_mix64(512 * (1 + i % 3), seed=11, base=i << 20)
+            d = C.c_uint64()
+            ref_lib.ref_store_put(st, w.ctypes.data_as(C.c_void_p), w.size, C.byref(d))
+            assert d.value == oracle_mod.digest_of_words(w)
+            blobs[d.value] = w.tobytes()
+        assert ref_lib.ref_store_persist(st, str(tmp_path).encode()) == 0
+    finally:
+        ref_lib.ref_store_free(st)
+    got = {str(p.relative_to(tmp_path)): p.read_bytes() for p in tmp_path.rglob("*") if p.is_file()}
+    assert got == oracle_mod.persisted_tree(blobs)
