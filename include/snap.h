@@ -273,6 +273,43 @@ int snap_restore_shards(snap_ctx* ctx, int src_rank, int verify);
  * collectives.cpp:147-154 local closer). Async. */
 int snap_allreduce(snap_ctx* ctx, int dtype, uint64_t addr, uint64_t elems);
 
+/* ------------------------------------- squash-window validation (§8f-3) */
+
+/* One entry of a rank's mutation set: ValidationRecord::mutations
+ * (splice.hpp:50-53), addr -> (bytes, digest after the window). */
+typedef struct {
+  uint64_t addr;
+  uint64_t bytes;
+  uint64_t digest;
+} snap_mutation;
+
+/* WorkerExec::do_window_open, validation branch (worker.cpp:355-362): K1
+ * digests every live, non-pending buffer of `rank` (SNAP_BUF_PENDING skipped)
+ * and keeps addr -> (bytes, digest) as the rank's open snapshot. Uses the
+ * ctx's auxiliary grid: the installed snapshot grid is left untouched. */
+int snap_window_open(snap_ctx* ctx, int rank, const snap_buf* bufs, uint64_t n);
+/* do_window_close, validation branch (worker.cpp:411-421): re-digests the
+ * rank's live, non-pending buffers; the mutation set = every buffer whose
+ * address is new or whose digest or size changed, in address order.
+ * *n_out = its size; `out` (capacity `cap`) may be NULL to query the size. */
+int snap_window_close(snap_ctx* ctx, int rank, const snap_buf* bufs, uint64_t n,
+                      snap_mutation* out, uint64_t cap, uint64_t* n_out);
+/* One rank's ValidationRecord: its mutation set (address order) and the
+ * in-window D2H copies as (bytes, digest) pairs in issue order
+ * (worker.cpp:664-669; digests from snap_digest_ranges). */
+typedef struct {
+  int32_t rank;
+  const snap_mutation* mutations;
+  uint64_t n_mutations;
+  const uint64_t* d2h; /* 2 * n_d2h words: bytes, digest */
+  uint64_t n_d2h;
+} snap_window_record;
+/* splice::validate_window (splice.cpp:21-61): records compared against the
+ * lowest rank's in rank order; returns 1 = pass, 0 = fail (reason written to
+ * `reason`, same text as the reference), <0 = error. Host only. */
+int snap_validate_window(const snap_window_record* recs, uint64_t n, char* reason,
+                         uint64_t cap);
+
 /* ------------------------------------- on-disk format (persist / load) */
 
 /* BlobStore::blob_rel_path (ckpt.cpp:35-40): "blobs/<2hex>/<16hex>" of the

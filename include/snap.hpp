@@ -10,15 +10,20 @@
 //   build_manifest device section    -> snapb200::ckpt::Snapshotter (ckpt.cpp:147-167)
 //   restore_job materialization      -> snapb200::ckpt::Snapshotter::restore* (ckpt.cpp:517-533)
 //   CollectiveEngine sum (sliced DP) -> snapb200::coll::grad_sum (collectives.cpp:137-144)
+//   splice::validate_window          -> snapb200::splice::validate_window (splice.cpp:21-61)
+//   window open/close mutation sets  -> snapb200::splice::WindowTracker (worker.cpp:351-421)
+//   BlobStore::persist + restore_job -> snapb200::ckpt::Snapshotter::persist/load (ckpt.cpp:42-52)
 //
 // Header-only; link libsnap.so.
 #pragma once
 
 #include <cstdint>
+#include <map>
 #include <optional>
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "snap.h"
@@ -220,6 +225,73 @@ class Splicer {
   vdev::Gpu* gpu_;
 };
 
+// splice.hpp:50-59
+struct ValidationRecord {
+  std::map<u64, std::pair<u64, sim::Digest>> mutations;  // addr -> (bytes, digest after window)
+  std::vector<std::pair<u64, sim::Digest>> d2h_copies;    // (bytes, digest)
+};
+struct ValidationOutcome {
+  bool pass = true;
+  std::string reason;
+};
+
+// splice.cpp:21-61 (same comparison order and reason text)
+inline ValidationOutcome validate_window(const std::map<RankId, ValidationRecord>& records) {
+  std::vector<std::vector<snap_mutation>> m;
+  std::vector<std::vector<u64>> d;
+  std::vector<snap_window_record> r;
+  for (const auto& [rank, rec] : records) {
+    m.emplace_back();
+    for (const auto& [a, bd] : rec.mutations) m.back().push_back({a, bd.first, bd.second.value});
+    d.emplace_back();
+    for (const auto& [b, dg] : rec.d2h_copies) {
+      d.back().push_back(b);
+      d.back().push_back(dg.value);
+    }
+  }
+  size_t i = 0;
+  for (const auto& [rank, rec] : records) {
+    r.push_back({rank, m[i].data(), m[i].size(), d[i].data(), rec.d2h_copies.size()});
+    ++i;
+  }
+  char why[512];
+  const int rc = snap_validate_window(r.data(), r.size(), why, sizeof why);
+  if (rc < 0) check(rc);
+  return {rc == 1, rc == 1 ? std::string() : std::string(why)};
+}
+
+// The validation branch of WorkerExec::do_window_open / do_window_close
+// (worker.cpp:355-362, 411-421) for one rank's live buffers.
+class WindowTracker {
+ public:
+  explicit WindowTracker(vdev::Gpu& gpu) : gpu_(&gpu) {}
+  void open(RankId r, const std::vector<RankBuf>& bufs) {
+    const auto b = live(r, bufs);
+    check(snap_window_open(gpu_->ctx(), r, b.data(), b.size()), gpu_->ctx());
+  }
+  // fills rec.mutations (d2h_copies are the caller's, worker.cpp:664-669)
+  void close(RankId r, const std::vector<RankBuf>& bufs, ValidationRecord& rec) {
+    const auto b = live(r, bufs);
+    std::vector<snap_mutation> out(b.size());
+    u64 n = 0;
+    check(snap_window_close(gpu_->ctx(), r, b.data(), b.size(), out.data(), out.size(), &n),
+          gpu_->ctx());
+    rec.mutations.clear();
+    for (u64 i = 0; i < n; ++i) rec.mutations[out[i].addr] = {out[i].bytes, {out[i].digest}};
+  }
+
+ private:
+  static std::vector<snap_buf> live(RankId r, const std::vector<RankBuf>& bufs) {
+    std::vector<snap_buf> b;
+    for (const auto& x : bufs)
+      if (x.live)
+        b.push_back({std::uint32_t(r), x.slot, x.addr, x.bytes, int(x.cat),
+                     x.pending_result ? SNAP_BUF_PENDING : 0u});
+    return b;
+  }
+  vdev::Gpu* gpu_;
+};
+
 }  // namespace splice
 
 namespace ckpt {
@@ -259,6 +331,26 @@ class Snapshotter {
   void commit() { check(snap_known_commit(gpu_->ctx()), gpu_->ctx()); }  // next one is incremental
   void restore_self(bool verify = true) {
     check(snap_restore_self(gpu_->ctx(), verify ? 1 : 0), gpu_->ctx());
+  }
+  // BlobStore::persist layout (ckpt.cpp:35-52) for this snapshot's staged chunks,
+  // plus the rank's layout + manifest; returns the stats
+  snap_persist_stats persist(const std::string& dir, int threads = 0) {
+    snap_persist_stats st{};
+    check(snap_persist(gpu_->ctx(), dir.c_str(), nullptr, 0, threads, &st), gpu_->ctx());
+    return st;
+  }
+  // restore_job materialization from a directory (ckpt.cpp:504-533); SimFault on a
+  // missing or corrupt blob (BlobStore::get, ckpt.cpp:23-29)
+  snap_persist_stats load(const std::string& dir, int rank = 0, bool verify = true) {
+    snap_persist_stats st{};
+    check(snap_load(gpu_->ctx(), dir.c_str(), rank, verify ? 1 : 0, 0, &st), gpu_->ctx());
+    nchunks_ = st.layout_chunks;
+    return st;
+  }
+  static std::string blob_rel_path(sim::Digest d) {  // ckpt.cpp:35-40
+    char b[40];
+    check(snap_blob_rel_path(d.value, b, sizeof b));
+    return b;
   }
 
  private:

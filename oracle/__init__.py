@@ -101,6 +101,9 @@ def ref():
         L.ref_store_count.argtypes = [C.c_void_p]
         L.ref_store_persist.restype = C.c_int
         L.ref_store_persist.argtypes = [C.c_void_p, C.c_char_p]
+        L.ref_validate_window.restype = C.c_int
+        L.ref_validate_window.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                          C.c_void_p, C.c_char_p, C.c_uint64]
         L.ref_blob_rel_path.restype = C.c_int
         L.ref_blob_rel_path.argtypes = [C.c_uint64, C.c_char_p, C.c_uint64]
         L.ref_alloc_new.restype = C.c_void_p

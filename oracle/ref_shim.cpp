@@ -6,6 +6,7 @@
 // cpu_baseline kind "reference"). Nothing in the product links it.
 #include <atomic>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <thread>
 #include <vector>
@@ -59,6 +60,26 @@ int ref_store_persist(void* s, const char* dir) {
   } catch (...) {
     return -1;
   }
+}
+// splice::validate_window (splice.cpp:21-61) over flattened records:
+// muts = (addr, bytes, digest) triples, d2h = (bytes, digest) pairs, rank-major.
+int ref_validate_window(int n, const int* ranks, const uint64_t* nmut, const uint64_t* muts,
+                        const uint64_t* nd2h, const uint64_t* d2h, char* reason, uint64_t cap) {
+  std::map<RankId, splice::ValidationRecord> recs;
+  uint64_t m = 0, c = 0;
+  for (int i = 0; i < n; ++i) {
+    splice::ValidationRecord r;
+    for (uint64_t k = 0; k < nmut[i]; ++k, ++m)
+      r.mutations[muts[3 * m]] = {muts[3 * m + 1], sim::Digest{muts[3 * m + 2]}};
+    for (uint64_t k = 0; k < nd2h[i]; ++k, ++c)
+      r.d2h_copies.push_back({d2h[2 * c], sim::Digest{d2h[2 * c + 1]}});
+    recs[ranks[i]] = std::move(r);
+  }
+  const auto out = splice::validate_window(recs);
+  const size_t k = std::min<size_t>(out.reason.size(), size_t(cap - 1));
+  std::memcpy(reason, out.reason.data(), k);
+  reason[k] = 0;
+  return out.pass ? 1 : 0;
 }
 int ref_blob_rel_path(uint64_t digest, char* out, uint64_t cap) {
   const std::string p = ckpt::BlobStore::blob_rel_path(sim::Digest{digest});

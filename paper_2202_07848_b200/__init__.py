@@ -79,6 +79,20 @@ class PersistStats(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class SnapMutation(C.Structure):
+    """snap_mutation: ValidationRecord::mutations entry (splice.hpp:50-53)."""
+
+    _fields_ = [("addr", C.c_uint64), ("bytes", C.c_uint64), ("digest", C.c_uint64)]
+
+
+class WindowRecord(C.Structure):
+    """snap_window_record: one rank's ValidationRecord (splice.hpp:50-54)."""
+
+    _fields_ = [("rank", C.c_int32), ("mutations", C.POINTER(SnapMutation)),
+                ("n_mutations", C.c_uint64), ("d2h", C.POINTER(C.c_uint64)),
+                ("n_d2h", C.c_uint64)]
+
+
 _SIGS = {
     "snap_open": (C.c_int, [C.c_int, C.c_uint64, C.POINTER(C.c_void_p)]),
     "snap_close": (C.c_int, [C.c_void_p]),
@@ -119,6 +133,10 @@ _SIGS = {
     "snap_host_free": (C.c_int, [C.c_void_p]),
     "snap_snapshot_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p,
                                      C.c_uint64, C.POINTER(C.c_uint64), C.c_void_p]),
+    "snap_window_open": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_uint64]),
+    "snap_window_close": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_uint64,
+                                    C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]),
+    "snap_validate_window": (C.c_int, [C.c_void_p, C.c_uint64, C.c_char_p, C.c_uint64]),
     "snap_blob_rel_path": (C.c_int, [C.c_uint64, C.c_char_p, C.c_uint64]),
     "snap_persist": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_uint64, C.c_int,
                                C.POINTER(PersistStats)]),
@@ -177,6 +195,24 @@ def exported_symbols():
     return list(_SIGS)
 
 
+def validate_window(records):
+    """splice::validate_window (splice.cpp:21-61). records: {rank: (mutations, d2h)} with
+    mutations = [(addr, bytes, digest)] in address order and d2h = [(bytes, digest)].
+    Returns (passed, reason)."""
+    keep, arr = [], (WindowRecord * max(1, len(records)))()
+    for i, (rank, (muts, d2h)) in enumerate(records.items()):
+        m = (SnapMutation * max(1, len(muts)))(*[SnapMutation(*x) for x in muts])
+        d = (C.c_uint64 * max(2, 2 * len(d2h)))(*[v for p in d2h for v in p])
+        keep += [m, d]
+        arr[i] = WindowRecord(rank, C.cast(m, C.POINTER(SnapMutation)), len(muts),
+                              C.cast(d, C.POINTER(C.c_uint64)), len(d2h))
+    reason = C.create_string_buffer(512)
+    rc = lib().snap_validate_window(arr, len(records), reason, 512)
+    if rc < 0:
+        raise SnapError(rc, "snap_validate_window")
+    return rc == 1, reason.value.decode()
+
+
 def blob_rel_path(digest: int) -> str:
     """BlobStore::blob_rel_path (ckpt.cpp:35-40) as the product library computes it."""
     b = C.create_string_buffer(40)
@@ -194,8 +230,10 @@ def bufs_array(bufs):
     arr = (SnapBuf * max(1, len(bufs)))()
     for i, b in enumerate(bufs):
         if isinstance(b, dict):
-            b = (b.get("rank", 0), b.get("slot", i), b["addr"], b["bytes"], b.get("cat", 0))
-        arr[i] = SnapBuf(b[0], b[1], b[2], b[3], b[4] if len(b) > 4 else 0, 0)
+            b = (b.get("rank", 0), b.get("slot", i), b["addr"], b["bytes"], b.get("cat", 0),
+                 b.get("flags", 0))
+        arr[i] = SnapBuf(b[0], b[1], b[2], b[3], b[4] if len(b) > 4 else 0,
+                         b[5] if len(b) > 5 else 0)
     return arr
 
 
@@ -441,6 +479,32 @@ class Ctx:
                                             _p(d) if d is not None else None),
                  "snap_snapshot_host")
         return sb.value
+
+    # -- ranges / squash-window validation (window.cpp)
+    def digest_ranges(self, bufs, page_bytes=4096, chunk_bytes=65536):
+        """Gpu::digest (vdev.cpp:118) of each (rank, slot, addr, bytes, cat) range, on the
+        auxiliary grid (the installed snapshot grid is untouched)."""
+        arr = bufs_array(bufs)
+        g = SnapGeom(page_bytes, chunk_bytes)
+        out = np.zeros(max(1, len(bufs)), np.uint64)
+        self._ck(self._L.snap_digest_ranges(self.h, arr, len(bufs), C.byref(g), _p(out)),
+                 "snap_digest_ranges")
+        return out[:len(bufs)]
+
+    def window_open(self, rank: int, bufs):
+        """do_window_open validation branch (worker.cpp:355-362)."""
+        arr = bufs_array(bufs)
+        self._ck(self._L.snap_window_open(self.h, rank, arr, len(bufs)), "snap_window_open")
+
+    def window_close(self, rank: int, bufs):
+        """do_window_close validation branch (worker.cpp:411-421): the mutation set
+        [(addr, bytes, digest)] in address order."""
+        arr = bufs_array(bufs)
+        out = (SnapMutation * max(1, len(bufs)))()
+        n = C.c_uint64()
+        self._ck(self._L.snap_window_close(self.h, rank, arr, len(bufs), out, len(bufs),
+                                           C.byref(n)), "snap_window_close")
+        return [(out[i].addr, out[i].bytes, out[i].digest) for i in range(n.value)]
 
     # -- on-disk format (BlobStore::persist, ckpt.cpp:42-52; restore_job, ckpt.cpp:504-533)
     def persist(self, directory, host_ptr: int = 0, host_bytes: int = 0, threads: int = 0):

@@ -6,6 +6,7 @@
 #include "ctx.h"
 
 void splice_release(snap_ctx* ctx);
+void window_release(snap_ctx* ctx);
 
 namespace {
 
@@ -364,6 +365,7 @@ int snap_close(snap_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   splice_release(ctx);
+  window_release(ctx);
   for (DevMem* m :
        {&ctx->d_addr, &ctx->d_bytes, &ctx->d_cstart, &ctx->d_lens, &ctx->d_dig, &ctx->d_bufdig,
         &ctx->dd_keys, &ctx->dd_vals, &ctx->dd_slot, &ctx->kn_keys, &ctx->kn_vals, &ctx->kn_list,
@@ -577,13 +579,6 @@ int snap_get_digests(snap_ctx* ctx, uint64_t* chunk_digests, uint32_t* chunk_len
   return SNAP_OK;
 }
 
-int snap_digest_ranges(snap_ctx* ctx, const snap_buf* bufs, uint64_t n, const snap_geom* geom,
-                       uint64_t* out) {
-  uint64_t nc = 0;
-  RC(snap_set_buffers(ctx, bufs, n, geom, &nc));
-  RC(snap_hash(ctx));
-  return snap_get_digests(ctx, nullptr, nullptr, out);
-}
 
 // ---------------------------------------------------------------- K2
 

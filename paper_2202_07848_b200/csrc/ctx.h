@@ -18,6 +18,7 @@ using snap::GridDev;
 using snap::TableDev;
 
 struct SpliceState;
+struct WindowState;
 
 struct DevMem {
   void* p = nullptr;
@@ -86,6 +87,7 @@ struct snap_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   Prof prof;
   SpliceState* splice = nullptr;
+  WindowState* win = nullptr;  // auxiliary grid + open window snapshots (window.cpp)
 
   // host-buffer pipeline (snap_snapshot_host): copy streams, events, host
   // mirror of the speculative layout, fix-up list

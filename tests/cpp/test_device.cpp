@@ -1,6 +1,8 @@
 // The reference's device/digest unit tests (proj/tests/test_vdev.cpp:79-96,
 // 171-179; test_simcore.cpp:107-117) restated against the B200 arena, plus the
 // checkpoint/splice round trips through the C++ mirror. Needs a B200.
+#include <filesystem>
+#include <unistd.h>
 #include <random>
 
 #include "mini_test.hpp"
@@ -84,6 +86,43 @@ TEST_CASE("splice: identical replicas move no bytes after the first switch") {
   CHECK(second.swap_out_bytes == 0 && second.swap_in_bytes == 0);
   CHECK(third.swap_out_bytes == 0 && third.swap_in_bytes == 0);
   CHECK(third.resident_bytes == (2u << 20));
+}
+
+TEST_CASE("window tracker + persist/load through the C++ mirror") {
+  vdev::Gpu g(0, 8 << 20);
+  std::vector<u64> img((4 << 20) / 8);
+  for (u64 i = 0; i < img.size(); ++i) img[i] = mix64(i ^ 77);
+  g.write_words({0, 4 << 20}, img);
+  std::vector<splice::RankBuf> bufs{{0, 0, 1 << 20, vdev::BufCat::Param, true, false},
+                                    {1, 1 << 20, 2 << 20, vdev::BufCat::OptState, true, false},
+                                    {2, 3 << 20, 1 << 20, vdev::BufCat::Grad, true, true}};
+  splice::WindowTracker w(g);
+  std::map<RankId, splice::ValidationRecord> recs;
+  for (int r = 0; r < 2; ++r) {
+    g.write_words({0, 4 << 20}, img);
+    w.open(r, bufs);
+    auto v = g.words({1 << 20, 256});
+    v[3] ^= 0x55;  // the step touches the optimizer state only
+    g.write_words({1 << 20, 256}, v);
+    w.close(r, bufs, recs[r]);
+  }
+  CHECK(recs[0].mutations.size() == 1 && recs[0].mutations.count(1 << 20) == 1);
+  CHECK(splice::validate_window(recs).pass);
+
+  ckpt::Snapshotter s(g);
+  s.set_buffers({{0, 0, 0, 1 << 20, 0, 0}, {0, 1, 1 << 20, 3 << 20, 1, 0}});
+  s.snapshot();
+  char tmpl[] = "/tmp/snap_cpp_XXXXXX";
+  const std::string dir = mkdtemp(tmpl);
+  auto st = s.persist(dir);
+  CHECK(st.written == 64 && st.layout_chunks == 64);
+  const auto before = g.words({0, 4 << 20});
+  g.write_words({0, 4 << 20}, std::vector<u64>(img.size(), 0));
+  auto ls = s.load(dir);
+  CHECK(ls.layout_blobs == 64);
+  const auto after = g.words({0, 4 << 20});
+  CHECK(after == before);
+  std::filesystem::remove_all(dir);
 }
 
 MINI_MAIN()

@@ -81,3 +81,49 @@ def test_persisted_tree_oracle_matches_reference_store(oracle_mod, ref_lib, tmp_
         ref_lib.ref_store_free(st)
     got = {str(p.relative_to(tmp_path)): p.read_bytes() for p in tmp_path.rglob("*") if p.is_file()}
     assert got == oracle_mod.persisted_tree(blobs)
+
+
+def _ref_validate(ref_lib, records):
+    import ctypes as C
+    import numpy as np
+    ranks = np.array(list(records), np.int32)
+    nmut = np.array([len(m) for m, _ in records.values()], np.uint64)
+    nd2h = np.array([len(d) for _, d in records.values()], np.uint64)
+    muts = np.array([v for m, _ in records.values() for t in m for v in t] or [0], np.uint64)
+    d2h = np.array([v for _, d in records.values() for t in d for v in t] or [0], np.uint64)
+    reason = C.create_string_buffer(512)
+    p = [a.ctypes.data_as(C.c_void_p) for a in (ranks, nmut, muts, nd2h, d2h)]
+    ok = ref_lib.ref_validate_window(len(records), *p, reason, 512)
+    return ok == 1, reason.value.decode()
+
+
+def test_validate_window_matches_reference(snap, ref_lib):
+    # splice::validate_window (splice.cpp:21-61): pass/fail and the exact reason text
+    import numpy as np
+    rng = np.random.default_rng(17)
+    for trial in range(400):
+        nr = int(rng.integers(1, 5))
+        base_m = sorted({int(rng.integers(0, 64)) * 256 for _ in range(int(rng.integers(0, 6)))})
+        muts = [(a, int(rng.integers(1, 4)) * 256, int(rng.integers(0, 2**63))) for a in base_m]
+        d2h = [(int(rng.integers(1, 4)) * 8, int(rng.integers(0, 2**63)))
+               for _ in range(int(rng.integers(0, 3)))]
+        recs = {}
+        for r in rng.permutation(8)[:nr]:
+            m, d = [list(x) for x in muts], list(d2h)
+            kind = int(rng.integers(0, 7)) if trial % 3 else 0
+            if kind == 1 and m:
+                m.pop(int(rng.integers(0, len(m))))
+            elif kind == 2 and m:
+                i = int(rng.integers(0, len(m)))
+                m[i][0] += 1 << 20
+                m.sort()
+            elif kind == 3 and m:
+                m[int(rng.integers(0, len(m)))][1] += 256
+            elif kind == 4 and m:
+                m[int(rng.integers(0, len(m)))][2] ^= 1
+            elif kind == 5:
+                d = d + [(8, 1)]
+            elif kind == 6 and d:
+                d[0] = (d[0][0], d[0][1] ^ 2)
+            recs[int(r)] = ([tuple(x) for x in m], d)
+        assert snap.validate_window(recs) == _ref_validate(ref_lib, recs), (trial, recs)
