@@ -310,6 +310,31 @@ typedef struct {
 int snap_validate_window(const snap_window_record* recs, uint64_t n, char* reason,
                          uint64_t cap);
 
+/* --------------------------------------------- host-page snapshot (§8f-4) */
+
+typedef struct {
+  uint64_t pages;        /* 4 KiB pages of the rank (WorkerSnapshot::pages size) */
+  uint64_t s_cr;         /* pages * 4096 (Manifest::s_cr contribution) */
+  uint64_t s_cr_inc;     /* bytes of pages absent from the previous page set */
+  uint64_t upload_bytes; /* bytes of fresh pages: first occurrence, not in the known set */
+} snap_pages_stats;
+#define SNAP_PAGE_FRESH 1u /* flags[p] bit: BlobStore::put would store it (ckpt.cpp:18-20) */
+#define SNAP_PAGE_INC 2u   /* flags[p] bit: not in the previous checkpoint's page set */
+
+/* build_manifest host section (ckpt.cpp:59-68, 116-130) for one rank: the
+ * host buffers (bufs[i], words[i] u64 words each, in slot order) are
+ * concatenated and zero-padded to 4 KiB pages (paged_host_words); the page
+ * digests digest_of_words(page) are computed on the GPU (H2D + K1 with
+ * page == chunk == 4 KiB), and each page is classified against the ctx's known
+ * set (the store index) and against prev_pages (the rank's page list in the
+ * previous manifest, may be NULL). page_digests (capacity cap) and flags
+ * (SNAP_PAGE_*) may be NULL; stats->pages is always set. The installed grid is
+ * not touched. Add the fresh digests to the known set (snap_known_add) once
+ * the pages are persisted. */
+int snap_host_pages(snap_ctx* ctx, const void* const* bufs, const uint64_t* words, uint64_t nbufs,
+                    const uint64_t* prev_pages, uint64_t n_prev, uint64_t* page_digests,
+                    uint64_t cap, uint8_t* flags, snap_pages_stats* stats);
+
 /* ------------------------------------- on-disk format (persist / load) */
 
 /* BlobStore::blob_rel_path (ckpt.cpp:35-40): "blobs/<2hex>/<16hex>" of the

@@ -175,6 +175,29 @@ def persisted_tree(blobs):
     return {blob_rel_path(d): bytes(b) for d, b in blobs.items()}
 
 
+def host_pages(host_bufs, prev_pages=None, known=()):
+    """build_manifest host section (ckpt.cpp:59-68 paged_host_words, 116-130): concatenate
+    the rank's host buffers, zero-pad to 512-word pages, digest_of_words per page; fresh =
+    first occurrence and not in the store (`known`), inc = not in the previous page set
+    (every page when there is no previous manifest). Pure numpy + the oracle digest."""
+    allw = np.concatenate([np.asarray(b, np.uint64) for b in host_bufs] or
+                          [np.zeros(0, np.uint64)])
+    pad = (-allw.size) % 512
+    allw = np.concatenate([allw, np.zeros(pad, np.uint64)])
+    dig = np.array([digest_of_words(allw[o:o + 512]) for o in range(0, allw.size, 512)],
+                   np.uint64)
+    seen, known, prev = set(), set(int(k) for k in known), (
+        None if prev_pages is None else set(int(p) for p in prev_pages))
+    flags = np.zeros(dig.size, np.uint8)
+    for i, d in enumerate(dig.tolist()):
+        if d not in known and d not in seen:
+            flags[i] |= 1
+        seen.add(d)
+        if prev is None or d not in prev:
+            flags[i] |= 2
+    return dig, flags
+
+
 def bufs_array(bufs):
     """bufs: iterable of (rank, slot, addr, bytes, cat) tuples or dicts."""
     arr = (OrBuf * max(1, len(bufs)))()

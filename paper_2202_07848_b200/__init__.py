@@ -79,6 +79,19 @@ class PersistStats(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class PagesStats(C.Structure):
+    """snap_pages_stats: the host-page sizes of build_manifest (ckpt.cpp:122-130)."""
+
+    _fields_ = [("pages", C.c_uint64), ("s_cr", C.c_uint64), ("s_cr_inc", C.c_uint64),
+                ("upload_bytes", C.c_uint64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+PAGE_FRESH, PAGE_INC = 1, 2
+
+
 class SnapMutation(C.Structure):
     """snap_mutation: ValidationRecord::mutations entry (splice.hpp:50-53)."""
 
@@ -133,6 +146,9 @@ _SIGS = {
     "snap_host_free": (C.c_int, [C.c_void_p]),
     "snap_snapshot_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p,
                                      C.c_uint64, C.POINTER(C.c_uint64), C.c_void_p]),
+    "snap_host_pages": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p,
+                                  C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p,
+                                  C.POINTER(PagesStats)]),
     "snap_window_open": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_uint64]),
     "snap_window_close": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_uint64,
                                     C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]),
@@ -490,6 +506,23 @@ class Ctx:
         self._ck(self._L.snap_digest_ranges(self.h, arr, len(bufs), C.byref(g), _p(out)),
                  "snap_digest_ranges")
         return out[:len(bufs)]
+
+    def host_pages(self, host_bufs, prev_pages=None):
+        """build_manifest host section (ckpt.cpp:116-130) for one rank: host_bufs = list of
+        uint64 arrays (slot order). Returns (page_digests, flags, stats)."""
+        arrs = [np.ascontiguousarray(b, dtype=np.uint64) for b in host_bufs]
+        ptrs = (C.c_void_p * max(1, len(arrs)))(*[a.ctypes.data for a in arrs])
+        words = np.array([a.size for a in arrs] or [0], np.uint64)
+        npages = (int(words[:len(arrs)].sum()) * 8 + 4095) // 4096
+        dig = np.zeros(max(1, npages), np.uint64)
+        flags = np.zeros(max(1, npages), np.uint8)
+        prev = None if prev_pages is None else np.ascontiguousarray(prev_pages, dtype=np.uint64)
+        st = PagesStats()
+        self._ck(self._L.snap_host_pages(self.h, ptrs, _p(words), len(arrs),
+                                         _p(prev) if prev is not None and prev.size else None,
+                                         0 if prev is None else prev.size, _p(dig), npages,
+                                         _p(flags), C.byref(st)), "snap_host_pages")
+        return dig[:npages], flags[:npages], st.as_dict()
 
     def window_open(self, rank: int, bufs):
         """do_window_open validation branch (worker.cpp:355-362)."""

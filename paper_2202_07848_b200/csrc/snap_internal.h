@@ -75,6 +75,11 @@ int launch_stripe_writer(const uint64_t* gdig, const uint32_t* glens, const uint
 int launch_shard_scan(const int32_t* writer, const uint32_t* glens, uint32_t nranks, uint64_t maxn,
                       int32_t q, bool write_list, uint64_t* scan_state, uint64_t* shard_off,
                       uint32_t* my_list, uint64_t* my_off, uint64_t* totals, cudaStream_t s);
+// host pages: first-occurrence / known-set / previous-page-set classification
+// (flags bit 1 fresh, bit 2 inc; counts[0..1] += fresh, inc; counts zeroed by the caller)
+int launch_page_classify(TableDev pages, TableDev known, bool use_known, TableDev prev,
+                         bool use_prev, const uint64_t* dig, uint64_t n, uint64_t* slot,
+                         uint8_t* flags, unsigned long long* counts, cudaStream_t s);
 int launch_resolve_dups(const uint8_t* sel, const uint64_t* owner, uint64_t* offsets, uint64_t n,
                         cudaStream_t s);
 

@@ -17,6 +17,8 @@
 struct AuxGrid {
   DevMem d_addr, d_bytes, d_cstart, d_dig, d_bufdig;
   GridDev grid;
+  // host-page snapshot scratch: paged image, slots, flags, counts, page + prev tables
+  DevMem d_img, d_slot, d_flags, d_counts, pt_keys, pt_vals, pv_keys, pv_vals, d_prev;
 };
 
 struct WindowState {
@@ -28,8 +30,10 @@ struct WindowState {
 void window_release(snap_ctx* ctx) {
   WindowState* W = ctx->win;
   if (!W) return;
-  for (DevMem* m : {&W->aux.d_addr, &W->aux.d_bytes, &W->aux.d_cstart, &W->aux.d_dig,
-                    &W->aux.d_bufdig})
+  AuxGrid& A = W->aux;
+  for (DevMem* m : {&A.d_addr, &A.d_bytes, &A.d_cstart, &A.d_dig, &A.d_bufdig, &A.d_img,
+                    &A.d_slot, &A.d_flags, &A.d_counts, &A.pt_keys, &A.pt_vals, &A.pv_keys,
+                    &A.pv_vals, &A.d_prev})
     release(*m);
   delete W;
   ctx->win = nullptr;
@@ -134,6 +138,79 @@ int snap_window_close(snap_ctx* ctx, int rank, const snap_buf* bufs, uint64_t n,
     for (const auto& [a, bd] : mut) out[k++] = snap_mutation{a, bd.first, bd.second};
   }
   state(ctx).open.erase(it);
+  return SNAP_OK;
+}
+
+int snap_host_pages(snap_ctx* ctx, const void* const* bufs, const uint64_t* words, uint64_t nbufs,
+                    const uint64_t* prev, uint64_t n_prev, uint64_t* page_digests, uint64_t cap,
+                    uint8_t* flags, snap_pages_stats* st) {
+  if (!ctx || (nbufs && (!bufs || !words)) || (n_prev && !prev)) return SNAP_EINVAL;
+  constexpr uint64_t kPage = 4096;
+  uint64_t total = 0;
+  for (uint64_t i = 0; i < nbufs; ++i) total += words[i] * 8;
+  const uint64_t npages = (total + kPage - 1) / kPage;
+  snap_pages_stats out{npages, npages * kPage, 0, 0};
+  if (st) *st = out;
+  if ((page_digests || flags) && cap < npages)
+    return fail(ctx, SNAP_EINVAL, "host_pages: output capacity below the page count");
+  if (npages == 0) return SNAP_OK;
+  if (npages >= (1ull << 31)) return fail(ctx, SNAP_EINVAL, "host_pages: too many pages");
+  CK(cudaSetDevice(ctx->device));
+  AuxGrid& A = state(ctx).aux;
+  uint8_t *img, *fl;
+  uint64_t *da, *db, *dc, *dd, *slot, *dp;
+  unsigned long long *cnt, *pk, *pv, *vk, *vv;
+  const uint64_t pcap = table_cap(npages), vcap = table_cap(std::max<uint64_t>(n_prev, 1));
+  RC(ensure(ctx, A.d_img, npages * kPage, &img));
+  RC(ensure(ctx, A.d_addr, 1, &da));
+  RC(ensure(ctx, A.d_bytes, 1, &db));
+  RC(ensure(ctx, A.d_cstart, 2, &dc));
+  RC(ensure(ctx, A.d_dig, npages, &dd));
+  RC(ensure(ctx, A.d_slot, npages, &slot));
+  RC(ensure(ctx, A.d_flags, npages, &fl));
+  RC(ensure(ctx, A.d_counts, 2, &cnt));
+  RC(ensure(ctx, A.pt_keys, pcap + 1, &pk));
+  RC(ensure(ctx, A.pt_vals, pcap + 1, &pv));
+  RC(ensure(ctx, A.pv_keys, vcap + 1, &vk));
+  RC(ensure(ctx, A.pv_vals, vcap + 1, &vv));
+  RC(ensure(ctx, A.d_prev, std::max<uint64_t>(n_prev, 1), &dp));
+  // paged_host_words (ckpt.cpp:59-68): buffers back to back, zero tail
+  uint64_t off = 0;
+  for (uint64_t i = 0; i < nbufs; ++i) {
+    if (words[i])
+      CK(cudaMemcpyAsync(img + off, bufs[i], words[i] * 8, cudaMemcpyHostToDevice, ctx->stream));
+    off += words[i] * 8;
+  }
+  if (npages * kPage > off) CK(cudaMemsetAsync(img + off, 0, npages * kPage - off, ctx->stream));
+  const uint64_t one[3] = {0, npages * kPage, npages};
+  CK(cudaMemcpyAsync(da, &one[0], 8, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(db, &one[1], 8, cudaMemcpyHostToDevice, ctx->stream));
+  const uint64_t cs[2] = {0, npages};
+  CK(cudaMemcpyAsync(dc, cs, 16, cudaMemcpyHostToDevice, ctx->stream));
+  if (n_prev) CK(cudaMemcpyAsync(dp, prev, n_prev * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemsetAsync(cnt, 0, 16, ctx->stream));
+  // K1: one "buffer" over the paged image, page == chunk == 4 KiB -> digest_of_words(page)
+  const GridDev g{da, db, dc, 1u, npages, 12u, 12u};
+  CKL(snap::launch_hash(img, g, dd, nullptr, nullptr, ctx->stream));
+  const TableDev pt{pk, pv, pcap - 1}, vt{vk, vv, vcap - 1};
+  CKL(snap::launch_table_clear(pt, ctx->stream));
+  if (n_prev) {
+    CKL(snap::launch_table_clear(vt, ctx->stream));
+    CKL(snap::launch_table_insert_min(vt, dp, n_prev, 0, ctx->stream));
+  }
+  const TableDev kn{P<unsigned long long>(ctx->kn_keys), P<unsigned long long>(ctx->kn_vals),
+                    ctx->kn_mask};
+  CKL(snap::launch_page_classify(pt, kn, ctx->kn_count > 0, vt, n_prev > 0, dd, npages,
+                                 slot, fl, cnt, ctx->stream));
+  unsigned long long c[2];
+  CK(cudaMemcpyAsync(c, cnt, 16, cudaMemcpyDeviceToHost, ctx->stream));
+  if (page_digests)
+    CK(cudaMemcpyAsync(page_digests, dd, npages * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (flags) CK(cudaMemcpyAsync(flags, fl, npages, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));  // `one`, `cs` die here
+  out.upload_bytes = c[0] * kPage;
+  out.s_cr_inc = c[1] * kPage;
+  if (st) *st = out;
   return SNAP_OK;
 }
 

@@ -142,3 +142,30 @@ def test_blobstore_golden(golden):
     assert np.array_equal(out, page)
     assert R.ref_store_get(s, dig.value ^ 1, out.ctypes.data, 512) == -1
     R.ref_store_free(s)
+
+
+def test_host_pages_oracle_vs_reference_store():
+    # the oracle's fresh flags == BlobStore::put's `fresh` for the same page sequence
+    # (ckpt.cpp:121-126), and its page digests == the reference digest of each page
+    import ctypes as C
+    R = O.ref()
+    if R is None:
+        pytest.skip("reference library not built here")
+    rng = np.random.default_rng(3)
+    bufs = [O.fill_mix64(700, 5, 0), np.zeros(300, np.uint64), O.fill_mix64(512, 5, 0),
+            O.fill_mix64(1100, 6, 0)]
+    dig, flags = O.host_pages(bufs)
+    allw = np.concatenate(bufs + [np.zeros((-sum(b.size for b in bufs)) % 512, np.uint64)])
+    st = R.ref_store_new()
+    try:
+        for i in range(dig.size):
+            page = np.ascontiguousarray(allw[i * 512:(i + 1) * 512])
+            d = C.c_uint64()
+            fresh = R.ref_store_put(st, page.ctypes.data_as(C.c_void_p), 512, C.byref(d))
+            assert d.value == int(dig[i]) and bool(fresh) == bool(flags[i] & 1)
+    finally:
+        R.ref_store_free(st)
+    _, f2 = O.host_pages(bufs, prev_pages=dig[:2])
+    prev = set(dig[:2].tolist())
+    assert [bool(f & 2) for f in f2] == [d not in prev for d in dig.tolist()]
+    del rng
