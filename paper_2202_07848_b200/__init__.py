@@ -14,7 +14,8 @@ import subprocess
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsnap.so")
+# SNAP_LIB_PATH: A/B tooling only (tools/ab_step.py), the default is the in-tree build
+LIB_PATH = os.environ.get("SNAP_LIB_PATH") or os.path.join(HERE, "libsnap.so")
 
 SNAP_OK, SNAP_EINVAL, SNAP_ENOMEM, SNAP_EFAULT, SNAP_ECUDA, SNAP_EINTERNAL = 0, -1, -2, -3, -4, -5
 U64, F32 = 0, 1

@@ -3,6 +3,8 @@
 // (vdev.hpp:65-122). Host code only; every byte of device work is one of the
 // sm_100a kernels in k_*.cu, issued on the ctx stream (NCCL collectives on the
 // same stream for the cross-rank exchange).
+#include <cstdlib>
+
 #include "ctx.h"
 
 void splice_release(snap_ctx* ctx);
@@ -75,30 +77,65 @@ int known_insert_dev(snap_ctx* ctx, const uint64_t* dev_digests, uint64_t n) {
 
 }  // namespace
 
-// Selection over a canonical vector against an explicit known table (the
-// splice chunk cache uses its own index as the known set).
-int select_with_known(snap_ctx* ctx, const uint64_t* dig, const uint32_t* lens, uint64_t n,
-                      TableDev kn, bool use_known) {
+// Dedup table + scan state for a selection over n entries: allocated, and
+// cleared only when they are not known to be empty (the resolve pass of the
+// previous selection leaves them empty).
+int prepare_dedup(snap_ctx* ctx, uint64_t n, TableDev* out, uint64_t** slot, uint64_t** scan) {
   const uint64_t cap = table_cap(n);
+  const uint64_t words = snap::scan_state_words(n) + 1;
   unsigned long long *k, *v;
+  const void* k_old = ctx->dd_keys.p;
+  const void* v_old = ctx->dd_vals.p;
+  const void* s_old = ctx->scan.p;
+  RC(ensure(ctx, ctx->dd_keys, cap + 1, &k));
+  RC(ensure(ctx, ctx->dd_vals, cap + 1, &v));
+  RC(ensure(ctx, ctx->dd_slot, n, slot));
+  RC(ensure(ctx, ctx->scan, words, scan));
+  if (k != k_old || v != v_old) ctx->dd_clean_mask = 0, ctx->dd_clean = false;
+  if (*scan != s_old) ctx->scan_clean_words = 0;
+  ctx->dd_mask = cap - 1;
+  *out = TableDev{k, v, ctx->dd_mask};
+  if (!ctx->dd_clean || ctx->dd_mask > ctx->dd_clean_mask) {
+    CKL(snap::launch_table_clear(*out, ctx->stream));
+    ctx->dd_clean_mask = ctx->dd_mask;
+  }
+  if (!ctx->dd_clean || words > ctx->scan_clean_words) {
+    CK(cudaMemsetAsync(*scan, 0, words * 8, ctx->stream));
+    ctx->scan_clean_words = words;
+  }
+  ctx->dd_clean = false;  // about to be filled
+  return SNAP_OK;
+}
+
+// Selection over a canonical vector against an explicit known table (the
+// splice chunk cache uses its own index as the known set). `inserted`: the K2
+// insert already ran inside K1 (hash_fused) into the prepared table.
+int select_with_known(snap_ctx* ctx, const uint64_t* dig, const uint32_t* lens, uint64_t n,
+                      TableDev kn, bool use_known, bool inserted, uint64_t* spec_next) {
   uint64_t *slot, *scan, *owner, *offsets, *totals;
   uint8_t* sel;
   uint32_t* list;
-  RC(ensure(ctx, ctx->dd_keys, cap + 1, &k));
-  RC(ensure(ctx, ctx->dd_vals, cap + 1, &v));
-  RC(ensure(ctx, ctx->dd_slot, n, &slot));
-  RC(ensure(ctx, ctx->scan, snap::scan_state_words(n) + 1, &scan));
+  TableDev dd;
+  if (inserted) {
+    dd = TableDev{P<unsigned long long>(ctx->dd_keys), P<unsigned long long>(ctx->dd_vals),
+                  ctx->dd_mask};
+    slot = P<uint64_t>(ctx->dd_slot);
+    scan = P<uint64_t>(ctx->scan);
+  } else {
+    RC(prepare_dedup(ctx, n, &dd, &slot, &scan));
+  }
   RC(ensure(ctx, ctx->sel, n, &sel));
   RC(ensure(ctx, ctx->owner, n, &owner));
   RC(ensure(ctx, ctx->offsets, n, &offsets));
   RC(ensure(ctx, ctx->sel_list, n, &list));
   RC(ensure(ctx, ctx->totals, 4, &totals));
-  ctx->dd_mask = cap - 1;
-  TableDev dd{k, v, ctx->dd_mask};
-  CKL(snap::launch_table_clear(dd, ctx->stream));
-  CKL(snap::launch_dedup_insert(dd, kn, use_known, dig, lens, n, slot, ctx->stream));
-  CKL(snap::launch_select(dd, slot, lens, n, scan, sel, owner, offsets, list, totals, ctx->stream));
-  CKL(snap::launch_resolve_dups(sel, owner, offsets, n, ctx->stream));
+  if (!inserted) CKL(snap::launch_dedup_insert(dd, kn, use_known, dig, lens, n, slot, ctx->stream));
+  CKL(snap::launch_select(dd, slot, lens, n, scan, sel, owner, offsets, list, totals, spec_next,
+                          ctx->stream));
+  const uint64_t words = snap::scan_state_words(n) + 1;
+  CKL(snap::launch_resolve_dups(sel, owner, offsets, n, dd, scan, words, ctx->stream));
+  ctx->dd_clean = true;
+  ctx->scan_clean_words = std::max(ctx->scan_clean_words, words);
   ctx->sel_n = n;
   return SNAP_OK;
 }
@@ -106,9 +143,10 @@ int select_with_known(snap_ctx* ctx, const uint64_t* dig, const uint32_t* lens, 
 namespace {
 
 // Selection over a canonical vector (local grid or allgathered global one).
-int select_impl(snap_ctx* ctx, const uint64_t* dig, const uint32_t* lens, uint64_t n) {
+int select_impl(snap_ctx* ctx, const uint64_t* dig, const uint32_t* lens, uint64_t n,
+                bool inserted = false, uint64_t* spec_next = nullptr) {
   TableDev kn{P<unsigned long long>(ctx->kn_keys), P<unsigned long long>(ctx->kn_vals), ctx->kn_mask};
-  RC(select_with_known(ctx, dig, lens, n, kn, ctx->kn_count > 0));
+  RC(select_with_known(ctx, dig, lens, n, kn, ctx->kn_count > 0, inserted, spec_next));
   ctx->selected = true;
   return SNAP_OK;
 }
@@ -162,11 +200,13 @@ int stripe_impl(snap_ctx* ctx) {
   RC(ensure(ctx, ctx->d_my_list, maxn, &my_list));
   RC(ensure(ctx, ctx->d_my_off, maxn, &my_off));
   RC(ensure(ctx, ctx->d_my_totals, 4, &my_tot));
+  uint64_t* scan2;
+  RC(ensure(ctx, ctx->scan2, snap::scan_state_words(n) + 1, &scan2));
   ctx->shard_offsets_all = false;
   CKL(snap::launch_stripe_writer(P<uint64_t>(ctx->d_gdig), P<uint32_t>(ctx->d_glens),
                                  P<uint8_t>(ctx->sel), ctx->nranks, maxn, writer, ctx->stream));
   CKL(snap::launch_shard_scan(writer, P<uint32_t>(ctx->d_glens), ctx->nranks, maxn, ctx->rank, true,
-                              P<uint64_t>(ctx->scan), shard_off, my_list, my_off, my_tot,
+                              scan2, shard_off, my_list, my_off, my_tot,
                               ctx->stream));
   return SNAP_OK;
 }
@@ -252,6 +292,27 @@ int hash_fused(snap_ctx* ctx, uint64_t c0 = 0, uint64_t c1 = 0) {
   GridDev g = ctx->grid;
   g.c_begin = c0;
   g.c_end = c1;
+  static const bool k1_insert = [] {
+    const char* e = std::getenv("SNAP_K1_INSERT");
+    return e && e[0] == '1';
+  }();
+  if (!ctx->comm && k1_insert) {
+    // SNAP_K1_INSERT=1 (single GPU): K1 also does the K2 insert of its chunks in
+    // a warp epilogue (the table is prepared once, before the first slice of the
+    // grid). Off by default: the epilogue costs more kernel tail (14 us on C2)
+    // than the standalone insert kernel (8 us).
+    if (c0 == 0) {
+      uint64_t *slot, *scan;
+      RC(prepare_dedup(ctx, ctx->nchunks, &g.dd, &slot, &scan));
+    }
+    g.dd = TableDev{P<unsigned long long>(ctx->dd_keys), P<unsigned long long>(ctx->dd_vals),
+                    ctx->dd_mask};
+    g.dd_slot = P<uint64_t>(ctx->dd_slot);
+    g.kn = TableDev{P<unsigned long long>(ctx->kn_keys), P<unsigned long long>(ctx->kn_vals),
+                    ctx->kn_mask};
+    g.kn_use = ctx->kn_count > 0 ? 1 : 0;
+    ctx->k1_inserted = true;
+  }
   if (ctx->kn_count > 0) {
     CKL(snap::launch_hash(ctx->arena, g, P<uint64_t>(ctx->d_dig), nullptr, nullptr, ctx->stream));
     ctx->spec_used = false;
@@ -285,8 +346,13 @@ int compact_impl(snap_ctx* ctx, uint32_t* moved = nullptr, unsigned int* nmoved 
   if (ctx->spec_used) {
     spec_cur = P<uint64_t>(ctx->d_spec[ctx->spec_cur]);
     RC(ensure(ctx, ctx->d_spec[1 - ctx->spec_cur], ctx->nchunks, &spec_next));
-    CK(cudaMemsetAsync(spec_next, 0xff, ctx->nchunks * 8, ctx->stream));
+    if (ctx->spec_next_done) {
+      spec_next = nullptr;  // the selection scan already wrote the next layout
+    } else {
+      CK(cudaMemsetAsync(spec_next, 0xff, ctx->nchunks * 8, ctx->stream));
+    }
   }
+  ctx->spec_next_done = false;
   if (nmoved) CK(cudaMemsetAsync(nmoved, 0, 4, ctx->stream));
   if (ctx->comm && ctx->exchanged) {
     CKL(snap::launch_gather(ctx->arena, ctx->grid, P<uint32_t>(ctx->d_lens),
@@ -373,7 +439,7 @@ int snap_close(snap_ctx* ctx) {
         &ctx->staging, &ctx->d_counts, &ctx->d_gdig, &ctx->d_glens, &ctx->d_writer,
         &ctx->d_shard_off, &ctx->d_my_list, &ctx->d_my_off, &ctx->d_my_totals, &ctx->d_dig2,
         &ctx->d_expect, &ctx->d_nbad, &ctx->d_srcoff, &ctx->d_spec[0], &ctx->d_spec[1],
-        &ctx->d_tmaps})
+        &ctx->d_tmaps, &ctx->scan2})
     release(*m);
   for (cudaEvent_t e : ctx->prof.pool) cudaEventDestroy(e);
   if (ctx->arena) cudaFree(ctx->arena);
@@ -541,6 +607,8 @@ int snap_set_buffers(snap_ctx* ctx, const snap_buf* bufs, uint64_t n, const snap
   ctx->glens_valid = false;
   ctx->spec_ready = false;
   ctx->spec_used = false;
+  ctx->k1_inserted = false;
+  ctx->spec_next_done = false;
   if (n_chunks) *n_chunks = ctx->nchunks;
   return SNAP_OK;
 }
@@ -554,6 +622,7 @@ int snap_hash(snap_ctx* ctx) {
                           ctx->stream));
   }
   ctx->spec_used = false;
+  ctx->k1_inserted = false;
   ctx->hashed = true;
   ctx->selected = false;
   ctx->exchanged = false;
@@ -640,7 +709,15 @@ int snap_select(snap_ctx* ctx) {
     return stripe_impl(ctx);
   }
   ProfScope ps(ctx, kProfSelect);
-  return select_impl(ctx, P<uint64_t>(ctx->d_dig), P<uint32_t>(ctx->d_lens), ctx->nchunks);
+  const bool inserted = ctx->k1_inserted;
+  ctx->k1_inserted = false;
+  uint64_t* spec_next = nullptr;
+  if (ctx->spec_used)  // the staging layout becomes the next speculation
+    RC(ensure(ctx, ctx->d_spec[1 - ctx->spec_cur], ctx->nchunks, &spec_next));
+  RC(select_impl(ctx, P<uint64_t>(ctx->d_dig), P<uint32_t>(ctx->d_lens), ctx->nchunks, inserted,
+                 spec_next));
+  ctx->spec_next_done = spec_next != nullptr;
+  return SNAP_OK;
 }
 
 int snap_get_selection(snap_ctx* ctx, uint8_t* sel, uint64_t* owner, uint64_t* offsets,
@@ -693,14 +770,13 @@ int snap_get_shard(snap_ctx* ctx, int32_t* writer, uint64_t* shard_off, uint64_t
   CK(cudaMemcpyAsync(tot, ctx->d_my_totals.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
   if (shard_off) {
     // offsets inside every writer's shard: one shard scan per writer rank
-    uint64_t dummy_tot[2];
-    (void)dummy_tot;
-    uint64_t* tt;
+    uint64_t *tt, *scan2;
     RC(ensure(ctx, ctx->d_nbad, 4, &tt));
+    RC(ensure(ctx, ctx->scan2, snap::scan_state_words(n) + 1, &scan2));
     CK(cudaMemsetAsync(ctx->d_shard_off.p, 0xff, n * 8, ctx->stream));
     for (int q = 0; q < ctx->nranks; ++q)
       CKL(snap::launch_shard_scan(P<int32_t>(ctx->d_writer), P<uint32_t>(ctx->d_glens), ctx->nranks,
-                                  ctx->maxn, q, false, P<uint64_t>(ctx->scan),
+                                  ctx->maxn, q, false, scan2,
                                   P<uint64_t>(ctx->d_shard_off), nullptr, nullptr, tt, ctx->stream));
     CK(cudaMemcpyAsync(shard_off, ctx->d_shard_off.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
   }
@@ -763,13 +839,14 @@ int snap_restore_shards(snap_ctx* ctx, int src_rank, int verify) {
     return fail(ctx, SNAP_EINVAL, "restore_shards: installed grid is not src_rank's layout");
   CK(cudaSetDevice(ctx->device));
   if (!ctx->shard_offsets_all) {
-    uint64_t* tt;
-    RC(ensure(ctx, ctx->d_nbad, 4, &tt));
+    uint64_t *tt, *scan2;
     const uint64_t n = uint64_t(ctx->nranks) * ctx->maxn;
+    RC(ensure(ctx, ctx->d_nbad, 4, &tt));
+    RC(ensure(ctx, ctx->scan2, snap::scan_state_words(n) + 1, &scan2));
     CK(cudaMemsetAsync(ctx->d_shard_off.p, 0xff, n * 8, ctx->stream));
     for (int q = 0; q < ctx->nranks; ++q)
       CKL(snap::launch_shard_scan(P<int32_t>(ctx->d_writer), P<uint32_t>(ctx->d_glens), ctx->nranks,
-                                  ctx->maxn, q, false, P<uint64_t>(ctx->scan),
+                                  ctx->maxn, q, false, scan2,
                                   P<uint64_t>(ctx->d_shard_off), nullptr, nullptr, tt, ctx->stream));
     ctx->shard_offsets_all = true;
   }

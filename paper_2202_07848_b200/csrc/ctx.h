@@ -56,6 +56,13 @@ struct snap_ctx {
   // dedup table (per snapshot) and known set (store index)
   DevMem dd_keys, dd_vals, dd_slot;
   uint64_t dd_mask = 0;
+  // the dedup table / select scan state are left empty by the resolve pass;
+  // dd_clean_mask / scan_clean_words = the extents known to be empty
+  bool dd_clean = false;
+  uint64_t dd_clean_mask = 0, scan_clean_words = 0;
+  bool k1_inserted = false;  // the last K1 (single-GPU snapshot) did the K2 insert
+  bool spec_next_done = false;  // the selection scan wrote the next speculative layout
+  DevMem scan2;              // scan state of the per-writer shard scans
   DevMem kn_keys, kn_vals, kn_list;
   uint64_t kn_mask = 0, kn_count = 0;
 
@@ -215,7 +222,8 @@ inline uint64_t table_cap(uint64_t n) {
 }
 
 int select_with_known(snap_ctx* ctx, const uint64_t* dig, const uint32_t* lens, uint64_t n,
-                      TableDev kn, bool use_known);
+                      TableDev kn, bool use_known, bool inserted = false,
+                      uint64_t* spec_next = nullptr);
 
 // Per-buffer TMA tensor maps for the hash-only TMA K1 variant (4 KiB pages; only
 // built when that variant is selected). On any

@@ -71,11 +71,37 @@ k_gather(const uint8_t* __restrict__ arena, GridDev g, const uint32_t* __restric
   const int lane = threadIdx.x & 31;
   const uint64_t w0 = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
   const uint64_t nw = (uint64_t(gridDim.x) * kThreads) >> 5;
+  if (spec_cur) {
+    // speculative layout: almost every chunk is already in place — check 32
+    // list entries per warp step (one per lane, coalesced), copy only the
+    // mismatches with the whole warp
+    for (uint64_t b = w0 * 32; b < nsel; b += nw * 32) {
+      const uint64_t k = b + lane;
+      uint32_t gc = 0;
+      uint64_t off = 0;
+      bool need = false;
+      if (k < nsel) {
+        gc = sel_list[k];
+        off = offsets[by_list ? k : gc];
+        if (spec_next) spec_next[gc] = off;
+        need = spec_cur[gc] != off;
+      }
+      unsigned m = __ballot_sync(0xffffffffu, need);
+      while (m) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1;
+        const uint32_t gj = __shfl_sync(0xffffffffu, gc, j);
+        const uint64_t oj = __shfl_sync(0xffffffffu, off, j);
+        warp_copy(staging + oj, chunk_ptr(arena, g, gj), lens[gj], lane);
+        if (moved && lane == 0) moved[atomicAdd(nmoved, 1u)] = static_cast<uint32_t>(b + j);
+      }
+    }
+    return;
+  }
   for (uint64_t w = w0; w < nsel; w += nw) {
     const uint32_t gc = sel_list[w];
     const uint64_t off = offsets[by_list ? w : gc];
     if (spec_next && lane == 0) spec_next[gc] = off;
-    if (spec_cur && spec_cur[gc] == off) continue;
     warp_copy(staging + off, chunk_ptr(arena, g, gc), lens[gc], lane);
     if (moved && lane == 0) moved[atomicAdd(nmoved, 1u)] = static_cast<uint32_t>(w);
   }
@@ -204,7 +230,8 @@ int launch_gather(const uint8_t* arena, const GridDev& g, const uint32_t* lens,
                   uint8_t* staging, uint64_t max_sel, cudaStream_t s, uint32_t* moved,
                   unsigned int* nmoved) {
   if (max_sel == 0) return 0;
-  uint64_t blocks = (max_sel * 32 + kThreads - 1) / kThreads;
+  // speculative path: one list entry per thread; otherwise one chunk per warp
+  uint64_t blocks = ((spec_cur ? max_sel : max_sel * 32) + kThreads - 1) / kThreads;
   if (blocks > copy_grid()) blocks = copy_grid();
   k_gather<<<unsigned(blocks), kThreads, 0, s>>>(arena, g, lens, sel_list, totals, offsets,
                                                  offsets_by_list ? 1 : 0, spec_cur, spec_next,

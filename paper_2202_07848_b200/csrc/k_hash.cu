@@ -21,6 +21,7 @@
 #include <cstdlib>
 
 #include "snap_internal.h"
+#include "table.cuh"
 
 namespace snap {
 namespace {
@@ -344,6 +345,18 @@ k_hash(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ chun
     }
   }
   cp_wait<0>();
+  if (g.dd.keys != nullptr) {
+    // fused K2 insert: this warp's chunks (whole chunks per task, since NP is
+    // a multiple of the pages per chunk), one chunk per lane, after the
+    // streaming loop so no atomic round trip ever stalls a slab
+    __syncwarp();
+    const uint32_t cpt = uint32_t(NP) >> ppc_shift;
+    for (uint64_t e = lane; e < my_tasks * cpt; e += 32) {
+      const uint64_t i = e / cpt;
+      const uint64_t c = ((slot_base + (gw + i * nw) * NP) >> ppc_shift) + (e - i * cpt);
+      if (c < c_end) k1_insert(g, c, chunk_dig[c]);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -636,6 +649,15 @@ k_hash_ws(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ c
 
 // Buffer digest = digest_of_words(chunk digests of the buffer); one thread
 // per buffer (digest vectors are 1/8192 of the data).
+// K2 insert over the chunk range of a K1 launch (for the K1 variants that do
+// not carry the fused epilogue: warp-specialized, TMA)
+__global__ void k_insert_range(GridDev g, const uint64_t* __restrict__ chunk_dig) {
+  const uint64_t c_end = g.c_end ? g.c_end : g.nchunks;
+  for (uint64_t c = g.c_begin + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < c_end;
+       c += uint64_t(gridDim.x) * blockDim.x)
+    k1_insert(g, c, chunk_dig[c]);
+}
+
 __global__ void k_buf_fold(GridDev g, const uint64_t* __restrict__ chunk_dig,
                            uint64_t* __restrict__ buf_dig) {
   const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -757,9 +779,29 @@ int hash_variant() {
 
 bool hash_tma_selected() { return hash_variant() == 10; }
 
+int launch_hash_variant(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
+                        const uint64_t* spec_off, uint8_t* staging, cudaStream_t s);
+
+// K1 launch; with g.dd set the K2 insert is fused into the k_hash epilogue, or
+// (other variants) runs as a range kernel right after.
 int launch_hash(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
                 const uint64_t* spec_off, uint8_t* staging, cudaStream_t s) {
   if (g.nchunks == 0) return 0;
+  const int v = hash_variant();
+  const bool epilogue = !((v >= 4 && v <= 6) || (v == 10 && !spec_off && hash_tma_ok(g)));
+  if (!g.dd.keys || epilogue) return launch_hash_variant(arena, g, chunk_dig, spec_off, staging, s);
+  GridDev h = g;
+  h.dd = TableDev{};
+  const int n = launch_hash_variant(arena, h, chunk_dig, spec_off, staging, s);
+  const uint64_t c_end = g.c_end ? g.c_end : g.nchunks;
+  uint64_t blocks = (c_end - g.c_begin + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks) k_insert_range<<<unsigned(blocks), 256, 0, s>>>(g, chunk_dig);
+  return n + (blocks ? 1 : 0);
+}
+
+int launch_hash_variant(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
+                        const uint64_t* spec_off, uint8_t* staging, cudaStream_t s) {
   // slabs of 128 B need pages >= 256 B; 64-B slabs are fine for every page size
   switch (hash_variant()) {
     case 1: return launch_hash_cfg<CfgB>(arena, g, chunk_dig, spec_off, staging, s);

@@ -18,6 +18,7 @@
 #include <cstring>
 
 #include "snap_internal.h"
+#include "table.cuh"
 
 namespace snap {
 namespace {

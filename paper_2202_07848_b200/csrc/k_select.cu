@@ -20,6 +20,8 @@
 #include <cuda_runtime.h>
 
 #include "snap_internal.h"
+#include <algorithm>
+
 #include "table.cuh"
 
 namespace snap {
@@ -186,7 +188,7 @@ k_select_scan(TableDev dedup, const uint64_t* __restrict__ slot, const uint32_t*
               uint64_t n, uint64_t* __restrict__ status, unsigned int* __restrict__ tile_counter,
               uint8_t* __restrict__ sel, uint64_t* __restrict__ owner,
               uint64_t* __restrict__ offsets, uint32_t* __restrict__ sel_list,
-              uint64_t* __restrict__ totals) {
+              uint64_t* __restrict__ totals, uint64_t* __restrict__ spec_next) {
   const uint64_t tile = next_tile(tile_counter);
   const uint64_t ntiles = (n + kTile - 1) / kTile;
   const uint64_t base = tile * kTile + uint64_t(threadIdx.x) * kItems;
@@ -208,8 +210,10 @@ k_select_scan(TableDev dedup, const uint64_t* __restrict__ slot, const uint32_t*
       const bool sl = val[j] != 0;
       sel[g] = sl;
       owner[g] = own[j];
-      offsets[g] = own[j] == ~0ull ? ~0ull : (run & ((1ull << kUnitBits) - 1)) << 8;
+      const uint64_t off = (run & ((1ull << kUnitBits) - 1)) << 8;
+      offsets[g] = own[j] == ~0ull ? ~0ull : off;
       if (sl) sel_list[run >> kUnitBits] = static_cast<uint32_t>(g);
+      if (spec_next) spec_next[g] = sl ? off : ~0ull;
     }
     run += val[j];
   }
@@ -252,13 +256,26 @@ k_shard_scan(const int32_t* __restrict__ writer, const uint32_t* __restrict__ gl
   }
 }
 
-// Duplicates point at their owner's staged bytes (restore source).
+// Duplicates point at their owner's staged bytes (restore source). The same
+// pass resets the dedup table and the scan state the selection just consumed,
+// so the next selection starts without a clear kernel or memset.
 __global__ void k_resolve_dups(const uint8_t* __restrict__ sel, const uint64_t* __restrict__ owner,
-                               uint64_t* __restrict__ offsets, uint64_t n) {
-  for (uint64_t g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < n;
+                               uint64_t* __restrict__ offsets, uint64_t n, TableDev clear,
+                               uint64_t* __restrict__ scan_state, uint64_t clear_words) {
+  const uint64_t tab = clear.keys ? clear.mask + 2 : 0;
+  const uint64_t end = n > tab ? (n > clear_words ? n : clear_words)
+                               : (tab > clear_words ? tab : clear_words);
+  for (uint64_t g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < end;
        g += uint64_t(gridDim.x) * blockDim.x) {
-    const uint64_t o = owner[g];
-    if (!sel[g] && o != ~0ull) offsets[g] = offsets[o];
+    if (g < n) {
+      const uint64_t o = owner[g];
+      if (!sel[g] && o != ~0ull) offsets[g] = offsets[o];
+    }
+    if (g < tab) {
+      clear.keys[g] = kEmptyKey;
+      clear.vals[g] = ~0ull;
+    }
+    if (g < clear_words) scan_state[g] = 0;
   }
 }
 
@@ -294,16 +311,15 @@ int launch_dedup_insert(TableDev dedup, TableDev known, bool use_known, const ui
 
 int launch_select(TableDev dedup, const uint64_t* slot, const uint32_t* lens, uint64_t n,
                   uint64_t* scan_state, uint8_t* sel, uint64_t* owner, uint64_t* offsets,
-                  uint32_t* sel_list, uint64_t* totals, cudaStream_t s) {
+                  uint32_t* sel_list, uint64_t* totals, uint64_t* spec_next, cudaStream_t s) {
   const uint64_t tiles = (n + kTile - 1) / kTile;
-  cudaMemsetAsync(scan_state, 0, (tiles + 1) * sizeof(uint64_t), s);
   if (n == 0) {
     cudaMemsetAsync(totals, 0, 2 * sizeof(uint64_t), s);
     return 0;
   }
   k_select_scan<<<unsigned(tiles), kThreads, 0, s>>>(
       dedup, slot, lens, n, scan_state, reinterpret_cast<unsigned int*>(scan_state + tiles), sel,
-      owner, offsets, sel_list, totals);
+      owner, offsets, sel_list, totals, spec_next);
   return 1;
 }
 
@@ -332,9 +348,13 @@ int launch_shard_scan(const int32_t* writer, const uint32_t* glens, uint32_t nra
 }
 
 int launch_resolve_dups(const uint8_t* sel, const uint64_t* owner, uint64_t* offsets, uint64_t n,
+                        TableDev clear, uint64_t* scan_state, uint64_t clear_words,
                         cudaStream_t s) {
-  if (n == 0) return 0;
-  k_resolve_dups<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(sel, owner, offsets, n);
+  const uint64_t tab = clear.keys ? clear.mask + 2 : 0;
+  const uint64_t end = std::max(n, std::max(tab, clear_words));
+  if (end == 0) return 0;
+  k_resolve_dups<<<grid_for(end, 256, 148 * 8), 256, 0, s>>>(sel, owner, offsets, n, clear,
+                                                            scan_state, clear_words);
   return 1;
 }
 

@@ -16,6 +16,13 @@ constexpr uint64_t kFnvOffset = 14695981039346656037ull;  // sim.hpp:57
 constexpr uint32_t kFnvPrimeLo = 0x1b3u;                   // prime = 2^40 + 0x1b3 (sim.hpp:58)
 
 // Device-resident buffer table for one installed grid.
+struct TableDev {
+  unsigned long long* keys = nullptr;  // kEmptyKey = unused
+  unsigned long long* vals = nullptr;  // min chunk index
+  uint64_t mask = 0;
+};
+constexpr unsigned long long kEmptyKey = 0xffffffffffffffffull;
+
 struct GridDev {
   const uint64_t* addr = nullptr;    // [nbufs]
   const uint64_t* bytes = nullptr;   // [nbufs]
@@ -30,15 +37,17 @@ struct GridDev {
   uint64_t c_end = 0;
   // per-buffer CUtensorMap array in device memory (4 KiB pages), or nullptr
   const void* tmaps = nullptr;
+  // Single-GPU snapshot: the K2 insert pass fused into K1 — the lane that
+  // finishes a chunk digest inserts it into `dd` (first occurrence by
+  // atomicMin, skipped when `kn` holds it and kn_use) and records the slot in
+  // dd_slot[chunk]. dd.keys == nullptr: off.
+  TableDev dd{};
+  TableDev kn{};
+  uint64_t* dd_slot = nullptr;
+  int kn_use = 0;
 };
 
 // Open-addressing digest table (dedup + known set), power-of-two capacity.
-struct TableDev {
-  unsigned long long* keys = nullptr;  // kEmptyKey = unused
-  unsigned long long* vals = nullptr;  // min chunk index
-  uint64_t mask = 0;
-};
-constexpr unsigned long long kEmptyKey = 0xffffffffffffffffull;
 
 // Launchers (each returns the number of kernels launched).
 // K1; with spec_off != nullptr also the fused speculative K3 (TMA bulk stores
@@ -65,9 +74,12 @@ int launch_table_insert_min(TableDev t, const uint64_t* keys, uint64_t n, uint64
 uint64_t scan_state_words(uint64_t n);
 int launch_dedup_insert(TableDev dedup, TableDev known, bool use_known, const uint64_t* dig,
                         const uint32_t* lens, uint64_t n, uint64_t* slot, cudaStream_t s);
+// scan_state must be zero on entry (left zero by launch_resolve_dups' clean-up);
+// spec_next (nullable) receives the staging layout (offset of selected chunks,
+// ~0 otherwise) — the next speculative layout of the fused K1.
 int launch_select(TableDev dedup, const uint64_t* slot, const uint32_t* lens, uint64_t n,
                   uint64_t* scan_state, uint8_t* sel, uint64_t* owner, uint64_t* offsets,
-                  uint32_t* sel_list, uint64_t* totals, cudaStream_t s);
+                  uint32_t* sel_list, uint64_t* totals, uint64_t* spec_next, cudaStream_t s);
 // Cross-rank striping: writer per selected global chunk, then one shard scan
 // per writer q (write_list for q == this rank: local chunk list + offsets).
 int launch_stripe_writer(const uint64_t* gdig, const uint32_t* glens, const uint8_t* sel,
@@ -80,7 +92,10 @@ int launch_shard_scan(const int32_t* writer, const uint32_t* glens, uint32_t nra
 int launch_page_classify(TableDev pages, TableDev known, bool use_known, TableDev prev,
                          bool use_prev, const uint64_t* dig, uint64_t n, uint64_t* slot,
                          uint8_t* flags, unsigned long long* counts, cudaStream_t s);
+// Also resets `clear` (the dedup table just consumed) and clear_words of
+// scan state to their empty values for the next selection (nullable).
 int launch_resolve_dups(const uint8_t* sel, const uint64_t* owner, uint64_t* offsets, uint64_t n,
+                        TableDev clear, uint64_t* scan_state, uint64_t clear_words,
                         cudaStream_t s);
 
 // K3 / K4 chunk copies.

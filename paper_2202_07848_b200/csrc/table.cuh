@@ -37,4 +37,16 @@ __device__ __forceinline__ uint64_t table_find(TableDev t, unsigned long long k)
   }
 }
 
+// The K2 insert of one finished chunk digest, done by K1 itself on the
+// single-GPU snapshot path (k_dedup_insert's body): known-set probe,
+// first-occurrence atomicMin, slot record.
+__device__ __forceinline__ void k1_insert(const GridDev& g, uint64_t chunk, uint64_t d) {
+  uint64_t s = ~0ull;
+  if (!(g.kn_use && table_find(g.kn, d) != ~0ull)) {
+    s = table_find_or_insert(g.dd, d);
+    atomicMin(g.dd.vals + s, static_cast<unsigned long long>(chunk));
+  }
+  g.dd_slot[chunk] = s;
+}
+
 }  // namespace snap
