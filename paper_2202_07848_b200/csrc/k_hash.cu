@@ -121,7 +121,7 @@ struct HashCfg {
 // also written to staging + offset with coalesced 16-byte streaming stores
 // read back from shared memory, so the image is read from HBM once for hash
 // and compaction together.
-template <class C, int PS>
+template <class C, int PS, int PPC>
 __global__ void __launch_bounds__(C::kWarps * 32, 1)
 k_hash(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ chunk_dig,
        const uint64_t* __restrict__ spec_off, uint8_t* __restrict__ staging) {
@@ -167,7 +167,15 @@ k_hash(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ chun
 
   bool reg0 = false, reg1 = false, wr0 = false, wr1 = false;
   const uint8_t *rsrc0 = nullptr, *rsrc1 = nullptr;
-  uint8_t *rdst0 = nullptr, *rdst1 = nullptr;
+  // staging destinations of the regular path, one base per chunk of the task:
+  // with <= 2 chunks per task (default geometry: 16 pages per chunk, 32 per
+  // task) each chunk is either not staged or staged contiguously, so striped
+  // layouts (alternate chunks of another rank) stay on the fast path; with
+  // more chunks per task the whole task must be contiguous (wshift = 31)
+  uint8_t *rdst0 = nullptr, *rdst1 = nullptr, *rdstb0 = nullptr, *rdstb1 = nullptr;
+  const uint32_t jb = 1u << ppc_shift;  // first page of the task's second chunk
+  const bool two_chunks = (uint32_t(NP) >> ppc_shift) <= 2;
+  const uint32_t wshift = two_chunks ? ppc_shift : 31;
   uint32_t ist = 0, cst = 0;  // stage of the next issue / of the step being consumed
 
   auto issue = [&](uint64_t p) {
@@ -181,7 +189,7 @@ k_hash(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ chun
         __syncwarp();
         bool allreg = true, anyw = false, dreg = true;
         const uint8_t* s0 = nullptr;
-        uint8_t* d0 = nullptr;
+        uint8_t *d0 = nullptr, *db = nullptr;
 #pragma unroll
         for (int c = 0; c < CH; ++c) {
           const int j = c * 32 + lane;
@@ -213,16 +221,18 @@ k_hash(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ chun
             s0 = reinterpret_cast<const uint8_t*>(__shfl_sync(kFull, reinterpret_cast<uint64_t>(src), 0));
             d0 = reinterpret_cast<uint8_t*>(__shfl_sync(kFull, reinterpret_cast<uint64_t>(dst), 0));
           }
+          if (two_chunks && jb < uint32_t(NP) && c == int(jb >> 5))
+            db = reinterpret_cast<uint8_t*>(__shfl_sync(kFull, reinterpret_cast<uint64_t>(dst), jb & 31));
           allreg = allreg && len == pb && src == s0 + uint64_t(j) * pb;
           anyw = anyw || dst != nullptr;
           dreg = dreg && d0 != nullptr && dst == d0 + uint64_t(j) * pb;
         }
         const bool w = __any_sync(kFull, anyw);
-        const bool r = __all_sync(kFull, allreg) && (!w || __all_sync(kFull, dreg));
+        const bool r = __all_sync(kFull, allreg) && (!w || two_chunks || __all_sync(kFull, dreg));
         if (par) {
-          reg1 = r; wr1 = w; rsrc1 = s0; rdst1 = d0;
+          reg1 = r; wr1 = w; rsrc1 = s0; rdst1 = d0; rdstb1 = db;
         } else {
-          reg0 = r; wr0 = w; rsrc0 = s0; rdst0 = d0;
+          reg0 = r; wr0 = w; rsrc0 = s0; rdst0 = d0; rdstb0 = db;
         }
         __syncwarp();
       }
@@ -257,10 +267,36 @@ k_hash(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ chun
     const uint8_t* sb = wbuf + st * C::kStageBytes;
     const uint32_t soff = s * SLAB + u * 16;
     if (par ? reg1 : reg0) {
-      uint8_t* dst = (par ? rdst1 : rdst0) + q * pb + soff;
+      uint8_t* da = par ? rdst1 : rdst0;
+      uint8_t* dbb = par ? rdstb1 : rdstb0;
+      if constexpr (PPC != 0 && NP / PPC <= 2 && PPC % PPI == 0) {
+        // pages per chunk known at compile time: the chunk split of the
+        // unrolled store loop is static (pages k*PPI + q, q < PPI)
+        constexpr int KA = PPC < NP ? PPC / PPI : C::kCopyInstr;
+        if (da) {
+          uint8_t* d = da + q * pb + soff;
 #pragma unroll
-      for (int k = 0; k < C::kCopyInstr; ++k)
-        st_stream16(dst + uint64_t(k) * PPI * pb, *reinterpret_cast<const uint4*>(sb + copy_off(k)));
+          for (int k = 0; k < KA; ++k)
+            st_stream16(d + uint64_t(k) * PPI * pb, *reinterpret_cast<const uint4*>(sb + copy_off(k)));
+        }
+        if (KA < C::kCopyInstr && dbb) {
+          uint8_t* d = dbb + q * pb + soff;
+#pragma unroll
+          for (int k = KA; k < C::kCopyInstr; ++k)
+            st_stream16(d + uint64_t(k - KA) * PPI * pb,
+                        *reinterpret_cast<const uint4*>(sb + copy_off(k)));
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < C::kCopyInstr; ++k) {
+          const uint32_t j = uint32_t(k * PPI) + q;
+          const uint32_t ch = j >> wshift;
+          uint8_t* base = ch ? dbb : da;
+          if (base)
+            st_stream16(base + uint64_t(j - (ch << wshift)) * pb + soff,
+                        *reinterpret_cast<const uint4*>(sb + copy_off(k)));
+        }
+      }
     } else {
 #pragma unroll
       for (int k = 0; k < C::kCopyInstr; ++k) {
@@ -747,8 +783,9 @@ int launch_hash_cfg(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
                     const uint64_t* spec_off, uint8_t* staging, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_hash<C, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem));
-    cudaFuncSetAttribute(k_hash<C, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem));
+    cudaFuncSetAttribute(k_hash<C, 12, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem));
+    cudaFuncSetAttribute(k_hash<C, 12, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem));
+    cudaFuncSetAttribute(k_hash<C, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem));
     attr = true;
   }
   const uint64_t c_end = g.c_end ? g.c_end : g.nchunks;
@@ -758,12 +795,17 @@ int launch_hash_cfg(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
   uint64_t blocks = (ntasks + C::kWarps - 1) / C::kWarps;
   const uint64_t cap = uint64_t(sm_count());
   if (blocks > cap) blocks = cap;
-  if (g.page_shift == 12)  // the reference's 4 KiB page: strides become immediates
-    k_hash<C, 12><<<unsigned(blocks), C::kWarps * 32, C::kSmem, s>>>(arena, g, chunk_dig, spec_off,
-                                                                     staging);
+  // the reference's 4 KiB page (strides become immediates) and the default
+  // 64 KiB chunk (static chunk split of the speculative stores)
+  if (g.page_shift == 12 && g.chunk_shift == 16)
+    k_hash<C, 12, 16><<<unsigned(blocks), C::kWarps * 32, C::kSmem, s>>>(arena, g, chunk_dig,
+                                                                         spec_off, staging);
+  else if (g.page_shift == 12)
+    k_hash<C, 12, 0><<<unsigned(blocks), C::kWarps * 32, C::kSmem, s>>>(arena, g, chunk_dig,
+                                                                        spec_off, staging);
   else
-    k_hash<C, 0><<<unsigned(blocks), C::kWarps * 32, C::kSmem, s>>>(arena, g, chunk_dig, spec_off,
-                                                                    staging);
+    k_hash<C, 0, 0><<<unsigned(blocks), C::kWarps * 32, C::kSmem, s>>>(arena, g, chunk_dig,
+                                                                       spec_off, staging);
   return 1;
 }
 
