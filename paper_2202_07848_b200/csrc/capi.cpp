@@ -171,11 +171,10 @@ int exchange_impl(snap_ctx* ctx) {
   uint32_t* glens;
   RC(ensure(ctx, ctx->d_gdig, n + maxn, &gdig));
   RC(ensure(ctx, ctx->d_glens, n + maxn, &glens));
-  // send buffers live past the gathered region: [n, n + maxn)
-  uint64_t* sdig = gdig + n;
-  if (ctx->nchunks)
-    CK(cudaMemcpyAsync(sdig, P<uint64_t>(ctx->d_dig), ctx->nchunks * 8, cudaMemcpyDeviceToDevice,
-                       ctx->stream));
+  // the digest vector is sent in place: d_dig holds >= maxn entries, the
+  // padding entries' values are ignored (their gathered lengths are 0)
+  uint64_t* sdig;
+  RC(ensure_keep(ctx, ctx->d_dig, maxn, ctx->nchunks * 8, &sdig));
   CKN(ncclAllGather(sdig, gdig, maxn, ncclUint64, ctx->comm, ctx->stream));
   if (!ctx->glens_valid) {
     uint32_t* slen = glens + n;
@@ -229,8 +228,15 @@ int staging_reserve(snap_ctx* ctx, uint64_t bytes, bool keep, uint8_t** out) {
   return ensure_keep(ctx, ctx->staging, bytes, keep ? ctx->staging.cap : 0, out);
 }
 
+// Staging capacity: the worst case (every chunk of this rank staged) unless the
+// grid is huge (C5: 80 GB per GPU), where a multi-rank shard is sized to the
+// predicted layout and grown on demand — at the price of one host sync per
+// snapshot to learn the actual shard size (compact_impl).
+constexpr uint64_t kFullStagingMax = 16ull << 30;
 uint64_t staging_target(const snap_ctx* ctx) {
-  if (!ctx->comm || ctx->nranks == 1 || ctx->spec_bytes == 0) return ctx->grid_bytes;
+  if (!ctx->comm || ctx->nranks == 1 || ctx->spec_bytes == 0 ||
+      ctx->grid_bytes <= kFullStagingMax)
+    return ctx->grid_bytes;
   return ctx->spec_bytes + ctx->spec_bytes / 16 + (64ull << 20);
 }
 
