@@ -914,7 +914,11 @@ int snapshot_host_pipelined(snap_ctx* ctx, const uint8_t* host_src, uint64_t add
                             uint64_t bytes, uint8_t* host_staging, uint64_t cap,
                             uint64_t* staged_bytes, uint64_t* host_digests) {
   const uint64_t n = ctx->nchunks;
-  const uint64_t slab = 64ull << 20;
+  static const uint64_t slab = [] {  // SNAP_HOST_SLAB_MB: pipeline granularity
+    const char* e = std::getenv("SNAP_HOST_SLAB_MB");
+    const long mb = e ? std::atol(e) : 0;
+    return uint64_t(mb > 0 ? mb : 64) << 20;
+  }();
   const uint64_t nslab = (bytes + slab - 1) / slab;
   if (!ctx->h2d) CK(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
   if (!ctx->d2h) CK(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
