@@ -151,9 +151,133 @@ int select_impl(snap_ctx* ctx, const uint64_t* dig, const uint32_t* lens, uint64
   return SNAP_OK;
 }
 
-// NCCL allgather of the per-rank digest vectors (and chunk lengths once per
-// grid), padded to the largest rank: the only bytes that cross NVLink (8 B
-// per 64 KiB chunk).
+// Exchange window layout (see ctx.h): flag lines, then two gathered vectors.
+uint64_t xflag_bytes(const snap_ctx* ctx) { return uint64_t(ctx->nranks) * 128; }
+uint64_t* gdig_region(const snap_ctx* ctx, uint64_t epoch) {
+  return reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(ctx->d_gdig.p) + xflag_bytes(ctx)) +
+         (epoch & 1) * uint64_t(ctx->nranks) * ctx->maxn;
+}
+
+void close_peer_windows(snap_ctx* ctx) {
+  for (size_t q = 0; q < ctx->xpeer.size(); ++q)
+    if (int(q) != ctx->rank && ctx->xpeer[q]) cudaIpcCloseMemHandle(ctx->xpeer[q]);
+  ctx->xpeer.clear();
+  ctx->xwin_ready = false;
+  ctx->k1_fanout = false;
+}
+
+// (Re)allocates this rank's exchange window for the grid's maxn and maps every
+// peer's window; collective (NCCL). Mode agreement: if any rank cannot map a
+// peer, every rank keeps the NCCL allgather (xwin_ready stays false).
+// Opt-in (SNAP_FUSED_EXCHANGE=1, same on every rank): measured on B200 at N = 2
+// and 4, the NVLink stores + system fence add as much to K1 as the barrier saves
+// over the NCCL allgather — the exchange step's cost is inter-GPU skew of K1
+// completion, which any barrier absorbs (profiles/r01_summary.md).
+int setup_exchange_window(snap_ctx* ctx) {
+  const int R = ctx->nranks;
+  close_peer_windows(ctx);
+  static const bool fused = [] {
+    const char* e = std::getenv("SNAP_FUSED_EXCHANGE");
+    return e && e[0] == '1';
+  }();
+  const uint64_t need = xflag_bytes(ctx) + 2 * uint64_t(R) * ctx->maxn * 8;
+  if (!fused) {  // NCCL allgather into the (unmapped) window
+    if (need > ctx->d_gdig.cap) {
+      release(ctx->d_gdig);
+      uint8_t* w;
+      RC(ensure(ctx, ctx->d_gdig, need, &w));
+    }
+    return SNAP_OK;
+  }
+  uint8_t* xh;
+  RC(ensure(ctx, ctx->d_xh, 64 * uint64_t(R) + 16, &xh));
+  int32_t* word = reinterpret_cast<int32_t*>(xh + 64 * uint64_t(R));
+  auto agree = [&](int32_t v, ncclRedOp_t op, int32_t* out) -> int {
+    CK(cudaMemcpyAsync(word, &v, 4, cudaMemcpyHostToDevice, ctx->stream));
+    CKN(ncclAllReduce(word, word, 1, ncclInt32, op, ctx->comm, ctx->stream));
+    CK(cudaMemcpyAsync(out, word, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return SNAP_OK;
+  };
+  // every importer has closed its mapping of the old windows once this
+  // collective returns, so a window may be freed and reallocated after it
+  int32_t any_grow = 0;
+  RC(agree(need > ctx->d_gdig.cap ? 1 : 0, ncclMax, &any_grow));
+  if (need > ctx->d_gdig.cap) {
+    release(ctx->d_gdig);
+    uint8_t* w;
+    RC(ensure(ctx, ctx->d_gdig, need, &w));
+  }
+  CK(cudaMemsetAsync(ctx->d_gdig.p, 0, xflag_bytes(ctx), ctx->stream));  // epochs restart
+  cudaIpcMemHandle_t h;
+  const bool ipc = cudaIpcGetMemHandle(&h, ctx->d_gdig.p) == cudaSuccess;
+  if (!ipc) {
+    cudaGetLastError();
+    std::memset(&h, 0, sizeof h);
+  }
+  CK(cudaMemcpyAsync(xh + 64 * ctx->rank, &h, 64, cudaMemcpyHostToDevice, ctx->stream));
+  CKN(ncclAllGather(xh + 64 * ctx->rank, xh, 64, ncclUint8, ctx->comm, ctx->stream));
+  std::vector<uint8_t> all(64 * size_t(R));
+  CK(cudaMemcpyAsync(all.data(), xh, all.size(), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->xpeer.assign(R, nullptr);
+  bool ok = true;
+  static const uint8_t zero[64] = {};
+  for (int q = 0; q < R; ++q) {
+    if (q == ctx->rank) {
+      ctx->xpeer[q] = ctx->d_gdig.p;
+      continue;
+    }
+    if (std::memcmp(all.data() + 64 * q, zero, 64) == 0) {
+      ok = false;
+      continue;
+    }
+    cudaIpcMemHandle_t ph;
+    std::memcpy(&ph, all.data() + 64 * q, 64);
+    if (cudaIpcOpenMemHandle(&ctx->xpeer[q], ph, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      ctx->xpeer[q] = nullptr;
+      ok = false;
+    }
+  }
+  int32_t all_ok = 0;
+  RC(agree(ok ? 1 : 0, ncclMin, &all_ok));
+  if (!all_ok) {
+    close_peer_windows(ctx);
+    return SNAP_OK;
+  }
+  std::vector<uint64_t*> xd(R), xf(R);
+  for (int q = 0; q < R; ++q) {
+    xf[q] = static_cast<uint64_t*>(ctx->xpeer[q]);
+    xd[q] = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(ctx->xpeer[q]) + xflag_bytes(ctx));
+  }
+  uint64_t **dxd, **dxf;
+  RC(ensure(ctx, ctx->d_xdig, R, &dxd));
+  RC(ensure(ctx, ctx->d_xflag, R, &dxf));
+  CK(cudaMemcpyAsync(dxd, xd.data(), 8 * R, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(dxf, xf.data(), 8 * R, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->xepoch = 0;
+  ctx->xwin_ready = true;
+  return SNAP_OK;
+}
+
+// K1 launches of a multi-rank ctx store their digests into every rank's
+// gathered vector of the coming exchange (epoch xepoch + 1) when the windows
+// are mapped; the exchange then reduces to the barrier.
+void k1_fanout(snap_ctx* ctx, GridDev& g) {
+  if (!ctx->comm || !ctx->xwin_ready) return;
+  g.xdig = P<uint64_t*>(ctx->d_xdig);
+  g.xn = uint32_t(ctx->nranks);
+  g.xoff = ((ctx->xepoch + 1) & 1) * uint64_t(ctx->nranks) * ctx->maxn +
+           uint64_t(ctx->rank) * ctx->maxn;
+  ctx->k1_fanout = true;
+}
+
+// The exchange step: per-rank digest vectors gathered (rank-major, padded to
+// the largest rank) — by K1's own NVLink stores + a peer barrier, or (first
+// snapshot of a grid, no IPC) by an NCCL allgather; chunk lengths once per
+// grid by NCCL. The only bytes that cross NVLink: 8 B per 64 KiB chunk.
 int exchange_impl(snap_ctx* ctx) {
   const int R = ctx->nranks;
   if (!ctx->glens_valid) {
@@ -165,18 +289,27 @@ int exchange_impl(snap_ctx* ctx) {
     CK(cudaMemcpyAsync(ctx->counts.data(), dc, 8 * R, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->maxn = *std::max_element(ctx->counts.begin(), ctx->counts.end());
+    ctx->k1_fanout = false;  // K1 ran before the windows existed for this grid
+    RC(setup_exchange_window(ctx));
   }
   const uint64_t maxn = ctx->maxn, n = uint64_t(R) * maxn;
-  uint64_t* gdig;
+  const uint64_t epoch = ctx->xepoch + 1;
+  uint64_t* gdig = gdig_region(ctx, epoch);
+  if (ctx->k1_fanout) {
+    CKL(snap::launch_peer_barrier(P<uint64_t*>(ctx->d_xflag), static_cast<uint64_t*>(ctx->d_gdig.p),
+                                  uint32_t(ctx->rank), uint32_t(R), epoch, ctx->stream));
+  } else {
+    // the digest vector is sent in place: d_dig holds >= maxn entries, the
+    // padding entries' values are ignored (their gathered lengths are 0)
+    uint64_t* sdig;
+    RC(ensure_keep(ctx, ctx->d_dig, maxn, ctx->nchunks * 8, &sdig));
+    CKN(ncclAllGather(sdig, gdig, maxn, ncclUint64, ctx->comm, ctx->stream));
+  }
+  ctx->k1_fanout = false;
+  ctx->xepoch = epoch;
   uint32_t* glens;
-  RC(ensure(ctx, ctx->d_gdig, n + maxn, &gdig));
-  RC(ensure(ctx, ctx->d_glens, n + maxn, &glens));
-  // the digest vector is sent in place: d_dig holds >= maxn entries, the
-  // padding entries' values are ignored (their gathered lengths are 0)
-  uint64_t* sdig;
-  RC(ensure_keep(ctx, ctx->d_dig, maxn, ctx->nchunks * 8, &sdig));
-  CKN(ncclAllGather(sdig, gdig, maxn, ncclUint64, ctx->comm, ctx->stream));
   if (!ctx->glens_valid) {
+    RC(ensure(ctx, ctx->d_glens, n + maxn, &glens));
     uint32_t* slen = glens + n;
     CK(cudaMemsetAsync(slen, 0, maxn * 4, ctx->stream));
     if (ctx->nchunks)
@@ -202,7 +335,7 @@ int stripe_impl(snap_ctx* ctx) {
   uint64_t* scan2;
   RC(ensure(ctx, ctx->scan2, snap::scan_state_words(n) + 1, &scan2));
   ctx->shard_offsets_all = false;
-  CKL(snap::launch_stripe_writer(P<uint64_t>(ctx->d_gdig), P<uint32_t>(ctx->d_glens),
+  CKL(snap::launch_stripe_writer(gdig_region(ctx, ctx->xepoch), P<uint32_t>(ctx->d_glens),
                                  P<uint8_t>(ctx->sel), ctx->nranks, maxn, writer, ctx->stream));
   CKL(snap::launch_shard_scan(writer, P<uint32_t>(ctx->d_glens), ctx->nranks, maxn, ctx->rank, true,
                               scan2, shard_off, my_list, my_off, my_tot,
@@ -319,6 +452,7 @@ int hash_fused(snap_ctx* ctx, uint64_t c0 = 0, uint64_t c1 = 0) {
     g.kn_use = ctx->kn_count > 0 ? 1 : 0;
     ctx->k1_inserted = true;
   }
+  k1_fanout(ctx, g);
   if (ctx->kn_count > 0) {
     CKL(snap::launch_hash(ctx->arena, g, P<uint64_t>(ctx->d_dig), nullptr, nullptr, ctx->stream));
     ctx->spec_used = false;
@@ -435,6 +569,7 @@ int snap_close(snap_ctx* ctx) {
   if (!ctx) return SNAP_OK;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  close_peer_windows(ctx);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   splice_release(ctx);
   window_release(ctx);
@@ -445,7 +580,7 @@ int snap_close(snap_ctx* ctx) {
         &ctx->staging, &ctx->d_counts, &ctx->d_gdig, &ctx->d_glens, &ctx->d_writer,
         &ctx->d_shard_off, &ctx->d_my_list, &ctx->d_my_off, &ctx->d_my_totals, &ctx->d_dig2,
         &ctx->d_expect, &ctx->d_nbad, &ctx->d_srcoff, &ctx->d_spec[0], &ctx->d_spec[1],
-        &ctx->d_tmaps, &ctx->scan2})
+        &ctx->d_tmaps, &ctx->scan2, &ctx->d_xdig, &ctx->d_xflag, &ctx->d_xh})
     release(*m);
   for (cudaEvent_t e : ctx->prof.pool) cudaEventDestroy(e);
   if (ctx->arena) cudaFree(ctx->arena);
@@ -615,6 +750,8 @@ int snap_set_buffers(snap_ctx* ctx, const snap_buf* bufs, uint64_t n, const snap
   ctx->spec_used = false;
   ctx->k1_inserted = false;
   ctx->spec_next_done = false;
+  ctx->xwin_ready = false;  // maxn may change: the next exchange re-maps the windows
+  ctx->k1_fanout = false;
   if (n_chunks) *n_chunks = ctx->nchunks;
   return SNAP_OK;
 }
@@ -624,8 +761,9 @@ int snap_hash(snap_ctx* ctx) {
   CK(cudaSetDevice(ctx->device));
   {
     ProfScope ps(ctx, kProfHash);
-    CKL(snap::launch_hash(ctx->arena, ctx->grid, P<uint64_t>(ctx->d_dig), nullptr, nullptr,
-                          ctx->stream));
+    GridDev g = ctx->grid;
+    k1_fanout(ctx, g);  // collective K1: digests straight into every rank's gathered vector
+    CKL(snap::launch_hash(ctx->arena, g, P<uint64_t>(ctx->d_dig), nullptr, nullptr, ctx->stream));
   }
   ctx->spec_used = false;
   ctx->k1_inserted = false;
@@ -691,7 +829,8 @@ int snap_known_commit(snap_ctx* ctx) {
     std::vector<uint32_t> gl(n);
     std::vector<uint64_t> gd(n), live;
     CK(cudaMemcpyAsync(gl.data(), ctx->d_glens.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaMemcpyAsync(gd.data(), ctx->d_gdig.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(gd.data(), gdig_region(ctx, ctx->xepoch), n * 8, cudaMemcpyDeviceToHost,
+                       ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     for (uint64_t i = 0; i < n; ++i)
       if (gl[i]) live.push_back(gd[i]);
@@ -710,7 +849,7 @@ int snap_select(snap_ctx* ctx) {
       RC(exchange_impl(ctx));
     }
     ProfScope ps(ctx, kProfSelect);
-    RC(select_impl(ctx, P<uint64_t>(ctx->d_gdig), P<uint32_t>(ctx->d_glens),
+    RC(select_impl(ctx, gdig_region(ctx, ctx->xepoch), P<uint32_t>(ctx->d_glens),
                    uint64_t(ctx->nranks) * ctx->maxn));
     return stripe_impl(ctx);
   }
@@ -759,7 +898,9 @@ int snap_get_global_digests(snap_ctx* ctx, uint64_t* gdig, uint32_t* glens) {
   if (!(ctx->comm && ctx->exchanged)) return fail(ctx, SNAP_EINVAL, "no exchanged digests");
   CK(cudaSetDevice(ctx->device));
   const uint64_t n = uint64_t(ctx->nranks) * ctx->maxn;
-  if (gdig) CK(cudaMemcpyAsync(gdig, ctx->d_gdig.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (gdig)
+    CK(cudaMemcpyAsync(gdig, gdig_region(ctx, ctx->xepoch), n * 8, cudaMemcpyDeviceToHost,
+                       ctx->stream));
   if (glens) CK(cudaMemcpyAsync(glens, ctx->d_glens.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return SNAP_OK;
@@ -873,7 +1014,7 @@ int snap_restore_shards(snap_ctx* ctx, int src_rank, int verify) {
                                       " chunk(s) have no source (known/older blobs)");
   if (!verify) return SNAP_OK;
   // expected digests: src_rank's row of the allgathered vector
-  return verify_grid(ctx, P<uint64_t>(ctx->d_gdig) + uint64_t(src_rank) * ctx->maxn);
+  return verify_grid(ctx, gdig_region(ctx, ctx->xepoch) + uint64_t(src_rank) * ctx->maxn);
 }
 
 // ---------------------------------------------------------------- K3
@@ -1204,6 +1345,9 @@ int snap_comm_init(snap_ctx* ctx, int nranks, int rank, const void* id128) {
   CKN(ncclCommInitRank(&ctx->comm, nranks, id, rank));
   ctx->nranks = nranks;
   ctx->rank = rank;
+  ctx->xepoch = 0;
+  ctx->xwin_ready = false;
+  ctx->k1_fanout = false;
   ctx->glens_valid = false;
   ctx->exchanged = false;
   ctx->spec_ready = false;
@@ -1220,6 +1364,7 @@ int snap_comm_destroy(snap_ctx* ctx) {
   for (size_t r = 0; r < ctx->peer_staging.size(); ++r)
     if (int(r) != ctx->rank && ctx->peer_staging[r]) cudaIpcCloseMemHandle(ctx->peer_staging[r]);
   ctx->peer_staging.clear();
+  close_peer_windows(ctx);
   CKN(ncclCommDestroy(ctx->comm));
   ctx->comm = nullptr;
   ctx->nranks = 1;

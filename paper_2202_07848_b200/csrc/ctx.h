@@ -87,6 +87,14 @@ struct snap_ctx {
   std::vector<uint64_t> counts;
   bool glens_valid = false;
   DevMem d_counts, d_gdig, d_glens, d_writer, d_shard_off, d_my_list, d_my_off, d_my_totals;
+  // Exchange window = d_gdig: [nranks flag lines of 128 B][2 gathered digest
+  // vectors of nranks * maxn, by epoch parity]. Every rank maps every peer's
+  // window (CUDA IPC); K1 stores its digests into all of them (fused exchange).
+  std::vector<void*> xpeer;   // [nranks] window bases (own = d_gdig.p)
+  DevMem d_xdig, d_xflag, d_xh;
+  bool xwin_ready = false;    // peers mapped for the current grid
+  bool k1_fanout = false;     // K1 stored the digests of the coming exchange
+  uint64_t xepoch = 0;        // exchanges done (gathered vector = parity xepoch & 1)
 
   // verify / restore scratch
   DevMem d_dig2, d_expect, d_nbad, d_srcoff;

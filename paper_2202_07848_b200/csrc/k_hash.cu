@@ -358,7 +358,7 @@ k_hash(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ chun
       for (int c = 0; c < CH; ++c) {
         const uint64_t myslot = slot0 + c * 32 + lane;
         if (ppc_shift == 0) {
-          if (mylen[c] > 0) chunk_dig[myslot] = (uint64_t(hi[c]) << 32) | lo[c];
+          if (mylen[c] > 0) k1_store_digest(g, myslot, (uint64_t(hi[c]) << 32) | lo[c], chunk_dig);
         } else {
           // chunk digest = digest_of_words(page digests), folded with
           // warp-uniform shuffles inside each group of ppc lanes
@@ -375,7 +375,8 @@ k_hash(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ chun
               fnv_word(flo, fhi, phi);
             }
           }
-          if (lane == base && mylen[c] > 0) chunk_dig[myslot >> ppc_shift] = (uint64_t(fhi) << 32) | flo;
+          if (lane == base && mylen[c] > 0)
+            k1_store_digest(g, myslot >> ppc_shift, (uint64_t(fhi) << 32) | flo, chunk_dig);
         }
       }
     }
@@ -393,6 +394,7 @@ k_hash(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ chun
       if (c < c_end) k1_insert(g, c, chunk_dig[c]);
     }
   }
+  if (g.xdig != nullptr) __threadfence_system();  // NVLink digest stores before the barrier
 }
 
 // ---------------------------------------------------------------------------
@@ -537,7 +539,7 @@ k_hash_ws(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ c
       if (s == ns - 1) {
         const uint64_t slot0 = slot_base + (gw + i * nw) * 32;
         if (ppc_shift == 0) {
-          if (mylen > 0) chunk_dig[slot0 + lane] = (uint64_t(hi) << 32) | lo;
+          if (mylen > 0) k1_store_digest(g, slot0 + lane, (uint64_t(hi) << 32) | lo, chunk_dig);
         } else {
           const uint32_t ppc = 1u << ppc_shift;
           const int base = lane & ~static_cast<int>(ppc - 1);
@@ -552,7 +554,8 @@ k_hash_ws(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ c
               fnv_word(flo, fhi, phi);
             }
           }
-          if (lane == base && mylen > 0) chunk_dig[(slot0 + lane) >> ppc_shift] = (uint64_t(fhi) << 32) | flo;
+          if (lane == base && mylen > 0)
+            k1_store_digest(g, (slot0 + lane) >> ppc_shift, (uint64_t(fhi) << 32) | flo, chunk_dig);
         }
       }
     }
@@ -681,6 +684,7 @@ k_hash_ws(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ c
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
   }
+  if (g.xdig != nullptr) __threadfence_system();
 }
 
 // Buffer digest = digest_of_words(chunk digests of the buffer); one thread

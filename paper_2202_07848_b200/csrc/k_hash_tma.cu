@@ -226,7 +226,7 @@ k_hash_tma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
     if (s == ns - 1) {
       const uint64_t slot0 = slot_base + (gw + i * nw) * 32;
       if (ppc_shift == 0) {
-        if (mylen > 0) chunk_dig[slot0 + lane] = (uint64_t(hi) << 32) | lo;
+        if (mylen > 0) k1_store_digest(g, slot0 + lane, (uint64_t(hi) << 32) | lo, chunk_dig);
       } else {
         const uint32_t ppc = 1u << ppc_shift;
         const int base = lane & ~static_cast<int>(ppc - 1);
@@ -241,10 +241,12 @@ k_hash_tma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
             fnv_word(flo, fhi, phi);
           }
         }
-        if (lane == base && mylen > 0) chunk_dig[(slot0 + lane) >> ppc_shift] = (uint64_t(fhi) << 32) | flo;
+        if (lane == base && mylen > 0)
+            k1_store_digest(g, (slot0 + lane) >> ppc_shift, (uint64_t(fhi) << 32) | flo, chunk_dig);
       }
     }
   }
+  if (g.xdig != nullptr) __threadfence_system();
 }
 
 constexpr int kTmaWarps = 16, kTmaStages = 3;

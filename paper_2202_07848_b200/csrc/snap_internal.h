@@ -45,6 +45,12 @@ struct GridDev {
   TableDev kn{};
   uint64_t* dd_slot = nullptr;
   int kn_use = 0;
+  // Multi-rank digest exchange fused into K1: every finished chunk digest is
+  // also stored into each rank's gathered vector over NVLink (xdig[q] = rank
+  // q's CUDA-IPC-mapped window, entry xoff + chunk). xdig == nullptr: off.
+  uint64_t* const* xdig = nullptr;
+  uint32_t xn = 0;
+  uint64_t xoff = 0;
 };
 
 // Open-addressing digest table (dedup + known set), power-of-two capacity.
@@ -61,6 +67,11 @@ int launch_hash_tma(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
 // host: one 128-byte CUtensorMap per buffer into host_maps; 0 on success
 int encode_tensor_maps(const uint8_t* arena, const uint64_t* addr, const uint64_t* bytes,
                        uint32_t nbufs, void* host_maps);
+// Cross-GPU barrier after a fused-exchange K1: signal every peer (flag slot
+// `rank` of its window := epoch, release.sys) and wait for every peer's
+// signal in this rank's window (acquire.sys); traps after ~30 s.
+int launch_peer_barrier(uint64_t* const* xflag, const uint64_t* myflag, uint32_t rank, uint32_t n,
+                        uint64_t epoch, cudaStream_t s);
 int launch_buf_fold(const GridDev& g, const uint64_t* chunk_dig, uint64_t* buf_dig, cudaStream_t s);
 int launch_fill_mix64(uint64_t* dst, uint64_t nwords, uint64_t seed, uint64_t base, cudaStream_t s);
 int launch_xor_words(uint8_t* arena, const uint64_t* addrs, uint64_t n, uint64_t value,

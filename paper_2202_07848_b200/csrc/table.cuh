@@ -37,6 +37,15 @@ __device__ __forceinline__ uint64_t table_find(TableDev t, unsigned long long k)
   }
 }
 
+// K1: store one finished chunk digest locally and, with the fused exchange, into
+// every rank's gathered vector (8-byte NVLink stores, fire and forget).
+__device__ __forceinline__ void k1_store_digest(const GridDev& g, uint64_t chunk, uint64_t d,
+                                                uint64_t* chunk_dig) {
+  chunk_dig[chunk] = d;
+  if (g.xdig != nullptr)
+    for (uint32_t q = 0; q < g.xn; ++q) g.xdig[q][g.xoff + chunk] = d;
+}
+
 // The K2 insert of one finished chunk digest, done by K1 itself on the
 // single-GPU snapshot path (k_dedup_insert's body): known-set probe,
 // first-occurrence atomicMin, slot record.

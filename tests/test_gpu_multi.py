@@ -19,14 +19,18 @@ def ngpus():
         return 0
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_dist_snapshot_parity(world):
+@pytest.mark.parametrize("world,fused", [(2, False), (4, False), (2, True)])
+def test_dist_snapshot_parity(world, fused):
+    """fused: the digest exchange done by K1's own NVLink stores into every rank's
+    CUDA-IPC-mapped window + a peer barrier (SNAP_FUSED_EXCHANGE=1) instead of NCCL
+    (the worker's second snapshot takes that path)."""
     if ngpus() < world:
         pytest.skip(f"needs {world} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={world}", "--master-addr=127.0.0.1", "--master-port=29533",
            os.path.join(ROOT, "tests", "dist_snapshot_worker.py")]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=ROOT)
+    env = dict(os.environ, SNAP_FUSED_EXCHANGE="1" if fused else "0")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=ROOT, env=env)
     print(r.stdout[-3000:], r.stderr[-3000:])
     assert r.returncode == 0
     assert "DIST PARITY OK" in r.stdout
