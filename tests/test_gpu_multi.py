@@ -49,3 +49,17 @@ def test_dist_resize_reshard(world):
     print(r.stdout[-3000:], r.stderr[-3000:])
     assert r.returncode == 0
     assert "RESIZE PARITY OK" in r.stdout
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_dist_spliced_grad_allreduce(world):
+    """K5 local accumulation of the co-sliced ranks + snap_allreduce across GPUs."""
+    if ngpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr=127.0.0.1", "--master-port=29535",
+           os.path.join(ROOT, "tests", "dist_grad_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=ROOT)
+    print(r.stdout[-3000:], r.stderr[-3000:])
+    assert r.returncode == 0
+    assert "GRAD PARITY OK" in r.stdout
