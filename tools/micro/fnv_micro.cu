@@ -70,6 +70,21 @@ __device__ __forceinline__ void stepH(uint32_t& lo, uint32_t& hi, uint32_t b) {
   lo = x * 0x1b3u;
 }
 
+// byte pairs: hi2 = hi*P^2 + (t0.hi*P + t1.hi) + 256*(lo1 + x1), because x0*P = lo1 (mod 2^32)
+__device__ __forceinline__ void stepG2(uint32_t& lo, uint32_t& hi, uint32_t b0, uint32_t b1) {
+  const uint32_t x0 = lo ^ (b0 & 0xffu);
+  const uint64_t t0 = (uint64_t)x0 * 0x1b3u;
+  const uint32_t l1 = (uint32_t)t0;
+  const uint32_t x1 = l1 ^ (b1 & 0xffu);
+  const uint64_t t1 = (uint64_t)x1 * 0x1b3u;
+  const uint32_t a = (uint32_t)(t0 >> 32) * 0x1b3u + (uint32_t)(t1 >> 32);
+  uint32_t bb;
+  asm("{\n\t.reg .u32 u;\n\tadd.u32 u, %1, %2;\n\tshl.b32 u, u, 8;\n\tadd.u32 %0, u, %3;\n\t}"
+      : "=r"(bb) : "r"(l1), "r"(x1), "r"(a));
+  hi = hi * 189225u + bb;
+  lo = (uint32_t)t1;
+}
+
 template <int V, int CH>
 __global__ void __launch_bounds__(512) k(uint64_t* out, int iters, uint32_t z) {
   uint32_t lo[CH], hi[CH];
@@ -82,8 +97,12 @@ __global__ void __launch_bounds__(512) k(uint64_t* out, int iters, uint32_t z) {
 #pragma unroll
       for (int c = 0; c < CH; ++c) {
         uint32_t ww = w ^ c;
+        if (V == 7) {
+          stepG2(lo[c], hi[c], ww, ww >> 8);
+          stepG2(lo[c], hi[c], ww >> 16, ww >> 24);
+        }
 #pragma unroll
-        for (int bb = 0; bb < 4; ++bb) {
+        for (int bb = 0; bb < 4 && V != 7; ++bb) {
           if (V == 0) stepA(lo[c], hi[c], ww >> (8 * bb));
           if (V == 1) stepB(lo[c], hi[c], ww >> (8 * bb));
           if (V == 2) stepC(lo[c], hi[c], ww >> (8 * bb));
@@ -128,5 +147,6 @@ int main() {
   run<4, 1>("E-wide", 512, 1); run<4, 2>("E-wide", 512, 1); run<4, 2>("E-wide", 1024, 1);
   run<5, 1>("F-prmt+", 512, 1); run<5, 2>("F-prmt+", 512, 1); run<5, 2>("F-prmt+", 1024, 1);
   run<6, 1>("H-hi", 512, 1); run<6, 2>("H-hi", 512, 1); run<6, 2>("H-hi", 1024, 1);
+  run<7, 1>("G-pair", 512, 1); run<7, 2>("G-pair", 512, 1); run<7, 4>("G-pair", 256, 1);
   return 0;
 }
