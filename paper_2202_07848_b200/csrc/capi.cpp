@@ -1257,6 +1257,7 @@ static int verify_grid(snap_ctx* ctx, const uint64_t* expect_dev) {
 int snap_restore(snap_ctx* ctx, const void* image, uint64_t image_bytes, const uint64_t* src_off,
                  const uint64_t* expect_digests, int verify) {
   if (!ctx || (!src_off && ctx->nchunks) || (!image && ctx->nchunks)) return SNAP_EINVAL;
+  if (ctx->nchunks == 0) return SNAP_OK;  // empty layout: nothing to write or verify
   for (uint64_t g = 0; g < ctx->nchunks; ++g)
     if (src_off[g] > image_bytes || ctx->h_lens[g] > image_bytes - src_off[g] || src_off[g] % 256)
       return fail(ctx, SNAP_EFAULT, "restore: chunk " + std::to_string(g) +

@@ -583,7 +583,14 @@ extern "C" int snap_load(snap_ctx* ctx, const char* dir, int rank, int verify, i
     for (const Blob& x : blobs) stats->layout_bytes += x.len;
   }
   tr.mark("blobs read + H2D");
-  const int rc = snap_restore(ctx, dimg, image, src.data(), dig.data(), verify);
+  RC(snap_restore(ctx, dimg, image, src.data(), dig.data(), verify));
   tr.mark("K4 scatter + verify");
-  return rc;
+  // the layout's digests become the context's (verified against the restored
+  // bytes when verify != 0): snap_get_digests works right after a load
+  if (nch) {
+    CK(cudaMemcpyAsync(ctx->d_dig.p, dig.data(), nch * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  ctx->hashed = true;
+  return SNAP_OK;
 }
