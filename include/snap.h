@@ -367,6 +367,11 @@ typedef struct {
  * nthreads <= 0: one writer thread per core, at most 16. */
 int snap_persist(snap_ctx* ctx, const char* dir, const void* host_image, uint64_t host_bytes,
                  int nthreads, snap_persist_stats* stats);
+/* snap_persist with an explicit layout id (time-sliced ranks share one GPU and
+ * one ctx: each rank's cut is persisted as layout.<its rank>). snap_persist
+ * uses the communicator rank (0 without one). */
+int snap_persist_rank(snap_ctx* ctx, const char* dir, int layout_rank, const void* host_image,
+                      uint64_t host_bytes, int nthreads, snap_persist_stats* stats);
 /* restore_job materialization from a directory (ckpt.cpp:504-533): installs
  * rank `rank`'s layout, streams every referenced blob through pinned slabs to
  * the device and scatters the chunks to their recorded addresses (K4).
@@ -374,6 +379,15 @@ int snap_persist(snap_ctx* ctx, const char* dir, const void* host_image, uint64_
  * ckpt.cpp:26-27): SNAP_EFAULT on a corrupt, truncated or missing blob. */
 int snap_load(snap_ctx* ctx, const char* dir, int rank, int verify, int nthreads,
               snap_persist_stats* stats);
+/* The rest of restore_job's materialization for a GPU (ckpt.cpp:517-528): a
+ * co-resident (time-sliced, currently inactive) rank's persisted layout
+ * becomes splice rank `splice_rank`'s buffer map, and every chunk whose digest
+ * the HBM chunk cache does not hold yet is streamed in from the blob files
+ * (the reference copies it into its host cache). A later snap_splice_switch to
+ * that rank restores it from the cache, or finds it resident. Needs
+ * snap_splice_init; SNAP_EFAULT on a missing or truncated blob. */
+int snap_splice_load(snap_ctx* ctx, const char* dir, int layout_rank, int splice_rank,
+                     int nthreads, snap_persist_stats* stats);
 
 /* ---------------------------------------------------------- timing */
 

@@ -159,6 +159,10 @@ _SIGS = {
                                C.POINTER(PersistStats)]),
     "snap_load": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int, C.c_int, C.c_int,
                             C.POINTER(PersistStats)]),
+    "snap_persist_rank": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int, C.c_void_p, C.c_uint64,
+                                    C.c_int, C.POINTER(PersistStats)]),
+    "snap_splice_load": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int, C.c_int, C.c_int,
+                                   C.POINTER(PersistStats)]),
     "snap_global_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "snap_get_global_digests": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "snap_get_shard": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64),
@@ -541,13 +545,27 @@ class Ctx:
         return [(out[i].addr, out[i].bytes, out[i].digest) for i in range(n.value)]
 
     # -- on-disk format (BlobStore::persist, ckpt.cpp:42-52; restore_job, ckpt.cpp:504-533)
-    def persist(self, directory, host_ptr: int = 0, host_bytes: int = 0, threads: int = 0):
-        """Writes the last snapshot's staged chunks as blobs/<2hex>/<16hex> plus this
-        rank's layout + manifest under `directory`; returns the stats dict."""
+    def persist(self, directory, host_ptr: int = 0, host_bytes: int = 0, threads: int = 0,
+                layout_rank=None):
+        """Writes the last snapshot's staged chunks as blobs/<2hex>/<16hex> plus the layout
+        + manifest (id = layout_rank, default the communicator rank) under `directory`."""
         st = PersistStats()
-        self._ck(self._L.snap_persist(self.h, os.fsencode(directory),
-                                      C.c_void_p(host_ptr) if host_ptr else None, host_bytes,
-                                      threads, C.byref(st)), "snap_persist")
+        hp = C.c_void_p(host_ptr) if host_ptr else None
+        if layout_rank is None:
+            rc = self._L.snap_persist(self.h, os.fsencode(directory), hp, host_bytes, threads,
+                                      C.byref(st))
+        else:
+            rc = self._L.snap_persist_rank(self.h, os.fsencode(directory), layout_rank, hp,
+                                           host_bytes, threads, C.byref(st))
+        self._ck(rc, "snap_persist")
+        return st.as_dict()
+
+    def splice_load(self, directory, layout_rank: int, splice_rank: int, threads: int = 0):
+        """restore_job cache seeding: a co-resident rank's persisted layout becomes splice
+        rank `splice_rank` and its chunks enter the HBM chunk cache."""
+        st = PersistStats()
+        self._ck(self._L.snap_splice_load(self.h, os.fsencode(directory), layout_rank,
+                                          splice_rank, threads, C.byref(st)), "snap_splice_load")
         return st.as_dict()
 
     def load(self, directory, rank: int = 0, verify: bool = True, threads: int = 0):

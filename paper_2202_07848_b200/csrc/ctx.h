@@ -229,6 +229,10 @@ inline uint64_t table_cap(uint64_t n) {
   return c;
 }
 
+// splice_host.cpp: seed the splice chunk cache with a rank's content (restore_job)
+int splice_seed(snap_ctx* ctx, int rank, const uint8_t* image, const uint64_t* src_off,
+                const uint64_t* dig);
+
 int select_with_known(snap_ctx* ctx, const uint64_t* dig, const uint32_t* lens, uint64_t n,
                       TableDev kn, bool use_known, bool inserted = false,
                       uint64_t* spec_next = nullptr);

@@ -146,6 +146,24 @@ k_scatter_shards(uint8_t* __restrict__ arena, GridDev g, const uint32_t* __restr
   if (lane == 0 && miss) atomicAdd(missing, miss);
 }
 
+// K3 from an image instead of the arena: list entry k (chunk sel_list[k]) is
+// copied from image + src_off[chunk] to dst + offsets[chunk] (splice cache
+// seeding from restored blobs).
+__global__ void __launch_bounds__(kThreads)
+k_gather_from(const uint8_t* __restrict__ image, const uint64_t* __restrict__ src_off,
+              const uint32_t* __restrict__ lens, const uint32_t* __restrict__ sel_list,
+              const uint64_t* __restrict__ totals, const uint64_t* __restrict__ offsets,
+              uint8_t* __restrict__ dst) {
+  const uint64_t nsel = totals[0];
+  const int lane = threadIdx.x & 31;
+  const uint64_t w0 = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * kThreads) >> 5;
+  for (uint64_t w = w0; w < nsel; w += nw) {
+    const uint32_t gc = sel_list[w];
+    warp_copy(dst + offsets[gc], image + src_off[gc], lens[gc], lane);
+  }
+}
+
 __global__ void k_compare(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b,
                           uint64_t n, unsigned long long* nbad) {
   unsigned long long bad = 0;
@@ -245,6 +263,17 @@ int launch_scatter(uint8_t* arena, const GridDev& g, const uint32_t* lens, const
   uint64_t blocks = (g.nchunks * 32 + kThreads - 1) / kThreads;
   if (blocks > copy_grid()) blocks = copy_grid();
   k_scatter<<<unsigned(blocks), kThreads, 0, s>>>(arena, g, lens, image, src_off);
+  return 1;
+}
+
+int launch_gather_from(const uint8_t* image, const uint64_t* src_off, const uint32_t* lens,
+                       const uint32_t* sel_list, const uint64_t* totals, const uint64_t* offsets,
+                       uint8_t* dst, uint64_t max_sel, cudaStream_t s) {
+  if (max_sel == 0) return 0;
+  uint64_t blocks = (max_sel * 32 + kThreads - 1) / kThreads;
+  if (blocks > copy_grid()) blocks = copy_grid();
+  k_gather_from<<<unsigned(blocks), kThreads, 0, s>>>(image, src_off, lens, sel_list, totals,
+                                                      offsets, dst);
   return 1;
 }
 

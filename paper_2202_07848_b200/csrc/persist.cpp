@@ -310,7 +310,14 @@ extern "C" int snap_blob_rel_path(uint64_t digest, char* out, uint64_t cap) {
 
 extern "C" int snap_persist(snap_ctx* ctx, const char* dir, const void* host_image,
                             uint64_t host_bytes, int nthreads, snap_persist_stats* stats) {
-  if (!ctx || !dir) return SNAP_EINVAL;
+  if (!ctx) return SNAP_EINVAL;
+  return snap_persist_rank(ctx, dir, ctx->rank, host_image, host_bytes, nthreads, stats);
+}
+
+extern "C" int snap_persist_rank(snap_ctx* ctx, const char* dir, int layout_rank,
+                                 const void* host_image, uint64_t host_bytes, int nthreads,
+                                 snap_persist_stats* stats) {
+  if (!ctx || !dir || layout_rank < 0) return SNAP_EINVAL;
   if (!ctx->selected) return fail(ctx, SNAP_EINVAL, "persist needs a prior snapshot");
   const int threads = pick_threads(nthreads);
   const uint64_t nch = ctx->nchunks;
@@ -410,7 +417,7 @@ extern "C" int snap_persist(snap_ctx* ctx, const char* dir, const void* host_ima
     st.layout_blobs = uniq.size();
   }
   std::vector<uint8_t> lay(sizeof(LayoutHdr) + ctx->bufs.size() * sizeof(LayoutRec) + nch * 8 + 8);
-  LayoutHdr h{kLayoutMagic, kLayoutVersion, ctx->rank, ctx->geom.page_bytes, ctx->geom.chunk_bytes,
+  LayoutHdr h{kLayoutMagic, kLayoutVersion, layout_rank, ctx->geom.page_bytes, ctx->geom.chunk_bytes,
               uint64_t(ctx->bufs.size()), nch};
   std::memcpy(lay.data(), &h, sizeof h);
   uint8_t* q = lay.data() + sizeof h;
@@ -423,10 +430,10 @@ extern "C" int snap_persist(snap_ctx* ctx, const char* dir, const void* host_ima
   q += nch * 8;
   const uint64_t trailer = fnv_bytes(lay.data(), size_t(q - lay.data()));
   std::memcpy(q, &trailer, 8);
-  const std::string rk = std::to_string(ctx->rank);
+  const std::string rk = std::to_string(layout_rank);
   int r = put_file(root + "/layout." + rk + ".snapl", lay.data(), lay.size(), false);
   if (r < 0) return fail(ctx, SNAP_EINVAL, std::string("persist: layout: ") + std::strerror(-r));
-  const std::string js = json_layout(ctx, ctx->rank, bufdig, trailer, st, s_g, staged);
+  const std::string js = json_layout(ctx, layout_rank, bufdig, trailer, st, s_g, staged);
   r = put_file(root + "/manifest.dev." + rk + ".json", js.data(), js.size(), false);
   if (r < 0) return fail(ctx, SNAP_EINVAL, std::string("persist: manifest: ") + std::strerror(-r));
   tr.mark("layout + manifest");
@@ -434,35 +441,35 @@ extern "C" int snap_persist(snap_ctx* ctx, const char* dir, const void* host_ima
   return SNAP_OK;
 }
 
-extern "C" int snap_load(snap_ctx* ctx, const char* dir, int rank, int verify, int nthreads,
-                         snap_persist_stats* stats) {
-  if (!ctx || !dir) return SNAP_EINVAL;
-  const int threads = pick_threads(nthreads);
-  const std::string root(dir);
-  Trace tr;
+namespace {
 
-  // 1. layout file: header, records, digests, trailer
+struct Layout {
+  LayoutHdr h{};
+  std::vector<snap_buf> bufs;
+  std::vector<uint64_t> dig;
+};
+
+// layout.<rank>.snapl: header, records, digests, FNV trailer (all checked)
+int read_layout(snap_ctx* ctx, const std::string& root, int rank, Layout& L) {
   const std::string lp = root + "/layout." + std::to_string(rank) + ".snapl";
   std::vector<uint8_t> lay;
-  {
-    const int fd = ::open(lp.c_str(), O_RDONLY | O_CLOEXEC);
-    if (fd < 0) return fail(ctx, SNAP_EINVAL, "load: " + lp + ": " + std::strerror(errno));
-    struct stat sb;
-    if (::fstat(fd, &sb) != 0) {
-      ::close(fd);
-      return fail(ctx, SNAP_EINVAL, "load: stat " + lp);
-    }
-    lay.resize(size_t(sb.st_size));
-    size_t got = 0;
-    while (got < lay.size()) {
-      const ssize_t n = ::pread(fd, lay.data() + got, lay.size() - got, off_t(got));
-      if (n <= 0) break;
-      got += size_t(n);
-    }
+  const int fd = ::open(lp.c_str(), O_RDONLY | O_CLOEXEC);
+  if (fd < 0) return fail(ctx, SNAP_EINVAL, "load: " + lp + ": " + std::strerror(errno));
+  struct stat sb;
+  if (::fstat(fd, &sb) != 0) {
     ::close(fd);
-    if (got != lay.size()) return fail(ctx, SNAP_EINVAL, "load: short read of " + lp);
+    return fail(ctx, SNAP_EINVAL, "load: stat " + lp);
   }
-  LayoutHdr h;
+  lay.resize(size_t(sb.st_size));
+  size_t got = 0;
+  while (got < lay.size()) {
+    const ssize_t n = ::pread(fd, lay.data() + got, lay.size() - got, off_t(got));
+    if (n <= 0) break;
+    got += size_t(n);
+  }
+  ::close(fd);
+  if (got != lay.size()) return fail(ctx, SNAP_EINVAL, "load: short read of " + lp);
+  LayoutHdr& h = L.h;
   if (lay.size() < sizeof h + 8) return fail(ctx, SNAP_EFAULT, "load: layout truncated");
   std::memcpy(&h, lay.data(), sizeof h);
   if (h.magic != kLayoutMagic || h.version != kLayoutVersion)
@@ -474,45 +481,50 @@ extern "C" int snap_load(snap_ctx* ctx, const char* dir, int rank, int verify, i
   std::memcpy(&trailer, lay.data() + want - 8, 8);
   if (fnv_bytes(lay.data(), size_t(want - 8)) != trailer)
     return fail(ctx, SNAP_EFAULT, "load: layout digest verification failed");
-  std::vector<snap_buf> bufs(h.nbufs);
+  L.bufs.resize(h.nbufs);
   const uint8_t* q = lay.data() + sizeof h;
   for (uint64_t b = 0; b < h.nbufs; ++b, q += sizeof(LayoutRec)) {
     LayoutRec r;
     std::memcpy(&r, q, sizeof r);
-    bufs[b] = snap_buf{r.rank, r.slot, r.addr, r.bytes, r.cat, r.flags};
+    L.bufs[b] = snap_buf{r.rank, r.slot, r.addr, r.bytes, r.cat, r.flags};
   }
-  std::vector<uint64_t> dig(h.nchunks);
-  if (h.nchunks) std::memcpy(dig.data(), q, h.nchunks * 8);
+  L.dig.resize(h.nchunks);
+  if (h.nchunks) std::memcpy(L.dig.data(), q, h.nchunks * 8);
+  return SNAP_OK;
+}
 
-  tr.mark("layout read");
-  // 2. install the layout; distinct blobs in first-reference order
-  snap_geom geom{h.page_bytes, h.chunk_bytes};
-  uint64_t nch = 0;
-  RC(snap_set_buffers(ctx, bufs.data(), bufs.size(), &geom, &nch));
-  if (nch != h.nchunks) return fail(ctx, SNAP_EFAULT, "load: layout chunk count mismatch");
+// chunk lengths of a layout's grid (the same arithmetic as snap_set_buffers)
+std::vector<uint32_t> layout_lens(const Layout& L) {
+  std::vector<uint32_t> lens;
+  for (const snap_buf& b : L.bufs)
+    for (uint64_t o = 0; o < b.bytes; o += L.h.chunk_bytes)
+      lens.push_back(uint32_t(std::min<uint64_t>(L.h.chunk_bytes, b.bytes - o)));
+  return lens;
+}
+
+// distinct blobs in first-reference order, laid out 256-B aligned in one image;
+// src[g] = image offset of chunk g's blob. Returns the image size.
+uint64_t plan_image(const std::vector<uint64_t>& dig, const std::vector<uint32_t>& lens,
+                    std::vector<Blob>& blobs, std::vector<uint64_t>& src) {
   std::unordered_map<uint64_t, uint64_t> at;  // digest -> image offset
-  at.reserve(size_t(nch * 2));
-  std::vector<Blob> blobs;
-  std::vector<uint64_t> src(nch);
+  at.reserve(dig.size() * 2);
+  src.assign(dig.size(), 0);
   uint64_t image = 0;
-  for (uint64_t g = 0; g < nch; ++g) {
+  for (uint64_t g = 0; g < dig.size(); ++g) {
     auto [it, fresh] = at.emplace(dig[g], image);
     if (fresh) {
-      blobs.push_back({dig[g], image, ctx->h_lens[g]});
-      image += (uint64_t(ctx->h_lens[g]) + 255) & ~255ull;
+      blobs.push_back({dig[g], image, lens[g]});
+      image += (uint64_t(lens[g]) + 255) & ~255ull;
     }
     src[g] = it->second;
   }
+  return image;
+}
 
-  tr.mark("layout installed");
-  // 3. blobs -> pinned slabs (reader threads) -> device image (copy stream)
-  CK(cudaSetDevice(ctx->device));
-  CK(cudaStreamSynchronize(ctx->stream));  // nothing in flight may still read the staging
-  uint8_t* dimg;
-  RC(ensure(ctx, ctx->staging, image, &dimg));
-  ctx->selected = false;  // the staging image now holds the loaded blobs
-  ctx->staging_valid = 0;
-  ctx->spec_ready = false;
+// blob files -> pinned slabs (reader threads) -> device image (copy stream).
+// A missing, truncated or unreadable blob is SNAP_EFAULT (BlobStore::get).
+int stream_blobs(snap_ctx* ctx, const std::string& root, int threads,
+                 const std::vector<Blob>& blobs, uint8_t* dimg, uint64_t* bytes_read) {
   Errors err;
   std::atomic<uint64_t> rd{0};
   if (!blobs.empty()) {
@@ -522,7 +534,6 @@ extern "C" int snap_load(snap_ctx* ctx, const char* dir, int rank, int verify, i
     uint8_t* pin[2];
     RC(io_slabs(ctx, cap, pin));
     RC(ensure_copy_streams(ctx));
-    tr.mark("pinned slabs");
     for (size_t k = 0; k < sl.size(); ++k) {
       if (k >= 2) CK(cudaEventSynchronize(ctx->pipe_ev[k & 1]));  // slab buffer free again
       const auto [a, b] = sl[k];
@@ -563,34 +574,101 @@ extern "C" int snap_load(snap_ctx* ctx, const char* dir, int rank, int verify, i
     }
     CK(cudaStreamSynchronize(ctx->h2d));
   }
-  if (err.code.load()) {
-    if (stats) {
-      *stats = snap_persist_stats{};
-      stats->layout_chunks = nch;
-      stats->layout_bufs = bufs.size();
-    }
-    return fail(ctx, err.code.load(), err.msg);
-  }
+  if (bytes_read) *bytes_read = rd.load();
+  if (err.code.load()) return fail(ctx, err.code.load(), err.msg);
+  return SNAP_OK;
+}
 
-  // 4. K4 scatter to the recorded addresses (+ K1 verification against the layout digests)
-  if (stats) {
+// the ctx staging buffer as the load image (nothing in flight may still read it)
+int load_image(snap_ctx* ctx, uint64_t bytes, uint8_t** dimg) {
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->stream));
+  RC(ensure(ctx, ctx->staging, bytes, dimg));
+  ctx->selected = false;  // the staging image now holds loaded blobs
+  ctx->staging_valid = 0;
+  ctx->spec_ready = false;
+  return SNAP_OK;
+}
+
+}  // namespace
+
+extern "C" int snap_load(snap_ctx* ctx, const char* dir, int rank, int verify, int nthreads,
+                         snap_persist_stats* stats) {
+  if (!ctx || !dir) return SNAP_EINVAL;
+  const int threads = pick_threads(nthreads);
+  const std::string root(dir);
+  Trace tr;
+  Layout L;
+  RC(read_layout(ctx, root, rank, L));
+  tr.mark("layout read");
+  // install the layout; distinct blobs in first-reference order
+  snap_geom geom{L.h.page_bytes, L.h.chunk_bytes};
+  uint64_t nch = 0;
+  RC(snap_set_buffers(ctx, L.bufs.data(), L.bufs.size(), &geom, &nch));
+  if (nch != L.h.nchunks) return fail(ctx, SNAP_EFAULT, "load: layout chunk count mismatch");
+  std::vector<Blob> blobs;
+  std::vector<uint64_t> src;
+  const uint64_t image = plan_image(L.dig, ctx->h_lens, blobs, src);
+  tr.mark("layout installed");
+  if (stats) {  // the layout is installed from here on, even if a blob fails
     *stats = snap_persist_stats{};
-    stats->blobs = blobs.size();
-    stats->bytes = rd.load();
     stats->layout_chunks = nch;
-    stats->layout_bufs = bufs.size();
+    stats->layout_bufs = L.bufs.size();
+  }
+  uint8_t* dimg;
+  RC(load_image(ctx, image, &dimg));
+  uint64_t rd = 0;
+  RC(stream_blobs(ctx, root, threads, blobs, dimg, &rd));
+  tr.mark("blobs read + H2D");
+  if (stats) {
+    stats->blobs = blobs.size();
+    stats->bytes = rd;
     stats->layout_blobs = blobs.size();
     for (const Blob& x : blobs) stats->layout_bytes += x.len;
   }
-  tr.mark("blobs read + H2D");
-  RC(snap_restore(ctx, dimg, image, src.data(), dig.data(), verify));
+  // K4 scatter to the recorded addresses (+ K1 verification against the layout digests)
+  RC(snap_restore(ctx, dimg, image, src.data(), L.dig.data(), verify));
   tr.mark("K4 scatter + verify");
   // the layout's digests become the context's (verified against the restored
   // bytes when verify != 0): snap_get_digests works right after a load
   if (nch) {
-    CK(cudaMemcpyAsync(ctx->d_dig.p, dig.data(), nch * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->d_dig.p, L.dig.data(), nch * 8, cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
   }
   ctx->hashed = true;
+  return SNAP_OK;
+}
+
+extern "C" int snap_splice_load(snap_ctx* ctx, const char* dir, int layout_rank, int splice_rank,
+                                int nthreads, snap_persist_stats* stats) {
+  if (!ctx || !dir || splice_rank < 0) return SNAP_EINVAL;
+  if (!ctx->splice) return fail(ctx, SNAP_EINVAL, "splice_load needs snap_splice_init");
+  const int threads = pick_threads(nthreads);
+  const std::string root(dir);
+  Layout L;
+  RC(read_layout(ctx, root, layout_rank, L));
+  // the persisted content of every buffer is real content: none is pending here
+  for (snap_buf& b : L.bufs) b.flags &= ~SNAP_BUF_PENDING;
+  snap_geom geom{L.h.page_bytes, L.h.chunk_bytes};
+  RC(snap_splice_set_rank(ctx, splice_rank, L.bufs.data(), L.bufs.size(), &geom));
+  const std::vector<uint32_t> lens = layout_lens(L);
+  if (lens.size() != L.dig.size()) return fail(ctx, SNAP_EFAULT, "load: layout chunk count mismatch");
+  std::vector<Blob> blobs;
+  std::vector<uint64_t> src;
+  const uint64_t image = plan_image(L.dig, lens, blobs, src);
+  uint8_t* dimg;
+  RC(load_image(ctx, image, &dimg));
+  uint64_t rd = 0;
+  RC(stream_blobs(ctx, root, threads, blobs, dimg, &rd));
+  RC(splice_seed(ctx, splice_rank, dimg, src.data(), L.dig.data()));
+  if (stats) {
+    *stats = snap_persist_stats{};
+    stats->blobs = blobs.size();
+    stats->bytes = rd;
+    stats->layout_chunks = L.dig.size();
+    stats->layout_bufs = L.bufs.size();
+    stats->layout_blobs = blobs.size();
+    for (const Blob& x : blobs) stats->layout_bytes += x.len;
+  }
   return SNAP_OK;
 }

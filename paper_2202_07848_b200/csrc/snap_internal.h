@@ -131,6 +131,10 @@ int launch_scatter_shards(uint8_t* arena, const GridDev& g, const uint32_t* lens
 int launch_compare(const uint64_t* a, const uint64_t* b, uint64_t n, unsigned long long* nbad,
                    cudaStream_t s);
 
+// K3 with an image source: chunk sel_list[k] from image + src_off[chunk].
+int launch_gather_from(const uint8_t* image, const uint64_t* src_off, const uint32_t* lens,
+                       const uint32_t* sel_list, const uint64_t* totals, const uint64_t* offsets,
+                       uint8_t* dst, uint64_t max_sel, cudaStream_t s);
 // Splice: chunk-cache index insert and the swap-in pass.
 int launch_cache_insert(TableDev cache, const uint64_t* dig, const uint32_t* sel_list,
                         const uint64_t* totals, const uint64_t* offsets, uint64_t base,

@@ -28,7 +28,7 @@ struct RankGrid {
 
 struct SpliceState {
   uint64_t cap = 0, cursor = 0, entries = 0;
-  DevMem cache, ck, cv, counters;
+  DevMem cache, ck, cv, counters, seed_off;
   uint64_t cmask = 0;
   std::map<int, RankGrid> ranks;
   std::map<std::pair<int, int>, DevMem> match;
@@ -42,7 +42,7 @@ void splice_release(snap_ctx* ctx) {
     for (DevMem* m : {&g.d_addr, &g.d_bytes, &g.d_cstart, &g.d_lens, &g.d_rec, &g.d_tmaps})
       release(*m);
   for (auto& [k, m] : S->match) release(m);
-  for (DevMem* m : {&S->cache, &S->ck, &S->cv, &S->counters}) release(*m);
+  for (DevMem* m : {&S->cache, &S->ck, &S->cv, &S->counters, &S->seed_off}) release(*m);
   delete S;
   ctx->splice = nullptr;
 }
@@ -207,6 +207,49 @@ int snap_splice_switch(snap_ctx* ctx, int from, int to, snap_switch_stats* st) {
                                       " chunk digest(s) lost (not resident, not cached)");
   return SNAP_OK;
 }
+
+}  // extern "C"
+
+// restore_job's cache seeding for a co-resident rank (ckpt.cpp:526-528): the
+// rank's recorded digests become `dig`, and every chunk whose digest the chunk
+// cache does not hold yet is copied in from image + src_off (device image,
+// host offsets, one per chunk of the rank's splice grid).
+int splice_seed(snap_ctx* ctx, int rank, const uint8_t* image, const uint64_t* src_off,
+                const uint64_t* dig) {
+  SpliceState* S = ctx->splice;
+  if (!S || !S->ranks.count(rank)) return fail(ctx, SNAP_EINVAL, "splice: unknown rank");
+  RankGrid& R = S->ranks[rank];
+  if (S->cursor + R.bytes > S->cap)
+    return fail(ctx, SNAP_ENOMEM, "splice: chunk cache full (" + std::to_string(S->cursor) +
+                                      " of " + std::to_string(S->cap) + " bytes used)");
+  CK(cudaSetDevice(ctx->device));
+  TableDev cache{P<unsigned long long>(S->ck), P<unsigned long long>(S->cv), S->cmask};
+  uint64_t* so;
+  RC(ensure(ctx, S->seed_off, R.nchunks, &so));
+  if (R.nchunks) {
+    CK(cudaMemcpyAsync(P<uint64_t>(R.d_rec), dig, R.nchunks * 8, cudaMemcpyHostToDevice,
+                       ctx->stream));
+    CK(cudaMemcpyAsync(so, src_off, R.nchunks * 8, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  RC(select_with_known(ctx, P<uint64_t>(R.d_rec), P<uint32_t>(R.d_lens), R.nchunks, cache,
+                       S->entries > 0));
+  ctx->selected = false;
+  CKL(snap::launch_gather_from(image, so, P<uint32_t>(R.d_lens), P<uint32_t>(ctx->sel_list),
+                               P<uint64_t>(ctx->totals), P<uint64_t>(ctx->offsets),
+                               P<uint8_t>(S->cache) + S->cursor, R.nchunks, ctx->stream));
+  CKL(snap::launch_cache_insert(cache, P<uint64_t>(R.d_rec), P<uint32_t>(ctx->sel_list),
+                                P<uint64_t>(ctx->totals), P<uint64_t>(ctx->offsets), S->cursor,
+                                R.nchunks, ctx->stream));
+  uint64_t tot[2] = {0, 0};
+  CK(cudaMemcpyAsync(tot, ctx->totals.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  S->cursor += tot[1];
+  S->entries += tot[0];
+  R.recorded = true;
+  return SNAP_OK;
+}
+
+extern "C" {
 
 int snap_splice_recorded(snap_ctx* ctx, int rank, uint64_t* digests, uint64_t* n) {
   if (!ctx || !ctx->splice || !ctx->splice->ranks.count(rank)) return SNAP_EINVAL;

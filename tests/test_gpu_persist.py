@@ -208,3 +208,53 @@ def test_load_detects_corrupt_truncated_and_missing_blobs(snap, tmp_path):
             c2.load(tmp_path)
         with pytest.raises(snap.SnapError):
             c2.load(tmp_path, rank=7)  # no such layout
+
+
+def test_migrate_time_sliced_ranks_through_the_blob_store(snap, tmp_path):
+    """restore_job on a new GPU for a 2-way time-sliced job (ckpt.cpp:504-533): the active
+    rank is materialized in the arena (snap_load), the co-resident rank's chunks are
+    seeded into the HBM chunk cache (snap_splice_load); switching then restores each
+    rank's bytes exactly — P/O identical across the replicas stay resident, only the
+    gradients move."""
+    arena = 16 << 20
+    po = [(0, 0, 0, 3 << 20, 0), (0, 1, 3 << 20, (2 << 20) + 768, 1)]   # identical replicas
+    gbuf = (0, 2, 6 << 20, 1 << 20, 2)                                    # per-rank gradient
+    state = {}
+
+    def held(c, bufs):  # the bytes the rank's buffers hold (gaps are not state)
+        return [c.read(b[2], b[3]) for b in bufs]
+
+    def same(a, b):
+        return all(np.array_equal(x, y) for x, y in zip(a, b))
+
+    with snap.Ctx(0, arena) as src:
+        for r in range(2):
+            src.fill_mix64(0, 6 << 20, 42, 0)            # same P/O on both ranks
+            src.fill_mix64(6 << 20, 1 << 20, 100 + r, 0)  # different G
+            bufs = [(r,) + b[1:] for b in po] + [(r,) + gbuf[1:]]
+            src.set_buffers(bufs)
+            src.snapshot()
+            src.persist(tmp_path, layout_rank=r)
+            state[r] = (bufs, held(src, bufs))
+    with snap.Ctx(0, arena) as dst:
+        dst.splice_init(16 << 20)  # room for the seed + a worst-case swap-out
+        ld = dst.load(tmp_path, rank=0)                  # active rank -> arena (verified)
+        assert ld["layout_chunks"] > 0
+        assert same(held(dst, state[0][0]), state[0][1])
+        dst.splice_set_rank(0, state[0][0])
+        seed = dst.splice_load(tmp_path, layout_rank=1, splice_rank=1)
+        assert seed["layout_bufs"] == 3
+        s01 = dst.splice_switch(0, 1)
+        assert same(held(dst, state[1][0]), state[1][1])
+        po_bytes = (3 << 20) + (2 << 20) + 768
+        assert s01["resident_bytes"] == po_bytes and s01["swap_in_bytes"] == 1 << 20
+        s10 = dst.splice_switch(1, 0)
+        assert same(held(dst, state[0][0]), state[0][1])
+        assert s10["swap_in_bytes"] == 1 << 20 and s10["resident_bytes"] == po_bytes
+        # a missing blob of the co-resident rank is a fault, not silent garbage
+        with snap.Ctx(0, arena) as probe:
+            probe.load(tmp_path, rank=1)
+            d1, _ = probe.digests()
+        os.remove(tmp_path / O.blob_rel_path(int(d1[-1])))
+        with pytest.raises(snap.SnapFault):
+            dst.splice_load(tmp_path, layout_rank=1, splice_rank=2)
