@@ -214,6 +214,13 @@ class Splicer {
                      x.pending_result ? SNAP_BUF_PENDING : 0u});
     check(snap_splice_set_rank(gpu_->ctx(), r, b.data(), b.size(), nullptr), gpu_->ctx());
   }
+  // restore_job cache seeding for a co-resident rank (ckpt.cpp:526-528): its persisted
+  // layout becomes rank r's buffer map and its chunks enter the HBM chunk cache
+  snap_persist_stats seed_from(const std::string& dir, RankId layout_rank, RankId r) {
+    snap_persist_stats st{};
+    check(snap_splice_load(gpu_->ctx(), dir.c_str(), layout_rank, r, 0, &st), gpu_->ctx());
+    return st;
+  }
   SwitchPlan switch_to(RankId from, RankId to) {
     snap_switch_stats s{};
     check(snap_splice_switch(gpu_->ctx(), from, to, &s), gpu_->ctx());
@@ -337,6 +344,13 @@ class Snapshotter {
   snap_persist_stats persist(const std::string& dir, int threads = 0) {
     snap_persist_stats st{};
     check(snap_persist(gpu_->ctx(), dir.c_str(), nullptr, 0, threads, &st), gpu_->ctx());
+    return st;
+  }
+  // the same under an explicit layout id (one cut per time-sliced rank of a GPU)
+  snap_persist_stats persist_as(const std::string& dir, RankId layout_rank, int threads = 0) {
+    snap_persist_stats st{};
+    check(snap_persist_rank(gpu_->ctx(), dir.c_str(), layout_rank, nullptr, 0, threads, &st),
+          gpu_->ctx());
     return st;
   }
   // restore_job materialization from a directory (ckpt.cpp:504-533); SimFault on a
