@@ -15,6 +15,10 @@
  *    image and (optionally) an NCCL communicator.
  *  - All device work is issued on the ctx's own CUDA stream, in call order.
  *    Calls that return host data synchronise that stream once per call.
+ *  - A ctx is used by one host thread at a time (the reference's proxy
+ *    serializes all device access); different ctxs are independent.
+ *    With a communicator attached, snapshot/select/exchange calls are
+ *    collective: every rank makes the same sequence of them.
  *  - Return codes (common.hpp:31-49 error conventions):
  *      SNAP_OK        success
  *      SNAP_EINVAL    bad argument / geometry          (ConfigError)
