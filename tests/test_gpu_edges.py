@@ -90,3 +90,17 @@ def test_splice_rank_without_buffers(snap):
         assert st["hashed_bytes"] == 1 << 20 and st["swap_in_bytes"] == 0
         st = c.splice_switch(1, 0)
         assert st["hashed_bytes"] == 0
+
+
+def test_no_digest_collisions_10k_buffers(snap):
+    # test_simcore.cpp:119-130 on the device: 10^4 random distinct buffers, distinct digests
+    rng = np.random.default_rng(7)
+    n = 10000
+    with snap.Ctx(0, n * 256) as c:
+        words = rng.integers(0, 2**64 - 1, size=n * 32, dtype=np.uint64)
+        c.write(0, words)
+        bufs = [(0, i, i * 256, 256, 0) for i in range(n)]
+        d = c.digest_ranges(bufs)
+        assert len(set(d.tolist())) == n
+        od = O.hash_chunks([words], bufs)[2]
+        assert np.array_equal(d, od)
