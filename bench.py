@@ -399,6 +399,44 @@ def incremental_bench(snap, device, gib=32, reps=3):
             "bound": "FNV-1a instruction issue (FMA-heavy pipe): W << R, no stores to overlap"}
 
 
+def c1_bench(snap, device, reps=20):
+    """C1 (BASELINE configs[0], the reference's CPU-runnable case): a 256 MiB single-rank
+    image (64 x 4 MiB buffers, words = mix64(1 ^ i)), 64 KiB chunks, snapshot + restore
+    round trip. GPU: snap_snapshot then snap_restore_self(verify) (K4 + K1 re-hash),
+    device-timed. Reference: BlobStore::put per chunk + BlobStore::get (digest-verified)
+    + write back (ref_restore_chunks), on all host threads and on one core."""
+    import oracle as O
+    nbytes, nb = 256 << 20, 4 << 20
+    bufs = [(0, i, i * nb, nb, 0) for i in range(nbytes // nb)]
+    with snap.Ctx(device, nbytes) as c:
+        c.fill_mix64(0, nbytes, 1, 0)
+        c.set_buffers(bufs)
+        for _ in range(3):
+            c.snapshot()
+            c.restore_self(verify=True)
+        c.sync()
+        c.timer_start()
+        for _ in range(reps):
+            c.snapshot()
+            c.restore_self(verify=True)
+        ms = c.timer_stop() / reps
+    out = {"workload": "C1: 256 MiB image (64 x 4 MiB buffers), 4096 x 64 KiB chunks, "
+                       "snapshot + digest-verified restore round trip",
+           "round_trip_ms": round(ms, 3), "round_trip_gbs": round(nbytes / ms / 1e6, 1)}
+    R = O.ref()
+    if R is not None:
+        img = O.fill_mix64(nbytes // 8, 1, 0)
+        back = np.empty_like(img)
+        th = min(os.cpu_count() or 1, 16)
+        for name, n in (("reference_ms", th), ("reference_1core_ms", 1)):
+            t = time.perf_counter()
+            rc = R.ref_restore_chunks(img.ctypes.data, nbytes, CHUNK, n, back.ctypes.data)
+            out[name] = round((time.perf_counter() - t) * 1e3, 1)
+            assert rc == 0 and np.array_equal(back, img)
+        out["reference_threads"] = th
+    return out
+
+
 def persist_bench(snap, device, mib=256):
     """§8f row 2, the on-disk format: C1's 256 MiB image (4096 unique 64 KiB chunks)
     snapshotted, persisted as blobs/<2hex>/<16hex> files straight from the device staging
@@ -672,11 +710,12 @@ def run_ours(args, dist):
         except Exception as e:  # an extra section must never cost the headline line
             return {"error": repr(e)[:300]}
 
-    splice = incremental = resize = persist = None
+    splice = incremental = resize = persist = c1 = None
     if dist.rank == 0 and N == 1 and not args.no_splice:
         splice = guarded(splice_bench, snap, dist.local)
         incremental = guarded(incremental_bench, snap, dist.local)
         persist = guarded(persist_bench, snap, dist.local)
+        c1 = guarded(c1_bench, snap, dist.local)
         if base is not None:
             base["splice"] = guarded(ref_splice_bench)
     if 1 < N <= 4 and not args.no_splice:
@@ -721,6 +760,7 @@ def run_ours(args, dist):
             "incremental": incremental,
             "resize": resize,
             "persist": persist,
+            "c1": c1,
         }
         print(json.dumps(line))
 
