@@ -66,12 +66,25 @@ def fill_rank(ctx, rank, replicated, per_rank, seed=1):
 
 
 def host_image(rank, replicated, per_rank, seed=1):
+    """Host copy of a rank's C2 image for the CPU-baseline legs only (cpu_baseline,
+    --impl reference): the oracle's OpenMP fill, the one place besides those legs'
+    reference calls where bench.py executes oracle/ code. Our arm reads its host image
+    back from the device arena instead."""
     import oracle as O
     img = np.empty((replicated + per_rank) // 8, np.uint64)
     O.lib().or_fill_mix64(img.ctypes.data, replicated // 8, seed, 0)
     O.lib().or_fill_mix64(img[replicated // 8:].ctypes.data, per_rank // 8, seed ^ (rank << 40),
                           replicated // 8)
     return img
+
+
+def mix64_np(x):
+    """sim::mix64 (sim.hpp:37-41), vectorized: synthetic input generation for the bench."""
+    x = np.asarray(x, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        x = (x ^ (x >> np.uint64(30))) * np.uint64(0xbf58476d1ce4e5b9)
+        x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94d049bb133111eb)
+    return x ^ (x >> np.uint64(31))
 
 
 # ------------------------------------------------------------------ plumbing
@@ -368,7 +381,6 @@ def incremental_bench(snap, device, gib=32, reps=3):
     """C4 on this GPU: 32 GiB image, first checkpoint committed to the store index, then
     5 % of the chunks dirtied (chunk c dirty iff mix64(seed ^ c) % 20 == 0) and the
     incremental snapshot (K1 + K2 vs known set + K3 gather of the dirty chunks) timed."""
-    import oracle as O
     nbytes = gib << 30
     nb = 256 << 20
     bufs = [(0, i, i * nb, nb, 1) for i in range(nbytes // nb)]
@@ -377,7 +389,7 @@ def incremental_bench(snap, device, gib=32, reps=3):
         n = c.set_buffers(bufs)
         c.snapshot()
         c.known_commit()
-        mix = np.array([O.mix64(99 ^ k) for k in range(n)], dtype=np.uint64)
+        mix = mix64_np(np.uint64(99) ^ np.arange(n, dtype=np.uint64))
         dirty = np.nonzero(mix % np.uint64(20) == 0)[0].astype(np.uint64) * 65536
         times, staged = [], 0
         for k in range(reps):
@@ -672,9 +684,8 @@ def run_ours(args, dist):
 
     # ---- e2e through the host-buffer entry point (pinned host image and staging)
     hostimg = snap.PinnedHost(image)
-    himg = host_image(dist.rank, replicated, per_rank)
-    hostimg.array[:] = himg.view(np.uint8)
-    del himg
+    # the host copy of this rank's image: the device arena (filled by fill_rank) read back
+    ctx._ck(ctx._L.snap_read(ctx.h, 0, snap.C.c_void_p(hostimg.ptr), image), "snap_read")
     hstage = snap.PinnedHost(image)
     hdig = np.zeros(nchunks, np.uint64)
     for _ in range(2):
