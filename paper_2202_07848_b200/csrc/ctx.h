@@ -237,8 +237,8 @@ int select_with_known(snap_ctx* ctx, const uint64_t* dig, const uint32_t* lens, 
                       TableDev kn, bool use_known, bool inserted = false,
                       uint64_t* spec_next = nullptr);
 
-// Per-buffer TMA tensor maps for the hash-only TMA K1 variant (4 KiB pages; only
-// built when that variant is selected). On any
+// Per-buffer TMA tensor maps for the hash-only TMA K1 (4 KiB pages; not built
+// when a cp.async variant is forced). On any
 // encode failure the grid simply keeps the cp.async kernel (tmaps = nullptr).
 inline void build_tmaps(snap_ctx* ctx, DevMem& m, const uint64_t* addr, const uint64_t* bytes,
                         uint32_t n, GridDev& g) {

@@ -749,10 +749,9 @@ int sm_count() {
 
 }  // namespace
 
-// Variant selection (SNAP_HASH_VARIANT env; default: CfgE for fused launches,
-// CfgA for hash-only launches — the fastest of the measured geometries; 10 = the
-// TMA tensor-load hash-only kernel, k_hash_tma.cu); all compute identical digests,
-// they only differ in how the bytes reach shared memory and in latency hiding.
+// Variant selection (SNAP_HASH_VARIANT env, 1-10; see choose_k1): all compute
+// identical digests, they only differ in how the bytes reach shared memory and
+// in latency hiding.
 using CfgA = HashCfg<1, 128, 3, 16>;  // 512 chains/SM, 128-B slabs
 using CfgB = HashCfg<2, 64, 2, 16>;   // 1024 chains/SM, 64-B slabs
 using CfgC = HashCfg<2, 64, 3, 12>;   // 768 chains/SM, deeper ring
@@ -823,55 +822,73 @@ int hash_variant() {
   return v;
 }
 
-bool hash_tma_selected() { return hash_variant() == 10; }
+// tensor maps are built for every grid unless a cp.async variant is forced
+bool hash_tma_selected() {
+  const int v = hash_variant();
+  return v == 10 || v == 99;
+}
 
-int launch_hash_variant(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
-                        const uint64_t* spec_off, uint8_t* staging, cudaStream_t s);
+// The K1 kernel a launch uses (SNAP_HASH_VARIANT forces one; the default is the
+// fastest measured per shape):
+//  * fused hash + speculative stores: CfgE — 256-B slabs keep the mixed
+//    read/write DRAM pattern at ~6 TB/s (128-B segments cap it at ~5.2,
+//    tools/micro/pattern_bw2.cu);
+//  * hash only (alternating same-box A/B over the C2 / C3 / C4 buffer shapes,
+//    tools/hash_variants.py): the TMA tensor-load kernel beats the cp.async
+//    CfgA by 1-2 % on every shape; two chains per lane (CfgB) win by another
+//    1 % on very large buffers but lose 14 % on small tensors.
+enum class K1 { A, B, C, D, E, F, WsA, WsB, WsC, Tma };
+K1 choose_k1(const GridDev& g, const uint64_t* spec_off) {
+  switch (hash_variant()) {
+    case 1: return K1::B;
+    case 2: return K1::C;
+    case 3: return K1::D;
+    case 4: return K1::WsA;
+    case 5: return K1::WsB;
+    case 6: return K1::WsC;
+    case 7: return K1::E;
+    case 8: return K1::F;
+    case 9: return K1::A;
+    default:
+      if (spec_off) return K1::E;
+      if (g.nbufs && (g.nchunks << g.chunk_shift) / g.nbufs >= (64ull << 20)) return K1::B;
+      return hash_tma_ok(g) ? K1::Tma : K1::A;
+  }
+}
+
+int launch_k1(K1 k, const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
+              const uint64_t* spec_off, uint8_t* staging, cudaStream_t s) {
+  switch (k) {
+    case K1::A: return launch_hash_cfg<CfgA>(arena, g, chunk_dig, spec_off, staging, s);
+    case K1::B: return launch_hash_cfg<CfgB>(arena, g, chunk_dig, spec_off, staging, s);
+    case K1::C: return launch_hash_cfg<CfgC>(arena, g, chunk_dig, spec_off, staging, s);
+    case K1::D: return launch_hash_cfg<CfgD>(arena, g, chunk_dig, spec_off, staging, s);
+    case K1::E: return launch_hash_cfg<CfgE>(arena, g, chunk_dig, spec_off, staging, s);
+    case K1::F: return launch_hash_cfg<CfgF>(arena, g, chunk_dig, spec_off, staging, s);
+    case K1::WsA: return launch_hash_ws<WsA>(arena, g, chunk_dig, spec_off, staging, s);
+    case K1::WsB: return launch_hash_ws<WsB>(arena, g, chunk_dig, spec_off, staging, s);
+    case K1::WsC: return launch_hash_ws<WsC>(arena, g, chunk_dig, spec_off, staging, s);
+    case K1::Tma: return launch_hash_tma(arena, g, chunk_dig, s);
+  }
+  return 0;
+}
 
 // K1 launch; with g.dd set the K2 insert is fused into the k_hash epilogue, or
-// (other variants) runs as a range kernel right after.
+// (warp-specialized / TMA kernels) runs as a range kernel right after.
 int launch_hash(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
                 const uint64_t* spec_off, uint8_t* staging, cudaStream_t s) {
   if (g.nchunks == 0) return 0;
-  const int v = hash_variant();
-  const bool epilogue = !((v >= 4 && v <= 6) || (v == 10 && !spec_off && hash_tma_ok(g)));
-  if (!g.dd.keys || epilogue) return launch_hash_variant(arena, g, chunk_dig, spec_off, staging, s);
+  const K1 k = choose_k1(g, spec_off);
+  const bool epilogue = !(k == K1::WsA || k == K1::WsB || k == K1::WsC || k == K1::Tma);
+  if (!g.dd.keys || epilogue) return launch_k1(k, arena, g, chunk_dig, spec_off, staging, s);
   GridDev h = g;
   h.dd = TableDev{};
-  const int n = launch_hash_variant(arena, h, chunk_dig, spec_off, staging, s);
+  const int n = launch_k1(k, arena, h, chunk_dig, spec_off, staging, s);
   const uint64_t c_end = g.c_end ? g.c_end : g.nchunks;
   uint64_t blocks = (c_end - g.c_begin + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
   if (blocks) k_insert_range<<<unsigned(blocks), 256, 0, s>>>(g, chunk_dig);
   return n + (blocks ? 1 : 0);
-}
-
-int launch_hash_variant(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
-                        const uint64_t* spec_off, uint8_t* staging, cudaStream_t s) {
-  // slabs of 128 B need pages >= 256 B; 64-B slabs are fine for every page size
-  switch (hash_variant()) {
-    case 1: return launch_hash_cfg<CfgB>(arena, g, chunk_dig, spec_off, staging, s);
-    case 2: return launch_hash_cfg<CfgC>(arena, g, chunk_dig, spec_off, staging, s);
-    case 3: return launch_hash_cfg<CfgD>(arena, g, chunk_dig, spec_off, staging, s);
-    case 4: return launch_hash_ws<WsA>(arena, g, chunk_dig, spec_off, staging, s);
-    case 5: return launch_hash_ws<WsB>(arena, g, chunk_dig, spec_off, staging, s);
-    case 6: return launch_hash_ws<WsC>(arena, g, chunk_dig, spec_off, staging, s);
-    case 7: return launch_hash_cfg<CfgE>(arena, g, chunk_dig, spec_off, staging, s);
-    case 8: return launch_hash_cfg<CfgF>(arena, g, chunk_dig, spec_off, staging, s);
-    case 9: return launch_hash_cfg<CfgA>(arena, g, chunk_dig, spec_off, staging, s);
-    case 10:
-      if (!spec_off && hash_tma_ok(g)) return launch_hash_tma(arena, g, chunk_dig, s);
-      [[fallthrough]];
-    default:
-      // fused hash + speculative stores: 256-B slabs (contiguous 256-B write
-      // segments per page keep mixed read/write DRAM traffic at ~6 TB/s;
-      // 128-B segments cap it at ~5.2, tools/micro/pattern_bw2.cu);
-      // hash only: 128-B slabs and 16 warps hide the FNV chain latency better
-      // (the TMA variant measured 3.66 TB/s vs 3.73: the kernel is bound by the
-      // FMA-heavy pipe, not by the copy instructions TMA removes)
-      if (spec_off) return launch_hash_cfg<CfgE>(arena, g, chunk_dig, spec_off, staging, s);
-      return launch_hash_cfg<CfgA>(arena, g, chunk_dig, spec_off, staging, s);
-  }
 }
 
 int launch_buf_fold(const GridDev& g, const uint64_t* chunk_dig, uint64_t* buf_dig,
