@@ -449,6 +449,40 @@ def c1_bench(snap, device, reps=20):
     return out
 
 
+def host_pages_bench(snap, device, mib=256, reps=5):
+    """§8f row 4: a rank's host state (64 host buffers, 256 MiB, mix64 content) paged into
+    4 KiB pages and classified (build_manifest host section, ckpt.cpp:116-130): H2D +
+    K1 (page = chunk = 4 KiB) + fresh/incremental classification, wall clock of the call.
+    Reference arm: BlobStore::put per page (hash + store), single-threaded as in
+    build_manifest."""
+    import oracle as O
+    nwords = (mib << 20) // 8
+    host = mix64_np(np.uint64(5) ^ np.arange(nwords, dtype=np.uint64))
+    bufs = np.array_split(host, 64)
+    with snap.Ctx(device, 64 << 20) as c:
+        dig, flags, st = c.host_pages(bufs)
+        t = time.perf_counter()
+        for _ in range(reps):
+            dig, flags, st = c.host_pages(bufs, prev_pages=dig)
+        dt = (time.perf_counter() - t) / reps
+    out = {"workload": f"{mib} MiB host state in 64 buffers, {st['pages']} x 4 KiB pages",
+           "ms": round(dt * 1e3, 2), "gbs": round((mib << 20) / dt / 1e9, 2),
+           "h2d": "pageable host buffers (the caller's memory)"}
+    R = O.ref()
+    if R is not None:
+        import ctypes as C
+        store = R.ref_store_new()
+        d = C.c_uint64()
+        t = time.perf_counter()
+        for k in range(0, nwords, 512):
+            R.ref_store_put(store, host[k:].ctypes.data_as(C.c_void_p), 512, C.byref(d))
+        tr = time.perf_counter() - t
+        R.ref_store_free(store)
+        out["reference_ms"] = round(tr * 1e3, 1)
+        out["reference_gbs"] = round((mib << 20) / tr / 1e9, 3)
+    return out
+
+
 def persist_bench(snap, device, mib=256):
     """§8f row 2, the on-disk format: C1's 256 MiB image (4096 unique 64 KiB chunks)
     snapshotted, persisted as blobs/<2hex>/<16hex> files straight from the device staging
@@ -721,12 +755,13 @@ def run_ours(args, dist):
         except Exception as e:  # an extra section must never cost the headline line
             return {"error": repr(e)[:300]}
 
-    splice = incremental = resize = persist = c1 = None
+    splice = incremental = resize = persist = c1 = pages = None
     if dist.rank == 0 and N == 1 and not args.no_splice:
         splice = guarded(splice_bench, snap, dist.local)
         incremental = guarded(incremental_bench, snap, dist.local)
         persist = guarded(persist_bench, snap, dist.local)
         c1 = guarded(c1_bench, snap, dist.local)
+        pages = guarded(host_pages_bench, snap, dist.local)
         if base is not None:
             base["splice"] = guarded(ref_splice_bench)
     if 1 < N <= 4 and not args.no_splice:
@@ -772,6 +807,7 @@ def run_ours(args, dist):
             "resize": resize,
             "persist": persist,
             "c1": c1,
+            "host_pages": pages,
         }
         print(json.dumps(line))
 
