@@ -408,6 +408,14 @@ int snap_timer_stop(snap_ctx* ctx, float* ms);
 int snap_prof_enable(snap_ctx* ctx, int on);
 int snap_prof_read(snap_ctx* ctx, int kind, float* total_ms, uint64_t* count);
 
+/* K1 kernel policy for this process (tuning / A-B measurement; no reference
+ * counterpart). -1 = default per-launch choice; 9 = cp.async kernel, 10 = TMA
+ * tensor loads, 11 = tensor-core FNV (8-bit chain on the CUDA cores + linear
+ * part as a tcgen05 int8 MMA); the other values force measured alternatives.
+ * Every variant yields identical digests. Applies to grids installed after
+ * the call (the TMA-based kernels need tensor maps built at install time). */
+int snap_set_k1_variant(int variant);
+
 #ifdef __cplusplus
 }
 #endif

@@ -168,6 +168,7 @@ _SIGS = {
     "snap_get_shard": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64),
                                  C.POINTER(C.c_uint64)]),
     "snap_prof_enable": (C.c_int, [C.c_void_p, C.c_int]),
+    "snap_set_k1_variant": (C.c_int, [C.c_int]),
     "snap_prof_read": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_float),
                                  C.POINTER(C.c_uint64)]),
     "snap_alloc_create": (C.c_int, [C.c_uint64, C.c_uint64, C.POINTER(C.c_void_p)]),
@@ -695,3 +696,11 @@ class Ctx:
         ms = C.c_float()
         self._ck(self._L.snap_timer_stop(self.h, C.byref(ms)), "snap_timer_stop")
         return ms.value
+
+
+def set_k1_variant(variant: int = -1) -> None:
+    """K1 kernel policy for this process (snap_set_k1_variant): -1 default, 11 tensor-core
+    FNV, 10 TMA loads, 9 cp.async; applies to grids installed afterwards."""
+    rc = lib().snap_set_k1_variant(int(variant))
+    if rc < 0:
+        raise SnapError(rc, "snap_set_k1_variant")

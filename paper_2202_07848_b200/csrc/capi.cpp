@@ -1405,6 +1405,11 @@ int snap_timer_stop(snap_ctx* ctx, float* ms) {
   return SNAP_OK;
 }
 
+int snap_set_k1_variant(int variant) {
+  snap::set_hash_variant(variant);
+  return SNAP_OK;
+}
+
 int snap_prof_enable(snap_ctx* ctx, int on) {
   if (!ctx) return SNAP_EINVAL;
   CK(cudaSetDevice(ctx->device));

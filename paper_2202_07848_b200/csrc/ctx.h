@@ -243,9 +243,13 @@ int select_with_known(snap_ctx* ctx, const uint64_t* dig, const uint32_t* lens, 
 inline void build_tmaps(snap_ctx* ctx, DevMem& m, const uint64_t* addr, const uint64_t* bytes,
                         uint32_t n, GridDev& g) {
   g.tmaps = nullptr;
+  g.tmaps64 = nullptr;
   if (!snap::hash_tma_selected() || g.page_shift != 12 || n == 0) return;
-  std::vector<uint8_t> host(size_t(n) * 128);
-  if (snap::encode_tensor_maps(ctx->arena, addr, bytes, n, host.data()) != 0) return;
+  // n maps with 128-byte boxes (k_hash_tma), then n with 64-byte boxes (k_hash_mma)
+  std::vector<uint8_t> host(size_t(n) * 256);
+  if (snap::encode_tensor_maps(ctx->arena, addr, bytes, n, host.data(), 128) != 0) return;
+  if (snap::encode_tensor_maps(ctx->arena, addr, bytes, n, host.data() + size_t(n) * 128, 64) != 0)
+    return;
   uint8_t* d;
   if (ensure(ctx, m, host.size(), &d) != SNAP_OK) return;
   if (cudaMemcpyAsync(d, host.data(), host.size(), cudaMemcpyHostToDevice, ctx->stream) !=
@@ -253,6 +257,7 @@ inline void build_tmaps(snap_ctx* ctx, DevMem& m, const uint64_t* addr, const ui
       cudaStreamSynchronize(ctx->stream) != cudaSuccess)
     return;
   g.tmaps = d;
+  g.tmaps64 = d + size_t(n) * 128;
 }
 
 inline int check_range(snap_ctx* ctx, uint64_t addr, uint64_t bytes) {

@@ -812,20 +812,22 @@ int launch_hash_cfg(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
   return 1;
 }
 
+int g_hash_variant = -1;
 int hash_variant() {
-  static int v = -1;
-  if (v < 0) {
+  if (g_hash_variant < 0) {
     const char* e = getenv("SNAP_HASH_VARIANT");
-    v = e ? atoi(e) : -1;
-    if (v < 0) v = 99;  // default policy
+    g_hash_variant = e ? atoi(e) : -1;
+    if (g_hash_variant < 0) g_hash_variant = 99;  // default policy
   }
-  return v;
+  return g_hash_variant;
 }
+
+void set_hash_variant(int v) { g_hash_variant = v < 0 ? 99 : v; }
 
 // tensor maps are built for every grid unless a cp.async variant is forced
 bool hash_tma_selected() {
   const int v = hash_variant();
-  return v == 10 || v == 99;
+  return v == 10 || v == 11 || v == 99;
 }
 
 // The K1 kernel a launch uses (SNAP_HASH_VARIANT forces one; the default is the
@@ -837,7 +839,7 @@ bool hash_tma_selected() {
 //    tools/hash_variants.py): the TMA tensor-load kernel beats the cp.async
 //    CfgA by 1-2 % on every shape; two chains per lane (CfgB) win by another
 //    1 % on very large buffers but lose 14 % on small tensors.
-enum class K1 { A, B, C, D, E, F, WsA, WsB, WsC, Tma };
+enum class K1 { A, B, C, D, E, F, WsA, WsB, WsC, Tma, Mma };
 K1 choose_k1(const GridDev& g, const uint64_t* spec_off) {
   switch (hash_variant()) {
     case 1: return K1::B;
@@ -849,6 +851,9 @@ K1 choose_k1(const GridDev& g, const uint64_t* spec_off) {
     case 7: return K1::E;
     case 8: return K1::F;
     case 9: return K1::A;
+    case 11:
+      if (spec_off) return K1::E;
+      return hash_mma_ok(g) ? K1::Mma : K1::A;
     default:
       if (spec_off) return K1::E;
       if (g.nbufs && (g.nchunks << g.chunk_shift) / g.nbufs >= (64ull << 20)) return K1::B;
@@ -869,6 +874,7 @@ int launch_k1(K1 k, const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
     case K1::WsB: return launch_hash_ws<WsB>(arena, g, chunk_dig, spec_off, staging, s);
     case K1::WsC: return launch_hash_ws<WsC>(arena, g, chunk_dig, spec_off, staging, s);
     case K1::Tma: return launch_hash_tma(arena, g, chunk_dig, s);
+    case K1::Mma: return launch_hash_mma(arena, g, chunk_dig, s);
   }
   return 0;
 }
@@ -879,7 +885,7 @@ int launch_hash(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
                 const uint64_t* spec_off, uint8_t* staging, cudaStream_t s) {
   if (g.nchunks == 0) return 0;
   const K1 k = choose_k1(g, spec_off);
-  const bool epilogue = !(k == K1::WsA || k == K1::WsB || k == K1::WsC || k == K1::Tma);
+  const bool epilogue = !(k == K1::WsA || k == K1::WsB || k == K1::WsC || k == K1::Tma || k == K1::Mma);
   if (!g.dd.keys || epilogue) return launch_k1(k, arena, g, chunk_dig, spec_off, staging, s);
   GridDev h = g;
   h.dd = TableDev{};

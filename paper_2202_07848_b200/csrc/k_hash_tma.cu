@@ -281,7 +281,7 @@ int launch_hash_tma(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
 // box 32 rows x 128 B, 128B swizzle). Buffers with no full page get an unused
 // zeroed entry (their tasks are irregular).
 int encode_tensor_maps(const uint8_t* arena, const uint64_t* addr, const uint64_t* bytes,
-                       uint32_t nbufs, void* host_maps /* nbufs x 128 B */) {
+                       uint32_t nbufs, void* host_maps /* nbufs x 128 B */, int box_bytes) {
   using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                 const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                 const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -302,11 +302,12 @@ int encode_tensor_maps(const uint8_t* arena, const uint64_t* addr, const uint64_
     if (rows == 0) continue;
     const cuuint64_t dims[2] = {4096, rows};
     const cuuint64_t strides[1] = {4096};
-    const cuuint32_t box[2] = {128, 32};
+    const cuuint32_t box[2] = {cuuint32_t(box_bytes), 32};
     const cuuint32_t estr[2] = {1, 1};
     CUresult r = encode(&maps[b], CU_TENSOR_MAP_DATA_TYPE_UINT8, 2,
                         const_cast<uint8_t*>(arena + addr[b]), dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        box_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return -2;
   }

@@ -35,8 +35,10 @@ struct GridDev {
   // snapshot hash each slab as soon as its H2D copy lands
   uint64_t c_begin = 0;
   uint64_t c_end = 0;
-  // per-buffer CUtensorMap array in device memory (4 KiB pages), or nullptr
+  // per-buffer CUtensorMap arrays in device memory (4 KiB pages), or nullptr:
+  // boxes of 32 pages x 128 B (SWIZZLE_128B) and 32 pages x 64 B (SWIZZLE_64B)
   const void* tmaps = nullptr;
+  const void* tmaps64 = nullptr;
   // Single-GPU snapshot: the K2 insert pass fused into K1 — the lane that
   // finishes a chunk digest inserts it into `dd` (first occurrence by
   // atomicMin, skipped when `kn` holds it and kn_use) and records the slot in
@@ -64,9 +66,16 @@ int launch_hash(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
 bool hash_tma_ok(const GridDev& g);
 bool hash_tma_selected();  // SNAP_HASH_VARIANT=10: tensor maps are built for the grid
 int launch_hash_tma(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig, cudaStream_t s);
-// host: one 128-byte CUtensorMap per buffer into host_maps; 0 on success
+// K1 hash-only on the tensor cores (k_hash_mma.cu: 8-bit FNV chain on the CUDA
+// cores + the linear part as a tcgen05 int8 MMA); needs the grid tensor maps.
+bool hash_mma_ok(const GridDev& g);
+int launch_hash_mma(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig, cudaStream_t s);
+// K1 kernel policy override (SNAP_HASH_VARIANT semantics; -1 = default policy)
+void set_hash_variant(int v);
+// host: one 128-byte CUtensorMap per buffer into host_maps (box of 32 pages x
+// box_bytes, box_bytes 128 -> SWIZZLE_128B, 64 -> SWIZZLE_64B); 0 on success
 int encode_tensor_maps(const uint8_t* arena, const uint64_t* addr, const uint64_t* bytes,
-                       uint32_t nbufs, void* host_maps);
+                       uint32_t nbufs, void* host_maps, int box_bytes = 128);
 // Cross-GPU barrier after a fused-exchange K1: signal every peer (flag slot
 // `rank` of its window := epoch, release.sys) and wait for every peer's
 // signal in this rank's window (acquire.sys); traps after ~30 s.

@@ -1,0 +1,93 @@
+"""GPU parity of the tensor-core K1 (k_hash_mma.cu: 8-bit FNV chain on the CUDA cores +
+the linear part of FNV-1a as a tcgen05 int8 MMA) against the reference golden vectors and
+the oracle, on the layouts that exercise its paths: TMA-box tasks, per-page bulk tasks
+(buffer edges, ragged tails, pages shorter than 4 KiB), partial groups and chunk sizes
+from 4 KiB to 128 KiB."""
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture()
+def mma(snap):
+    snap.set_k1_variant(11)
+    yield snap
+    snap.set_k1_variant(-1)
+
+
+def test_c1_golden_mma(mma, c1_golden):
+    with mma.Ctx(0, 256 << 20) as c:
+        c.fill_mix64(0, 256 << 20, 0, 0)
+        bufs = [(0, 0, 0, 256 << 20, 0)]
+        assert c.set_buffers(bufs, 4096, 65536) == 4096
+        c.hash()
+        d, _, bd = c.digests(buf_digests=True)
+        assert np.array_equal(d, c1_golden["merkle"])
+        assert int(bd[0]) == int(c1_golden["buf"][0])
+
+
+def test_ragged_golden_mma(mma, golden):
+    rag = golden["ragged"]
+    with mma.Ctx(0, 64 << 20) as c:
+        arena = O.fill_mix64(rag["arena_bytes"] // 8, rag["seed"], 0)
+        src, dst, n = rag["dup"]
+        arena[dst // 8:(dst + n) // 8] = arena[src // 8:(src + n) // 8]
+        c.write(0, arena)
+        bufs = [tuple(b) for b in rag["bufs"]]
+        c.set_buffers(bufs, 4096, 65536)
+        c.hash()
+        d, lens, bd = c.digests(buf_digests=True)
+        exp = golden["ragged"]["4096_65536"]
+        assert [f"{x:016x}" for x in d] == exp["chunks"]
+        assert [f"{x:016x}" for x in bd] == exp["bufs"]
+
+
+@pytest.mark.parametrize("chunk", [4096, 16384, 65536, 131072])
+def test_random_layouts_mma(mma, chunk):
+    rng = np.random.default_rng(chunk)
+    arena_bytes = 96 << 20
+    with mma.Ctx(0, arena_bytes) as c:
+        for trial in range(3):
+            c.fill_mix64(0, arena_bytes, 7 + trial, 0)
+            host = c.read(0, arena_bytes)
+            bufs, addr, slot = [], 0, 0
+            while True:
+                kind = rng.integers(0, 4)
+                if kind == 0:
+                    nb = int(rng.integers(1, 16)) * 256          # sub-page buffers
+                elif kind == 1:
+                    nb = int(rng.integers(1, 64)) * 4096 + int(rng.integers(0, 16)) * 256
+                else:
+                    nb = int(rng.integers(1, 700)) * 4096        # page-multiple, TMA tasks
+                if addr + nb > arena_bytes:
+                    break
+                bufs.append((0, slot, addr, nb, int(rng.integers(0, 3))))
+                slot += 1
+                addr += nb + int(rng.integers(0, 3)) * 256
+            c.set_buffers(bufs, 4096, chunk)
+            c.hash()
+            d, lens = c.digests()
+            od, olens, _ = O.hash_chunks([host], bufs, 4096, chunk)
+            assert np.array_equal(lens, olens)
+            bad = np.nonzero(d != od)[0]
+            assert bad.size == 0, f"trial {trial}: {bad.size} chunk digests differ, first {bad[:5]}"
+
+
+def test_mma_equals_default_large(snap):
+    """Same 1 GiB image (one 768 MiB buffer + 64 x 4 MiB): default kernel vs the MMA kernel."""
+    nbytes = 1 << 30
+    bufs = [(0, 0, 0, 768 << 20, 1)] + [(0, 1 + i, (768 << 20) + i * (4 << 20), 4 << 20, 0)
+                                        for i in range(64)]
+    out = []
+    for v in (-1, 11):
+        snap.set_k1_variant(v)
+        with snap.Ctx(0, nbytes) as c:
+            c.fill_mix64(0, nbytes, 99, 0)
+            c.set_buffers(bufs)
+            c.hash()
+            out.append(c.digests()[0])
+    snap.set_k1_variant(-1)
+    assert np.array_equal(out[0], out[1])
