@@ -408,7 +408,7 @@ def incremental_bench(snap, device, gib=32, reps=3):
             "ms": round(ms, 3), "R_gbs": round(nbytes / ms / 1e6, 1), "W_bytes": int(staged),
             "rw_gbs": round((nbytes + staged) / ms / 1e6, 1),
             "hbm_frac": round((nbytes + staged) / ms / 1e6 / peak, 4),
-            "bound": "FNV-1a instruction issue (FMA-heavy pipe): W << R, no stores to overlap"}
+            "bound": "hbm (hash-only K1 on the tensor cores: 8-bit FNV chain + int8 MMA, k_hash_mma)"}
 
 
 def c1_bench(snap, device, reps=20):

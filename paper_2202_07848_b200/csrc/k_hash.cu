@@ -830,15 +830,16 @@ bool hash_tma_selected() {
   return v == 10 || v == 11 || v == 99;
 }
 
-// The K1 kernel a launch uses (SNAP_HASH_VARIANT forces one; the default is the
-// fastest measured per shape):
+// The K1 kernel a launch uses (SNAP_HASH_VARIANT / snap_set_k1_variant force
+// one; the default is the fastest measured per shape):
 //  * fused hash + speculative stores: CfgE — 256-B slabs keep the mixed
 //    read/write DRAM pattern at ~6 TB/s (128-B segments cap it at ~5.2,
 //    tools/micro/pattern_bw2.cu);
-//  * hash only (alternating same-box A/B over the C2 / C3 / C4 buffer shapes,
-//    tools/hash_variants.py): the TMA tensor-load kernel beats the cp.async
-//    CfgA by 1-2 % on every shape; two chains per lane (CfgB) win by another
-//    1 % on very large buffers but lose 14 % on small tensors.
+//  * hash only, >= 512 MiB: the tensor-core FNV kernel (k_hash_mma.cu);
+//  * hash only, smaller grids (alternating same-box A/B over the C2 / C3 / C4
+//    buffer shapes, tools/hash_variants.py): the TMA tensor-load kernel beats
+//    the cp.async CfgA by 1-2 % on every shape; two chains per lane (CfgB) win
+//    by another 1 % on very large buffers but lose 14 % on small tensors.
 enum class K1 { A, B, C, D, E, F, WsA, WsB, WsC, Tma, Mma };
 K1 choose_k1(const GridDev& g, const uint64_t* spec_off) {
   switch (hash_variant()) {
@@ -854,10 +855,18 @@ K1 choose_k1(const GridDev& g, const uint64_t* spec_off) {
     case 11:
       if (spec_off) return K1::E;
       return hash_mma_ok(g) ? K1::Mma : K1::A;
-    default:
+    default: {
       if (spec_off) return K1::E;
+      // tensor-core FNV: one 1024-page group per SM at a time, so it needs
+      // >= 128 groups (512 MiB) to fill the GPU (tools/hash_sizes.py:
+      // 4.9-6.0 TB/s from 512 MiB up vs 3.0-3.6 for the TMA kernel; below
+      // that the TMA kernel's 32-page tasks spread over more SMs)
+      const uint64_t c_end = g.c_end ? g.c_end : g.nchunks;
+      const uint64_t pages = (c_end - g.c_begin) << (g.chunk_shift - g.page_shift);
+      if (hash_mma_ok(g) && pages >= 128 * 1024) return K1::Mma;
       if (g.nbufs && (g.nchunks << g.chunk_shift) / g.nbufs >= (64ull << 20)) return K1::B;
       return hash_tma_ok(g) ? K1::Tma : K1::A;
+    }
   }
 }
 
