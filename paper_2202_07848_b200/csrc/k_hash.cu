@@ -840,7 +840,7 @@ bool hash_tma_selected() {
 //    buffer shapes, tools/hash_variants.py): the TMA tensor-load kernel beats
 //    the cp.async CfgA by 1-2 % on every shape; two chains per lane (CfgB) win
 //    by another 1 % on very large buffers but lose 14 % on small tensors.
-enum class K1 { A, B, C, D, E, F, WsA, WsB, WsC, Tma, Mma };
+enum class K1 { A, B, C, D, E, F, WsA, WsB, WsC, Tma, Mma, MmaF };
 K1 choose_k1(const GridDev& g, const uint64_t* spec_off) {
   switch (hash_variant()) {
     case 1: return K1::B;
@@ -853,7 +853,7 @@ K1 choose_k1(const GridDev& g, const uint64_t* spec_off) {
     case 8: return K1::F;
     case 9: return K1::A;
     case 11:
-      if (spec_off) return K1::E;
+      if (spec_off) return hash_mma_ok(g) ? K1::MmaF : K1::E;
       return hash_mma_ok(g) ? K1::Mma : K1::A;
     default: {
       if (spec_off) return K1::E;
@@ -884,6 +884,7 @@ int launch_k1(K1 k, const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
     case K1::WsC: return launch_hash_ws<WsC>(arena, g, chunk_dig, spec_off, staging, s);
     case K1::Tma: return launch_hash_tma(arena, g, chunk_dig, s);
     case K1::Mma: return launch_hash_mma(arena, g, chunk_dig, s);
+    case K1::MmaF: return launch_hash_mma_fused(arena, g, chunk_dig, spec_off, staging, s);
   }
   return 0;
 }
@@ -894,7 +895,8 @@ int launch_hash(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
                 const uint64_t* spec_off, uint8_t* staging, cudaStream_t s) {
   if (g.nchunks == 0) return 0;
   const K1 k = choose_k1(g, spec_off);
-  const bool epilogue = !(k == K1::WsA || k == K1::WsB || k == K1::WsC || k == K1::Tma || k == K1::Mma);
+  const bool epilogue = !(k == K1::WsA || k == K1::WsB || k == K1::WsC || k == K1::Tma || k == K1::Mma ||
+                          k == K1::MmaF);
   if (!g.dd.keys || epilogue) return launch_k1(k, arena, g, chunk_dig, spec_off, staging, s);
   GridDev h = g;
   h.dd = TableDev{};

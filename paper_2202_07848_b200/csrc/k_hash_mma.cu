@@ -54,33 +54,62 @@ namespace snap {
 namespace {
 
 constexpr uint32_t kFull = 0xffffffffu;
-constexpr int kCW = 8;                        // compute warps (2 per SM sub-partition)
-constexpr int kThreads = (kCW + 1) * 32;      // + MMA warp
-constexpr int kSlab = 64;                     // bytes of a page per data stage
-constexpr int kWarpStage = 4 * 32 * kSlab;    // 4 tasks x 32 pages x 64 B
-constexpr int kST = 3;                        // data ring depth per warp
-constexpr int kGroupPages = kCW * 128;        // page slots per group
-constexpr int kStages = 4096 / kSlab;         // data stages per page
 constexpr int kBSteps = 32;                   // byte-steps per MMA batch
 constexpr int kBatches = 4096 / kBSteps;      // batches per 4 KiB page
 constexpr int kBBytes = 16 * 128;             // one B slice: 16 rows x (64 B u | 64 B l)
 constexpr int kBR = 8;                        // B-slice ring depth
-// TMEM columns: kNA A buffers of 4 pair-sets x 32 columns (16 u words, 16 l
-// words), then kNDB accumulator buffers of 4 pair-sets x 16 columns.
-constexpr int kSets = 4, kNA = 3, kNDB = 2;
-constexpr uint32_t kASet = 32, kABuf = kSets * kASet, kDCol = kNA * kABuf, kDBuf = kSets * 16;
-static_assert(kDCol + kNDB * kDBuf <= 512, "TMEM budget");
 constexpr uint64_t kP = 0x100000001b3ull;
 // table tail (after the kBatches B slices): HP[17], IP[17], K0
 constexpr size_t kBTab = size_t(kBatches) * kBBytes;
 constexpr size_t kBTabAll = kBTab + (17 + 17 + 1) * 8;
 
-constexpr size_t kSmemData = size_t(kCW) * kST * kWarpStage;
-constexpr size_t kSmemB = size_t(kBR) * kBBytes;
-constexpr size_t kSmemDig = size_t(kCW) * 128 * 8;
-constexpr size_t kSmemZero = 128;             // zero slab: LDS source for absent pages
-constexpr int kNBars = kCW * kST + kNA + kNA + kNDB + kNDB + kBR;
-constexpr size_t kSmem = 1024 + kSmemData + kSmemB + kSmemDig + kSmemZero + kNBars * 8 + 16;
+// Kernel geometry. CW compute warps (a multiple of 4: TMEM lane quadrants),
+// PAIRS chain pairs per thread, SLAB bytes of each page per data stage (TMA
+// boxes of 32 pages x BOXW bytes, SWIZZLE_64B / _128B), ST-deep ring per
+// warp, FUSED: also write every predicted-staged chunk's slab to staging.
+template <int CW_, int PAIRS_, int SLAB_, int ST_, bool FUSED_>
+struct MmaCfg {
+  static constexpr int CW = CW_, PAIRS = PAIRS_, SLAB = SLAB_, ST = ST_;
+  static constexpr bool FUSED = FUSED_;
+  static constexpr int TPW = 2 * PAIRS;                 // 32-page tasks per warp
+  static constexpr int PPW = 32 * TPW;                  // pages per warp
+  static constexpr int GP = CW * PPW;                   // page slots per group
+  static constexpr int BOXW = SLAB >= 128 ? 128 : 64;   // box width = swizzle span
+  static constexpr int NBOX = SLAB / BOXW;              // boxes per task and stage
+  static constexpr int SUB = 32 * BOXW;                 // bytes of one box
+  static constexpr int TASKB = NBOX * SUB;              // bytes per task and stage
+  static constexpr int WSTAGE = TPW * TASKB;            // bytes per warp and stage
+  static constexpr int STAGES = 4096 / SLAB;            // data stages per page
+  static constexpr int UNITS = SLAB / 16;               // 16-B units per page and stage
+  static constexpr int UPB = BOXW / 16;                 // units per box row
+  static constexpr int BPS = UNITS / 2;                 // 32-step batches per stage
+  static constexpr int SETS = (CW / 4) * PAIRS;         // pair sets (M = 128 rows each)
+  static constexpr int NA = 3, NDB = 2;                 // A ring, accumulator buffers
+  static constexpr uint32_t ASET = 32, ABUF = SETS * ASET, DCOL = NA * ABUF, DBUF = SETS * 16;
+  static constexpr uint32_t TUSED = DCOL + NDB * DBUF;
+  static constexpr uint32_t TCOLS = TUSED <= 32 ? 32 : TUSED <= 64 ? 64 : TUSED <= 128 ? 128
+                                  : TUSED <= 256 ? 256 : 512;
+  static_assert(TUSED <= 512, "TMEM budget");
+  static constexpr int THREADS = (CW + 1) * 32;         // + MMA warp
+  static constexpr size_t SM_DATA = size_t(CW) * ST * WSTAGE;
+  static constexpr size_t SM_B = size_t(kBR) * kBBytes;
+  static constexpr size_t SM_DIG = size_t(GP) * 8;
+  static constexpr size_t SM_ZERO = 128;                // zero slab: LDS source for absent pages
+  // FUSED: staging writes go out in 256-byte segments per page, SEG = 256 / SLAB
+  // consecutive stages at a time (the load of the next stage into a slot is
+  // then issued after the slot's store instead of before the compute)
+  static constexpr int SEG = SLAB >= 256 ? 1 : 256 / SLAB;
+  static constexpr int NBARS = CW * ST + NA + NA + NDB + NDB + kBR;
+  static constexpr size_t SMEM = 1024 + SM_DATA + SM_B + SM_DIG + SM_ZERO + NBARS * 8 + 16;
+  static_assert(SMEM <= 232448, "shared memory");
+};
+// hash only: 1024 pages in flight per SM (2 chain pairs per thread, 2 warps
+// per SM sub-partition) for latency hiding; 64-byte slabs keep 3 stages in
+// shared memory. Fused: reads and writes share HBM, so half the chains
+// suffice (one pair per thread, 128-byte slabs) and the staging writes leave
+// in 256-byte segments per page (two stages at a time).
+using MmaHash = MmaCfg<8, 2, 64, 3, false>;
+using MmaFused = MmaCfg<8, 1, 128, 3, true>;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -165,6 +194,20 @@ __device__ __forceinline__ void tc_ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : "memory");
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void st_stream16(uint8_t* p, uint4 v) {
+  __stcs(reinterpret_cast<uint4*>(p), v);  // evict-first: the staging image is not re-read soon
+}
 // D[tmem] (+)= A[tmem] x B[smem desc], M=128 N=16 K=32, u8 x u8 -> s32
 __device__ __forceinline__ void tc_mma_i8(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc,
                                           uint32_t acc) {
@@ -247,52 +290,55 @@ __device__ __forceinline__ void chain16(uint32_t& L, const uint4& va, const uint
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+template <class C>
+__global__ void __launch_bounds__(C::THREADS, 1)
 k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ chunk_dig,
-           const uint8_t* __restrict__ btab, int dbg) {
+           const uint8_t* __restrict__ btab, const uint64_t* __restrict__ spec_off,
+           uint8_t* __restrict__ staging, int dbg) {
+  constexpr int CW = C::CW, ST = C::ST, NA = C::NA, NDB = C::NDB, GP = C::GP, PPW = C::PPW;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   // warp index through a shuffle: the compiler then treats it as warp-uniform
   // (TMEM addresses and ring offsets stay in uniform registers)
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
-  uint8_t* bring = smem + kSmemData;
-  uint64_t* dsm = reinterpret_cast<uint64_t*>(bring + kSmemB);
-  uint8_t* zero = reinterpret_cast<uint8_t*>(dsm + kCW * 128);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(zero + kSmemZero);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + kNBars);
-  const uint32_t bar_full = smem_u32(bars);              // [kCW][kST]
-  const uint32_t bar_afull = bar_full + 8 * kCW * kST;   // [kNA]
-  const uint32_t bar_afree = bar_afull + 8 * kNA;        // [kNA]
-  const uint32_t bar_dfull = bar_afree + 8 * kNA;        // [kNDB]
-  const uint32_t bar_dfree = bar_dfull + 8 * kNDB;       // [kNDB]
-  const uint32_t bar_bfull = bar_dfree + 8 * kNDB;       // [kBR]
+  uint8_t* bring = smem + C::SM_DATA;
+  uint64_t* dsm = reinterpret_cast<uint64_t*>(bring + C::SM_B);
+  uint8_t* zero = reinterpret_cast<uint8_t*>(dsm + GP);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(zero + C::SM_ZERO);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + C::NBARS);
+  const uint32_t bar_full = smem_u32(bars);              // [CW][ST]
+  const uint32_t bar_afull = bar_full + 8 * CW * ST;     // [NA]
+  const uint32_t bar_afree = bar_afull + 8 * NA;         // [NA]
+  const uint32_t bar_dfull = bar_afree + 8 * NA;         // [NDB]
+  const uint32_t bar_dfree = bar_dfull + 8 * NDB;        // [NDB]
+  const uint32_t bar_bfull = bar_dfree + 8 * NDB;        // [kBR]
 
   const uint32_t ppc_shift = g.chunk_shift - 12;
   const uint64_t c_end = g.c_end ? g.c_end : g.nchunks;
   const uint64_t slot_base = g.c_begin << ppc_shift;
   const uint64_t nslots = (c_end - g.c_begin) << ppc_shift;
-  const uint64_t ngroups = (nslots + kGroupPages - 1) / kGroupPages;
+  const uint64_t ngroups = (nslots + GP - 1) / GP;
   if (blockIdx.x >= ngroups) return;
   const uint64_t ngl = (ngroups - blockIdx.x + gridDim.x - 1) / gridDim.x;  // my groups
 
-  if (threadIdx.x < kSmemZero / 16) reinterpret_cast<uint4*>(zero)[threadIdx.x] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x < C::SM_ZERO / 16) reinterpret_cast<uint4*>(zero)[threadIdx.x] = make_uint4(0, 0, 0, 0);
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kCW * kST; ++i) mbar_init(bar_full + 8 * i, 1);
-    for (int i = 0; i < kNA; ++i) {
-      mbar_init(bar_afull + 8 * i, kCW * 32);
+    for (int i = 0; i < CW * ST; ++i) mbar_init(bar_full + 8 * i, 1);
+    for (int i = 0; i < NA; ++i) {
+      mbar_init(bar_afull + 8 * i, CW * 32);
       mbar_init(bar_afree + 8 * i, 1);
     }
-    for (int i = 0; i < kNDB; ++i) {
+    for (int i = 0; i < NDB; ++i) {
       mbar_init(bar_dfull + 8 * i, 1);
-      mbar_init(bar_dfree + 8 * i, kCW * 32);
+      mbar_init(bar_dfree + 8 * i, CW * 32);
     }
     for (int i = 0; i < kBR; ++i) mbar_init(bar_bfull + 8 * i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == kCW) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                     smem_u32(tslot))
+  if (warp == CW) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tslot)), "n"(C::TCOLS)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -301,7 +347,7 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
   tc_fence_after();
   const uint32_t tbase = *tslot;
 
-  if (warp == kCW) {
+  if (warp == CW) {
     // ------------------------------------------------------------ MMA warp
     // the whole warp runs the loop (warp-uniform operands stay in uniform
     // registers); one elected lane issues the TMA, MMA and commit instructions
@@ -321,25 +367,25 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
     for (uint64_t gb = 0; gb < nb; ++gb) {
       const uint64_t i = gb / kBatches;
       const uint32_t b = static_cast<uint32_t>(gb % kBatches);
-      const uint32_t ab = static_cast<uint32_t>(gb % kNA), db = static_cast<uint32_t>(i % kNDB);
-      if (b == 0 && i >= kNDB)
-        mbar_wait(bar_dfree + 8 * db, static_cast<uint32_t>((i / kNDB - 1) & 1));
-      mbar_wait(bar_afull + 8 * ab, static_cast<uint32_t>((gb / kNA) & 1));
-      // A buffer gb % kNA was refilled only after batch gb - kNA's MMAs
+      const uint32_t ab = static_cast<uint32_t>(gb % NA), db = static_cast<uint32_t>(i % NDB);
+      if (b == 0 && i >= NDB)
+        mbar_wait(bar_dfree + 8 * db, static_cast<uint32_t>((i / NDB - 1) & 1));
+      mbar_wait(bar_afull + 8 * ab, static_cast<uint32_t>((gb / NA) & 1));
+      // A buffer gb % NA was refilled only after batch gb - NA's MMAs
       // completed, so that batch's B slot is free: refill it kBR ahead
-      if (gb >= kNA && gb - kNA + kBR < nb) load_b(gb - kNA + kBR);
+      if (gb >= NA && gb - NA + kBR < nb) load_b(gb - NA + kBR);
       mbar_wait(bar_bfull + 8 * (gb % kBR), static_cast<uint32_t>((gb / kBR) & 1));
       tc_fence_after();
       if (leader) {
         const uint64_t bdesc = sw128_desc(bring_u + static_cast<uint32_t>(gb % kBR) * kBBytes);
-        const uint32_t dcol = tbase + kDCol + db * kDBuf, acol = tbase + ab * kABuf;
+        const uint32_t dcol = tbase + C::DCOL + db * C::DBUF, acol = tbase + ab * C::ABUF;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
 #pragma unroll
-          for (int ps = 0; ps < kSets; ++ps)
+          for (int ps = 0; ps < C::SETS; ++ps)
             if (!(dbg & 2))
-              tc_mma_i8(dcol + ps * 16, acol + ps * kASet + 8 * kk, bdesc + uint64_t(2 * kk), idesc,
-                        (b > 0 || kk > 0) ? 1u : 0u);
+              tc_mma_i8(dcol + ps * 16, acol + ps * C::ASET + 8 * kk, bdesc + uint64_t(2 * kk),
+                        idesc, (b > 0 || kk > 0) ? 1u : 0u);
         tc_commit(bar_afree + 8 * ab);
         if (b == kBatches - 1) tc_commit(bar_dfull + 8 * db);
       }
@@ -347,32 +393,35 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
     }
   } else {
     // ------------------------------------------------------- compute warps
-    // warp w: tasks 4w..4w+3 of each group; pair sets 2 (w / 4) + {0, 1}
-    // in TMEM lanes 32 (w % 4) + lane
-    const CUtensorMap* maps = static_cast<const CUtensorMap*>(g.tmaps64);
-    const uint32_t ring = smem_u32(smem + warp * kST * kWarpStage);
-    const uint32_t fbar = bar_full + 8 * warp * kST;
-    const uint32_t trow = tbase + (static_cast<uint32_t>(32 * (warp & 3)) << 16) +
-                          static_cast<uint32_t>(warp >> 2) * 2 * kASet;
-    const uint32_t drow = tbase + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + kDCol +
-                          static_cast<uint32_t>(warp >> 2) * 32;
-    const uint32_t nst = static_cast<uint32_t>(ngl) * kStages;  // data stages of this warp
+    // warp w: tasks TPW*w .. TPW*w + TPW-1 of each group; chain pair p of a
+    // thread = pages (task 2p, task 2p+1) at its lane; TMEM pair set
+    // (w / 4) * PAIRS + p in lanes 32 (w % 4) + lane
+    constexpr int TPW = C::TPW, PAIRS = C::PAIRS, SLAB = C::SLAB, BOXW = C::BOXW;
+    const CUtensorMap* maps =
+        static_cast<const CUtensorMap*>(BOXW == 64 ? g.tmaps64 : g.tmaps);
+    const uint32_t ring = smem_u32(smem + warp * ST * C::WSTAGE);
+    const uint32_t fbar = bar_full + 8 * warp * ST;
+    const uint32_t tl = static_cast<uint32_t>(32 * (warp & 3)) << 16;
+    const uint32_t trow = tbase + tl + static_cast<uint32_t>(warp >> 2) * PAIRS * C::ASET;
+    const uint32_t drow = tbase + tl + C::DCOL + static_cast<uint32_t>(warp >> 2) * PAIRS * 16;
+    const uint32_t nst = static_cast<uint32_t>(ngl) * C::STAGES;  // data stages of this warp
     const uint64_t* htab = reinterpret_cast<const uint64_t*>(btab + kBTab);
 
     // producer state of the group being loaded
-    uint32_t p_reg = 0, p_map[4] = {0, 0, 0, 0}, p_row[4] = {0, 0, 0, 0}, p_len[4];
-    const uint8_t* p_src[4];
-    uint32_t reg_bits[2] = {0, 0};  // per group parity: bit q = task q loaded by TMA 2D
+    uint32_t p_reg = 0, p_map[TPW], p_row[TPW], p_len[TPW];
+    const uint8_t* p_src[TPW];
+    uint32_t reg_bits[2] = {0, 0};  // per group parity: bit t = task t loaded by TMA 2D
     uint32_t ist = 0, cst = 0;
 
-    auto page_info = [&](uint32_t i, int q, const uint8_t*& src, uint32_t& len, uint32_t& b,
-                         uint32_t& row) {
+    auto page_info = [&](uint32_t i, int t, const uint8_t*& src, uint32_t& len, uint32_t& b,
+                         uint32_t& row, uint64_t& gcout) {
       const uint64_t gi = blockIdx.x + uint64_t(i) * gridDim.x;
-      const uint64_t rel = gi * kGroupPages + 128 * warp + 32 * q + lane;
+      const uint64_t rel = gi * GP + PPW * warp + 32 * t + lane;
       src = nullptr;
       len = 0;
       b = 0xffffffffu;
       row = 0;
+      gcout = ~0ull;
       if (rel < nslots) {
         const uint64_t slot = slot_base + rel;
         const uint64_t gc = slot >> ppc_shift;
@@ -385,185 +434,260 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
           len = static_cast<uint32_t>(rem < 4096 ? rem : 4096);
           src = arena + __ldg(g.addr + b) + off;
           row = static_cast<uint32_t>(off >> 12);
+          gcout = gc;
         }
       }
     };
 
     auto issue = [&](uint32_t p) {
       const uint32_t st = ist;
-      ist = ist + 1 == kST ? 0 : ist + 1;
+      ist = ist + 1 == ST ? 0 : ist + 1;
       if (p >= nst) return;
-      const uint32_t i = p / kStages;
-      const uint32_t s = p % kStages;
+      const uint32_t i = p / C::STAGES;
+      const uint32_t s = p % C::STAGES;
       if (s == 0) {
         p_reg = 0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int t = 0; t < TPW; ++t) {
           uint32_t b, row;
-          page_info(i, q, p_src[q], p_len[q], b, row);
+          uint64_t gc;
+          page_info(i, t, p_src[t], p_len[t], b, row, gc);
           const uint32_t b0 = __shfl_sync(kFull, b, 0);
           const uint32_t r0 = __shfl_sync(kFull, row, 0);
-          if (__all_sync(kFull, b == b0 && p_len[q] == 4096 && row == r0 + lane)) p_reg |= 1u << q;
-          p_map[q] = b0;
-          p_row[q] = r0;
+          if (__all_sync(kFull, b == b0 && p_len[t] == 4096 && row == r0 + lane)) p_reg |= 1u << t;
+          p_map[t] = b0;
+          p_row[t] = r0;
         }
         reg_bits[i & 1] = p_reg;
       }
       const uint32_t bar = fbar + 8 * st;
-      const uint32_t dst = ring + st * kWarpStage;
-      if (p_reg == 0xfu) {
-        // regular group: four TMA boxes, one elected lane
+      const uint32_t dst = ring + st * C::WSTAGE;
+      if (p_reg == (1u << TPW) - 1) {
+        // regular group: one elected lane, NBOX TMA boxes per task
         if (lane == 0) {
-          mbar_arrive_tx(bar, 4 * 32 * kSlab);
+          mbar_arrive_tx(bar, C::WSTAGE);
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            tma_load_2d(dst + q * 32 * kSlab, maps + p_map[q], static_cast<int>(s * kSlab),
-                        static_cast<int>(p_row[q]), bar);
+          for (int t = 0; t < TPW; ++t)
+#pragma unroll
+            for (int x = 0; x < C::NBOX; ++x)
+              tma_load_2d(dst + t * C::TASKB + x * C::SUB, maps + p_map[t],
+                          static_cast<int>(s * SLAB + x * BOXW), static_cast<int>(p_row[t]), bar);
         }
         return;
       }
       uint32_t tx = 0;
-      uint32_t vmask[4];
+      uint32_t vmask[TPW];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        vmask[q] = __ballot_sync(kFull, s * kSlab < p_len[q]);
-        tx += (p_reg >> q) & 1 ? 32u * kSlab : __popc(vmask[q]) * kSlab;
+      for (int t = 0; t < TPW; ++t) {
+        vmask[t] = __ballot_sync(kFull, s * SLAB < p_len[t]);
+        tx += (p_reg >> t) & 1 ? uint32_t(C::TASKB) : __popc(vmask[t]) * SLAB;
       }
       if (lane == 0) mbar_arrive_tx(bar, tx);
       __syncwarp();
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if ((p_reg >> q) & 1) {
+      for (int t = 0; t < TPW; ++t) {
+        if ((p_reg >> t) & 1) {
           if (lane == 0)
-            tma_load_2d(dst + q * 32 * kSlab, maps + p_map[q], static_cast<int>(s * kSlab),
-                        static_cast<int>(p_row[q]), bar);
-        } else if ((vmask[q] >> lane) & 1) {
-          bulk_load(dst + q * 32 * kSlab + lane * kSlab, p_src[q] + s * kSlab, kSlab, bar);
+#pragma unroll
+            for (int x = 0; x < C::NBOX; ++x)
+              tma_load_2d(dst + t * C::TASKB + x * C::SUB, maps + p_map[t],
+                          static_cast<int>(s * SLAB + x * BOXW), static_cast<int>(p_row[t]), bar);
+        } else if ((vmask[t] >> lane) & 1) {
+#pragma unroll
+          for (int x = 0; x < C::NBOX; ++x)
+            bulk_load(dst + t * C::TASKB + x * C::SUB + lane * BOXW, p_src[t] + s * SLAB + x * BOXW,
+                      BOXW, bar);
         }
       }
     };
 
 #pragma unroll
-    for (int p = 0; p < kST - 1; ++p) issue(p);
+    for (int p = 0; p < ST - 1; ++p) issue(p);
+    if constexpr (C::FUSED) issue(ST - 1);  // fused: the issue for a slot follows its store
 
-    uint32_t c_len[4] = {0, 0, 0, 0};
-    uint32_t L0 = 0, L1 = 0;
+    uint32_t c_len[TPW];
+    uint8_t* c_dst[TPW];  // FUSED: staging address of this lane's page, or null
+    uint32_t L[PAIRS];
     bool c_full = false;  // every page of the group is a full page of a TMA-loaded task
     const uint32_t zbase = smem_u32(zero);
-    // SWIZZLE_64B: 16-B unit u of box row j lives at unit u ^ ((j >> 1) & 3)
-    const uint32_t swz = static_cast<uint32_t>((lane >> 1) & 3) << 4;
-    uint32_t ph_full = 0;  // parity of the data ring's next wrap
+    // box row j: 16-B unit x stored at x ^ (j & 7) (SWIZZLE_128B) or
+    // x ^ ((j >> 1) & 3) (SWIZZLE_64B)
+    const uint32_t swz = static_cast<uint32_t>(BOXW == 128 ? (lane & 7) : ((lane >> 1) & 3)) << 4;
+    uint32_t ph_full = 0;  // parity of the data ring's current wrap
     for (uint32_t p = 0; p < nst; ++p) {
-      issue(p + kST - 1);
+      if constexpr (!C::FUSED) issue(p + ST - 1);
       const uint32_t st = cst;
-      cst = cst + 1 == kST ? 0 : cst + 1;
-      const uint32_t i = p / kStages;
-      const uint32_t s = p % kStages;
+      cst = cst + 1 == ST ? 0 : cst + 1;
+      const uint32_t i = p / C::STAGES;
+      const uint32_t s = p % C::STAGES;
       if (s == 0) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int t = 0; t < TPW; ++t) {
           const uint8_t* src;
           uint32_t b, row;
-          page_info(i, q, src, c_len[q], b, row);
+          uint64_t gc;
+          page_info(i, t, src, c_len[t], b, row, gc);
+          c_dst[t] = nullptr;
+          if (C::FUSED && gc != ~0ull) {
+            const uint64_t so = __ldg(spec_off + gc);
+            if (so != ~0ull) {
+              const uint64_t gi = blockIdx.x + uint64_t(i) * gridDim.x;
+              const uint64_t slot = slot_base + gi * GP + PPW * warp + 32 * t + lane;
+              c_dst[t] = staging + so + ((slot & ((1u << ppc_shift) - 1)) << 12);
+            }
+          }
         }
-        c_full = reg_bits[i & 1] == 0xfu;
-        L0 = L1 = 0x00250025u;  // l_0 = low byte of the FNV offset basis, both lanes
+        c_full = reg_bits[i & 1] == (1u << TPW) - 1;
+#pragma unroll
+        for (int q = 0; q < PAIRS; ++q) L[q] = 0x00250025u;  // l_0 = 0x25 in both lanes
       }
       mbar_wait(fbar + 8 * st, ph_full);
-      if (st == kST - 1) ph_full ^= 1u;
-      // per page: slab address with its swizzle bits (unit uu at addr ^ (uu << 4));
-      // pages without bytes in this stage read the zero slab (their chain
-      // continues over zeros, which adds nothing to the digest sum)
-      const uint32_t sbase = ring + st * kWarpStage + lane * kSlab;
-      uint32_t pa[4];
+      if (st == ST - 1) ph_full ^= 1u;
+      // per page: row address with its swizzle bits (unit x at addr ^ (x << 4),
+      // next box + SUB); pages without bytes in this stage read the zero slab
+      // (their chain continues over zeros, which adds nothing to the sum)
+      const uint32_t sbase = ring + st * C::WSTAGE + lane * BOXW;
+      uint32_t pa[TPW], pb[TPW];
       if (c_full) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) pa[q] = (sbase + q * 32 * kSlab) | swz;
+        for (int t = 0; t < TPW; ++t) {
+          pa[t] = (sbase + t * C::TASKB) | swz;
+          pb[t] = C::SUB;
+        }
       } else {
         const uint32_t rb = reg_bits[i & 1];
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          pa[q] = s * kSlab < c_len[q] ? (sbase + q * 32 * kSlab) | ((rb >> q) & 1 ? swz : 0u) : zbase;
+        for (int t = 0; t < TPW; ++t) {
+          const bool v = s * SLAB < c_len[t];
+          pa[t] = v ? (sbase + t * C::TASKB) | ((rb >> t) & 1 ? swz : 0u) : zbase;
+          pb[t] = v ? C::SUB : 0u;
+        }
       }
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t gb = 2 * p + h;
-        const uint32_t ab = gb % kNA;
-        if (gb >= kNA) mbar_wait(bar_afree + 8 * ab, (gb / kNA - 1) & 1);
+      for (int h = 0; h < C::BPS; ++h) {
+        const uint32_t gb = C::BPS * p + h;
+        const uint32_t ab = gb % NA;
+        if (gb >= NA) mbar_wait(bar_afree + 8 * ab, (gb / NA - 1) & 1);
         tc_fence_after();
-        const uint32_t acol = trow + ab * kABuf;
+        const uint32_t acol = trow + ab * C::ABUF;
 #pragma unroll
         for (int uu = 0; uu < 2; ++uu) {
           const uint32_t unit = 2 * h + uu;
-          uint4 v[4];
+          const uint32_t ux = (unit % C::UPB) << 4, uo = unit / C::UPB;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) v[q] = ld_shared16(pa[q] ^ (unit << 4));
-          uint32_t upk0[8], lpk0[8], upk1[8], lpk1[8];
-          if (dbg & 1) {
+          for (int q = 0; q < PAIRS; ++q) {
+            const uint4 va = ld_shared16((pa[2 * q] ^ ux) + uo * pb[2 * q]);
+            const uint4 vb = ld_shared16((pa[2 * q + 1] ^ ux) + uo * pb[2 * q + 1]);
+            uint32_t upk[8], lpk[8];
+            if (dbg & 1) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              upk0[j] = v[0].x + j; lpk0[j] = v[1].y + j; upk1[j] = v[2].z + j; lpk1[j] = v[3].w + j;
+              for (int j = 0; j < 8; ++j) {
+                upk[j] = va.x + j;
+                lpk[j] = vb.y + j;
+              }
+            } else {
+              chain16(L[q], va, vb, upk, lpk);
             }
-          } else {
-            chain16(L0, v[0], v[1], upk0, lpk0);
-            chain16(L1, v[2], v[3], upk1, lpk1);
+            tc_st8(acol + q * C::ASET + 8 * uu, upk);
+            tc_st8(acol + q * C::ASET + 16 + 8 * uu, lpk);
           }
-          tc_st8(acol + 8 * uu, upk0);
-          tc_st8(acol + 16 + 8 * uu, lpk0);
-          tc_st8(acol + kASet + 8 * uu, upk1);
-          tc_st8(acol + kASet + 16 + 8 * uu, lpk1);
         }
         tc_wait_st();
         tc_fence_before();
         mbar_arrive(bar_afull + 8 * ab);
       }
+      if constexpr (C::FUSED) {
+        // speculative compaction: every page of a predicted-staged chunk
+        // writes the last SEG stages' slabs (SEG * SLAB = 256 contiguous
+        // bytes) to staging, 16 lanes per page (coalesced), read back from
+        // the shared-memory ring; then the slot of stage p - SEG + 1 is free
+        if (s % C::SEG == C::SEG - 1) {
+          constexpr int UPS = C::SEG * C::UNITS;  // 16-B units per page segment
+          constexpr int PPI = 32 / UPS;
+          const uint32_t x = lane % UPS, jj = lane / UPS;
+          const uint32_t xs = x / C::UNITS, xu = x % C::UNITS;  // sub-stage, unit in the slab
+          // ring slot of sub-stage xs (stage p - SEG + 1 + xs)
+          const uint32_t sl = (st + ST - (C::SEG - 1) + xs) % ST;
+          const uint32_t s0 = s - (C::SEG - 1);
+          const uint32_t rb = reg_bits[i & 1];
+#pragma unroll
+          for (int t = 0; t < TPW; ++t) {
+            const uint32_t vm = __ballot_sync(kFull, c_dst[t] != nullptr && s0 * SLAB < c_len[t]);
+            if (vm == 0) continue;
+            const uint32_t tb = ring + sl * C::WSTAGE + t * C::TASKB;
+#pragma unroll
+            for (int k = 0; k < 32 / PPI; ++k) {
+              const uint32_t j = k * PPI + jj;
+              uint8_t* d = reinterpret_cast<uint8_t*>(
+                  __shfl_sync(kFull, reinterpret_cast<uint64_t>(c_dst[t]), j));
+              if ((vm >> j) & 1) {
+                const uint32_t sw = (rb >> t) & 1 ? (BOXW == 128 ? (j & 7) : ((j >> 1) & 3)) : 0u;
+                const uint32_t a = tb + (xu / C::UPB) * C::SUB + j * BOXW + (((xu % C::UPB) ^ sw) << 4);
+                st_stream16(d + s0 * SLAB + x * 16, ld_shared16(a));
+              }
+            }
+          }
+          __syncwarp();
+#pragma unroll
+          for (int k = 0; k < C::SEG; ++k) issue(p + ST - (C::SEG - 1) + k);
+        }
+      }
       __syncwarp();  // the stage slot is refilled by this warp's next issue
-      if (s == kStages - 1) {
+      if (s == C::STAGES - 1) {
         // ---- epilogue of group i: accumulators -> page digests -> chunk digests
-        const uint32_t db = i % kNDB;
-        mbar_wait(bar_dfull + 8 * db, (i / kNDB) & 1);
+        const uint32_t db = i % NDB;
+        mbar_wait(bar_dfull + 8 * db, (i / NDB) & 1);
         tc_fence_after();
-        uint32_t d[32];  // d[16 ps + 8 pg + j] = limb j of page (pair ps, lane pg)
-        tc_ld32(drow + db * kDBuf, d);
+        // d[16 q + 8 pg + j] = limb j of page (pair q, lane pg)
+        uint32_t d[16 * PAIRS];
+        if constexpr (PAIRS == 2) {
+          uint32_t (&dd)[32] = reinterpret_cast<uint32_t (&)[32]>(d);
+          tc_ld32(drow + db * C::DBUF, dd);
+        } else {
+          uint32_t (&dd)[16] = reinterpret_cast<uint32_t (&)[16]>(d);
+          tc_ld16(drow + db * C::DBUF, dd);
+        }
         tc_fence_before();
         mbar_arrive(bar_dfree + 8 * db);
         const uint64_t k0 = __ldg(htab + 34);
-        uint32_t vm[4];
+        uint32_t vm[TPW];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int ps = q >> 1, pg = q & 1;
+        for (int t = 0; t < TPW; ++t) {
+          const int q = t >> 1, pg = t & 1;
           uint64_t S = 0;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) S += static_cast<uint64_t>(d[16 * ps + 8 * pg + j]) << (8 * j);
-          const uint32_t Lf = ps ? L1 : L0;
-          const uint64_t ln = (Lf >> (16 * pg)) & 0xffu;
-          const uint32_t n = c_len[q];
+          for (int j = 0; j < 8; ++j) S += static_cast<uint64_t>(d[16 * q + 8 * pg + j]) << (8 * j);
+          const uint64_t ln = (L[q] >> (16 * pg)) & 0xffu;
+          const uint32_t n = c_len[t];
           uint64_t hv = 0;
           if (n > 0) {
             const uint32_t m = n >> 8;
             hv = __ldg(htab + m) + __ldg(htab + 17 + m) * (S + ln - k0);
           }
-          dsm[warp * 128 + 32 * q + lane] = hv;
-          vm[q] = __ballot_sync(kFull, n > 0);
+          dsm[warp * PPW + 32 * t + lane] = hv;
+          vm[t] = __ballot_sync(kFull, n > 0);
         }
         __syncwarp();
         const uint64_t gi = blockIdx.x + uint64_t(i) * gridDim.x;
-        const uint64_t slot0 = slot_base + gi * kGroupPages + 128 * warp;
+        const uint64_t slot0 = slot_base + gi * GP + PPW * warp;
         const uint32_t ppc = 1u << ppc_shift;
-        for (uint32_t c = lane; c < (128u >> ppc_shift); c += 32) {
+        for (uint32_t c = lane; c < (uint32_t(PPW) >> ppc_shift); c += 32) {
           const uint32_t p0 = c << ppc_shift;
-          const uint32_t q0 = p0 >> 5;
-          const uint32_t vq = q0 == 0 ? vm[0] : q0 == 1 ? vm[1] : q0 == 2 ? vm[2] : vm[3];
+          const uint32_t t0 = p0 >> 5;
+          uint32_t vq = vm[0];
+#pragma unroll
+          for (int t = 1; t < TPW; ++t)
+            if (t0 == uint32_t(t)) vq = vm[t];
           if (!((vq >> (p0 & 31)) & 1)) continue;
           uint64_t hv;
           if (ppc_shift == 0) {
-            hv = dsm[warp * 128 + p0];
+            hv = dsm[warp * PPW + p0];
           } else {
             // a chunk's pages lie in one task (ppc <= 32): valid pages are a prefix
             hv = kFnvOffset;
             for (uint32_t j = 0; j < ppc; ++j) {
               if (!((vq >> ((p0 + j) & 31)) & 1)) break;
-              hv = fnv_u64(hv, dsm[warp * 128 + p0 + j]);
+              hv = fnv_u64(hv, dsm[warp * PPW + p0 + j]);
             }
           }
           k1_store_digest(g, (slot0 + p0) >> ppc_shift, hv, chunk_dig);
@@ -574,9 +698,10 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == kCW) {
+  if (warp == CW) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(C::TCOLS)
+                 : "memory");
   }
   if (g.xdig != nullptr) __threadfence_system();
 }
@@ -650,27 +775,42 @@ const uint8_t* device_btab() {
 }  // namespace
 
 bool hash_mma_ok(const GridDev& g) {
-  return g.tmaps64 != nullptr && g.page_shift == 12 && g.chunk_shift >= 12 && g.chunk_shift <= 17;
+  return g.tmaps64 != nullptr && g.tmaps != nullptr && g.page_shift == 12 && g.chunk_shift >= 12 &&
+         g.chunk_shift <= 17;
 }
 
-int launch_hash_mma(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig, cudaStream_t s) {
+namespace {
+template <class C>
+int launch_mma(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
+               const uint64_t* spec_off, uint8_t* staging, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_hash_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmem));
+    cudaFuncSetAttribute(k_hash_mma<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
     attr = true;
   }
   const uint64_t c_end = g.c_end ? g.c_end : g.nchunks;
   if (c_end <= g.c_begin) return 0;
   const uint8_t* bt = device_btab();
   if (!bt) return -1;
-  const uint64_t ngroups = (((c_end - g.c_begin) << (g.chunk_shift - 12)) + kGroupPages - 1) / kGroupPages;
+  const uint64_t ngroups = (((c_end - g.c_begin) << (g.chunk_shift - 12)) + C::GP - 1) / C::GP;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint64_t blocks = ngroups < uint64_t(sms) ? ngroups : uint64_t(sms);
   static const int dbg = getenv("SNAP_MMA_DEBUG") ? atoi(getenv("SNAP_MMA_DEBUG")) : 0;
-  k_hash_mma<<<unsigned(blocks), kThreads, kSmem, s>>>(arena, g, chunk_dig, bt, dbg);
+  k_hash_mma<C><<<unsigned(blocks), C::THREADS, C::SMEM, s>>>(arena, g, chunk_dig, bt, spec_off,
+                                                               staging, dbg);
   return 1;
+}
+}  // namespace
+
+int launch_hash_mma(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig, cudaStream_t s) {
+  return launch_mma<MmaHash>(arena, g, chunk_dig, nullptr, nullptr, s);
+}
+
+int launch_hash_mma_fused(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
+                          const uint64_t* spec_off, uint8_t* staging, cudaStream_t s) {
+  return launch_mma<MmaFused>(arena, g, chunk_dig, spec_off, staging, s);
 }
 
 }  // namespace snap

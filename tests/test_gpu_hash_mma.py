@@ -91,3 +91,42 @@ def test_mma_equals_default_large(snap):
             out.append(c.digests()[0])
     snap.set_k1_variant(-1)
     assert np.array_equal(out[0], out[1])
+
+
+def _snapshot_check(c, host, bufs):
+    c.set_buffers(bufs)
+    for rep in range(2):  # second pass: speculation from the previous layout
+        c.snapshot()
+        d, lens = c.digests()
+        sel, owner, off, sbytes, _ = c.selection()
+        od, olens, _ = O.hash_chunks([host], bufs)
+        osel, oown, ooff, otot = O.select(od, olens)
+        assert np.array_equal(d, od), f"pass {rep}: digests differ"
+        assert np.array_equal(sel, osel) and np.array_equal(off, ooff) and sbytes == otot
+        img = c.read_staging(0, sbytes)
+        assert np.array_equal(img, O.compact([host], bufs, 65536, osel, ooff, otot)), \
+            f"pass {rep}: staging image differs"
+
+
+def test_fused_snapshot_mma(mma):
+    """Fused hash + speculative compaction on the tensor-core kernel: regular 4 MiB buffers,
+    ragged buffers (tails, sub-page buffers), duplicated content (dedup moves offsets)."""
+    rng = np.random.default_rng(11)
+    nbytes = 160 << 20
+    with mma.Ctx(0, nbytes) as c:
+        c.fill_mix64(0, nbytes, 21, 0)
+        # duplicates: buffer 3 = buffer 1, buffer 7 = buffer 2
+        c.write(3 * (4 << 20), c.read(1 * (4 << 20), 4 << 20))
+        c.write(7 * (4 << 20), c.read(2 * (4 << 20), 4 << 20))
+        host = c.read(0, nbytes)
+        regular = [(0, i, i * (4 << 20), 4 << 20, i % 3) for i in range(16)]
+        _snapshot_check(c, host, regular)
+        bufs, addr, slot = [], 64 << 20, 0
+        while True:
+            nb = int(rng.integers(1, 900)) * 256 * (1 + 15 * int(rng.integers(0, 2)))
+            if addr + nb > nbytes:
+                break
+            bufs.append((0, slot, addr, nb, int(rng.integers(0, 3))))
+            slot += 1
+            addr += nb + int(rng.integers(0, 2)) * 4096
+        _snapshot_check(c, host, regular[:8] + bufs)

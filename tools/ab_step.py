@@ -17,6 +17,8 @@ bufs, rep, per = c2_layout()
 image = rep + per
 ctx = snap.Ctx(0, image + (64 << 20))
 fill_rank(ctx, 0, rep, per)
+if len(sys.argv) > 2 and sys.argv[2] == "regular":  # 512 x 4 MiB buffers, same image
+    bufs = [(0, i, i * (4 << 20), 4 << 20, 0) for i in range(image // (4 << 20))]
 ctx.set_buffers(bufs)
 for _ in range(5):
     ctx.snapshot()
