@@ -574,22 +574,28 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
         for (int uu = 0; uu < 2; ++uu) {
           const uint32_t unit = 2 * h + uu;
           const uint32_t ux = (unit % C::UPB) << 4, uo = unit / C::UPB;
+          // all loads, then the chains (independent: the compiler interleaves
+          // them), then the TMEM stores (volatile asm: nothing moves across)
+          uint4 v[TPW];
+#pragma unroll
+          for (int t = 0; t < TPW; ++t) v[t] = ld_shared16((pa[t] ^ ux) + uo * pb[t]);
+          uint32_t upk[PAIRS][8], lpk[PAIRS][8];
 #pragma unroll
           for (int q = 0; q < PAIRS; ++q) {
-            const uint4 va = ld_shared16((pa[2 * q] ^ ux) + uo * pb[2 * q]);
-            const uint4 vb = ld_shared16((pa[2 * q + 1] ^ ux) + uo * pb[2 * q + 1]);
-            uint32_t upk[8], lpk[8];
             if (dbg & 1) {
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
-                upk[j] = va.x + j;
-                lpk[j] = vb.y + j;
+                upk[q][j] = v[2 * q].x + j;
+                lpk[q][j] = v[2 * q + 1].y + j;
               }
             } else {
-              chain16(L[q], va, vb, upk, lpk);
+              chain16(L[q], v[2 * q], v[2 * q + 1], upk[q], lpk[q]);
             }
-            tc_st8(acol + q * C::ASET + 8 * uu, upk);
-            tc_st8(acol + q * C::ASET + 16 + 8 * uu, lpk);
+          }
+#pragma unroll
+          for (int q = 0; q < PAIRS; ++q) {
+            tc_st8(acol + q * C::ASET + 8 * uu, upk[q]);
+            tc_st8(acol + q * C::ASET + 16 + 8 * uu, lpk[q]);
           }
         }
         tc_wait_st();
