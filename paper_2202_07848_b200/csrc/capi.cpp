@@ -461,6 +461,7 @@ int hash_fused(snap_ctx* ctx, uint64_t c0 = 0, uint64_t c1 = 0) {
   if (!ctx->spec_ready) RC(init_spec(ctx));
   uint8_t* st;
   RC(staging_reserve(ctx, staging_target(ctx), true, &st));
+  g.spec_bytes = ctx->spec_bytes;
   CKL(snap::launch_hash(ctx->arena, g, P<uint64_t>(ctx->d_dig),
                         P<uint64_t>(ctx->d_spec[ctx->spec_cur]), st, ctx->stream));
   ctx->spec_used = true;

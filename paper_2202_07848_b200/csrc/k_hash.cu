@@ -840,7 +840,7 @@ bool hash_tma_selected() {
 //    buffer shapes, tools/hash_variants.py): the TMA tensor-load kernel beats
 //    the cp.async CfgA by 1-2 % on every shape; two chains per lane (CfgB) win
 //    by another 1 % on very large buffers but lose 14 % on small tensors.
-enum class K1 { A, B, C, D, E, F, WsA, WsB, WsC, Tma, Mma, MmaF };
+enum class K1 { A, B, C, D, E, F, WsA, WsB, WsC, Tma, Mma, MmaF, MmaFL };
 K1 choose_k1(const GridDev& g, const uint64_t* spec_off) {
   switch (hash_variant()) {
     case 1: return K1::B;
@@ -852,17 +852,23 @@ K1 choose_k1(const GridDev& g, const uint64_t* spec_off) {
     case 7: return K1::E;
     case 8: return K1::F;
     case 9: return K1::A;
+    case 12:
+      if (spec_off) return hash_mma_ok(g) ? K1::MmaFL : K1::E;
+      return hash_mma_ok(g) ? K1::Mma : K1::A;
     case 11:
       if (spec_off) return hash_mma_ok(g) ? K1::MmaF : K1::E;
       return hash_mma_ok(g) ? K1::Mma : K1::A;
     default: {
+      const uint64_t c_end = g.c_end ? g.c_end : g.nchunks;
+      const uint64_t pages = (c_end - g.c_begin) << (g.chunk_shift - g.page_shift);
+      // fused hash + speculative stores: CfgE. The tensor-core variants (11,
+      // 12) measured equal on C2 at N = 1, 2 and 4 (same-box A/B): the mixed
+      // read/write stream, not the hash, bounds the fused pass
       if (spec_off) return K1::E;
       // tensor-core FNV: one 1024-page group per SM at a time, so it needs
       // >= 128 groups (512 MiB) to fill the GPU (tools/hash_sizes.py:
       // 4.9-6.0 TB/s from 512 MiB up vs 3.0-3.6 for the TMA kernel; below
       // that the TMA kernel's 32-page tasks spread over more SMs)
-      const uint64_t c_end = g.c_end ? g.c_end : g.nchunks;
-      const uint64_t pages = (c_end - g.c_begin) << (g.chunk_shift - g.page_shift);
       if (hash_mma_ok(g) && pages >= 128 * 1024) return K1::Mma;
       if (g.nbufs && (g.nchunks << g.chunk_shift) / g.nbufs >= (64ull << 20)) return K1::B;
       return hash_tma_ok(g) ? K1::Tma : K1::A;
@@ -884,7 +890,8 @@ int launch_k1(K1 k, const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
     case K1::WsC: return launch_hash_ws<WsC>(arena, g, chunk_dig, spec_off, staging, s);
     case K1::Tma: return launch_hash_tma(arena, g, chunk_dig, s);
     case K1::Mma: return launch_hash_mma(arena, g, chunk_dig, s);
-    case K1::MmaF: return launch_hash_mma_fused(arena, g, chunk_dig, spec_off, staging, s);
+    case K1::MmaF: return launch_hash_mma_fused(arena, g, chunk_dig, spec_off, staging, s, false);
+    case K1::MmaFL: return launch_hash_mma_fused(arena, g, chunk_dig, spec_off, staging, s, true);
   }
   return 0;
 }
@@ -896,7 +903,7 @@ int launch_hash(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
   if (g.nchunks == 0) return 0;
   const K1 k = choose_k1(g, spec_off);
   const bool epilogue = !(k == K1::WsA || k == K1::WsB || k == K1::WsC || k == K1::Tma || k == K1::Mma ||
-                          k == K1::MmaF);
+                          k == K1::MmaF || k == K1::MmaFL);
   if (!g.dd.keys || epilogue) return launch_k1(k, arena, g, chunk_dig, spec_off, staging, s);
   GridDev h = g;
   h.dd = TableDev{};

@@ -67,7 +67,7 @@ constexpr size_t kBTabAll = kBTab + (17 + 17 + 1) * 8;
 // PAIRS chain pairs per thread, SLAB bytes of each page per data stage (TMA
 // boxes of 32 pages x BOXW bytes, SWIZZLE_64B / _128B), ST-deep ring per
 // warp, FUSED: also write every predicted-staged chunk's slab to staging.
-template <int CW_, int PAIRS_, int SLAB_, int ST_, bool FUSED_>
+template <int CW_, int PAIRS_, int SLAB_, int ST_, bool FUSED_, int SEG_ = 0>
 struct MmaCfg {
   static constexpr int CW = CW_, PAIRS = PAIRS_, SLAB = SLAB_, ST = ST_;
   static constexpr bool FUSED = FUSED_;
@@ -95,10 +95,10 @@ struct MmaCfg {
   static constexpr size_t SM_B = size_t(kBR) * kBBytes;
   static constexpr size_t SM_DIG = size_t(GP) * 8;
   static constexpr size_t SM_ZERO = 128;                // zero slab: LDS source for absent pages
-  // FUSED: staging writes go out in 256-byte segments per page, SEG = 256 / SLAB
+  // FUSED: staging writes go out in SEG * SLAB-byte segments per page (default 256 B)
   // consecutive stages at a time (the load of the next stage into a slot is
   // then issued after the slot's store instead of before the compute)
-  static constexpr int SEG = SLAB >= 256 ? 1 : 256 / SLAB;
+  static constexpr int SEG = SEG_ ? SEG_ : (SLAB >= 256 ? 1 : 256 / SLAB);
   static constexpr int NBARS = CW * ST + NA + NA + NDB + NDB + kBR;
   static constexpr size_t SMEM = 1024 + SM_DATA + SM_B + SM_DIG + SM_ZERO + NBARS * 8 + 16;
   static_assert(SMEM <= 232448, "shared memory");
@@ -110,6 +110,9 @@ struct MmaCfg {
 // in 256-byte segments per page (two stages at a time).
 using MmaHash = MmaCfg<8, 2, 64, 3, false>;
 using MmaFused = MmaCfg<8, 1, 128, 3, true>;
+// fused, few chunks staged (multi-rank striping: each GPU writes ~1/N of the
+// replicated state): the hash-only geometry, 128-byte staging segments
+using MmaFusedLight = MmaCfg<8, 2, 64, 3, true, 2>;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -815,7 +818,8 @@ int launch_hash_mma(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
 }
 
 int launch_hash_mma_fused(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
-                          const uint64_t* spec_off, uint8_t* staging, cudaStream_t s) {
+                          const uint64_t* spec_off, uint8_t* staging, cudaStream_t s, bool light) {
+  if (light) return launch_mma<MmaFusedLight>(arena, g, chunk_dig, spec_off, staging, s);
   return launch_mma<MmaFused>(arena, g, chunk_dig, spec_off, staging, s);
 }
 

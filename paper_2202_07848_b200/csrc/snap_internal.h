@@ -53,6 +53,8 @@ struct GridDev {
   uint64_t* const* xdig = nullptr;
   uint32_t xn = 0;
   uint64_t xoff = 0;
+  // fused K1: predicted staged bytes of this launch's layout (kernel choice)
+  uint64_t spec_bytes = 0;
 };
 
 // Open-addressing digest table (dedup + known set), power-of-two capacity.
@@ -70,9 +72,11 @@ int launch_hash_tma(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
 // cores + the linear part as a tcgen05 int8 MMA); needs the grid tensor maps.
 bool hash_mma_ok(const GridDev& g);
 int launch_hash_mma(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig, cudaStream_t s);
-// the same with the speculative K3 stores fused (spec_off / staging as launch_hash)
+// the same with the speculative K3 stores fused (spec_off / staging as launch_hash);
+// light: geometry for few staged chunks (hash-only chain count, 128-B segments)
 int launch_hash_mma_fused(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
-                          const uint64_t* spec_off, uint8_t* staging, cudaStream_t s);
+                          const uint64_t* spec_off, uint8_t* staging, cudaStream_t s,
+                          bool light);
 // K1 kernel policy override (SNAP_HASH_VARIANT semantics; -1 = default policy)
 void set_hash_variant(int v);
 // host: one 128-byte CUtensorMap per buffer into host_maps (box of 32 pages x

@@ -108,11 +108,22 @@ def _snapshot_check(c, host, bufs):
             f"pass {rep}: staging image differs"
 
 
-def test_fused_snapshot_mma(mma):
-    """Fused hash + speculative compaction on the tensor-core kernel: regular 4 MiB buffers,
-    ragged buffers (tails, sub-page buffers), duplicated content (dedup moves offsets)."""
+@pytest.mark.parametrize("variant", [11, 12])
+def test_fused_snapshot_mma(snap, variant):
+    """Fused hash + speculative compaction on the tensor-core kernels (11: 128-B slabs,
+    12: the light-write geometry used for striped multi-rank layouts): regular 4 MiB
+    buffers, ragged buffers (tails, sub-page buffers), duplicated content (dedup moves
+    offsets)."""
+    snap.set_k1_variant(variant)
     rng = np.random.default_rng(11)
     nbytes = 160 << 20
+    try:
+        _fused_case(snap, rng, nbytes)
+    finally:
+        snap.set_k1_variant(-1)
+
+
+def _fused_case(mma, rng, nbytes):
     with mma.Ctx(0, nbytes) as c:
         c.fill_mix64(0, nbytes, 21, 0)
         # duplicates: buffer 3 = buffer 1, buffer 7 = buffer 2
