@@ -233,10 +233,20 @@ def test_fused_speculation_learns_and_recovers(snap, ctx, golden):
     check(host)
 
 
-def test_snapshot_host_pipelined(snap):
+@pytest.mark.parametrize("variant", [-1, 11, 12])
+def test_snapshot_host_pipelined(snap, variant):
     """snap_snapshot_host (pinned host image -> arena -> K1..K3 -> staging to host), slab
     pipelined: staging image == oracle compaction, through mispredicted, learned and
-    incremental layouts, and through the non-pipelined fallback (unsorted buffers)."""
+    incremental layouts, and through the non-pipelined fallback (unsorted buffers).
+    variant 11/12: the tensor-core K1 kernels on every slab (grid slices c_begin..c_end)."""
+    snap.set_k1_variant(variant)
+    try:
+        _host_pipelined(snap)
+    finally:
+        snap.set_k1_variant(-1)
+
+
+def _host_pipelined(snap):
     nbytes = 160 << 20
     img = O.fill_mix64(nbytes // 8, 21, 0)
     # buffers spanning several 64 MiB slabs, a duplicate (mispredicted speculation)
