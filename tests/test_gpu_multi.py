@@ -19,17 +19,20 @@ def ngpus():
         return 0
 
 
-@pytest.mark.parametrize("world,fused", [(2, False), (4, False), (2, True)])
-def test_dist_snapshot_parity(world, fused):
+@pytest.mark.parametrize("world,fused,k1", [(2, False, -1), (4, False, -1), (2, True, -1),
+                                           (2, False, 11), (2, True, 12)])
+def test_dist_snapshot_parity(world, fused, k1):
     """fused: the digest exchange done by K1's own NVLink stores into every rank's
     CUDA-IPC-mapped window + a peer barrier (SNAP_FUSED_EXCHANGE=1) instead of NCCL
-    (the worker's second snapshot takes that path)."""
+    (the worker's second snapshot takes that path). k1 11/12: the tensor-core K1
+    kernels on every launch (striped speculative stores, incremental hash-only)."""
     if ngpus() < world:
         pytest.skip(f"needs {world} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={world}", "--master-addr=127.0.0.1", "--master-port=29533",
            os.path.join(ROOT, "tests", "dist_snapshot_worker.py")]
-    env = dict(os.environ, SNAP_FUSED_EXCHANGE="1" if fused else "0")
+    env = dict(os.environ, SNAP_FUSED_EXCHANGE="1" if fused else "0",
+               SNAP_HASH_VARIANT=str(k1))
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=ROOT, env=env)
     print(r.stdout[-3000:], r.stderr[-3000:])
     assert r.returncode == 0
