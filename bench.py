@@ -699,6 +699,7 @@ def run_ours(args, dist):
     clocks.window(tw0, time.perf_counter())
     clk = clocks.stop()
     launches = ctx.launches - l0
+    k1_kernel = snap.last_k1_kernel()  # the K1 the timed steps ran (policy: k_hash.cu choose_k1)
     t_hash, n_hash = ctx.prof_read(snap.PROF_HASH)
     t_sel, n_sel = ctx.prof_read(snap.PROF_SELECT)
     t_cmp, n_cmp = ctx.prof_read(snap.PROF_COMPACT)
@@ -783,12 +784,13 @@ def run_ours(args, dist):
                        "chunks_per_rank": nchunks, "parallelism": f"dp{N} (1 rank/GPU)",
                        "l2": "inputs 2 GiB/GPU > 126 MB L2 (no flush needed)",
                        "staged_bytes_total": int(w_total), "unique_bytes_global": int(g_bytes)},
-            "roofline": {"bound": "hbm", "kernel": "k_hash (K1 + fused K3 stores)",
+            "roofline": {"bound": "hbm", "kernel": k1_kernel,
                          "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": int(k_bytes),
                          "algorithmic_bytes": "R (image bytes hashed) + W (shard bytes staged)",
-                         "traffic": traffic_for("k_hash")},
+                         "traffic": traffic_for("k_hash" if k1_kernel.startswith("k_hash<")
+                                                else f"{k1_kernel.split(' (')[0]} N={N}")},
             "step_hbm": {"rw_bytes_per_gpu": int(image + my_bytes),
                          "rw_gbs_per_gpu": round((image + my_bytes) / step_s / 1e9, 1),
                          "frac": round((image + my_bytes) / step_s / 1e9 / peak, 4)},

@@ -415,6 +415,9 @@ int snap_prof_read(snap_ctx* ctx, int kind, float* total_ms, uint64_t* count);
  * Every variant yields identical digests. Applies to grids installed after
  * the call (the TMA-based kernels need tensor maps built at install time). */
 int snap_set_k1_variant(int variant);
+/* Name of the K1 kernel the most recent hash launch of this process used
+ * (measurement labels; static string). */
+const char* snap_last_k1_kernel(void);
 
 #ifdef __cplusplus
 }

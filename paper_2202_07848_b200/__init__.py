@@ -169,6 +169,7 @@ _SIGS = {
                                  C.POINTER(C.c_uint64)]),
     "snap_prof_enable": (C.c_int, [C.c_void_p, C.c_int]),
     "snap_set_k1_variant": (C.c_int, [C.c_int]),
+    "snap_last_k1_kernel": (C.c_char_p, []),
     "snap_prof_read": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_float),
                                  C.POINTER(C.c_uint64)]),
     "snap_alloc_create": (C.c_int, [C.c_uint64, C.c_uint64, C.POINTER(C.c_void_p)]),
@@ -704,3 +705,8 @@ def set_k1_variant(variant: int = -1) -> None:
     rc = lib().snap_set_k1_variant(int(variant))
     if rc < 0:
         raise SnapError(rc, "snap_set_k1_variant")
+
+
+def last_k1_kernel() -> str:
+    """Name of the K1 kernel the most recent hash launch used (snap_last_k1_kernel)."""
+    return lib().snap_last_k1_kernel().decode()

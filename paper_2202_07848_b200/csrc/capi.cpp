@@ -379,10 +379,32 @@ bool replicated_hint(const snap_buf& b) {
   return b.cat == 0 || b.cat == 1;  // Param / OptState: identical across DP replicas
 }
 
+// SNAP_SPEC_STRIPE=N (measurement aid, single GPU): every snapshot predicts the
+// layout rank 0 of an N-rank job stages, so K1's fused stores can be timed at
+// the write fraction of an N-GPU run on one GPU (tools/stripe_emu.py)
+int spec_stripe_emu() {
+  static const int v = getenv("SNAP_SPEC_STRIPE") ? atoi(getenv("SNAP_SPEC_STRIPE")) : 0;
+  return v;
+}
+
 int init_spec(snap_ctx* ctx) {
   const uint64_t n = ctx->nchunks;
   std::vector<uint64_t> spec(n, ~0ull);
-  if (!ctx->comm || ctx->nranks == 1) {
+  const int emu = spec_stripe_emu();
+  if ((!ctx->comm || ctx->nranks == 1) && emu > 1) {
+    // measurement aid: predict the layout rank 0 of an emu-rank job stages
+    // (private chunks + every emu-th replicated chunk); the fix-up copies the rest
+    std::vector<uint8_t> rep(n, 0);
+    for (size_t b = 0; b < ctx->bufs.size(); ++b)
+      for (uint64_t g = ctx->h_cstart[b]; g < ctx->h_cstart[b + 1]; ++g)
+        rep[g] = replicated_hint(ctx->bufs[b]);
+    uint64_t off = 0;
+    for (uint64_t g = 0; g < n; ++g)
+      if (!rep[g] || g % uint64_t(emu) == 0) {
+        spec[g] = off;
+        off += ctx->h_lens[g];
+      }
+  } else if (!ctx->comm || ctx->nranks == 1) {
     uint64_t off = 0;
     for (uint64_t g = 0; g < n; ++g) {
       spec[g] = off;
@@ -458,7 +480,7 @@ int hash_fused(snap_ctx* ctx, uint64_t c0 = 0, uint64_t c1 = 0) {
     ctx->spec_used = false;
     return SNAP_OK;
   }
-  if (!ctx->spec_ready) RC(init_spec(ctx));
+  if (!ctx->spec_ready || spec_stripe_emu() > 1) RC(init_spec(ctx));
   uint8_t* st;
   RC(staging_reserve(ctx, staging_target(ctx), true, &st));
   g.spec_bytes = ctx->spec_bytes;
@@ -1410,6 +1432,8 @@ int snap_set_k1_variant(int variant) {
   snap::set_hash_variant(variant);
   return SNAP_OK;
 }
+
+const char* snap_last_k1_kernel(void) { return snap::last_k1_name(); }
 
 int snap_prof_enable(snap_ctx* ctx, int on) {
   if (!ctx) return SNAP_EINVAL;

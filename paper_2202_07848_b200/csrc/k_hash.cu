@@ -823,11 +823,12 @@ int hash_variant() {
 }
 
 void set_hash_variant(int v) { g_hash_variant = v < 0 ? 99 : v; }
+const char* last_k1_name();
 
 // tensor maps are built for every grid unless a cp.async variant is forced
 bool hash_tma_selected() {
   const int v = hash_variant();
-  return v == 10 || v == 11 || v == 99;
+  return v == 10 || v == 11 || v == 12 || v == 99;
 }
 
 // The K1 kernel a launch uses (SNAP_HASH_VARIANT / snap_set_k1_variant force
@@ -861,10 +862,20 @@ K1 choose_k1(const GridDev& g, const uint64_t* spec_off) {
     default: {
       const uint64_t c_end = g.c_end ? g.c_end : g.nchunks;
       const uint64_t pages = (c_end - g.c_begin) << (g.chunk_shift - g.page_shift);
-      // fused hash + speculative stores: CfgE. The tensor-core variants (11,
-      // 12) measured equal on C2 at N = 1, 2 and 4 (same-box A/B): the mixed
-      // read/write stream, not the hash, bounds the fused pass
-      if (spec_off) return K1::E;
+      // fused hash + speculative stores. Most chunks staged (single GPU, first
+      // snapshot): CfgE — the mixed read/write DRAM stream bounds the pass and
+      // its 256-B segments win (0.79 vs 0.83-0.96 ms on C2). Few staged
+      // (multi-GPU striping: rank r writes its private state + 1/N of the
+      // replicated state): the hash dominates -> tensor-core FNV with the
+      // stores fused (hash-only geometry, 64-B segments). Same-box A/B at the
+      // N = 2 / 4 / 8 write fraction of C2 (tools/stripe_emu.py): 0.755 /
+      // 0.712 / 0.686 ms vs CfgE 0.817 / 0.792 / 0.788.
+      if (spec_off) {
+        const uint64_t grid_bytes = (c_end - g.c_begin) << g.chunk_shift;
+        if (hash_mma_ok(g) && pages >= 128 * 1024 && g.spec_bytes * 10 < grid_bytes * 7)
+          return K1::MmaFL;
+        return K1::E;
+      }
       // tensor-core FNV: one 1024-page group per SM at a time, so it needs
       // >= 128 groups (512 MiB) to fill the GPU (tools/hash_sizes.py:
       // 4.9-6.0 TB/s from 512 MiB up vs 3.0-3.6 for the TMA kernel; below
@@ -898,10 +909,31 @@ int launch_k1(K1 k, const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
 
 // K1 launch; with g.dd set the K2 insert is fused into the k_hash epilogue, or
 // (warp-specialized / TMA kernels) runs as a range kernel right after.
+const char* k1_name(K1 k) {
+  switch (k) {
+    case K1::A: return "k_hash<CfgA> (FNV chain, cp.async)";
+    case K1::B: return "k_hash<CfgB> (FNV chain, 2 chains/lane)";
+    case K1::C: return "k_hash<CfgC>";
+    case K1::D: return "k_hash<CfgD>";
+    case K1::E: return "k_hash<CfgE> (FNV chain + fused K3 stores, 256-B slabs)";
+    case K1::F: return "k_hash<CfgF>";
+    case K1::WsA: return "k_hash_ws<WsA>";
+    case K1::WsB: return "k_hash_ws<WsB>";
+    case K1::WsC: return "k_hash_ws<WsC>";
+    case K1::Tma: return "k_hash_tma (FNV chain, TMA loads)";
+    case K1::Mma: return "k_hash_mma (tensor-core FNV, hash only)";
+    case K1::MmaF: return "k_hash_mma fused (tensor-core FNV + fused K3 stores)";
+    case K1::MmaFL: return "k_hash_mma fused-light";
+  }
+  return "?";
+}
+const char* g_last_k1 = "";
+
 int launch_hash(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
                 const uint64_t* spec_off, uint8_t* staging, cudaStream_t s) {
   if (g.nchunks == 0) return 0;
   const K1 k = choose_k1(g, spec_off);
+  g_last_k1 = k1_name(k);
   const bool epilogue = !(k == K1::WsA || k == K1::WsB || k == K1::WsC || k == K1::Tma || k == K1::Mma ||
                           k == K1::MmaF || k == K1::MmaFL);
   if (!g.dd.keys || epilogue) return launch_k1(k, arena, g, chunk_dig, spec_off, staging, s);
@@ -914,6 +946,8 @@ int launch_hash(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
   if (blocks) k_insert_range<<<unsigned(blocks), 256, 0, s>>>(g, chunk_dig);
   return n + (blocks ? 1 : 0);
 }
+
+const char* last_k1_name() { return g_last_k1; }
 
 int launch_buf_fold(const GridDev& g, const uint64_t* chunk_dig, uint64_t* buf_dig,
                     cudaStream_t s) {

@@ -105,14 +105,14 @@ struct MmaCfg {
 };
 // hash only: 1024 pages in flight per SM (2 chain pairs per thread, 2 warps
 // per SM sub-partition) for latency hiding; 64-byte slabs keep 3 stages in
-// shared memory. Fused: reads and writes share HBM, so half the chains
-// suffice (one pair per thread, 128-byte slabs) and the staging writes leave
-// in 256-byte segments per page (two stages at a time).
+// shared memory. Fused, few chunks staged (multi-GPU striping, the default
+// when the predicted staging is < 70 % of the grid): the same geometry, each
+// stage's staged slabs written right after it is hashed (64-byte segments,
+// full prefetch depth). Variant 11 (8 warps x 1 pair, 128-byte slabs) is kept
+// selectable: 3-7 % slower on C2 at the N = 2..8 write fractions.
 using MmaHash = MmaCfg<8, 2, 64, 3, false>;
-using MmaFused = MmaCfg<8, 1, 128, 3, true>;
-// fused, few chunks staged (multi-rank striping: each GPU writes ~1/N of the
-// replicated state): the hash-only geometry, 128-byte staging segments
-using MmaFusedLight = MmaCfg<8, 2, 64, 3, true, 2>;
+using MmaFused = MmaCfg<8, 1, 128, 3, true, 1>;
+using MmaFusedLight = MmaCfg<8, 2, 64, 3, true, 1>;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -506,7 +506,10 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
 
 #pragma unroll
     for (int p = 0; p < ST - 1; ++p) issue(p);
-    if constexpr (C::FUSED) issue(ST - 1);  // fused: the issue for a slot follows its store
+    // SEG > 1: a slot's next load is issued after its stage's store (the store
+    // needs SEG consecutive stages resident)
+    constexpr bool kLate = C::FUSED && C::SEG > 1;
+    if constexpr (kLate) issue(ST - 1);
 
     uint32_t c_len[TPW];
     uint8_t* c_dst[TPW];  // FUSED: staging address of this lane's page, or null
@@ -518,7 +521,7 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
     const uint32_t swz = static_cast<uint32_t>(BOXW == 128 ? (lane & 7) : ((lane >> 1) & 3)) << 4;
     uint32_t ph_full = 0;  // parity of the data ring's current wrap
     for (uint32_t p = 0; p < nst; ++p) {
-      if constexpr (!C::FUSED) issue(p + ST - 1);
+      if constexpr (!kLate) issue(p + ST - 1);
       const uint32_t st = cst;
       cst = cst + 1 == ST ? 0 : cst + 1;
       const uint32_t i = p / C::STAGES;
@@ -638,7 +641,8 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
           }
           __syncwarp();
 #pragma unroll
-          for (int k = 0; k < C::SEG; ++k) issue(p + ST - (C::SEG - 1) + k);
+          if constexpr (kLate)
+            for (int k = 0; k < C::SEG; ++k) issue(p + ST - (C::SEG - 1) + k);
         }
       }
       __syncwarp();  // the stage slot is refilled by this warp's next issue

@@ -79,6 +79,8 @@ int launch_hash_mma_fused(const uint8_t* arena, const GridDev& g, uint64_t* chun
                           bool light);
 // K1 kernel policy override (SNAP_HASH_VARIANT semantics; -1 = default policy)
 void set_hash_variant(int v);
+// name of the K1 kernel the last launch_hash call chose (process-wide)
+const char* last_k1_name();
 // host: one 128-byte CUtensorMap per buffer into host_maps (box of 32 pages x
 // box_bytes, box_bytes 128 -> SWIZZLE_128B, 64 -> SWIZZLE_64B); 0 on success
 int encode_tensor_maps(const uint8_t* arena, const uint64_t* addr, const uint64_t* bytes,
