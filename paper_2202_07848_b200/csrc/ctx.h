@@ -244,11 +244,19 @@ inline void build_tmaps(snap_ctx* ctx, DevMem& m, const uint64_t* addr, const ui
                         uint32_t n, GridDev& g) {
   g.tmaps = nullptr;
   g.tmaps64 = nullptr;
+  g.tmaps64c = nullptr;
   if (!snap::hash_tma_selected() || g.page_shift != 12 || n == 0) return;
-  // n maps with 128-byte boxes (k_hash_tma), then n with 64-byte boxes (k_hash_mma)
-  std::vector<uint8_t> host(size_t(n) * 256);
+  // n maps with 128-byte boxes (k_hash_tma), n with 64-byte boxes (k_hash_mma),
+  // n with chunk-sized 64-byte boxes (k_hash_mma at task edges; 8-32 pages/chunk)
+  const int ppc = 1 << (g.chunk_shift - g.page_shift);
+  const bool chunk_maps = ppc >= 8 && ppc <= 32;
+  std::vector<uint8_t> host(size_t(n) * (chunk_maps ? 384 : 256));
   if (snap::encode_tensor_maps(ctx->arena, addr, bytes, n, host.data(), 128) != 0) return;
   if (snap::encode_tensor_maps(ctx->arena, addr, bytes, n, host.data() + size_t(n) * 128, 64) != 0)
+    return;
+  if (chunk_maps && snap::encode_tensor_maps(ctx->arena, addr, bytes, n,
+                                             host.data() + size_t(n) * 256, 64, ppc,
+                                             ctx->arena_bytes) != 0)
     return;
   uint8_t* d;
   if (ensure(ctx, m, host.size(), &d) != SNAP_OK) return;
@@ -258,6 +266,7 @@ inline void build_tmaps(snap_ctx* ctx, DevMem& m, const uint64_t* addr, const ui
     return;
   g.tmaps = d;
   g.tmaps64 = d + size_t(n) * 128;
+  if (chunk_maps) g.tmaps64c = d + size_t(n) * 256;
 }
 
 inline int check_range(snap_ctx* ctx, uint64_t addr, uint64_t bytes) {

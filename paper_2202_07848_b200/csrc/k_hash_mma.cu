@@ -95,12 +95,13 @@ struct MmaCfg {
   static constexpr size_t SM_B = size_t(kBR) * kBBytes;
   static constexpr size_t SM_DIG = size_t(GP) * 8;
   static constexpr size_t SM_ZERO = 128;                // zero slab: LDS source for absent pages
+  static constexpr size_t SM_CTAB = size_t(CW) * TPW * 4 * 8;  // chunk-box (map, row) per task
   // FUSED: staging writes go out in SEG * SLAB-byte segments per page (default 256 B)
   // consecutive stages at a time (the load of the next stage into a slot is
   // then issued after the slot's store instead of before the compute)
   static constexpr int SEG = SEG_ ? SEG_ : (SLAB >= 256 ? 1 : 256 / SLAB);
   static constexpr int NBARS = CW * ST + NA + NA + NDB + NDB + kBR;
-  static constexpr size_t SMEM = 1024 + SM_DATA + SM_B + SM_DIG + SM_ZERO + NBARS * 8 + 16;
+  static constexpr size_t SMEM = 1024 + SM_DATA + SM_B + SM_DIG + SM_ZERO + SM_CTAB + NBARS * 8 + 16;
   static_assert(SMEM <= 232448, "shared memory");
 };
 // hash only: 1024 pages in flight per SM (2 chain pairs per thread, 2 warps
@@ -308,7 +309,8 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
   uint8_t* bring = smem + C::SM_DATA;
   uint64_t* dsm = reinterpret_cast<uint64_t*>(bring + C::SM_B);
   uint8_t* zero = reinterpret_cast<uint8_t*>(dsm + GP);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(zero + C::SM_ZERO);
+  uint32_t* ctab_all = reinterpret_cast<uint32_t*>(zero + C::SM_ZERO);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(zero + C::SM_ZERO + C::SM_CTAB);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + C::NBARS);
   const uint32_t bar_full = smem_u32(bars);              // [CW][ST]
   const uint32_t bar_afull = bar_full + 8 * CW * ST;     // [NA]
@@ -411,9 +413,15 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
     const uint64_t* htab = reinterpret_cast<const uint64_t*>(btab + kBTab);
 
     // producer state of the group being loaded
-    uint32_t p_reg = 0, p_map[TPW], p_row[TPW], p_len[TPW];
+    uint32_t p_reg = 0, p_chk = 0, p_nch[TPW], p_map[TPW], p_row[TPW], p_len[TPW];
+    // tasks that are not one 32-page run of one buffer load one TMA box per
+    // chunk (its buffer's chunk-box map, (map, row) per chunk in ctab)
+    const CUtensorMap* cmaps = static_cast<const CUtensorMap*>(g.tmaps64c);
+    const bool cbox = BOXW == 64 && C::NBOX == 1 && cmaps != nullptr;
+    uint32_t* ctab = ctab_all + warp * TPW * 8;
     const uint8_t* p_src[TPW];
-    uint32_t reg_bits[2] = {0, 0};  // per group parity: bit t = task t loaded by TMA 2D
+    uint32_t reg_bits[2] = {0, 0};   // per group parity: bit t = task t loaded by TMA 2D (swizzled)
+    uint32_t full_bits[2] = {0, 0};  // per group parity: bit t = task t is 32 full pages
     uint32_t ist = 0, cst = 0;
 
     auto page_info = [&](uint32_t i, int t, const uint8_t*& src, uint32_t& len, uint32_t& b,
@@ -450,6 +458,7 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
       const uint32_t s = p % C::STAGES;
       if (s == 0) {
         p_reg = 0;
+        p_chk = 0;
 #pragma unroll
         for (int t = 0; t < TPW; ++t) {
           uint32_t b, row;
@@ -460,8 +469,28 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
           if (__all_sync(kFull, b == b0 && p_len[t] == 4096 && row == r0 + lane)) p_reg |= 1u << t;
           p_map[t] = b0;
           p_row[t] = r0;
+          p_nch[t] = 0;
+          if (cbox && !((p_reg >> t) & 1)) {
+            const uint32_t halves = 32u >> ppc_shift;
+#pragma unroll
+            for (uint32_t hh = 0; hh < 4; ++hh) {
+              if (hh < halves) {
+                const int src = static_cast<int>(hh << ppc_shift);
+                const uint32_t bh = __shfl_sync(kFull, b, src);
+                const uint32_t rh = __shfl_sync(kFull, row, src);
+                const uint32_t vh = __shfl_sync(kFull, p_len[t] > 0 ? 1u : 0u, src);
+                if (lane == 0) {
+                  ctab[(t * 4 + hh) * 2] = vh ? bh : 0xffffffffu;
+                  ctab[(t * 4 + hh) * 2 + 1] = rh;
+                }
+                p_nch[t] += vh;
+              }
+            }
+            p_chk |= 1u << t;
+          }
         }
-        reg_bits[i & 1] = p_reg;
+        reg_bits[i & 1] = p_reg | p_chk;
+        full_bits[i & 1] = p_reg;
       }
       const uint32_t bar = fbar + 8 * st;
       const uint32_t dst = ring + st * C::WSTAGE;
@@ -483,13 +512,27 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
 #pragma unroll
       for (int t = 0; t < TPW; ++t) {
         vmask[t] = __ballot_sync(kFull, s * SLAB < p_len[t]);
-        tx += (p_reg >> t) & 1 ? uint32_t(C::TASKB) : __popc(vmask[t]) * SLAB;
+        tx += (p_reg >> t) & 1   ? uint32_t(C::TASKB)
+              : (p_chk >> t) & 1 ? p_nch[t] * (BOXW << ppc_shift)
+                                 : __popc(vmask[t]) * SLAB;
       }
       if (lane == 0) mbar_arrive_tx(bar, tx);
       __syncwarp();
 #pragma unroll
       for (int t = 0; t < TPW; ++t) {
-        if ((p_reg >> t) & 1) {
+        if ((p_chk >> t) & 1) {
+          // one box of ppc rows per chunk of the task (OOB rows read as zeros)
+          if (lane == 0) {
+            const uint32_t halves = 32u >> ppc_shift;
+            for (uint32_t hh = 0; hh < halves; ++hh) {
+              const uint32_t mb = ctab[(t * 4 + hh) * 2];
+              if (mb != 0xffffffffu)
+                tma_load_2d(dst + t * C::TASKB + (hh << ppc_shift) * BOXW, cmaps + mb,
+                            static_cast<int>(s * SLAB), static_cast<int>(ctab[(t * 4 + hh) * 2 + 1]),
+                            bar);
+            }
+          }
+        } else if ((p_reg >> t) & 1) {
           if (lane == 0)
 #pragma unroll
             for (int x = 0; x < C::NBOX; ++x)
@@ -543,7 +586,7 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
             }
           }
         }
-        c_full = reg_bits[i & 1] == (1u << TPW) - 1;
+        c_full = full_bits[i & 1] == (1u << TPW) - 1;
 #pragma unroll
         for (int q = 0; q < PAIRS; ++q) L[q] = 0x00250025u;  // l_0 = 0x25 in both lanes
       }

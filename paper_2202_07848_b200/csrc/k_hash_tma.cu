@@ -281,7 +281,8 @@ int launch_hash_tma(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
 // box 32 rows x 128 B, 128B swizzle). Buffers with no full page get an unused
 // zeroed entry (their tasks are irregular).
 int encode_tensor_maps(const uint8_t* arena, const uint64_t* addr, const uint64_t* bytes,
-                       uint32_t nbufs, void* host_maps /* nbufs x 128 B */, int box_bytes) {
+                       uint32_t nbufs, void* host_maps /* nbufs x 128 B */, int box_bytes,
+                       int box_rows, uint64_t arena_bytes) {
   using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                 const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                 const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -298,11 +299,14 @@ int encode_tensor_maps(const uint8_t* arena, const uint64_t* addr, const uint64_
   CUtensorMap* maps = static_cast<CUtensorMap*>(host_maps);
   for (uint32_t b = 0; b < nbufs; ++b) {
     std::memset(&maps[b], 0, sizeof(CUtensorMap));
-    const cuuint64_t rows = bytes[b] >> 12;
+    // arena_bytes != 0: the buffer's partial last page is a row too (its tail
+    // beyond the buffer is loaded but never hashed), if the row fits the arena
+    cuuint64_t rows = bytes[b] >> 12;
+    if (arena_bytes && (bytes[b] & 4095) && addr[b] + ((rows + 1) << 12) <= arena_bytes) ++rows;
     if (rows == 0) continue;
     const cuuint64_t dims[2] = {4096, rows};
     const cuuint64_t strides[1] = {4096};
-    const cuuint32_t box[2] = {cuuint32_t(box_bytes), 32};
+    const cuuint32_t box[2] = {cuuint32_t(box_bytes), cuuint32_t(box_rows)};
     const cuuint32_t estr[2] = {1, 1};
     CUresult r = encode(&maps[b], CU_TENSOR_MAP_DATA_TYPE_UINT8, 2,
                         const_cast<uint8_t*>(arena + addr[b]), dims, strides, box, estr,

@@ -39,6 +39,10 @@ struct GridDev {
   // boxes of 32 pages x 128 B (SWIZZLE_128B) and 32 pages x 64 B (SWIZZLE_64B)
   const void* tmaps = nullptr;
   const void* tmaps64 = nullptr;
+  // boxes of one chunk (pages per chunk in 8..32) x 64 B, rows include a
+  // partial last page: chunk-granular TMA loads where a 32-page task spans
+  // buffers or a buffer tail (k_hash_mma)
+  const void* tmaps64c = nullptr;
   // Single-GPU snapshot: the K2 insert pass fused into K1 — the lane that
   // finishes a chunk digest inserts it into `dd` (first occurrence by
   // atomicMin, skipped when `kn` holds it and kn_use) and records the slot in
@@ -83,8 +87,11 @@ void set_hash_variant(int v);
 const char* last_k1_name();
 // host: one 128-byte CUtensorMap per buffer into host_maps (box of 32 pages x
 // box_bytes, box_bytes 128 -> SWIZZLE_128B, 64 -> SWIZZLE_64B); 0 on success
+// box_rows rows per box; arena_bytes != 0: a partial last page counts as a row
+// (when it fits the arena), for chunk-sized boxes at buffer tails
 int encode_tensor_maps(const uint8_t* arena, const uint64_t* addr, const uint64_t* bytes,
-                       uint32_t nbufs, void* host_maps, int box_bytes = 128);
+                       uint32_t nbufs, void* host_maps, int box_bytes = 128, int box_rows = 32,
+                       uint64_t arena_bytes = 0);
 // Cross-GPU barrier after a fused-exchange K1: signal every peer (flag slot
 // `rank` of its window := epoch, release.sys) and wait for every peer's
 // signal in this rank's window (acquire.sys); traps after ~30 s.
