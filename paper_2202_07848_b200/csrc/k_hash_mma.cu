@@ -853,7 +853,13 @@ int launch_mma(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint64_t blocks = ngroups < uint64_t(sms) ? ngroups : uint64_t(sms);
+#ifdef SNAP_MMA_DEBUG_MODES
+  // timing-only modes (1: no chain, 2: no MMA; digests are wrong), build with
+  // make EXTRA=-DSNAP_MMA_DEBUG_MODES and set SNAP_MMA_DEBUG
   static const int dbg = getenv("SNAP_MMA_DEBUG") ? atoi(getenv("SNAP_MMA_DEBUG")) : 0;
+#else
+  const int dbg = 0;
+#endif
   k_hash_mma<C><<<unsigned(blocks), C::THREADS, C::SMEM, s>>>(arena, g, chunk_dig, bt, spec_off,
                                                                staging, dbg);
   return 1;
