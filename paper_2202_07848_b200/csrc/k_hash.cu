@@ -765,11 +765,10 @@ using WsC = WsCfg<12, 4, 4>;          // 12 hash + 4 copy warps, deeper ring
 template <class C>
 int launch_hash_ws(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
                    const uint64_t* spec_off, uint8_t* staging, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static uint64_t attr = 0;
+  once_per_device(attr, [] {
     cudaFuncSetAttribute(k_hash_ws<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem));
-    attr = true;
-  }
+  });
   const uint64_t c_end = g.c_end ? g.c_end : g.nchunks;
   if (c_end <= g.c_begin) return 0;
   const uint64_t ntasks = (((c_end - g.c_begin) << (g.chunk_shift - g.page_shift)) + 31) / 32;
@@ -784,13 +783,12 @@ int launch_hash_ws(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
 template <class C>
 int launch_hash_cfg(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
                     const uint64_t* spec_off, uint8_t* staging, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static uint64_t attr = 0;
+  once_per_device(attr, [] {
     cudaFuncSetAttribute(k_hash<C, 12, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem));
     cudaFuncSetAttribute(k_hash<C, 12, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem));
     cudaFuncSetAttribute(k_hash<C, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem));
-    attr = true;
-  }
+  });
   const uint64_t c_end = g.c_end ? g.c_end : g.nchunks;
   if (c_end <= g.c_begin) return 0;
   const uint64_t ntasks =

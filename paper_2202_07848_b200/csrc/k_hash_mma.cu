@@ -815,9 +815,11 @@ std::vector<uint8_t> make_btab() {
 
 const uint8_t* device_btab() {
   static const uint8_t* tabs[64] = {};
+  static std::mutex m;
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(m);
   if (!tabs[dev]) {
     const std::vector<uint8_t> h = make_btab();
     void* d = nullptr;
@@ -839,11 +841,10 @@ namespace {
 template <class C>
 int launch_mma(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
                const uint64_t* spec_off, uint8_t* staging, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static uint64_t attr = 0;
+  once_per_device(attr, [] {
     cudaFuncSetAttribute(k_hash_mma<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
-    attr = true;
-  }
+  });
   const uint64_t c_end = g.c_end ? g.c_end : g.nchunks;
   if (c_end <= g.c_begin) return 0;
   const uint8_t* bt = device_btab();

@@ -258,12 +258,11 @@ constexpr size_t kTmaSmem = size_t(kTmaWarps) * kTmaStages * kStageBytes +
 bool hash_tma_ok(const GridDev& g) { return g.tmaps != nullptr && g.page_shift == 12; }
 
 int launch_hash_tma(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static uint64_t attr = 0;
+  once_per_device(attr, [] {
     cudaFuncSetAttribute(k_hash_tma<kTmaWarps, kTmaStages>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTmaSmem));
-    attr = true;
-  }
+  });
   const uint64_t c_end = g.c_end ? g.c_end : g.nchunks;
   if (c_end <= g.c_begin) return 0;
   const uint64_t ntasks = (((c_end - g.c_begin) << (g.chunk_shift - g.page_shift)) + 31) / 32;

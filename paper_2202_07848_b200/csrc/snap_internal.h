@@ -5,12 +5,28 @@
 #include <nccl.h>
 #include <stdint.h>
 
+#include <mutex>
 #include <string>
 #include <vector>
 
 #include "snap.h"
 
 namespace snap {
+
+// Per-(kernel, device) one-time setup, e.g. cudaFuncSetAttribute (which only
+// applies to the current device): runs f() the first time this device is seen
+// for `done`. Thread-safe; a process may drive several GPUs (one ctx each).
+template <class F>
+void once_per_device(uint64_t& done, F&& f) {
+  static std::mutex m;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  std::lock_guard<std::mutex> lock(m);
+  if (done & bit) return;
+  f();
+  done |= bit;
+}
 
 constexpr uint64_t kFnvOffset = 14695981039346656037ull;  // sim.hpp:57
 constexpr uint32_t kFnvPrimeLo = 0x1b3u;                   // prime = 2^40 + 0x1b3 (sim.hpp:58)
