@@ -45,7 +45,7 @@ def test_ragged_golden_mma(mma, golden):
         assert [f"{x:016x}" for x in bd] == exp["bufs"]
 
 
-@pytest.mark.parametrize("chunk", [4096, 16384, 65536, 131072])
+@pytest.mark.parametrize("chunk", [4096, 8192, 16384, 32768, 65536, 131072])
 def test_random_layouts_mma(mma, chunk):
     rng = np.random.default_rng(chunk)
     arena_bytes = 96 << 20
