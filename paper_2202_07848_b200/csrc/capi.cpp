@@ -574,7 +574,9 @@ int snap_open(int device, uint64_t arena_bytes, snap_ctx** out) {
   if (cudaSetDevice(device) != cudaSuccess) return bail(SNAP_ECUDA);
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess)
     return bail(SNAP_ECUDA);
-  e = cudaMalloc(&ctx->arena, arena_bytes);
+  // + one page of padding: the tensor-core K1's arena-wide tensor maps may read
+  // a partial last page as a whole 4 KiB row (bytes past a buffer are never hashed)
+  e = cudaMalloc(&ctx->arena, arena_bytes + 4096);
   if (e != cudaSuccess) {
     cudaGetLastError();
     return bail(e == cudaErrorMemoryAllocation ? SNAP_ENOMEM : SNAP_ECUDA);

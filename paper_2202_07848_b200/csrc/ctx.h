@@ -246,17 +246,15 @@ inline void build_tmaps(snap_ctx* ctx, DevMem& m, const uint64_t* addr, const ui
   g.tmaps64 = nullptr;
   g.tmaps64c = nullptr;
   if (!snap::hash_tma_selected() || g.page_shift != 12 || n == 0) return;
-  // n maps with 128-byte boxes (k_hash_tma), n with 64-byte boxes (k_hash_mma),
-  // n with chunk-sized 64-byte boxes (k_hash_mma at task edges; 8-32 pages/chunk)
+  // n per-buffer maps with 128-byte boxes (k_hash_tma), then the arena-wide
+  // maps of k_hash_mma: 16 with 32-page boxes, 16 with chunk boxes (8-32 pages)
   const int ppc = 1 << (g.chunk_shift - g.page_shift);
   const bool chunk_maps = ppc >= 8 && ppc <= 32;
-  std::vector<uint8_t> host(size_t(n) * (chunk_maps ? 384 : 256));
+  std::vector<uint8_t> host(size_t(n) * 128 + 32 * 128);
   if (snap::encode_tensor_maps(ctx->arena, addr, bytes, n, host.data(), 128) != 0) return;
-  if (snap::encode_tensor_maps(ctx->arena, addr, bytes, n, host.data() + size_t(n) * 128, 64) != 0)
-    return;
-  if (chunk_maps && snap::encode_tensor_maps(ctx->arena, addr, bytes, n,
-                                             host.data() + size_t(n) * 256, 64, ppc,
-                                             ctx->arena_bytes) != 0)
+  uint8_t* a64 = host.data() + size_t(n) * 128;
+  if (snap::encode_arena_maps(ctx->arena, ctx->arena_bytes, 64, 32, a64) != 0) return;
+  if (chunk_maps && snap::encode_arena_maps(ctx->arena, ctx->arena_bytes, 64, ppc, a64 + 16 * 128) != 0)
     return;
   uint8_t* d;
   if (ensure(ctx, m, host.size(), &d) != SNAP_OK) return;
@@ -266,7 +264,7 @@ inline void build_tmaps(snap_ctx* ctx, DevMem& m, const uint64_t* addr, const ui
     return;
   g.tmaps = d;
   g.tmaps64 = d + size_t(n) * 128;
-  if (chunk_maps) g.tmaps64c = d + size_t(n) * 256;
+  if (chunk_maps) g.tmaps64c = d + size_t(n) * 128 + 16 * 128;
 }
 
 inline int check_range(snap_ctx* ctx, uint64_t addr, uint64_t bytes) {

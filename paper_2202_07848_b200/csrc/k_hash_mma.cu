@@ -109,10 +109,9 @@ struct MmaCfg {
 // shared memory. Fused, few chunks staged (multi-GPU striping, the default
 // when the predicted staging is < 70 % of the grid): the same geometry, each
 // stage's staged slabs written right after it is hashed (64-byte segments,
-// full prefetch depth). Variant 11 (8 warps x 1 pair, 128-byte slabs) is kept
-// selectable: 3-7 % slower on C2 at the N = 2..8 write fractions.
+// full prefetch depth). (Measured and dropped: 8 warps x 1 pair with 128-byte
+// slabs and 128/256-byte segments, 3-7 % slower at the N = 2..8 write fractions.)
 using MmaHash = MmaCfg<8, 2, 64, 3, false>;
-using MmaFused = MmaCfg<8, 1, 128, 3, true, 1>;
 using MmaFusedLight = MmaCfg<8, 2, 64, 3, true, 1>;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -402,8 +401,8 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
     // thread = pages (task 2p, task 2p+1) at its lane; TMEM pair set
     // (w / 4) * PAIRS + p in lanes 32 (w % 4) + lane
     constexpr int TPW = C::TPW, PAIRS = C::PAIRS, SLAB = C::SLAB, BOXW = C::BOXW;
-    const CUtensorMap* maps =
-        static_cast<const CUtensorMap*>(BOXW == 64 ? g.tmaps64 : g.tmaps);
+    static_assert(BOXW == 64, "the arena-wide maps have 64-byte boxes");
+    const CUtensorMap* maps = static_cast<const CUtensorMap*>(g.tmaps64);
     const uint32_t ring = smem_u32(smem + warp * ST * C::WSTAGE);
     const uint32_t fbar = bar_full + 8 * warp * ST;
     const uint32_t tl = static_cast<uint32_t>(32 * (warp & 3)) << 16;
@@ -464,11 +463,14 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
           uint32_t b, row;
           uint64_t gc;
           page_info(i, t, p_src[t], p_len[t], b, row, gc);
-          const uint32_t b0 = __shfl_sync(kFull, b, 0);
-          const uint32_t r0 = __shfl_sync(kFull, row, 0);
-          if (__all_sync(kFull, b == b0 && p_len[t] == 4096 && row == r0 + lane)) p_reg |= 1u << t;
-          p_map[t] = b0;
-          p_row[t] = r0;
+          // arena-wide maps: a page at arena offset a is row a >> 12 of the
+          // map of its 256-B alignment class (a >> 8) & 15
+          const uint64_t ao = p_len[t] ? static_cast<uint64_t>(p_src[t] - arena) : 0;
+          const uint64_t a0 = __shfl_sync(kFull, ao, 0);
+          if (__all_sync(kFull, p_len[t] == 4096 && ao == a0 + uint64_t(lane) * 4096))
+            p_reg |= 1u << t;
+          p_map[t] = static_cast<uint32_t>(a0 >> 8) & 15u;
+          p_row[t] = static_cast<uint32_t>(a0 >> 12);
           p_nch[t] = 0;
           if (cbox && !((p_reg >> t) & 1)) {
             const uint32_t halves = 32u >> ppc_shift;
@@ -476,12 +478,11 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
             for (uint32_t hh = 0; hh < 4; ++hh) {
               if (hh < halves) {
                 const int src = static_cast<int>(hh << ppc_shift);
-                const uint32_t bh = __shfl_sync(kFull, b, src);
-                const uint32_t rh = __shfl_sync(kFull, row, src);
+                const uint64_t ah = __shfl_sync(kFull, ao, src);
                 const uint32_t vh = __shfl_sync(kFull, p_len[t] > 0 ? 1u : 0u, src);
                 if (lane == 0) {
-                  ctab[(t * 4 + hh) * 2] = vh ? bh : 0xffffffffu;
-                  ctab[(t * 4 + hh) * 2 + 1] = rh;
+                  ctab[(t * 4 + hh) * 2] = vh ? static_cast<uint32_t>(ah >> 8) & 15u : 0xffffffffu;
+                  ctab[(t * 4 + hh) * 2 + 1] = static_cast<uint32_t>(ah >> 12);
                 }
                 p_nch[t] += vh;
               }
@@ -833,7 +834,7 @@ const uint8_t* device_btab() {
 }  // namespace
 
 bool hash_mma_ok(const GridDev& g) {
-  return g.tmaps64 != nullptr && g.tmaps != nullptr && g.page_shift == 12 && g.chunk_shift >= 12 &&
+  return g.tmaps64 != nullptr && g.page_shift == 12 && g.chunk_shift >= 12 &&
          g.chunk_shift <= 17;
 }
 
@@ -872,9 +873,8 @@ int launch_hash_mma(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
 }
 
 int launch_hash_mma_fused(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
-                          const uint64_t* spec_off, uint8_t* staging, cudaStream_t s, bool light) {
-  if (light) return launch_mma<MmaFusedLight>(arena, g, chunk_dig, spec_off, staging, s);
-  return launch_mma<MmaFused>(arena, g, chunk_dig, spec_off, staging, s);
+                          const uint64_t* spec_off, uint8_t* staging, cudaStream_t s) {
+  return launch_mma<MmaFusedLight>(arena, g, chunk_dig, spec_off, staging, s);
 }
 
 }  // namespace snap

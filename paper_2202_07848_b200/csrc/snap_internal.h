@@ -51,13 +51,13 @@ struct GridDev {
   // snapshot hash each slab as soon as its H2D copy lands
   uint64_t c_begin = 0;
   uint64_t c_end = 0;
-  // per-buffer CUtensorMap arrays in device memory (4 KiB pages), or nullptr:
-  // boxes of 32 pages x 128 B (SWIZZLE_128B) and 32 pages x 64 B (SWIZZLE_64B)
+  // per-buffer CUtensorMap array in device memory (4 KiB pages), or nullptr:
+  // boxes of 32 pages x 128 B (SWIZZLE_128B, k_hash_tma)
   const void* tmaps = nullptr;
+  // arena-wide maps (16 alignment classes, encode_arena_maps) with 64-byte
+  // boxes (SWIZZLE_64B) of 32 pages (task loads) and of one chunk (pages per
+  // chunk 8..32: tasks spanning buffers or buffer tails), for k_hash_mma
   const void* tmaps64 = nullptr;
-  // boxes of one chunk (pages per chunk in 8..32) x 64 B, rows include a
-  // partial last page: chunk-granular TMA loads where a 32-page task spans
-  // buffers or a buffer tail (k_hash_mma)
   const void* tmaps64c = nullptr;
   // Single-GPU snapshot: the K2 insert pass fused into K1 — the lane that
   // finishes a chunk digest inserts it into `dd` (first occurrence by
@@ -92,17 +92,19 @@ int launch_hash_tma(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
 // cores + the linear part as a tcgen05 int8 MMA); needs the grid tensor maps.
 bool hash_mma_ok(const GridDev& g);
 int launch_hash_mma(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig, cudaStream_t s);
-// the same with the speculative K3 stores fused (spec_off / staging as launch_hash);
-// light: geometry for few staged chunks (hash-only chain count, 128-B segments)
+// the same with the speculative K3 stores fused (spec_off / staging as launch_hash),
+// for grids where few chunks are staged (multi-GPU striping)
 int launch_hash_mma_fused(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
-                          const uint64_t* spec_off, uint8_t* staging, cudaStream_t s,
-                          bool light);
+                          const uint64_t* spec_off, uint8_t* staging, cudaStream_t s);
 // K1 kernel policy override (SNAP_HASH_VARIANT semantics; -1 = default policy)
 void set_hash_variant(int v);
 // name of the K1 kernel the last launch_hash call chose (process-wide)
 const char* last_k1_name();
 // host: one 128-byte CUtensorMap per buffer into host_maps (box of 32 pages x
 // box_bytes, box_bytes 128 -> SWIZZLE_128B, 64 -> SWIZZLE_64B); 0 on success
+// 16 arena-wide maps (one per 256-B alignment class of a page start), see k_hash_tma.cu
+int encode_arena_maps(const uint8_t* arena, uint64_t arena_bytes, int box_bytes, int box_rows,
+                      void* host_maps);
 // box_rows rows per box; arena_bytes != 0: a partial last page counts as a row
 // (when it fits the arena), for chunk-sized boxes at buffer tails
 int encode_tensor_maps(const uint8_t* arena, const uint64_t* addr, const uint64_t* bytes,
