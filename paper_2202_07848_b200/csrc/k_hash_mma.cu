@@ -95,7 +95,7 @@ struct MmaCfg {
   static constexpr size_t SM_B = size_t(kBR) * kBBytes;
   static constexpr size_t SM_DIG = size_t(GP) * 8;
   static constexpr size_t SM_ZERO = 128;                // zero slab: LDS source for absent pages
-  static constexpr size_t SM_CTAB = size_t(CW) * TPW * 4 * 8;  // chunk-box (map, row) per task
+  static constexpr size_t SM_CTAB = size_t(CW) * TPW * 4 * 16;  // per-warp TMA issue plan
   // FUSED: staging writes go out in SEG * SLAB-byte segments per page (default 256 B)
   // consecutive stages at a time (the load of the next stage into a slot is
   // then issued after the slot's store instead of before the compute)
@@ -412,12 +412,16 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
     const uint64_t* htab = reinterpret_cast<const uint64_t*>(btab + kBTab);
 
     // producer state of the group being loaded
-    uint32_t p_reg = 0, p_chk = 0, p_nch[TPW], p_map[TPW], p_row[TPW], p_len[TPW];
+    uint32_t p_reg = 0, p_chk = 0, p_map[TPW], p_row[TPW], p_len[TPW];
     // tasks that are not one 32-page run of one buffer load one TMA box per
     // chunk (its buffer's chunk-box map, (map, row) per chunk in ctab)
     const CUtensorMap* cmaps = static_cast<const CUtensorMap*>(g.tmaps64c);
     const bool cbox = BOXW == 64 && C::NBOX == 1 && cmaps != nullptr;
-    uint32_t* ctab = ctab_all + warp * TPW * 8;
+    // per-group TMA issue plan of a warp whose tasks are not all regular: up to
+    // TPW * 4 boxes {map pointer, row, stage offset}, issued by lane 0 each stage
+    uint32_t* plan = ctab_all + warp * TPW * 16;
+    uint32_t p_nplan = 0, p_tx = 0;
+    bool p_generic = false;  // some task needs per-page bulk copies
     const uint8_t* p_src[TPW];
     uint32_t reg_bits[2] = {0, 0};   // per group parity: bit t = task t loaded by TMA 2D (swizzled)
     uint32_t full_bits[2] = {0, 0};  // per group parity: bit t = task t is 32 full pages
@@ -471,27 +475,54 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
             p_reg |= 1u << t;
           p_map[t] = static_cast<uint32_t>(a0 >> 8) & 15u;
           p_row[t] = static_cast<uint32_t>(a0 >> 12);
-          p_nch[t] = 0;
-          if (cbox && !((p_reg >> t) & 1)) {
-            const uint32_t halves = 32u >> ppc_shift;
-#pragma unroll
-            for (uint32_t hh = 0; hh < 4; ++hh) {
-              if (hh < halves) {
-                const int src = static_cast<int>(hh << ppc_shift);
-                const uint64_t ah = __shfl_sync(kFull, ao, src);
-                const uint32_t vh = __shfl_sync(kFull, p_len[t] > 0 ? 1u : 0u, src);
-                if (lane == 0) {
-                  ctab[(t * 4 + hh) * 2] = vh ? static_cast<uint32_t>(ah >> 8) & 15u : 0xffffffffu;
-                  ctab[(t * 4 + hh) * 2 + 1] = static_cast<uint32_t>(ah >> 12);
-                }
-                p_nch[t] += vh;
-              }
-            }
-            p_chk |= 1u << t;
-          }
+          if (cbox && !((p_reg >> t) & 1)) p_chk |= 1u << t;  // one box per chunk
         }
         reg_bits[i & 1] = p_reg | p_chk;
         full_bits[i & 1] = p_reg;
+        // issue plan (uniform): one box per regular task, one per valid chunk
+        // of a chunk-box task; per-page bulk copies otherwise (generic path)
+        p_generic = (p_reg | p_chk) != (1u << TPW) - 1;
+        p_nplan = 0;
+        p_tx = 0;
+        if (p_reg != (1u << TPW) - 1 && !p_generic) {
+#pragma unroll
+          for (int t = 0; t < TPW; ++t) {
+            const uint64_t ao = p_len[t] ? static_cast<uint64_t>(p_src[t] - arena) : 0;
+            if ((p_reg >> t) & 1) {
+              if (lane == 0) {
+                const uint64_t mp = reinterpret_cast<uint64_t>(maps + p_map[t]);
+                plan[p_nplan * 4] = static_cast<uint32_t>(mp);
+                plan[p_nplan * 4 + 1] = static_cast<uint32_t>(mp >> 32);
+                plan[p_nplan * 4 + 2] = p_row[t];
+                plan[p_nplan * 4 + 3] = t * C::TASKB;
+              }
+              ++p_nplan;
+              p_tx += C::TASKB;
+            } else {
+              const uint32_t halves = 32u >> ppc_shift;
+#pragma unroll
+              for (uint32_t hh = 0; hh < 4; ++hh) {
+                if (hh < halves) {
+                  const int src = static_cast<int>(hh << ppc_shift);
+                  const uint64_t ah = __shfl_sync(kFull, ao, src);
+                  const uint32_t vh = __shfl_sync(kFull, p_len[t] > 0 ? 1u : 0u, src);
+                  if (vh) {
+                    if (lane == 0) {
+                      const uint64_t mp =
+                          reinterpret_cast<uint64_t>(cmaps + (static_cast<uint32_t>(ah >> 8) & 15u));
+                      plan[p_nplan * 4] = static_cast<uint32_t>(mp);
+                      plan[p_nplan * 4 + 1] = static_cast<uint32_t>(mp >> 32);
+                      plan[p_nplan * 4 + 2] = static_cast<uint32_t>(ah >> 12);
+                      plan[p_nplan * 4 + 3] = t * C::TASKB + (hh << ppc_shift) * BOXW;
+                    }
+                    ++p_nplan;
+                    p_tx += BOXW << ppc_shift;
+                  }
+                }
+              }
+            }
+          }
+        }
       }
       const uint32_t bar = fbar + 8 * st;
       const uint32_t dst = ring + st * C::WSTAGE;
@@ -508,32 +539,30 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
         }
         return;
       }
+      if (!p_generic) {
+        // mixed regular / chunk-box group: the plan, one elected lane
+        if (lane == 0) {
+          mbar_arrive_tx(bar, p_tx);
+          for (uint32_t e = 0; e < p_nplan; ++e) {
+            const uint4 pe = *reinterpret_cast<const uint4*>(plan + e * 4);
+            const void* mp = reinterpret_cast<const void*>((uint64_t(pe.y) << 32) | pe.x);
+            tma_load_2d(dst + pe.w, mp, static_cast<int>(s * SLAB), static_cast<int>(pe.z), bar);
+          }
+        }
+        return;
+      }
       uint32_t tx = 0;
       uint32_t vmask[TPW];
 #pragma unroll
       for (int t = 0; t < TPW; ++t) {
         vmask[t] = __ballot_sync(kFull, s * SLAB < p_len[t]);
-        tx += (p_reg >> t) & 1   ? uint32_t(C::TASKB)
-              : (p_chk >> t) & 1 ? p_nch[t] * (BOXW << ppc_shift)
-                                 : __popc(vmask[t]) * SLAB;
+        tx += (p_reg >> t) & 1 ? uint32_t(C::TASKB) : __popc(vmask[t]) * SLAB;
       }
       if (lane == 0) mbar_arrive_tx(bar, tx);
       __syncwarp();
 #pragma unroll
       for (int t = 0; t < TPW; ++t) {
-        if ((p_chk >> t) & 1) {
-          // one box of ppc rows per chunk of the task (OOB rows read as zeros)
-          if (lane == 0) {
-            const uint32_t halves = 32u >> ppc_shift;
-            for (uint32_t hh = 0; hh < halves; ++hh) {
-              const uint32_t mb = ctab[(t * 4 + hh) * 2];
-              if (mb != 0xffffffffu)
-                tma_load_2d(dst + t * C::TASKB + (hh << ppc_shift) * BOXW, cmaps + mb,
-                            static_cast<int>(s * SLAB), static_cast<int>(ctab[(t * 4 + hh) * 2 + 1]),
-                            bar);
-            }
-          }
-        } else if ((p_reg >> t) & 1) {
+        if ((p_reg >> t) & 1) {
           if (lane == 0)
 #pragma unroll
             for (int x = 0; x < C::NBOX; ++x)
