@@ -67,7 +67,7 @@ constexpr size_t kBTabAll = kBTab + (17 + 17 + 1) * 8;
 // PAIRS chain pairs per thread, SLAB bytes of each page per data stage (TMA
 // boxes of 32 pages x BOXW bytes, SWIZZLE_64B / _128B), ST-deep ring per
 // warp, FUSED: also write every predicted-staged chunk's slab to staging.
-template <int CW_, int PAIRS_, int SLAB_, int ST_, bool FUSED_, int SEG_ = 0>
+template <int CW_, int PAIRS_, int SLAB_, int ST_, bool FUSED_>
 struct MmaCfg {
   static constexpr int CW = CW_, PAIRS = PAIRS_, SLAB = SLAB_, ST = ST_;
   static constexpr bool FUSED = FUSED_;
@@ -95,11 +95,9 @@ struct MmaCfg {
   static constexpr size_t SM_B = size_t(kBR) * kBBytes;
   static constexpr size_t SM_DIG = size_t(GP) * 8;
   static constexpr size_t SM_ZERO = 128;                // zero slab: LDS source for absent pages
-  static constexpr size_t SM_CTAB = size_t(CW) * TPW * 4 * 16;  // per-warp TMA issue plan
-  // FUSED: staging writes go out in SEG * SLAB-byte segments per page (default 256 B)
+  static constexpr size_t SM_CTAB = size_t(CW) * (TPW * 16 + 4) * 4;  // per-warp TMA issue plan
   // consecutive stages at a time (the load of the next stage into a slot is
   // then issued after the slot's store instead of before the compute)
-  static constexpr int SEG = SEG_ ? SEG_ : (SLAB >= 256 ? 1 : 256 / SLAB);
   static constexpr int NBARS = CW * ST + NA + NA + NDB + NDB + kBR;
   static constexpr size_t SMEM = 1024 + SM_DATA + SM_B + SM_DIG + SM_ZERO + SM_CTAB + NBARS * 8 + 16;
   static_assert(SMEM <= 232448, "shared memory");
@@ -112,7 +110,7 @@ struct MmaCfg {
 // full prefetch depth). (Measured and dropped: 8 warps x 1 pair with 128-byte
 // slabs and 128/256-byte segments, 3-7 % slower at the N = 2..8 write fractions.)
 using MmaHash = MmaCfg<8, 2, 64, 3, false>;
-using MmaFusedLight = MmaCfg<8, 2, 64, 3, true, 1>;
+using MmaFusedLight = MmaCfg<8, 2, 64, 3, true>;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -419,9 +417,8 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
     const bool cbox = BOXW == 64 && C::NBOX == 1 && cmaps != nullptr;
     // per-group TMA issue plan of a warp whose tasks are not all regular: up to
     // TPW * 4 boxes {map pointer, row, stage offset}, issued by lane 0 each stage
-    uint32_t* plan = ctab_all + warp * TPW * 16;
-    uint32_t p_nplan = 0, p_tx = 0;
-    bool p_generic = false;  // some task needs per-page bulk copies
+    // (entry 0 of the table: {count, tx bytes}; boxes from entry 1)
+    uint32_t* plan = ctab_all + warp * (TPW * 16 + 4);
     const uint8_t* p_src[TPW];
     uint32_t reg_bits[2] = {0, 0};   // per group parity: bit t = task t loaded by TMA 2D (swizzled)
     uint32_t full_bits[2] = {0, 0};  // per group parity: bit t = task t is 32 full pages
@@ -481,10 +478,8 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
         full_bits[i & 1] = p_reg;
         // issue plan (uniform): one box per regular task, one per valid chunk
         // of a chunk-box task; per-page bulk copies otherwise (generic path)
-        p_generic = (p_reg | p_chk) != (1u << TPW) - 1;
-        p_nplan = 0;
-        p_tx = 0;
-        if (p_reg != (1u << TPW) - 1 && !p_generic) {
+        uint32_t p_nplan = 1, p_tx = 0;
+        if (p_reg != (1u << TPW) - 1 && (p_reg | p_chk) == (1u << TPW) - 1) {
 #pragma unroll
           for (int t = 0; t < TPW; ++t) {
             const uint64_t ao = p_len[t] ? static_cast<uint64_t>(p_src[t] - arena) : 0;
@@ -522,6 +517,10 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
               }
             }
           }
+          if (lane == 0) {
+            plan[0] = p_nplan - 1;
+            plan[1] = p_tx;
+          }
         }
       }
       const uint32_t bar = fbar + 8 * st;
@@ -539,11 +538,12 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
         }
         return;
       }
-      if (!p_generic) {
+      if ((p_reg | p_chk) == (1u << TPW) - 1) {
         // mixed regular / chunk-box group: the plan, one elected lane
         if (lane == 0) {
-          mbar_arrive_tx(bar, p_tx);
-          for (uint32_t e = 0; e < p_nplan; ++e) {
+          const uint32_t np = plan[0];
+          mbar_arrive_tx(bar, plan[1]);
+          for (uint32_t e = 1; e <= np; ++e) {
             const uint4 pe = *reinterpret_cast<const uint4*>(plan + e * 4);
             const void* mp = reinterpret_cast<const void*>((uint64_t(pe.y) << 32) | pe.x);
             tma_load_2d(dst + pe.w, mp, static_cast<int>(s * SLAB), static_cast<int>(pe.z), bar);
@@ -579,10 +579,6 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
 
 #pragma unroll
     for (int p = 0; p < ST - 1; ++p) issue(p);
-    // SEG > 1: a slot's next load is issued after its stage's store (the store
-    // needs SEG consecutive stages resident)
-    constexpr bool kLate = C::FUSED && C::SEG > 1;
-    if constexpr (kLate) issue(ST - 1);
 
     uint32_t c_len[TPW];
     uint8_t* c_dst[TPW];  // FUSED: staging address of this lane's page, or null
@@ -594,7 +590,7 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
     const uint32_t swz = static_cast<uint32_t>(BOXW == 128 ? (lane & 7) : ((lane >> 1) & 3)) << 4;
     uint32_t ph_full = 0;  // parity of the data ring's current wrap
     for (uint32_t p = 0; p < nst; ++p) {
-      if constexpr (!kLate) issue(p + ST - 1);
+      issue(p + ST - 1);
       const uint32_t st = cst;
       cst = cst + 1 == ST ? 0 : cst + 1;
       const uint32_t i = p / C::STAGES;
@@ -682,40 +678,28 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
         mbar_arrive(bar_afull + 8 * ab);
       }
       if constexpr (C::FUSED) {
-        // speculative compaction: every page of a predicted-staged chunk
-        // writes the last SEG stages' slabs (SEG * SLAB = 256 contiguous
-        // bytes) to staging, 16 lanes per page (coalesced), read back from
-        // the shared-memory ring; then the slot of stage p - SEG + 1 is free
-        if (s % C::SEG == C::SEG - 1) {
-          constexpr int UPS = C::SEG * C::UNITS;  // 16-B units per page segment
-          constexpr int PPI = 32 / UPS;
-          const uint32_t x = lane % UPS, jj = lane / UPS;
-          const uint32_t xs = x / C::UNITS, xu = x % C::UNITS;  // sub-stage, unit in the slab
-          // ring slot of sub-stage xs (stage p - SEG + 1 + xs)
-          const uint32_t sl = (st + ST - (C::SEG - 1) + xs) % ST;
-          const uint32_t s0 = s - (C::SEG - 1);
-          const uint32_t rb = reg_bits[i & 1];
+        // speculative compaction: every page of a predicted-staged chunk writes
+        // this stage's slab to staging, UNITS lanes per page (coalesced
+        // SLAB-byte segments), read back from the shared-memory stage before
+        // the slot is refilled
+        constexpr int PPI = 32 / C::UNITS;
+        const uint32_t x = lane % C::UNITS, jj = lane / C::UNITS;
+        const uint32_t rb = reg_bits[i & 1];
 #pragma unroll
-          for (int t = 0; t < TPW; ++t) {
-            const uint32_t vm = __ballot_sync(kFull, c_dst[t] != nullptr && s0 * SLAB < c_len[t]);
-            if (vm == 0) continue;
-            const uint32_t tb = ring + sl * C::WSTAGE + t * C::TASKB;
+        for (int t = 0; t < TPW; ++t) {
+          const uint32_t vm = __ballot_sync(kFull, c_dst[t] != nullptr && s * SLAB < c_len[t]);
+          if (vm == 0) continue;
+          const uint32_t tb = ring + st * C::WSTAGE + t * C::TASKB;
 #pragma unroll
-            for (int k = 0; k < 32 / PPI; ++k) {
-              const uint32_t j = k * PPI + jj;
-              uint8_t* d = reinterpret_cast<uint8_t*>(
-                  __shfl_sync(kFull, reinterpret_cast<uint64_t>(c_dst[t]), j));
-              if ((vm >> j) & 1) {
-                const uint32_t sw = (rb >> t) & 1 ? (BOXW == 128 ? (j & 7) : ((j >> 1) & 3)) : 0u;
-                const uint32_t a = tb + (xu / C::UPB) * C::SUB + j * BOXW + (((xu % C::UPB) ^ sw) << 4);
-                st_stream16(d + s0 * SLAB + x * 16, ld_shared16(a));
-              }
+          for (int k = 0; k < 32 / PPI; ++k) {
+            const uint32_t j = k * PPI + jj;
+            uint8_t* d = reinterpret_cast<uint8_t*>(
+                __shfl_sync(kFull, reinterpret_cast<uint64_t>(c_dst[t]), j));
+            if ((vm >> j) & 1) {
+              const uint32_t sw = (rb >> t) & 1 ? ((j >> 1) & 3) : 0u;  // SWIZZLE_64B row j
+              st_stream16(d + s * SLAB + x * 16, ld_shared16(tb + j * BOXW + ((x ^ sw) << 4)));
             }
           }
-          __syncwarp();
-#pragma unroll
-          if constexpr (kLate)
-            for (int k = 0; k < C::SEG; ++k) issue(p + ST - (C::SEG - 1) + k);
         }
       }
       __syncwarp();  // the stage slot is refilled by this warp's next issue
