@@ -33,13 +33,17 @@
 // short page's end, where u = l makes every term vanish). Bit-exact with the
 // reference digest: tests compare every chunk digest with the oracle.
 //
-// CTA = 4 compute warps (threads 0..127 = TMEM lanes 0..127; each thread
-// owns 4 pages = 2 chain pairs) + 1 MMA warp. Group = 512 page slots
-// (16 chunk-aligned tasks of 32 pages); warp w owns tasks 4w..4w+3 and loads
-// them itself (TMA 2D box of 32 pages x 128 B per regular task, 1D bulk per
-// page otherwise) into a 3-stage ring. Per 64 byte-steps the warps write
-// 2 x 64 TMEM columns (3-deep ring) and the MMA warp issues 2 x 8 MMAs
-// (M=128, N=16, K=32, kind::i8, A from TMEM) into per-group accumulators.
+// CTA = 8 compute warps (threads 0..255; warp w writes TMEM lanes 32 (w % 4)
+// + lane; each thread owns 4 pages = 2 chain pairs) + 1 MMA warp. Group =
+// 1024 page slots (32 chunk-aligned tasks of 32 pages); warp w owns 4 tasks and
+// loads them itself into a 3-stage ring (64-byte slabs): one TMA 2D box of
+// 32 rows x 64 B per task that is contiguous in memory, one box per chunk
+// otherwise (16 arena-wide tensor maps, one per 256-byte alignment class of a
+// page start), per-page bulk copies only for chunk sizes below 8 pages. Per
+// 32 byte-steps the warps write 4 pair-sets x 32 TMEM columns (3-deep ring)
+// and the MMA warp issues 16 MMAs (M=128, N=16, K=32, kind::i8, A from TMEM)
+// into double-buffered accumulators. The fused variant also stores each
+// hashed slab of a predicted-staged page to the staging image.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -96,8 +100,6 @@ struct MmaCfg {
   static constexpr size_t SM_DIG = size_t(GP) * 8;
   static constexpr size_t SM_ZERO = 128;                // zero slab: LDS source for absent pages
   static constexpr size_t SM_CTAB = size_t(CW) * (TPW * 16 + 4) * 4;  // per-warp TMA issue plan
-  // consecutive stages at a time (the load of the next stage into a slot is
-  // then issued after the slot's store instead of before the compute)
   static constexpr int NBARS = CW * ST + NA + NA + NDB + NDB + kBR;
   static constexpr size_t SMEM = 1024 + SM_DATA + SM_B + SM_DIG + SM_ZERO + SM_CTAB + NBARS * 8 + 16;
   static_assert(SMEM <= 232448, "shared memory");
