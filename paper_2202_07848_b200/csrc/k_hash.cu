@@ -826,7 +826,7 @@ const char* last_k1_name();
 // tensor maps are built for every grid unless a cp.async variant is forced
 bool hash_tma_selected() {
   const int v = hash_variant();
-  return v == 10 || v == 11 || v == 12 || v == 99;
+  return v == 10 || v == 11 || v == 12 || v == 13 || v == 99;
 }
 
 // The K1 kernel a launch uses (SNAP_HASH_VARIANT / snap_set_k1_variant force
@@ -839,7 +839,7 @@ bool hash_tma_selected() {
 //    buffer shapes, tools/hash_variants.py): the TMA tensor-load kernel beats
 //    the cp.async CfgA by 1-2 % on every shape; two chains per lane (CfgB) win
 //    by another 1 % on very large buffers but lose 14 % on small tensors.
-enum class K1 { A, B, C, D, E, F, WsA, WsB, WsC, Tma, Mma, MmaFL };
+enum class K1 { A, B, C, D, E, F, WsA, WsB, WsC, Tma, Mma, MmaFL, TmaF };
 K1 choose_k1(const GridDev& g, const uint64_t* spec_off) {
   switch (hash_variant()) {
     case 1: return K1::B;
@@ -851,6 +851,9 @@ K1 choose_k1(const GridDev& g, const uint64_t* spec_off) {
     case 7: return K1::E;
     case 8: return K1::F;
     case 9: return K1::A;
+    case 13:  // fused: TMA-load FNV kernel (CfgE geometry)
+      if (spec_off) return hash_tma_ok(g) ? K1::TmaF : K1::E;
+      return hash_tma_ok(g) ? K1::Tma : K1::A;
     case 11:
     case 12:  // the tensor-core kernels for every launch (hash only and fused)
       if (spec_off) return hash_mma_ok(g) ? K1::MmaFL : K1::E;
@@ -898,6 +901,7 @@ int launch_k1(K1 k, const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
     case K1::Tma: return launch_hash_tma(arena, g, chunk_dig, s);
     case K1::Mma: return launch_hash_mma(arena, g, chunk_dig, s);
     case K1::MmaFL: return launch_hash_mma_fused(arena, g, chunk_dig, spec_off, staging, s);
+    case K1::TmaF: return launch_hash_tma_fused(arena, g, chunk_dig, spec_off, staging, s);
   }
   return 0;
 }
@@ -918,6 +922,7 @@ const char* k1_name(K1 k) {
     case K1::Tma: return "k_hash_tma (FNV chain, TMA loads)";
     case K1::Mma: return "k_hash_mma (tensor-core FNV, hash only)";
     case K1::MmaFL: return "k_hash_mma fused-light (tensor-core FNV + fused K3 stores)";
+    case K1::TmaF: return "k_hash_tma_fused (FNV chain, TMA loads + fused K3 stores)";
   }
   return "?";
 }
@@ -929,7 +934,7 @@ int launch_hash(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
   const K1 k = choose_k1(g, spec_off);
   g_last_k1 = k1_name(k);
   const bool epilogue = !(k == K1::WsA || k == K1::WsB || k == K1::WsC || k == K1::Tma || k == K1::Mma ||
-                          k == K1::MmaFL);
+                          k == K1::MmaFL || k == K1::TmaF);
   if (!g.dd.keys || epilogue) return launch_k1(k, arena, g, chunk_dig, spec_off, staging, s);
   GridDev h = g;
   h.dd = TableDev{};

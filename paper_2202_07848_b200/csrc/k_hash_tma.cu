@@ -249,6 +249,199 @@ k_hash_tma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
   if (g.xdig != nullptr) __threadfence_system();
 }
 
+
+// Fused K1 (hash + speculative K3 stores) with TMA tensor loads: CfgE's
+// geometry (12 warps, 2 stages, 256-byte slabs per page = two 32 x 128 B
+// SWIZZLE_128B boxes per task) without the per-lane cp.async address math.
+// After a stage is hashed, the warp writes the slabs of its predicted-staged
+// pages to staging + spec_off[chunk] + page offset, 16 lanes per page
+// (256 contiguous bytes), read back from the swizzled stage.
+template <int WARPS, int ST>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+k_hash_tma_fused(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ chunk_dig,
+                 const uint64_t* __restrict__ spec_off, uint8_t* __restrict__ staging) {
+  constexpr uint32_t page_shift = 12, SLAB = 256, ns = 4096 / SLAB;  // 16 stages per page
+  constexpr uint32_t kStage = 32 * SLAB;                             // 2 boxes of 4 KiB
+  constexpr uint64_t pb = 1ull << page_shift;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t wbuf_u = smem_u32(smem + warp * ST * kStage);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * ST * kStage) + warp * ST;
+  const uint32_t bar0 = smem_u32(bars);
+  const CUtensorMap* maps = static_cast<const CUtensorMap*>(g.tmaps);
+
+  const uint32_t ppc_shift = g.chunk_shift - page_shift;
+  const uint64_t c_end = g.c_end ? g.c_end : g.nchunks;
+  const uint64_t slot_base = g.c_begin << ppc_shift;
+  const uint64_t nslots = (c_end - g.c_begin) << ppc_shift;
+  const uint64_t ntasks = (nslots + 31) >> 5;
+  const uint64_t gw = uint64_t(blockIdx.x) * WARPS + warp;
+  const uint64_t nw = uint64_t(gridDim.x) * WARPS;
+  if (gw >= ntasks) return;
+  const uint64_t nsteps = ((ntasks - gw + nw - 1) / nw) * ns;
+
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < ST; ++s) mbar_init(bar0 + 8 * s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+
+  auto page = [&](uint64_t i, const uint8_t*& src, uint32_t& len, uint32_t& b, uint32_t& row,
+                  uint64_t& gc) {
+    const uint64_t slot = slot_base + (gw + i * nw) * 32 + lane;
+    gc = slot >> ppc_shift;
+    b = 0xffffffffu;
+    row = 0;
+    src = nullptr;
+    len = 0;
+    if (gc < c_end) {
+      b = find_buf(g, gc);
+      const uint64_t k = gc - __ldg(g.cstart + b);
+      const uint64_t off = (k << g.chunk_shift) + ((slot & ((1u << ppc_shift) - 1)) << page_shift);
+      const uint64_t bytes = __ldg(g.bytes + b);
+      if (off < bytes) {
+        const uint64_t rem = bytes - off;
+        len = static_cast<uint32_t>(rem < pb ? rem : pb);
+        src = arena + __ldg(g.addr + b) + off;
+        row = static_cast<uint32_t>(off >> page_shift);
+      }
+    }
+  };
+
+  bool p_reg = false;
+  uint32_t p_map = 0, p_row = 0, p_len = 0;
+  const uint8_t* p_src = nullptr;
+  uint32_t reg_bits = 0;  // bit (i & 1): task i was loaded through the tensor path
+  uint32_t ist = 0, cst = 0;
+
+  auto issue = [&](uint64_t p) {
+    const uint32_t st = ist;
+    ist = ist + 1 == ST ? 0 : ist + 1;
+    if (p >= nsteps) return;
+    const uint64_t i = p / ns;
+    const uint32_t s = static_cast<uint32_t>(p % ns);
+    if (s == 0) {
+      uint32_t b, row;
+      uint64_t gc;
+      page(i, p_src, p_len, b, row, gc);
+      const uint32_t b0 = __shfl_sync(kFull, b, 0);
+      const uint32_t r0 = __shfl_sync(kFull, row, 0);
+      p_reg = __all_sync(kFull, b == b0 && p_len == pb && row == r0 + lane);
+      p_map = b0;
+      p_row = r0;
+      if (p_reg) reg_bits |= 1u << (i & 1); else reg_bits &= ~(1u << (i & 1));
+    }
+    const uint32_t bar = bar0 + 8 * st;
+    const uint32_t dst = wbuf_u + st * kStage;
+    if (p_reg) {
+      if (lane == 0) {
+        mbar_arrive_tx(bar, kStage);
+        tma_load_2d(dst, maps + p_map, static_cast<int>(s * SLAB), static_cast<int>(p_row), bar);
+        tma_load_2d(dst + 4096, maps + p_map, static_cast<int>(s * SLAB + 128),
+                    static_cast<int>(p_row), bar);
+      }
+    } else {
+      const bool valid = s * SLAB < p_len;
+      const uint32_t nvalid = __popc(__ballot_sync(kFull, valid));
+      if (lane == 0) mbar_arrive_tx(bar, nvalid * SLAB);
+      __syncwarp();
+      if (valid) {
+        bulk_load(dst + lane * 128, p_src + s * SLAB, 128, bar);
+        bulk_load(dst + 4096 + lane * 128, p_src + s * SLAB + 128, 128, bar);
+      }
+    }
+  };
+
+#pragma unroll
+  for (int p = 0; p < ST - 1; ++p) issue(p);
+
+  uint32_t lo = 0, hi = 0, mylen = 0;
+  uint8_t* mydst = nullptr;
+  for (uint64_t t = 0; t < nsteps; ++t) {
+    issue(t + ST - 1);
+    const uint32_t st = cst;
+    cst = cst + 1 == ST ? 0 : cst + 1;
+    const uint64_t i = t / ns;
+    const uint32_t s = static_cast<uint32_t>(t % ns);
+    if (s == 0) {
+      const uint8_t* src;
+      uint32_t b, row;
+      uint64_t gc;
+      page(i, src, mylen, b, row, gc);
+      mydst = nullptr;
+      if (mylen > 0) {
+        const uint64_t so = __ldg(spec_off + gc);
+        if (so != ~0ull) {
+          const uint64_t slot = slot_base + (gw + i * nw) * 32 + lane;
+          mydst = staging + so + ((slot & ((1u << ppc_shift) - 1)) << page_shift);
+        }
+      }
+      lo = static_cast<uint32_t>(kFnvOffset);
+      hi = static_cast<uint32_t>(kFnvOffset >> 32);
+    }
+    mbar_wait(bar0 + 8 * st, static_cast<uint32_t>((t / ST) & 1));
+    const bool reg = (reg_bits >> (i & 1)) & 1;
+    const uint32_t sbase = wbuf_u + st * kStage;
+    const uint32_t a = (sbase + lane * 128) | (reg ? static_cast<uint32_t>(lane & 7) << 4 : 0u);
+    const bool valid = s * SLAB < mylen;
+    if (valid) {
+#pragma unroll
+      for (int uu = 0; uu < 16; ++uu) {
+        const uint4 v = ld_shared16((a ^ ((uu & 7) << 4)) + (uu >> 3) * 4096);
+        fnv_word(lo, hi, v.x);
+        fnv_word(lo, hi, v.y);
+        fnv_word(lo, hi, v.z);
+        fnv_word(lo, hi, v.w);
+      }
+    }
+    // speculative compaction of this stage: 16 lanes per page, 2 pages per store
+    const uint32_t vm = __ballot_sync(kFull, valid && mydst != nullptr);
+    if (vm) {
+      const uint32_t x = lane & 15, jj = lane >> 4;
+#pragma unroll 4
+      for (int k = 0; k < 16; ++k) {
+        const uint32_t j = 2 * k + jj;
+        uint8_t* d = reinterpret_cast<uint8_t*>(
+            __shfl_sync(kFull, reinterpret_cast<uint64_t>(mydst), j));
+        if ((vm >> j) & 1) {
+          const uint32_t sw = reg ? (j & 7) : 0u;
+          const uint4 v = ld_shared16(sbase + (x >> 3) * 4096 + j * 128 + (((x & 7) ^ sw) << 4));
+          __stcs(reinterpret_cast<uint4*>(d + s * SLAB + x * 16), v);
+        }
+      }
+    }
+    __syncwarp();  // the slot is refilled ST - 1 steps later by this warp's lane 0
+    if (s == ns - 1) {
+      const uint64_t slot0 = slot_base + (gw + i * nw) * 32;
+      if (ppc_shift == 0) {
+        if (mylen > 0) k1_store_digest(g, slot0 + lane, (uint64_t(hi) << 32) | lo, chunk_dig);
+      } else {
+        const uint32_t ppc = 1u << ppc_shift;
+        const int base = lane & ~static_cast<int>(ppc - 1);
+        uint32_t flo = static_cast<uint32_t>(kFnvOffset);
+        uint32_t fhi = static_cast<uint32_t>(kFnvOffset >> 32);
+        for (uint32_t qq = 0; qq < ppc; ++qq) {
+          const uint32_t plo = __shfl_sync(kFull, lo, base + qq);
+          const uint32_t phi = __shfl_sync(kFull, hi, base + qq);
+          const uint32_t pl = __shfl_sync(kFull, mylen, base + qq);
+          if (pl > 0) {
+            fnv_word(flo, fhi, plo);
+            fnv_word(flo, fhi, phi);
+          }
+        }
+        if (lane == base && mylen > 0)
+          k1_store_digest(g, (slot0 + lane) >> ppc_shift, (uint64_t(fhi) << 32) | flo, chunk_dig);
+      }
+    }
+  }
+  if (g.xdig != nullptr) __threadfence_system();
+}
+
+constexpr int kTfWarps = 12, kTfStages = 2;
+constexpr size_t kTfSmem = size_t(kTfWarps) * kTfStages * 32 * 256 + size_t(kTfWarps) * kTfStages * 8 + 1024;
+
 constexpr int kTmaWarps = 16, kTmaStages = 3;
 constexpr size_t kTmaSmem = size_t(kTmaWarps) * kTmaStages * kStageBytes +
                             size_t(kTmaWarps) * kTmaStages * 8 + 1024;
@@ -273,6 +466,26 @@ int launch_hash_tma(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
   if (blocks > uint64_t(sms)) blocks = uint64_t(sms);
   k_hash_tma<kTmaWarps, kTmaStages><<<unsigned(blocks), kTmaWarps * 32, kTmaSmem, s>>>(arena, g,
                                                                                      chunk_dig);
+  return 1;
+}
+
+int launch_hash_tma_fused(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
+                          const uint64_t* spec_off, uint8_t* staging, cudaStream_t s) {
+  static uint64_t attr = 0;
+  once_per_device(attr, [] {
+    cudaFuncSetAttribute(k_hash_tma_fused<kTfWarps, kTfStages>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTfSmem));
+  });
+  const uint64_t c_end = g.c_end ? g.c_end : g.nchunks;
+  if (c_end <= g.c_begin) return 0;
+  const uint64_t ntasks = (((c_end - g.c_begin) << (g.chunk_shift - g.page_shift)) + 31) / 32;
+  uint64_t blocks = (ntasks + kTfWarps - 1) / kTfWarps;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (blocks > uint64_t(sms)) blocks = uint64_t(sms);
+  k_hash_tma_fused<kTfWarps, kTfStages><<<unsigned(blocks), kTfWarps * 32, kTfSmem, s>>>(
+      arena, g, chunk_dig, spec_off, staging);
   return 1;
 }
 

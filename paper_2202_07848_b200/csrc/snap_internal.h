@@ -88,6 +88,9 @@ int launch_hash(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
 bool hash_tma_ok(const GridDev& g);
 bool hash_tma_selected();  // SNAP_HASH_VARIANT=10: tensor maps are built for the grid
 int launch_hash_tma(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig, cudaStream_t s);
+// fused K1 with TMA tensor loads (CfgE geometry; needs the per-buffer maps)
+int launch_hash_tma_fused(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
+                          const uint64_t* spec_off, uint8_t* staging, cudaStream_t s);
 // K1 hash-only on the tensor cores (k_hash_mma.cu: 8-bit FNV chain on the CUDA
 // cores + the linear part as a tcgen05 int8 MMA); needs the grid tensor maps.
 bool hash_mma_ok(const GridDev& g);

@@ -108,7 +108,7 @@ def _snapshot_check(c, host, bufs):
             f"pass {rep}: staging image differs"
 
 
-@pytest.mark.parametrize("variant", [11, 12])
+@pytest.mark.parametrize("variant", [11, 12, 13])
 def test_fused_snapshot_mma(snap, variant):
     """Fused hash + speculative compaction on the tensor-core kernels (11: 128-B slabs,
     12: the light-write geometry used for striped multi-rank layouts): regular 4 MiB

@@ -233,7 +233,7 @@ def test_fused_speculation_learns_and_recovers(snap, ctx, golden):
     check(host)
 
 
-@pytest.mark.parametrize("variant", [-1, 11, 12])
+@pytest.mark.parametrize("variant", [-1, 11, 12, 13])
 def test_snapshot_host_pipelined(snap, variant):
     """snap_snapshot_host (pinned host image -> arena -> K1..K3 -> staging to host), slab
     pipelined: staging image == oracle compaction, through mispredicted, learned and
