@@ -269,7 +269,7 @@ k_hash(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ chun
     if (par ? reg1 : reg0) {
       uint8_t* da = par ? rdst1 : rdst0;
       uint8_t* dbb = par ? rdstb1 : rdstb0;
-      if constexpr (PPC != 0 && NP / PPC <= 2 && PPC % PPI == 0) {
+      if constexpr (PPC != 0 && NP / (PPC ? PPC : 1) <= 2 && PPC % PPI == 0) {
         // pages per chunk known at compile time: the chunk split of the
         // unrolled store loop is static (pages k*PPI + q, q < PPI)
         constexpr int KA = PPC < NP ? PPC / PPI : C::kCopyInstr;
