@@ -67,6 +67,7 @@ k_gather(const uint8_t* __restrict__ arena, GridDev g, const uint32_t* __restric
          const uint64_t* __restrict__ offsets, int by_list, const uint64_t* __restrict__ spec_cur,
          uint64_t* __restrict__ spec_next, uint8_t* __restrict__ staging,
          uint32_t* __restrict__ moved, unsigned int* __restrict__ nmoved) {
+  griddep_wait();
   const uint64_t nsel = totals[0];
   const int lane = threadIdx.x & 31;
   const uint64_t w0 = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
@@ -251,9 +252,8 @@ int launch_gather(const uint8_t* arena, const GridDev& g, const uint32_t* lens,
   // speculative path: one list entry per thread; otherwise one chunk per warp
   uint64_t blocks = ((spec_cur ? max_sel : max_sel * 32) + kThreads - 1) / kThreads;
   if (blocks > copy_grid()) blocks = copy_grid();
-  k_gather<<<unsigned(blocks), kThreads, 0, s>>>(arena, g, lens, sel_list, totals, offsets,
-                                                 offsets_by_list ? 1 : 0, spec_cur, spec_next,
-                                                 staging, moved, nmoved);
+  launch_pdl(k_gather, unsigned(blocks), kThreads, 0, s, arena, g, lens, sel_list, totals, offsets,
+             offsets_by_list ? 1 : 0, spec_cur, spec_next, staging, moved, nmoved);
   return 1;
 }
 

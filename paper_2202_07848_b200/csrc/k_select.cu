@@ -51,6 +51,7 @@ __global__ void k_table_insert_min(TableDev t, const uint64_t* __restrict__ keys
 __global__ void k_dedup_insert(TableDev dedup, TableDev known, int use_known,
                                const uint64_t* __restrict__ dig, const uint32_t* __restrict__ lens,
                                uint64_t n, uint64_t* __restrict__ slot) {
+  griddep_wait();
   for (uint64_t g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < n;
        g += uint64_t(gridDim.x) * blockDim.x) {
     uint64_t s = ~0ull;
@@ -70,6 +71,7 @@ __global__ void k_dedup_insert(TableDev dedup, TableDev known, int use_known,
 __global__ void k_stripe_writer(const uint64_t* __restrict__ gdig, const uint32_t* __restrict__ glens,
                                 const uint8_t* __restrict__ sel, uint32_t nranks, uint64_t maxn,
                                 int32_t* __restrict__ writer) {
+  griddep_wait();
   const uint64_t n = uint64_t(nranks) * maxn;
   for (uint64_t g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < n;
        g += uint64_t(gridDim.x) * blockDim.x) {
@@ -189,6 +191,7 @@ k_select_scan(TableDev dedup, const uint64_t* __restrict__ slot, const uint32_t*
               uint8_t* __restrict__ sel, uint64_t* __restrict__ owner,
               uint64_t* __restrict__ offsets, uint32_t* __restrict__ sel_list,
               uint64_t* __restrict__ totals, uint64_t* __restrict__ spec_next) {
+  griddep_wait();
   const uint64_t tile = next_tile(tile_counter);
   const uint64_t ntiles = (n + kTile - 1) / kTile;
   const uint64_t base = tile * kTile + uint64_t(threadIdx.x) * kItems;
@@ -262,6 +265,7 @@ k_shard_scan(const int32_t* __restrict__ writer, const uint32_t* __restrict__ gl
 __global__ void k_resolve_dups(const uint8_t* __restrict__ sel, const uint64_t* __restrict__ owner,
                                uint64_t* __restrict__ offsets, uint64_t n, TableDev clear,
                                uint64_t* __restrict__ scan_state, uint64_t clear_words) {
+  griddep_wait();
   const uint64_t tab = clear.keys ? clear.mask + 2 : 0;
   const uint64_t end = n > tab ? (n > clear_words ? n : clear_words)
                                : (tab > clear_words ? tab : clear_words);
@@ -304,8 +308,8 @@ int launch_table_insert_min(TableDev t, const uint64_t* keys, uint64_t n, uint64
 int launch_dedup_insert(TableDev dedup, TableDev known, bool use_known, const uint64_t* dig,
                         const uint32_t* lens, uint64_t n, uint64_t* slot, cudaStream_t s) {
   if (n == 0) return 0;
-  k_dedup_insert<<<grid_for(n, 128, 148 * 32), 128, 0, s>>>(dedup, known, use_known ? 1 : 0, dig,
-                                                             lens, n, slot);
+  launch_pdl(k_dedup_insert, grid_for(n, 128, 148 * 32), 128, 0, s, dedup, known,
+             use_known ? 1 : 0, dig, lens, n, slot);
   return 1;
 }
 
@@ -317,9 +321,9 @@ int launch_select(TableDev dedup, const uint64_t* slot, const uint32_t* lens, ui
     cudaMemsetAsync(totals, 0, 2 * sizeof(uint64_t), s);
     return 0;
   }
-  k_select_scan<<<unsigned(tiles), kThreads, 0, s>>>(
-      dedup, slot, lens, n, scan_state, reinterpret_cast<unsigned int*>(scan_state + tiles), sel,
-      owner, offsets, sel_list, totals, spec_next);
+  launch_pdl(k_select_scan, unsigned(tiles), kThreads, 0, s, dedup, slot, lens, n, scan_state,
+             reinterpret_cast<unsigned int*>(scan_state + tiles), sel, owner, offsets, sel_list,
+             totals, spec_next);
   return 1;
 }
 
@@ -327,7 +331,8 @@ int launch_stripe_writer(const uint64_t* gdig, const uint32_t* glens, const uint
                          uint32_t nranks, uint64_t maxn, int32_t* writer, cudaStream_t s) {
   const uint64_t n = uint64_t(nranks) * maxn;
   if (n == 0) return 0;
-  k_stripe_writer<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(gdig, glens, sel, nranks, maxn, writer);
+  launch_pdl(k_stripe_writer, grid_for(n, 256, 148 * 16), 256, 0, s, gdig, glens, sel, nranks, maxn,
+             writer);
   return 1;
 }
 
@@ -353,8 +358,8 @@ int launch_resolve_dups(const uint8_t* sel, const uint64_t* owner, uint64_t* off
   const uint64_t tab = clear.keys ? clear.mask + 2 : 0;
   const uint64_t end = std::max(n, std::max(tab, clear_words));
   if (end == 0) return 0;
-  k_resolve_dups<<<grid_for(end, 256, 148 * 8), 256, 0, s>>>(sel, owner, offsets, n, clear,
-                                                            scan_state, clear_words);
+  launch_pdl(k_resolve_dups, grid_for(end, 256, 148 * 8), 256, 0, s, sel, owner, offsets, n,
+             clear, scan_state, clear_words);
   return 1;
 }
 

@@ -6,12 +6,32 @@
 #include <stdint.h>
 
 #include <mutex>
+#include <utility>
 #include <string>
 #include <vector>
 
 #include "snap.h"
 
 namespace snap {
+
+// Programmatic dependent launch: the kernel may be scheduled while the previous
+// kernel of the stream drains; it must call griddep_wait() before touching
+// anything that kernel wrote (K2 / K3 follow K1 and each other on one stream).
+template <class... P, class... A>
+inline cudaError_t launch_pdl(void (*k)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              A&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...);
+}
 
 // Per-(kernel, device) one-time setup, e.g. cudaFuncSetAttribute (which only
 // applies to the current device): runs f() the first time this device is seen

@@ -8,6 +8,13 @@
 
 namespace snap {
 
+// PDL: wait until the previous kernel of the stream has completed and its
+// writes are visible (no-op without a programmatic dependency)
+__device__ __forceinline__ void griddep_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+
 __device__ __forceinline__ uint64_t tmix64(uint64_t x) {
   x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
   x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
