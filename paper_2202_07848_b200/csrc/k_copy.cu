@@ -182,6 +182,7 @@ __global__ void k_cache_insert(TableDev cache, const uint64_t* __restrict__ dig,
                                const uint32_t* __restrict__ sel_list,
                                const uint64_t* __restrict__ totals,
                                const uint64_t* __restrict__ offsets, uint64_t base) {
+  griddep_wait();
   const uint64_t n = totals[0];
   for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
        k += uint64_t(gridDim.x) * blockDim.x) {
@@ -202,6 +203,7 @@ k_splice_in(uint8_t* __restrict__ arena, GridDev to, const uint32_t* __restrict_
             const uint64_t* __restrict__ want, const int64_t* __restrict__ match,
             const uint64_t* __restrict__ dig_from, TableDev cache,
             const uint8_t* __restrict__ cache_base, unsigned long long* __restrict__ counters) {
+  griddep_wait();
   const int lane = threadIdx.x & 31;
   const uint64_t w0 = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
   const uint64_t nw = (uint64_t(gridDim.x) * kThreads) >> 5;
@@ -283,7 +285,8 @@ int launch_cache_insert(TableDev cache, const uint64_t* dig, const uint32_t* sel
   if (max_n == 0) return 0;
   uint64_t blocks = (max_n + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  k_cache_insert<<<unsigned(blocks), 256, 0, s>>>(cache, dig, sel_list, totals, offsets, base);
+  launch_pdl(k_cache_insert, unsigned(blocks), 256, 0, s, cache, dig, sel_list, totals, offsets,
+             base);
   return 1;
 }
 
@@ -294,8 +297,8 @@ int launch_splice_in(uint8_t* arena, const GridDev& to, const uint32_t* lens, co
   if (to.nchunks == 0) return 0;
   uint64_t blocks = (to.nchunks * 32 + kThreads - 1) / kThreads;
   if (blocks > copy_grid()) blocks = copy_grid();
-  k_splice_in<<<unsigned(blocks), kThreads, 0, s>>>(arena, to, lens, want, match, dig_from, cache,
-                                                    cache_base, counters);
+  launch_pdl(k_splice_in, unsigned(blocks), kThreads, 0, s, arena, to, lens, want, match, dig_from,
+             cache, cache_base, counters);
   return 1;
 }
 
