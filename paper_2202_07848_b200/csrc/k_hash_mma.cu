@@ -413,8 +413,8 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
 
     // producer state of the group being loaded
     uint32_t p_reg = 0, p_chk = 0, p_map[TPW], p_row[TPW], p_len[TPW];
-    // tasks that are not one 32-page run of one buffer load one TMA box per
-    // chunk (its buffer's chunk-box map, (map, row) per chunk in ctab)
+    // tasks that are not 32 contiguous full pages load one TMA box per chunk
+    // (the arena-wide chunk-box maps), replayed from the warp's issue plan
     const CUtensorMap* cmaps = static_cast<const CUtensorMap*>(g.tmaps64c);
     const bool cbox = BOXW == 64 && C::NBOX == 1 && cmaps != nullptr;
     // per-group TMA issue plan of a warp whose tasks are not all regular: up to
