@@ -834,7 +834,7 @@ bool hash_tma_selected() {
 //  * fused hash + speculative stores: CfgE — 256-B slabs keep the mixed
 //    read/write DRAM pattern at ~6 TB/s (128-B segments cap it at ~5.2,
 //    tools/micro/pattern_bw2.cu);
-//  * hash only, >= 512 MiB: the tensor-core FNV kernel (k_hash_mma.cu);
+//  * hash only, >= 320 MiB: the tensor-core FNV kernel (k_hash_mma.cu);
 //  * hash only, smaller grids (alternating same-box A/B over the C2 / C3 / C4
 //    buffer shapes, tools/hash_variants.py): the TMA tensor-load kernel beats
 //    the cp.async CfgA by 1-2 % on every shape; two chains per lane (CfgB) win
@@ -875,11 +875,10 @@ K1 choose_k1(const GridDev& g, const uint64_t* spec_off) {
           return K1::MmaFL;
         return K1::E;
       }
-      // tensor-core FNV: one 1024-page group per SM at a time, so it needs
-      // >= 128 groups (512 MiB) to fill the GPU (tools/hash_sizes.py:
-      // 4.9-6.0 TB/s from 512 MiB up vs 3.0-3.6 for the TMA kernel; below
-      // that the TMA kernel's 32-page tasks spread over more SMs)
-      if (hash_mma_ok(g) && pages >= 128 * 1024) return K1::Mma;
+      // tensor-core FNV: one 1024-page group per SM at a time, so small grids
+      // leave SMs idle (tools/hash_sizes.py: 256 MiB 2.56 vs 2.85 TB/s for the
+      // TMA kernel, 384 MiB 3.75 vs 2.29, 512 MiB+ 4.8-6.0 vs 3.0-3.6)
+      if (hash_mma_ok(g) && pages >= 80 * 1024) return K1::Mma;
       if (g.nbufs && (g.nchunks << g.chunk_shift) / g.nbufs >= (64ull << 20)) return K1::B;
       return hash_tma_ok(g) ? K1::Tma : K1::A;
     }

@@ -10,7 +10,7 @@ import paper_2202_07848_b200 as snap  # noqa: E402
 out = {"variant": os.environ.get("SNAP_HASH_VARIANT", "default")}
 with snap.Ctx(0, (4 << 30) + (1 << 20)) as c:
     c.fill_mix64(0, 4 << 30, 5, 0)
-    for mib in (16, 64, 256, 512, 1024, 4096):
+    for mib in (16, 64, 128, 256, 384, 512, 1024, 4096):
         nb = 4 << 20
         bufs = [(0, i, i * nb, nb, 0) for i in range(mib // 4)]
         c.set_buffers(bufs)
