@@ -137,6 +137,7 @@ int select_with_known(snap_ctx* ctx, const uint64_t* dig, const uint32_t* lens, 
   ctx->dd_clean = true;
   ctx->scan_clean_words = std::max(ctx->scan_clean_words, words);
   ctx->sel_n = n;
+  ctx->global_offsets_pending = false;
   return SNAP_OK;
 }
 
@@ -322,24 +323,61 @@ int exchange_impl(snap_ctx* ctx) {
   return SNAP_OK;
 }
 
-int stripe_impl(snap_ctx* ctx) {
+// The multi-rank step's selection: owners (dedup over the gathered vectors),
+// stripe writers and this rank's shard scan — all the compaction needs. The
+// global image's staging offsets (read only by snap_get_selection) are left
+// to global_offsets(), which scans the owners this step recorded.
+int select_stripe_impl(snap_ctx* ctx) {
   const uint64_t maxn = ctx->maxn, n = uint64_t(ctx->nranks) * maxn;
+  TableDev kn{P<unsigned long long>(ctx->kn_keys), P<unsigned long long>(ctx->kn_vals), ctx->kn_mask};
+  TableDev dd;
+  uint64_t *slot, *scan, *owner, *shard_off, *my_off, *my_tot, *scan2;
+  uint8_t* sel;
   int32_t* writer;
-  uint64_t *shard_off, *my_off, *my_tot;
   uint32_t* my_list;
+  RC(prepare_dedup(ctx, n, &dd, &slot, &scan));
+  RC(ensure(ctx, ctx->sel, n, &sel));
+  RC(ensure(ctx, ctx->owner, n, &owner));
   RC(ensure(ctx, ctx->d_writer, n, &writer));
   RC(ensure(ctx, ctx->d_shard_off, n, &shard_off));
   RC(ensure(ctx, ctx->d_my_list, maxn, &my_list));
   RC(ensure(ctx, ctx->d_my_off, maxn, &my_off));
   RC(ensure(ctx, ctx->d_my_totals, 4, &my_tot));
-  uint64_t* scan2;
   RC(ensure(ctx, ctx->scan2, snap::scan_state_words(n) + 1, &scan2));
+  const uint64_t* gdig = gdig_region(ctx, ctx->xepoch);
+  const uint32_t* glens = P<uint32_t>(ctx->d_glens);
+  CKL(snap::launch_dedup_insert(dd, kn, ctx->kn_count > 0, gdig, glens, n, slot, ctx->stream));
+  CKL(snap::launch_select_stripe(dd, slot, gdig, glens, ctx->nranks, maxn, ctx->rank, sel, owner,
+                                 writer, scan2, shard_off, my_list, my_off, my_tot, ctx->stream));
+  ctx->dd_clean = true;  // the shard scan emptied the table
+  ctx->sel_n = n;
+  ctx->selected = true;
   ctx->shard_offsets_all = false;
-  CKL(snap::launch_stripe_writer(gdig_region(ctx, ctx->xepoch), P<uint32_t>(ctx->d_glens),
-                                 P<uint8_t>(ctx->sel), ctx->nranks, maxn, writer, ctx->stream));
-  CKL(snap::launch_shard_scan(writer, P<uint32_t>(ctx->d_glens), ctx->nranks, maxn, ctx->rank, true,
-                              scan2, shard_off, my_list, my_off, my_tot,
-                              ctx->stream));
+  ctx->global_offsets_pending = true;
+  return SNAP_OK;
+}
+
+// Global staging offsets of the last multi-rank step, from its owners.
+int global_offsets(snap_ctx* ctx) {
+  if (!ctx->global_offsets_pending) return SNAP_OK;
+  const uint64_t n = ctx->sel_n;
+  const uint64_t words = snap::scan_state_words(n) + 1;
+  uint64_t *scan, *offsets, *totals;
+  uint32_t* list;
+  const void* s_old = ctx->scan.p;
+  RC(ensure(ctx, ctx->scan, words, &scan));
+  if (scan != s_old) ctx->scan_clean_words = 0;
+  if (words > ctx->scan_clean_words) CK(cudaMemsetAsync(scan, 0, words * 8, ctx->stream));
+  RC(ensure(ctx, ctx->offsets, n, &offsets));
+  RC(ensure(ctx, ctx->sel_list, n, &list));
+  RC(ensure(ctx, ctx->totals, 4, &totals));
+  CKL(snap::launch_select(TableDev{}, nullptr, P<uint32_t>(ctx->d_glens), n, scan,
+                          P<uint8_t>(ctx->sel), P<uint64_t>(ctx->owner), offsets, list, totals,
+                          nullptr, ctx->stream));
+  CKL(snap::launch_resolve_dups(P<uint8_t>(ctx->sel), P<uint64_t>(ctx->owner), offsets, n,
+                                TableDev{}, scan, words, ctx->stream));
+  ctx->scan_clean_words = std::max(ctx->scan_clean_words, words);
+  ctx->global_offsets_pending = false;
   return SNAP_OK;
 }
 
@@ -874,9 +912,7 @@ int snap_select(snap_ctx* ctx) {
       RC(exchange_impl(ctx));
     }
     ProfScope ps(ctx, kProfSelect);
-    RC(select_impl(ctx, gdig_region(ctx, ctx->xepoch), P<uint32_t>(ctx->d_glens),
-                   uint64_t(ctx->nranks) * ctx->maxn));
-    return stripe_impl(ctx);
+    return select_stripe_impl(ctx);
   }
   ProfScope ps(ctx, kProfSelect);
   const bool inserted = ctx->k1_inserted;
@@ -895,6 +931,7 @@ int snap_get_selection(snap_ctx* ctx, uint8_t* sel, uint64_t* owner, uint64_t* o
   if (!ctx) return SNAP_EINVAL;
   if (!ctx->selected) return fail(ctx, SNAP_EINVAL, "get_selection before snap_select");
   CK(cudaSetDevice(ctx->device));
+  RC(global_offsets(ctx));
   const uint64_t n = ctx->sel_n;
   uint64_t tot[2] = {0, 0};
   if (n) {

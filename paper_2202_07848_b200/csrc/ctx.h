@@ -116,6 +116,9 @@ struct snap_ctx {
   std::vector<void*> peer_staging;  // [nranks]; own rank = local staging
   DevMem d_peers;
   bool shard_offsets_all = false;   // d_shard_off valid for every writer
+  // multi-rank step: global staging offsets (offsets/sel_list/totals) not yet
+  // computed from the step's owners (global_offsets() does it on demand)
+  bool global_offsets_pending = false;
   DevMem d_tmaps;  // per-buffer TMA tensor maps of the installed grid
   // predicted staging bytes (multi-rank shards are sized to the prediction and
   // grown on demand instead of reserving a whole image per GPU)

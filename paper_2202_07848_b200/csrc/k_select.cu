@@ -67,32 +67,56 @@ __global__ void k_dedup_insert(TableDev dedup, TableDev known, int use_known,
   }
 }
 
-// Stripe writer of every selected global chunk (rank-major, `maxn` per rank).
-__global__ void k_stripe_writer(const uint64_t* __restrict__ gdig, const uint32_t* __restrict__ glens,
-                                const uint8_t* __restrict__ sel, uint32_t nranks, uint64_t maxn,
-                                int32_t* __restrict__ writer) {
+// Multi-rank step (writer and owner only; the global staging offsets are
+// computed on demand, snap_get_selection): per global chunk g, owner = first
+// occurrence (the dedup table's min index), selected iff owner == g, and the
+// stripe writer of a selected chunk: holders = ranks whose chunk at the same
+// local index i has the same digest and length, writer = holders[i % |holders|]
+// (rank-major global index, `maxn` per rank). Also zeroes the
+// shard scan's state (the next kernel on the stream), so the step needs no memset.
+__global__ void k_select_stripe(TableDev dedup, const uint64_t* __restrict__ slot,
+                                const uint64_t* __restrict__ gdig, const uint32_t* __restrict__ glens,
+                                uint32_t nranks, uint64_t maxn, uint8_t* __restrict__ sel,
+                                uint64_t* __restrict__ owner, int32_t* __restrict__ writer,
+                                uint64_t* __restrict__ scan_state, uint64_t scan_words) {
   griddep_wait();
   const uint64_t n = uint64_t(nranks) * maxn;
-  for (uint64_t g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < n;
+  const uint64_t end = n > scan_words ? n : scan_words;
+  for (uint64_t g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < end;
        g += uint64_t(gridDim.x) * blockDim.x) {
+    if (g < scan_words) scan_state[g] = 0;
+    if (g >= n) continue;
+    const uint64_t s = slot[g];
+    const uint64_t own = s == ~0ull ? ~0ull : dedup.vals[s];
     int32_t w = -1;
-    if (sel[g]) {
+    if (own == g) {
       const uint64_t i = g % maxn;
       const uint64_t d = gdig[g];
       const uint32_t ln = glens[g];
-      uint32_t nh = 0;
-      for (uint32_t q = 0; q < nranks; ++q)
-        nh += (glens[q * maxn + i] == ln && gdig[q * maxn + i] == d);
-      uint32_t pick = static_cast<uint32_t>(i % nh), seen = 0;
-      for (uint32_t q = 0; q < nranks; ++q)
-        if (glens[q * maxn + i] == ln && gdig[q * maxn + i] == d) {
-          if (seen == pick) {
-            w = static_cast<int32_t>(q);
-            break;
+      uint32_t hold = 0, nh = 0;  // holder ranks as a bit set (nranks <= 32 fast path)
+      if (nranks <= 32) {
+        for (uint32_t q = 0; q < nranks; ++q)
+          if (glens[q * maxn + i] == ln && gdig[q * maxn + i] == d) hold |= 1u << q;
+        nh = __popc(hold);
+        uint32_t pick = static_cast<uint32_t>(i % nh);
+        for (; pick; --pick) hold &= hold - 1;
+        w = __ffs(hold) - 1;
+      } else {
+        for (uint32_t q = 0; q < nranks; ++q)
+          nh += (glens[q * maxn + i] == ln && gdig[q * maxn + i] == d);
+        uint32_t pick = static_cast<uint32_t>(i % nh), seen = 0;
+        for (uint32_t q = 0; q < nranks; ++q)
+          if (glens[q * maxn + i] == ln && gdig[q * maxn + i] == d) {
+            if (seen == pick) {
+              w = static_cast<int32_t>(q);
+              break;
+            }
+            ++seen;
           }
-          ++seen;
-        }
+      }
     }
+    sel[g] = own == g;
+    owner[g] = own;
     writer[g] = w;
   }
 }
@@ -188,7 +212,7 @@ __device__ __forceinline__ uint64_t next_tile(unsigned int* counter) {
 __global__ void __launch_bounds__(kThreads)
 k_select_scan(TableDev dedup, const uint64_t* __restrict__ slot, const uint32_t* __restrict__ lens,
               uint64_t n, uint64_t* __restrict__ status, unsigned int* __restrict__ tile_counter,
-              uint8_t* __restrict__ sel, uint64_t* __restrict__ owner,
+              uint8_t* __restrict__ sel, uint64_t* owner,
               uint64_t* __restrict__ offsets, uint32_t* __restrict__ sel_list,
               uint64_t* __restrict__ totals, uint64_t* __restrict__ spec_next) {
   griddep_wait();
@@ -198,10 +222,12 @@ k_select_scan(TableDev dedup, const uint64_t* __restrict__ slot, const uint32_t*
   uint64_t val[kItems], own[kItems], local = 0;
   uint64_t s[kItems];
 #pragma unroll
-  for (int j = 0; j < kItems; ++j) s[j] = base + j < n ? slot[base + j] : ~0ull;
+  for (int j = 0; j < kItems; ++j)
+    s[j] = base + j >= n ? ~0ull : slot ? slot[base + j] : owner[base + j];
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
-    own[j] = s[j] == ~0ull ? ~0ull : dedup.vals[s[j]];
+    // slot == nullptr: the owners are already known (multi-rank, on demand)
+    own[j] = s[j] == ~0ull ? ~0ull : slot ? dedup.vals[s[j]] : s[j];
     val[j] = own[j] == base + j ? (1ull << kUnitBits) | (lens[base + j] >> 8) : 0;
     local += val[j];
   }
@@ -230,7 +256,16 @@ k_shard_scan(const int32_t* __restrict__ writer, const uint32_t* __restrict__ gl
              uint64_t maxn, int32_t me, int write_list, uint64_t* __restrict__ status,
              unsigned int* __restrict__ tile_counter, uint64_t* __restrict__ shard_off,
              uint32_t* __restrict__ my_list, uint64_t* __restrict__ my_off,
-             uint64_t* __restrict__ totals) {
+             uint64_t* __restrict__ totals, TableDev clear) {
+  griddep_wait();
+  if (clear.keys) {  // the dedup table the previous kernel consumed: left empty
+    const uint64_t tab = clear.mask + 2;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < tab;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+      clear.keys[i] = kEmptyKey;
+      clear.vals[i] = ~0ull;
+    }
+  }
   const uint64_t tile = next_tile(tile_counter);
   const uint64_t ntiles = (n + kTile - 1) / kTile;
   const uint64_t base = tile * kTile + uint64_t(threadIdx.x) * kItems;
@@ -327,15 +362,6 @@ int launch_select(TableDev dedup, const uint64_t* slot, const uint32_t* lens, ui
   return 1;
 }
 
-int launch_stripe_writer(const uint64_t* gdig, const uint32_t* glens, const uint8_t* sel,
-                         uint32_t nranks, uint64_t maxn, int32_t* writer, cudaStream_t s) {
-  const uint64_t n = uint64_t(nranks) * maxn;
-  if (n == 0) return 0;
-  launch_pdl(k_stripe_writer, grid_for(n, 256, 148 * 16), 256, 0, s, gdig, glens, sel, nranks, maxn,
-             writer);
-  return 1;
-}
-
 int launch_shard_scan(const int32_t* writer, const uint32_t* glens, uint32_t nranks, uint64_t maxn,
                       int32_t q, bool write_list, uint64_t* scan_state, uint64_t* shard_off,
                       uint32_t* my_list, uint64_t* my_off, uint64_t* totals, cudaStream_t s) {
@@ -348,8 +374,28 @@ int launch_shard_scan(const int32_t* writer, const uint32_t* glens, uint32_t nra
   }
   k_shard_scan<<<unsigned(tiles), kThreads, 0, s>>>(
       writer, glens, n, maxn, q, write_list ? 1 : 0, scan_state,
-      reinterpret_cast<unsigned int*>(scan_state + tiles), shard_off, my_list, my_off, totals);
+      reinterpret_cast<unsigned int*>(scan_state + tiles), shard_off, my_list, my_off, totals,
+      TableDev{});
   return 1;
+}
+
+int launch_select_stripe(TableDev dedup, const uint64_t* slot, const uint64_t* gdig,
+                         const uint32_t* glens, uint32_t nranks, uint64_t maxn, int32_t me,
+                         uint8_t* sel, uint64_t* owner, int32_t* writer, uint64_t* scan_state,
+                         uint64_t* shard_off, uint32_t* my_list, uint64_t* my_off,
+                         uint64_t* totals, cudaStream_t s) {
+  const uint64_t n = uint64_t(nranks) * maxn;
+  const uint64_t tiles = (n + kTile - 1) / kTile;
+  if (n == 0) {
+    cudaMemsetAsync(totals, 0, 2 * sizeof(uint64_t), s);
+    return 0;
+  }
+  launch_pdl(k_select_stripe, grid_for(n, 256, 148 * 16), 256, 0, s, dedup, slot, gdig, glens,
+             nranks, maxn, sel, owner, writer, scan_state, tiles + 1);
+  launch_pdl(k_shard_scan, unsigned(tiles), kThreads, 0, s, writer, glens, n, maxn, me, 1,
+             scan_state, reinterpret_cast<unsigned int*>(scan_state + tiles), shard_off, my_list,
+             my_off, totals, dedup);
+  return 2;
 }
 
 int launch_resolve_dups(const uint8_t* sel, const uint64_t* owner, uint64_t* offsets, uint64_t n,

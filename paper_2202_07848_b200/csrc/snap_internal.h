@@ -157,13 +157,19 @@ int launch_dedup_insert(TableDev dedup, TableDev known, bool use_known, const ui
 int launch_select(TableDev dedup, const uint64_t* slot, const uint32_t* lens, uint64_t n,
                   uint64_t* scan_state, uint8_t* sel, uint64_t* owner, uint64_t* offsets,
                   uint32_t* sel_list, uint64_t* totals, uint64_t* spec_next, cudaStream_t s);
-// Cross-rank striping: writer per selected global chunk, then one shard scan
-// per writer q (write_list for q == this rank: local chunk list + offsets).
-int launch_stripe_writer(const uint64_t* gdig, const uint32_t* glens, const uint8_t* sel,
-                         uint32_t nranks, uint64_t maxn, int32_t* writer, cudaStream_t s);
+// Shard scan of writer q over the global writer vector (write_list for q ==
+// this rank: local chunk list + offsets).
 int launch_shard_scan(const int32_t* writer, const uint32_t* glens, uint32_t nranks, uint64_t maxn,
                       int32_t q, bool write_list, uint64_t* scan_state, uint64_t* shard_off,
                       uint32_t* my_list, uint64_t* my_off, uint64_t* totals, cudaStream_t s);
+// Multi-rank step: owner / sel / writer per global chunk from the filled dedup
+// table (k_select_stripe), then rank `me`'s shard scan, which also empties the
+// table; the global staging offsets are left to launch_select (on demand).
+int launch_select_stripe(TableDev dedup, const uint64_t* slot, const uint64_t* gdig,
+                         const uint32_t* glens, uint32_t nranks, uint64_t maxn, int32_t me,
+                         uint8_t* sel, uint64_t* owner, int32_t* writer, uint64_t* scan_state,
+                         uint64_t* shard_off, uint32_t* my_list, uint64_t* my_off,
+                         uint64_t* totals, cudaStream_t s);
 // host pages: first-occurrence / known-set / previous-page-set classification
 // (flags bit 1 fresh, bit 2 inc; counts[0..1] += fresh, inc; counts zeroed by the caller)
 int launch_page_classify(TableDev pages, TableDev known, bool use_known, TableDev prev,
