@@ -248,12 +248,20 @@ inline void build_tmaps(snap_ctx* ctx, DevMem& m, const uint64_t* addr, const ui
   g.tmaps = nullptr;
   g.tmaps64 = nullptr;
   g.tmaps64c = nullptr;
+  g.gsched = nullptr;
+  g.gs_bins = 0;
   if (!snap::hash_tma_selected() || g.page_shift != 12 || n == 0) return;
   // n per-buffer maps with 128-byte boxes (k_hash_tma), then the arena-wide
   // maps of k_hash_mma: 16 with 32-page boxes, 16 with chunk boxes (8-32 pages)
   const int ppc = 1 << (g.chunk_shift - g.page_shift);
   const bool chunk_maps = ppc >= 8 && ppc <= 32;
-  std::vector<uint8_t> host(size_t(n) * 128 + 32 * 128);
+  // + the balanced k_hash_mma group schedule after the maps
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device) != cudaSuccess) sms = 0;
+  std::vector<uint32_t> sched;
+  const uint32_t bins = snap::mma_schedule(addr, bytes, n, g.page_shift, g.chunk_shift, sms, sched);
+  std::vector<uint8_t> host(size_t(n) * 128 + 32 * 128 + sched.size() * 4);
+  if (!sched.empty()) std::memcpy(host.data() + size_t(n) * 128 + 32 * 128, sched.data(), sched.size() * 4);
   if (snap::encode_tensor_maps(ctx->arena, addr, bytes, n, host.data(), 128) != 0) return;
   uint8_t* a64 = host.data() + size_t(n) * 128;
   if (snap::encode_arena_maps(ctx->arena, ctx->arena_bytes, 64, 32, a64) != 0) return;
@@ -268,6 +276,8 @@ inline void build_tmaps(snap_ctx* ctx, DevMem& m, const uint64_t* addr, const ui
   g.tmaps = d;
   g.tmaps64 = d + size_t(n) * 128;
   if (chunk_maps) g.tmaps64c = d + size_t(n) * 128 + 16 * 128;
+  g.gsched = bins ? reinterpret_cast<const uint32_t*>(d + size_t(n) * 128 + 32 * 128) : nullptr;
+  g.gs_bins = bins;
 }
 
 inline int check_range(snap_ctx* ctx, uint64_t addr, uint64_t bytes) {

@@ -47,6 +47,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -324,7 +325,16 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
   const uint64_t nslots = (c_end - g.c_begin) << ppc_shift;
   const uint64_t ngroups = (nslots + GP - 1) / GP;
   if (blockIdx.x >= ngroups) return;
-  const uint64_t ngl = (ngroups - blockIdx.x + gridDim.x - 1) / gridDim.x;  // my groups
+  // my groups: the grid's balanced schedule (mma_schedule), else round robin
+  // (recomputed from the kernel parameter at each use: no registers held;
+  // hash-only variant only — the fused one stays at its register budget)
+  const uint32_t* gs = C::FUSED ? nullptr : g.gsched;
+  const uint64_t ngl = gs ? __ldg(gs + blockIdx.x + 1) - __ldg(gs + blockIdx.x)
+                          : (ngroups - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  auto group_of = [&g](uint32_t i) -> uint64_t {
+    return !C::FUSED && g.gsched ? __ldg(g.gsched + gridDim.x + 1 + __ldg(g.gsched + blockIdx.x) + i)
+                                 : blockIdx.x + uint64_t(i) * gridDim.x;
+  };
 
   if (threadIdx.x < C::SM_ZERO / 16) reinterpret_cast<uint4*>(zero)[threadIdx.x] = make_uint4(0, 0, 0, 0);
   if (threadIdx.x == 0) {
@@ -428,7 +438,7 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
 
     auto page_info = [&](uint32_t i, int t, const uint8_t*& src, uint32_t& len, uint32_t& b,
                          uint32_t& row, uint64_t& gcout) {
-      const uint64_t gi = blockIdx.x + uint64_t(i) * gridDim.x;
+      const uint64_t gi = group_of(i);
       const uint64_t rel = gi * GP + PPW * warp + 32 * t + lane;
       src = nullptr;
       len = 0;
@@ -608,7 +618,7 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
           if (C::FUSED && gc != ~0ull) {
             const uint64_t so = __ldg(spec_off + gc);
             if (so != ~0ull) {
-              const uint64_t gi = blockIdx.x + uint64_t(i) * gridDim.x;
+              const uint64_t gi = group_of(i);
               const uint64_t slot = slot_base + gi * GP + PPW * warp + 32 * t + lane;
               c_dst[t] = staging + so + ((slot & ((1u << ppc_shift) - 1)) << 12);
             }
@@ -740,7 +750,7 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
           vm[t] = __ballot_sync(kFull, n > 0);
         }
         __syncwarp();
-        const uint64_t gi = blockIdx.x + uint64_t(i) * gridDim.x;
+        const uint64_t gi = group_of(i);
         const uint64_t slot0 = slot_base + gi * GP + PPW * warp;
         const uint32_t ppc = 1u << ppc_shift;
         for (uint32_t c = lane; c < (uint32_t(PPW) >> ppc_shift); c += 32) {
@@ -848,6 +858,62 @@ const uint8_t* device_btab() {
 
 }  // namespace
 
+uint32_t mma_schedule(const uint64_t* addr, const uint64_t* bytes, uint32_t n,
+                      uint32_t page_shift, uint32_t chunk_shift, int sms,
+                      std::vector<uint32_t>& out) {
+  out.clear();
+  if (page_shift != 12 || chunk_shift < 12 || chunk_shift > 17 || n == 0 || sms <= 0) return 0;
+  using C = MmaHash;
+  static_assert(MmaHash::GP == MmaFusedLight::GP, "one schedule for both variants");
+  const uint64_t cb = 1ull << chunk_shift;
+  std::vector<uint64_t> caddr;  // chunk address, ~0 for a partial chunk
+  for (uint32_t b = 0; b < n; ++b)
+    for (uint64_t o = 0; o < bytes[b]; o += cb) caddr.push_back(o + cb <= bytes[b] ? addr[b] + o : ~0ull);
+  const uint64_t nch = caddr.size();
+  const uint32_t ppc_shift = chunk_shift - 12;
+  const uint64_t nslots = nch << ppc_shift;
+  const uint64_t ngroups = (nslots + C::GP - 1) / C::GP;
+  if (ngroups == 0 || ngroups >= (1ull << 32)) return 0;
+  const uint32_t bins = uint32_t(ngroups < uint64_t(sms) ? ngroups : uint64_t(sms));
+  // a task (32 page slots) is regular iff its chunks are full and contiguous
+  const uint64_t cpt = 32 >> ppc_shift;  // chunks per task
+  std::vector<uint8_t> heavy(ngroups, 0);
+  for (uint64_t gi = 0; gi < ngroups; ++gi)
+    for (uint64_t t = 0; t < C::GP / 32 && !heavy[gi]; ++t) {
+      const uint64_t c0 = ((gi * C::GP) >> ppc_shift) + t * cpt;
+      bool reg = c0 + cpt <= nch;
+      for (uint64_t k = 0; reg && k < cpt; ++k)
+        reg = caddr[c0 + k] != ~0ull && caddr[c0 + k] == caddr[c0] + k * cb;
+      heavy[gi] = !reg;
+    }
+  // longest processing time first: heavy groups (cost 112), then regular (100),
+  // each to the least-loaded CTA
+  std::vector<std::vector<uint32_t>> per(bins);
+  std::vector<uint64_t> load(bins, 0);
+  auto cmp = [&](uint32_t a, uint32_t b2) { return load[a] != load[b2] ? load[a] > load[b2] : a > b2; };
+  std::vector<uint32_t> h(bins);
+  for (uint32_t b = 0; b < bins; ++b) h[b] = b;
+  std::make_heap(h.begin(), h.end(), cmp);
+  for (int pass = 0; pass < 2; ++pass)
+    for (uint64_t gi = 0; gi < ngroups; ++gi) {
+      if (heavy[gi] != (pass == 0)) continue;
+      std::pop_heap(h.begin(), h.end(), cmp);
+      const uint32_t b = h.back();
+      per[b].push_back(uint32_t(gi));
+      load[b] += pass == 0 ? 112 : 100;
+      std::push_heap(h.begin(), h.end(), cmp);
+    }
+  out.resize(bins + 1 + ngroups);
+  out[0] = 0;
+  uint64_t k = bins + 1;
+  for (uint32_t b = 0; b < bins; ++b) {
+    std::sort(per[b].begin(), per[b].end());
+    out[b + 1] = out[b] + uint32_t(per[b].size());
+    for (uint32_t x : per[b]) out[k++] = x;
+  }
+  return bins;
+}
+
 bool hash_mma_ok(const GridDev& g) {
   return g.tmaps64 != nullptr && g.page_shift == 12 && g.chunk_shift >= 12 &&
          g.chunk_shift <= 17;
@@ -877,7 +943,12 @@ int launch_mma(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
 #else
   const int dbg = 0;
 #endif
-  k_hash_mma<C><<<unsigned(blocks), C::THREADS, C::SMEM, s>>>(arena, g, chunk_dig, bt, spec_off,
+  // the balanced schedule covers the whole grid on exactly `blocks` CTAs
+  // (SNAP_MMA_SCHED=0: round robin, for A/B measurements)
+  static const bool sched_on = !(getenv("SNAP_MMA_SCHED") && getenv("SNAP_MMA_SCHED")[0] == '0');
+  GridDev gg = g;
+  if (C::FUSED || !sched_on || !(g.c_begin == 0 && c_end == g.nchunks && g.gs_bins == blocks)) gg.gsched = nullptr;
+  k_hash_mma<C><<<unsigned(blocks), C::THREADS, C::SMEM, s>>>(arena, gg, chunk_dig, bt, spec_off,
                                                                staging, dbg);
   return 1;
 }

@@ -95,7 +95,19 @@ struct GridDev {
   uint64_t xoff = 0;
   // fused K1: predicted staged bytes of this launch's layout (kernel choice)
   uint64_t spec_bytes = 0;
+  // k_hash_mma group schedule of the whole grid (mma_schedule), or nullptr
+  // (round robin): gsched[0..gs_bins] = per-CTA start, then the group order
+  const uint32_t* gsched = nullptr;
+  uint32_t gs_bins = 0;
 };
+
+// Host: balanced k_hash_mma group schedule for a grid of n buffers over `sms`
+// CTAs (groups holding a task that is not 32 contiguous full pages run ~12 %
+// slower; longest-processing-time assignment). out = [bins + 1] starts, then
+// the group indices of CTA 0, CTA 1, ...; returns bins (0: no schedule).
+uint32_t mma_schedule(const uint64_t* addr, const uint64_t* bytes, uint32_t n,
+                      uint32_t page_shift, uint32_t chunk_shift, int sms,
+                      std::vector<uint32_t>& out);
 
 // Open-addressing digest table (dedup + known set), power-of-two capacity.
 
