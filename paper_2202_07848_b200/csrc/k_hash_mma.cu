@@ -886,9 +886,9 @@ uint32_t mma_schedule(const uint64_t* addr, const uint64_t* bytes, uint32_t n,
         reg = caddr[c0 + k] != ~0ull && caddr[c0 + k] == caddr[c0] + k * cb;
       heavy[gi] = !reg;
     }
-  // longest processing time first: heavy groups (cost 200), then regular (100),
+  // longest processing time first: heavy groups (cost 150), then regular (100),
   // each to the least-loaded CTA (SNAP_MMA_HEAVY overrides the heavy cost)
-  static const uint64_t heavy_cost = getenv("SNAP_MMA_HEAVY") ? strtoull(getenv("SNAP_MMA_HEAVY"), nullptr, 10) : 200;
+  static const uint64_t heavy_cost = getenv("SNAP_MMA_HEAVY") ? strtoull(getenv("SNAP_MMA_HEAVY"), nullptr, 10) : 150;
   std::vector<std::vector<uint32_t>> per(bins);
   std::vector<uint64_t> load(bins, 0);
   auto cmp = [&](uint32_t a, uint32_t b2) { return load[a] != load[b2] ? load[a] > load[b2] : a > b2; };

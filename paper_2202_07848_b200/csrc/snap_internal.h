@@ -103,8 +103,9 @@ struct GridDev {
 
 // Host: balanced k_hash_mma group schedule for a grid of n buffers over `sms`
 // CTAs (groups holding a task that is not 32 contiguous full pages run slower;
-// longest-processing-time assignment with those weighted 2x — C3 A/B over
-// weights 1.12 / 1.3 / 1.5 / 2: 2 best, 0.873 -> 0.860 ms per switch). out = [bins + 1] starts, then
+// longest-processing-time assignment with those weighted 1.5x — C3 A/B over
+// weights 1.12 / 1.3 / 1.5 / 2: 1.5 and 2 best, 0.873 -> 0.860 ms per switch;
+// 3 over-weights them: C3 -10 %, CTAs with one heavy group get 9 groups). out = [bins + 1] starts, then
 // the group indices of CTA 0, CTA 1, ...; returns bins (0: no schedule).
 uint32_t mma_schedule(const uint64_t* addr, const uint64_t* bytes, uint32_t n,
                       uint32_t page_shift, uint32_t chunk_shift, int sms,
