@@ -141,3 +141,31 @@ def _fused_case(mma, rng, nbytes):
             slot += 1
             addr += nb + int(rng.integers(0, 2)) * 4096
         _snapshot_check(c, host, regular[:8] + bufs)
+
+
+def test_scheduled_groups_mma(mma):
+    """The balanced group schedule (mma_schedule: groups with buffer-tail tasks spread over
+    the CTAs first, several groups per CTA): 1.5 GiB of buffers of random sizes (~390
+    groups over 148 CTAs, heavy and regular groups interleaved) vs the oracle, twice (the
+    schedule is built once per grid)."""
+    rng = np.random.default_rng(2202)
+    arena_bytes = 3 << 29
+    with mma.Ctx(0, arena_bytes) as c:
+        c.fill_mix64(0, arena_bytes, 31, 0)
+        host = c.read(0, arena_bytes)
+        bufs, addr, slot = [], 0, 0
+        while True:
+            nb = int(rng.integers(1, 6 << 20) // 256 + 1) * 256
+            if addr + nb > arena_bytes:
+                break
+            bufs.append((0, slot, addr, nb, 0))
+            slot += 1
+            addr += nb
+        c.set_buffers(bufs)
+        od, olens, _ = O.hash_chunks([host], bufs)
+        for rep in range(2):
+            c.hash()
+            d, lens = c.digests()
+            assert np.array_equal(lens, olens)
+            bad = np.nonzero(d != od)[0]
+            assert bad.size == 0, f"rep {rep}: {bad.size} chunk digests differ, first {bad[:5]}"
