@@ -111,7 +111,8 @@ int prepare_dedup(snap_ctx* ctx, uint64_t n, TableDev* out, uint64_t** slot, uin
 // splice chunk cache uses its own index as the known set). `inserted`: the K2
 // insert already ran inside K1 (hash_fused) into the prepared table.
 int select_with_known(snap_ctx* ctx, const uint64_t* dig, const uint32_t* lens, uint64_t n,
-                      TableDev kn, bool use_known, bool inserted, uint64_t* spec_next) {
+                      TableDev kn, bool use_known, bool inserted, uint64_t* spec_next,
+                      const uint64_t* fix_spec, uint8_t* fix_staging) {
   uint64_t *slot, *scan, *owner, *offsets, *totals;
   uint8_t* sel;
   uint32_t* list;
@@ -131,7 +132,7 @@ int select_with_known(snap_ctx* ctx, const uint64_t* dig, const uint32_t* lens, 
   RC(ensure(ctx, ctx->totals, 4, &totals));
   if (!inserted) CKL(snap::launch_dedup_insert(dd, kn, use_known, dig, lens, n, slot, ctx->stream));
   CKL(snap::launch_select(dd, slot, lens, n, scan, sel, owner, offsets, list, totals, spec_next,
-                          ctx->stream));
+                          ctx->stream, fix_spec, ctx->arena, &ctx->grid, fix_staging));
   const uint64_t words = snap::scan_state_words(n) + 1;
   CKL(snap::launch_resolve_dups(sel, owner, offsets, n, dd, scan, words, ctx->stream));
   ctx->dd_clean = true;
@@ -145,9 +146,11 @@ namespace {
 
 // Selection over a canonical vector (local grid or allgathered global one).
 int select_impl(snap_ctx* ctx, const uint64_t* dig, const uint32_t* lens, uint64_t n,
-                bool inserted = false, uint64_t* spec_next = nullptr) {
+                bool inserted = false, uint64_t* spec_next = nullptr,
+                const uint64_t* fix_spec = nullptr, uint8_t* fix_staging = nullptr) {
   TableDev kn{P<unsigned long long>(ctx->kn_keys), P<unsigned long long>(ctx->kn_vals), ctx->kn_mask};
-  RC(select_with_known(ctx, dig, lens, n, kn, ctx->kn_count > 0, inserted, spec_next));
+  RC(select_with_known(ctx, dig, lens, n, kn, ctx->kn_count > 0, inserted, spec_next, fix_spec,
+                       fix_staging));
   ctx->selected = true;
   return SNAP_OK;
 }
@@ -554,8 +557,12 @@ int compact_impl(snap_ctx* ctx, uint32_t* moved = nullptr, unsigned int* nmoved 
     }
   }
   ctx->spec_next_done = false;
+  const bool fixed = ctx->fixup_done && !shard && ctx->spec_used && !moved;
+  ctx->fixup_done = false;
   if (nmoved) CK(cudaMemsetAsync(nmoved, 0, 4, ctx->stream));
-  if (ctx->comm && ctx->exchanged) {
+  if (fixed) {
+    // the selection scan already copied the mismatched chunks
+  } else if (ctx->comm && ctx->exchanged) {
     CKL(snap::launch_gather(ctx->arena, ctx->grid, P<uint32_t>(ctx->d_lens),
                             P<uint32_t>(ctx->d_my_list), P<uint64_t>(ctx->d_my_totals),
                             P<uint64_t>(ctx->d_my_off), true, spec_cur, spec_next, st,
@@ -920,9 +927,14 @@ int snap_select(snap_ctx* ctx) {
   uint64_t* spec_next = nullptr;
   if (ctx->spec_used)  // the staging layout becomes the next speculation
     RC(ensure(ctx, ctx->d_spec[1 - ctx->spec_cur], ctx->nchunks, &spec_next));
+  // snap_snapshot: the scan also does the K3 fix-up when the staging image
+  // already holds a whole grid (nothing to grow before the copies)
+  const bool fix = ctx->fixup_request && ctx->spec_used && ctx->staging.cap >= ctx->grid_bytes;
   RC(select_impl(ctx, P<uint64_t>(ctx->d_dig), P<uint32_t>(ctx->d_lens), ctx->nchunks, inserted,
-                 spec_next));
+                 spec_next, fix ? P<uint64_t>(ctx->d_spec[ctx->spec_cur]) : nullptr,
+                 fix ? static_cast<uint8_t*>(ctx->staging.p) : nullptr));
   ctx->spec_next_done = spec_next != nullptr;
+  ctx->fixup_done = fix;
   return SNAP_OK;
 }
 
@@ -1099,7 +1111,10 @@ int snap_snapshot(snap_ctx* ctx) {
   ctx->hashed = true;
   ctx->selected = false;
   ctx->exchanged = false;
-  RC(snap_select(ctx));
+  ctx->fixup_request = true;
+  const int rc = snap_select(ctx);
+  ctx->fixup_request = false;
+  if (rc != SNAP_OK) return rc;
   return snap_compact(ctx);
 }
 

@@ -119,6 +119,9 @@ struct snap_ctx {
   // multi-rank step: global staging offsets (offsets/sel_list/totals) not yet
   // computed from the step's owners (global_offsets() does it on demand)
   bool global_offsets_pending = false;
+  // snap_snapshot asks the single-GPU selection to do the K3 fix-up too
+  // (fixup_request); fixup_done tells compact_impl nothing is left to copy
+  bool fixup_request = false, fixup_done = false;
   DevMem d_tmaps;  // per-buffer TMA tensor maps of the installed grid
   // predicted staging bytes (multi-rank shards are sized to the prediction and
   // grown on demand instead of reserving a whole image per GPU)
@@ -238,7 +241,8 @@ int splice_seed(snap_ctx* ctx, int rank, const uint8_t* image, const uint64_t* s
 
 int select_with_known(snap_ctx* ctx, const uint64_t* dig, const uint32_t* lens, uint64_t n,
                       TableDev kn, bool use_known, bool inserted = false,
-                      uint64_t* spec_next = nullptr);
+                      uint64_t* spec_next = nullptr, const uint64_t* fix_spec = nullptr,
+                      uint8_t* fix_staging = nullptr);
 
 // Per-buffer TMA tensor maps for the hash-only TMA K1 (4 KiB pages; not built
 // when a cp.async variant is forced). On any

@@ -27,6 +27,24 @@
 namespace snap {
 namespace {
 
+// chunk address and warp copy (as in k_copy.cu) for the fix-up fused into the scan
+__device__ __forceinline__ const uint8_t* chunk_ptr(const uint8_t* arena, const GridDev& g,
+                                                    uint64_t gc) {
+  uint32_t lo = 0, hi = g.nbufs;
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (__ldg(g.cstart + mid) <= gc) lo = mid; else hi = mid;
+  }
+  return arena + __ldg(g.addr + lo) + ((gc - __ldg(g.cstart + lo)) << g.chunk_shift);
+}
+
+__device__ __forceinline__ void warp_copy(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src,
+                                          uint32_t len, int lane) {
+  const uint4* s = reinterpret_cast<const uint4*>(src);
+  uint4* d = reinterpret_cast<uint4*>(dst);
+  for (uint32_t i = lane; i < (len >> 4); i += 32) __stcs(d + i, __ldcs(s + i));
+}
+
 __global__ void k_table_clear(TableDev t) {
   const uint64_t n = t.mask + 2;
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -214,7 +232,9 @@ k_select_scan(TableDev dedup, const uint64_t* __restrict__ slot, const uint32_t*
               uint64_t n, uint64_t* __restrict__ status, unsigned int* __restrict__ tile_counter,
               uint8_t* __restrict__ sel, uint64_t* owner,
               uint64_t* __restrict__ offsets, uint32_t* __restrict__ sel_list,
-              uint64_t* __restrict__ totals, uint64_t* __restrict__ spec_next) {
+              uint64_t* __restrict__ totals, uint64_t* __restrict__ spec_next,
+              const uint64_t* __restrict__ spec_cur, const uint8_t* __restrict__ arena,
+              GridDev grid, uint8_t* __restrict__ staging) {
   griddep_wait();
   const uint64_t tile = next_tile(tile_counter);
   const uint64_t ntiles = (n + kTile - 1) / kTile;
@@ -245,6 +265,28 @@ k_select_scan(TableDev dedup, const uint64_t* __restrict__ slot, const uint32_t*
       if (spec_next) spec_next[g] = sl ? off : ~0ull;
     }
     run += val[j];
+  }
+  if (spec_cur) {
+    // K3 fix-up fused (single GPU, speculative K1 layout): a selected chunk the
+    // fused K1 did not already store at its final offset is copied from the
+    // arena by the whole warp (rare: only when the layout changed)
+    const int lane = threadIdx.x & 31;
+    run = run - local;  // this thread's first exclusive prefix again
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+      const uint64_t g = base + j;
+      const uint64_t off = (run & ((1ull << kUnitBits) - 1)) << 8;
+      const bool need = g < n && val[j] != 0 && spec_cur[g] != off;
+      unsigned m = __ballot_sync(0xffffffffu, need);
+      while (m) {
+        const int q = __ffs(m) - 1;
+        m &= m - 1;
+        const uint64_t gq = __shfl_sync(0xffffffffu, g, q);
+        const uint64_t oq = __shfl_sync(0xffffffffu, off, q);
+        warp_copy(staging + oq, chunk_ptr(arena, grid, gq), lens[gq], lane);
+      }
+      run += val[j];
+    }
   }
 }
 
@@ -350,7 +392,9 @@ int launch_dedup_insert(TableDev dedup, TableDev known, bool use_known, const ui
 
 int launch_select(TableDev dedup, const uint64_t* slot, const uint32_t* lens, uint64_t n,
                   uint64_t* scan_state, uint8_t* sel, uint64_t* owner, uint64_t* offsets,
-                  uint32_t* sel_list, uint64_t* totals, uint64_t* spec_next, cudaStream_t s) {
+                  uint32_t* sel_list, uint64_t* totals, uint64_t* spec_next, cudaStream_t s,
+                  const uint64_t* spec_cur, const uint8_t* arena, const GridDev* grid,
+                  uint8_t* staging) {
   const uint64_t tiles = (n + kTile - 1) / kTile;
   if (n == 0) {
     cudaMemsetAsync(totals, 0, 2 * sizeof(uint64_t), s);
@@ -358,7 +402,7 @@ int launch_select(TableDev dedup, const uint64_t* slot, const uint32_t* lens, ui
   }
   launch_pdl(k_select_scan, unsigned(tiles), kThreads, 0, s, dedup, slot, lens, n, scan_state,
              reinterpret_cast<unsigned int*>(scan_state + tiles), sel, owner, offsets, sel_list,
-             totals, spec_next);
+             totals, spec_next, spec_cur, arena, grid ? *grid : GridDev{}, staging);
   return 1;
 }
 

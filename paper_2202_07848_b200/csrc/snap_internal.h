@@ -168,9 +168,13 @@ int launch_dedup_insert(TableDev dedup, TableDev known, bool use_known, const ui
 // scan_state must be zero on entry (left zero by launch_resolve_dups' clean-up);
 // spec_next (nullable) receives the staging layout (offset of selected chunks,
 // ~0 otherwise) — the next speculative layout of the fused K1.
+// spec_cur (nullable): the fused K1's speculative layout — the scan also does
+// the K3 fix-up (copies selected chunks whose offset differs from arena to staging).
 int launch_select(TableDev dedup, const uint64_t* slot, const uint32_t* lens, uint64_t n,
                   uint64_t* scan_state, uint8_t* sel, uint64_t* owner, uint64_t* offsets,
-                  uint32_t* sel_list, uint64_t* totals, uint64_t* spec_next, cudaStream_t s);
+                  uint32_t* sel_list, uint64_t* totals, uint64_t* spec_next, cudaStream_t s,
+                  const uint64_t* spec_cur = nullptr, const uint8_t* arena = nullptr,
+                  const GridDev* grid = nullptr, uint8_t* staging = nullptr);
 // Shard scan of writer q over the global writer vector (write_list for q ==
 // this rank: local chunk list + offsets).
 int launch_shard_scan(const int32_t* writer, const uint32_t* glens, uint32_t nranks, uint64_t maxn,
