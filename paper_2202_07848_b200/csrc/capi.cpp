@@ -350,8 +350,22 @@ int select_stripe_impl(snap_ctx* ctx) {
   const uint64_t* gdig = gdig_region(ctx, ctx->xepoch);
   const uint32_t* glens = P<uint32_t>(ctx->d_glens);
   CKL(snap::launch_dedup_insert(dd, kn, ctx->kn_count > 0, gdig, glens, n, slot, ctx->stream));
+  // snap_snapshot with a whole-grid staging image: the shard scan also does
+  // the K3 fix-up and writes the next speculative layout
+  snap::FixUp fix;
+  if (ctx->fixup_request && ctx->spec_used && ctx->staging.cap >= ctx->grid_bytes) {
+    fix.spec_cur = P<uint64_t>(ctx->d_spec[ctx->spec_cur]);
+    RC(ensure(ctx, ctx->d_spec[1 - ctx->spec_cur], ctx->nchunks, &fix.spec_next));
+    fix.nlocal = ctx->nchunks;
+    fix.arena = ctx->arena;
+    fix.grid = ctx->grid;
+    fix.staging = static_cast<uint8_t*>(ctx->staging.p);
+  }
   CKL(snap::launch_select_stripe(dd, slot, gdig, glens, ctx->nranks, maxn, ctx->rank, sel, owner,
-                                 writer, scan2, shard_off, my_list, my_off, my_tot, ctx->stream));
+                                 writer, scan2, shard_off, my_list, my_off, my_tot, ctx->stream,
+                                 fix));
+  ctx->fixup_done = fix.staging != nullptr;
+  ctx->spec_next_done = fix.staging != nullptr;
   ctx->dd_clean = true;  // the shard scan emptied the table
   ctx->sel_n = n;
   ctx->selected = true;
@@ -557,7 +571,7 @@ int compact_impl(snap_ctx* ctx, uint32_t* moved = nullptr, unsigned int* nmoved 
     }
   }
   ctx->spec_next_done = false;
-  const bool fixed = ctx->fixup_done && !shard && ctx->spec_used && !moved;
+  const bool fixed = ctx->fixup_done && ctx->spec_used && !moved;
   ctx->fixup_done = false;
   if (nmoved) CK(cudaMemsetAsync(nmoved, 0, 4, ctx->stream));
   if (fixed) {

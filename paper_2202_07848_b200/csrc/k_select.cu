@@ -96,13 +96,15 @@ __global__ void k_select_stripe(TableDev dedup, const uint64_t* __restrict__ slo
                                 const uint64_t* __restrict__ gdig, const uint32_t* __restrict__ glens,
                                 uint32_t nranks, uint64_t maxn, uint8_t* __restrict__ sel,
                                 uint64_t* __restrict__ owner, int32_t* __restrict__ writer,
-                                uint64_t* __restrict__ scan_state, uint64_t scan_words) {
+                                uint64_t* __restrict__ scan_state, uint64_t scan_words,
+                                uint64_t* __restrict__ spec_next, uint64_t nlocal) {
   griddep_wait();
   const uint64_t n = uint64_t(nranks) * maxn;
   const uint64_t end = n > scan_words ? n : scan_words;
   for (uint64_t g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < end;
        g += uint64_t(gridDim.x) * blockDim.x) {
     if (g < scan_words) scan_state[g] = 0;
+    if (spec_next && g < nlocal) spec_next[g] = ~0ull;
     if (g >= n) continue;
     const uint64_t s = slot[g];
     const uint64_t own = s == ~0ull ? ~0ull : dedup.vals[s];
@@ -298,7 +300,7 @@ k_shard_scan(const int32_t* __restrict__ writer, const uint32_t* __restrict__ gl
              uint64_t maxn, int32_t me, int write_list, uint64_t* __restrict__ status,
              unsigned int* __restrict__ tile_counter, uint64_t* __restrict__ shard_off,
              uint32_t* __restrict__ my_list, uint64_t* __restrict__ my_off,
-             uint64_t* __restrict__ totals, TableDev clear) {
+             uint64_t* __restrict__ totals, TableDev clear, FixUp fix) {
   griddep_wait();
   if (clear.keys) {  // the dedup table the previous kernel consumed: left empty
     const uint64_t tab = clear.mask + 2;
@@ -333,6 +335,34 @@ k_shard_scan(const int32_t* __restrict__ writer, const uint32_t* __restrict__ gl
       }
     }
     run += val[j];
+  }
+  if (fix.staging) {
+    // K3 fix-up fused (speculative K1 layout): this rank's chunks whose final
+    // shard offset differs from the speculated one are copied from the arena
+    // (local chunk g % maxn holds the bytes: same digest and length)
+    const int lane = threadIdx.x & 31;
+    run = run - local;
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+      const uint64_t g = base + j;
+      const uint64_t off = (run & ((1ull << kUnitBits) - 1)) << 8;
+      const uint64_t i = g % maxn;
+      bool need = false;
+      if (val[j]) {
+        if (fix.spec_next) fix.spec_next[i] = off;
+        need = fix.spec_cur[i] != off;
+      }
+      unsigned m = __ballot_sync(0xffffffffu, need);
+      while (m) {
+        const int q = __ffs(m) - 1;
+        m &= m - 1;
+        const uint64_t iq = __shfl_sync(0xffffffffu, i, q);
+        const uint64_t oq = __shfl_sync(0xffffffffu, off, q);
+        warp_copy(fix.staging + oq, chunk_ptr(fix.arena, fix.grid, iq), glens[iq + uint64_t(me) * maxn],
+                  lane);
+      }
+      run += val[j];
+    }
   }
 }
 
@@ -419,7 +449,7 @@ int launch_shard_scan(const int32_t* writer, const uint32_t* glens, uint32_t nra
   k_shard_scan<<<unsigned(tiles), kThreads, 0, s>>>(
       writer, glens, n, maxn, q, write_list ? 1 : 0, scan_state,
       reinterpret_cast<unsigned int*>(scan_state + tiles), shard_off, my_list, my_off, totals,
-      TableDev{});
+      TableDev{}, FixUp{});
   return 1;
 }
 
@@ -427,7 +457,7 @@ int launch_select_stripe(TableDev dedup, const uint64_t* slot, const uint64_t* g
                          const uint32_t* glens, uint32_t nranks, uint64_t maxn, int32_t me,
                          uint8_t* sel, uint64_t* owner, int32_t* writer, uint64_t* scan_state,
                          uint64_t* shard_off, uint32_t* my_list, uint64_t* my_off,
-                         uint64_t* totals, cudaStream_t s) {
+                         uint64_t* totals, cudaStream_t s, const FixUp& fix) {
   const uint64_t n = uint64_t(nranks) * maxn;
   const uint64_t tiles = (n + kTile - 1) / kTile;
   if (n == 0) {
@@ -435,10 +465,11 @@ int launch_select_stripe(TableDev dedup, const uint64_t* slot, const uint64_t* g
     return 0;
   }
   launch_pdl(k_select_stripe, grid_for(n, 256, 148 * 16), 256, 0, s, dedup, slot, gdig, glens,
-             nranks, maxn, sel, owner, writer, scan_state, tiles + 1);
+             nranks, maxn, sel, owner, writer, scan_state, tiles + 1,
+             fix.staging ? fix.spec_next : nullptr, fix.nlocal);
   launch_pdl(k_shard_scan, unsigned(tiles), kThreads, 0, s, writer, glens, n, maxn, me, 1,
              scan_state, reinterpret_cast<unsigned int*>(scan_state + tiles), shard_off, my_list,
-             my_off, totals, dedup);
+             my_off, totals, dedup, fix);
   return 2;
 }
 

@@ -180,6 +180,17 @@ int launch_select(TableDev dedup, const uint64_t* slot, const uint32_t* lens, ui
 int launch_shard_scan(const int32_t* writer, const uint32_t* glens, uint32_t nranks, uint64_t maxn,
                       int32_t q, bool write_list, uint64_t* scan_state, uint64_t* shard_off,
                       uint32_t* my_list, uint64_t* my_off, uint64_t* totals, cudaStream_t s);
+// K3 fix-up fused into the multi-rank selection (staging == nullptr: off):
+// spec_next[0..nlocal) reset by k_select_stripe, then written and the
+// mismatched chunks copied by this rank's shard scan.
+struct FixUp {
+  const uint64_t* spec_cur = nullptr;
+  uint64_t* spec_next = nullptr;
+  uint64_t nlocal = 0;
+  const uint8_t* arena = nullptr;
+  GridDev grid{};
+  uint8_t* staging = nullptr;
+};
 // Multi-rank step: owner / sel / writer per global chunk from the filled dedup
 // table (k_select_stripe), then rank `me`'s shard scan, which also empties the
 // table; the global staging offsets are left to launch_select (on demand).
@@ -187,7 +198,7 @@ int launch_select_stripe(TableDev dedup, const uint64_t* slot, const uint64_t* g
                          const uint32_t* glens, uint32_t nranks, uint64_t maxn, int32_t me,
                          uint8_t* sel, uint64_t* owner, int32_t* writer, uint64_t* scan_state,
                          uint64_t* shard_off, uint32_t* my_list, uint64_t* my_off,
-                         uint64_t* totals, cudaStream_t s);
+                         uint64_t* totals, cudaStream_t s, const FixUp& fix = FixUp{});
 // host pages: first-occurrence / known-set / previous-page-set classification
 // (flags bit 1 fresh, bit 2 inc; counts[0..1] += fresh, inc; counts zeroed by the caller)
 int launch_page_classify(TableDev pages, TableDev known, bool use_known, TableDev prev,
