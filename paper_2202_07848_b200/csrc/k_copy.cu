@@ -208,23 +208,44 @@ k_splice_in(uint8_t* __restrict__ arena, GridDev to, const uint32_t* __restrict_
   const uint64_t w0 = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
   const uint64_t nw = (uint64_t(gridDim.x) * kThreads) >> 5;
   unsigned long long swapped = 0, resident = 0, missing = 0;
-  for (uint64_t g = w0; g < to.nchunks; g += nw) {
-    const uint64_t d = want[g];
-    const uint32_t len = lens[g];
-    const int64_t m = match ? match[g] : -1;
-    if (m >= 0 && dig_from[m] == d) {
-      resident += len;
-      continue;
+  // resident test of 8 chunks per warp step (lanes 0-7; the grid keeps about
+  // one step per warp, so swap-ins still spread over every warp); the chunks
+  // that need bytes from the cache are copied one at a time by the whole warp
+  constexpr int kTest = 8;
+  const int tl = lane & (kTest - 1);
+  for (uint64_t b = w0 * kTest; b < to.nchunks; b += nw * kTest) {
+    const uint64_t g = b + tl;
+    uint64_t d = 0;
+    uint32_t len = 0;
+    bool need = false;
+    if (g < to.nchunks) {
+      d = want[g];
+      len = lens[g];
+      const int64_t m = match ? match[g] : -1;
+      if (m >= 0 && dig_from[m] == d) {
+        if (lane < kTest) resident += len;
+      } else {
+        need = true;
+      }
     }
-    const uint64_t s = table_find(cache, d);
-    if (s == ~0ull) {
-      missing += 1;
-      continue;
+    unsigned msk = __ballot_sync(0xffffffffu, need) & ((1u << kTest) - 1);
+    while (msk) {
+      const int q = __ffs(msk) - 1;
+      msk &= msk - 1;
+      const uint64_t gq = __shfl_sync(0xffffffffu, g, q);
+      const uint64_t dq = __shfl_sync(0xffffffffu, d, q);
+      const uint32_t lq = __shfl_sync(0xffffffffu, len, q);
+      const uint64_t s = table_find(cache, dq);
+      if (s == ~0ull) {
+        if (lane == 0) missing += 1;
+        continue;
+      }
+      uint8_t* dst = const_cast<uint8_t*>(chunk_ptr(arena, to, gq));
+      warp_copy(dst, cache_base + cache.vals[s], lq, lane);
+      if (lane == 0) swapped += lq;
     }
-    uint8_t* dst = const_cast<uint8_t*>(chunk_ptr(arena, to, g));
-    warp_copy(dst, cache_base + cache.vals[s], len, lane);
-    swapped += len;
   }
+  for (int o = 16; o > 0; o >>= 1) resident += __shfl_xor_sync(0xffffffffu, resident, o);
   if (lane == 0) {
     if (swapped) atomicAdd(counters + 0, swapped);
     if (resident) atomicAdd(counters + 1, resident);
@@ -295,7 +316,7 @@ int launch_splice_in(uint8_t* arena, const GridDev& to, const uint32_t* lens, co
                      const uint8_t* cache_base, unsigned long long* counters, cudaStream_t s) {
   cudaMemsetAsync(counters, 0, 3 * sizeof(unsigned long long), s);
   if (to.nchunks == 0) return 0;
-  uint64_t blocks = (to.nchunks * 32 + kThreads - 1) / kThreads;
+  uint64_t blocks = (to.nchunks * 4 + kThreads - 1) / kThreads;  // 8 chunks per warp step
   if (blocks > copy_grid()) blocks = copy_grid();
   launch_pdl(k_splice_in, unsigned(blocks), kThreads, 0, s, arena, to, lens, want, match, dig_from,
              cache, cache_base, counters);
