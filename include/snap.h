@@ -17,8 +17,13 @@
  *    Calls that return host data synchronise that stream once per call.
  *  - A ctx is used by one host thread at a time (the reference's proxy
  *    serializes all device access); different ctxs are independent.
- *    With a communicator attached, snapshot/select/exchange calls are
- *    collective: every rank makes the same sequence of them.
+ *    With a communicator attached, snap_snapshot / snap_select /
+ *    snap_snapshot_host / snap_known_commit AND every call that installs a grid
+ *    (snap_set_buffers, snap_load) are collective: every rank makes the same
+ *    sequence of them (the grid's chunk counts and lengths are exchanged when
+ *    it is installed, so a snapshot always issues the same NCCL sequence).
+ *    snap_comm_init / snap_comm_destroy are collective over the new / current
+ *    communicator.
  *  - Return codes (common.hpp:31-49 error conventions):
  *      SNAP_OK        success
  *      SNAP_EINVAL    bad argument / geometry          (ConfigError)
@@ -215,9 +220,11 @@ int snap_restore_self(snap_ctx* ctx, int verify);
 
 #define SNAP_U64 0
 #define SNAP_F32 1
+#define SNAP_BF16 2
 /* K5: dst[i] = sum_r src_r[i] over `nsrc` arena ranges, fixed ascending order
- * (u64 modular: collectives.cpp:140-141; f32: ((s0+s1)+s2)+..., IEEE RN).
- * With accumulate != 0, dst is the first addend. Async. */
+ * (u64 modular: collectives.cpp:140-141; f32: ((s0+s1)+s2)+..., IEEE RN;
+ * bf16: the same left-to-right sum in fp32 of the bf16 values, rounded once to
+ * bf16, RN-even). With accumulate != 0, dst is the first addend. Async. */
 int snap_grad_sum(snap_ctx* ctx, int dtype, const uint64_t* src_addrs, uint32_t nsrc,
                   uint64_t dst_addr, uint64_t elems, int accumulate);
 
@@ -226,19 +233,40 @@ int snap_grad_sum(snap_ctx* ctx, int dtype, const uint64_t* src_addrs, uint32_t 
 /* Context switch between time-sliced ranks sharing this GPU
  * (GpuLedger::plan_switch + execute_switch, splice.cpp:167-306, called by
  * JobRuntime::switch_to, job.cpp:146-198). The reference's host cache becomes a
- * digest-indexed chunk cache of `cache_bytes` in HBM. */
+ * digest-indexed chunk cache in HBM: a fixed array of chunk slots whose chunks
+ * no rank records any more are reclaimed when a swap-out could run out of
+ * slots (the reference's std::map only grows, splice.hpp:128). */
 typedef struct {
   uint64_t hashed_bytes;   /* live bytes of the outgoing rank digested (K1) */
   uint64_t swap_out_bytes; /* bytes newly saved to the chunk cache (K3) */
   uint64_t swap_in_bytes;  /* bytes restored from the chunk cache (K4) */
   uint64_t resident_bytes; /* incoming bytes already in place (same range, same digest) */
-  uint64_t cache_bytes;    /* chunk cache occupancy after the switch */
+  uint64_t cache_bytes;    /* bytes of the chunks the cache holds after the switch */
+  uint64_t install_bytes;  /* queued collective results installed (switch_report, job.cpp:165-171) */
+  uint64_t cache_free_bytes; /* free slot capacity after the switch */
+  uint64_t reclaimed_bytes;  /* bytes reclaimed by the cache so far (cumulative) */
 } snap_switch_stats;
+/* cache_bytes of HBM in 64 KiB slots (snap_splice_init) or slot_bytes slots
+ * (power of two >= 256; a rank's chunk_bytes must not exceed it). */
 int snap_splice_init(snap_ctx* ctx, uint64_t cache_bytes);
+int snap_splice_init_slots(snap_ctx* ctx, uint64_t cache_bytes, uint32_t slot_bytes);
 int snap_splice_set_rank(snap_ctx* ctx, int rank, const snap_buf* bufs, uint64_t n,
                          const snap_geom* geom);
 int snap_splice_switch(snap_ctx* ctx, int from, int to, snap_switch_stats* stats);
 int snap_splice_recorded(snap_ctx* ctx, int rank, uint64_t* digests, uint64_t* n);
+/* Collective-result install for the sliced ranks of this GPU
+ * (JobRuntime::on_coll_complete, job.cpp:206-222 -> GpuLedger::install_result,
+ * splice.cpp:142-148): the result at arena [src_addr, +bytes) is written into
+ * rank ranks[i]'s buffer at dst_addrs[i]. The active rank (the `to` of the last
+ * switch; rank < 0 or a ctx without splicing: immediately) gets it now; the
+ * others queue it (ProxyServer::install_queue, proxy.hpp:75-79; one library
+ * copy of the result shared by the queued entries) and the next
+ * snap_splice_switch to that rank applies it after its swap-ins
+ * (switch_to, job.cpp:164-171), reported as install_bytes. 16-byte aligned. */
+int snap_splice_install(snap_ctx* ctx, const int* ranks, const uint64_t* dst_addrs, uint32_t n,
+                        uint64_t src_addr, uint64_t bytes);
+/* Queued installs of `rank`: number and bytes. */
+int snap_splice_pending(snap_ctx* ctx, int rank, uint64_t* count, uint64_t* bytes);
 
 /* ------------------------------------------------ multi-GPU (NCCL/NVLink) */
 
@@ -274,8 +302,30 @@ int snap_ipc_import(snap_ctx* ctx, int nranks, const void* handles);
 int snap_restore_shards(snap_ctx* ctx, int src_rank, int verify);
 
 /* Device-level allreduce of a gradient range (after K5 local sum,
- * collectives.cpp:147-154 local closer). Async. */
+ * collectives.cpp:147-154 local closer) through NCCL (its own reduction
+ * order; exact for u64). Async. */
 int snap_allreduce(snap_ctx* ctx, int dtype, uint64_t addr, uint64_t elems);
+/* Fixed-order device-level allreduce (the CollectiveEngine sum,
+ * collectives.cpp:137-154, with the north star's fixed-order fp32 mode),
+ * collective: every GPU passes the gradients of its sliced ranks (nlocal <= 16
+ * arena ranges, each with a globally unique order key, e.g. its dp rank) and
+ * the destination range of its own result. The sum over every source of every
+ * GPU is taken in ascending key order, ((g_k0 + g_k1) + g_k2) + ... (u64 mod
+ * 2^64; f32 IEEE RN; bf16 in fp32, rounded once) — bit-identical on every GPU
+ * and to a CPU left-to-right sum. One fused kernel per GPU reads its 1/N slice
+ * of every source (peer arenas over NVLink, CUDA IPC) and stores the summed
+ * slice into every GPU's destination: reduce-scatter + all-gather in one pass
+ * over peer memory. The destination may be one of the sources. Passing one
+ * K5 partial sum per GPU (key = GPU index) gives the hierarchical order. */
+int snap_allreduce_ordered(snap_ctx* ctx, int dtype, const uint32_t* keys, const uint64_t* src_addrs,
+                           uint32_t nlocal, uint64_t dst_addr, uint64_t elems);
+/* In-process communicator: `nranks` ctxs driven by threads of one process
+ * (e.g. N ranks emulated on one GPU, the reference's whole-fleet-in-one-process
+ * model) join the group named `key`; every collective entry point then works
+ * as with NCCL (collectives through host memory, IPC handles of this process
+ * resolved to the exporting ctx's buffers). Blocks until all ranks joined.
+ * Released by snap_comm_destroy / snap_close. */
+int snap_comm_init_local(snap_ctx* ctx, int nranks, int rank, const char* key);
 
 /* ------------------------------------- squash-window validation (§8f-3) */
 

@@ -71,6 +71,7 @@ def lib():
                                  C.c_void_p]
         L.or_grad_sum_u64.argtypes = [C.c_void_p, C.c_uint32, C.c_uint64, C.c_void_p]
         L.or_grad_sum_f32.argtypes = [C.c_void_p, C.c_uint32, C.c_uint64, C.c_void_p]
+        L.or_grad_sum_bf16.argtypes = [C.c_void_p, C.c_uint32, C.c_uint64, C.c_void_p]
         _lib = L
     return _lib
 
@@ -133,6 +134,22 @@ def ref():
         L.ref_splice_read.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64]
         L.ref_splice_switch.restype = C.c_int
         L.ref_splice_switch.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p]
+        L.ref_manifest_run.restype = C.c_void_p
+        L.ref_manifest_run.argtypes = [C.c_char_p]
+        L.ref_manifest_free.argtypes = [C.c_void_p]
+        L.ref_manifest_count.restype = C.c_int
+        L.ref_manifest_count.argtypes = [C.c_void_p]
+        L.ref_manifest_stats.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+        L.ref_manifest_ndev.restype = C.c_int
+        L.ref_manifest_ndev.argtypes = [C.c_void_p, C.c_int, C.c_int]
+        L.ref_manifest_dev.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                       C.c_void_p]
+        L.ref_splice_switch2.restype = C.c_int
+        L.ref_splice_switch2.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p]
+        L.ref_splice_mark_pending.restype = C.c_int
+        L.ref_splice_mark_pending.argtypes = [C.c_void_p, C.c_int, C.c_int]
+        L.ref_splice_install.restype = C.c_int
+        L.ref_splice_install.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_uint64]
         _ref = L
     return _ref
 
@@ -285,9 +302,53 @@ def grad_sum_u64(grads):
     return out
 
 
+def grad_sum_bf16(grads):
+    """bf16 gradients as uint16 arrays: ascending-order fp32 chain, one bf16 rounding."""
+    gs = [np.ascontiguousarray(g, dtype=np.uint16) for g in grads]
+    ptrs = (C.c_void_p * len(gs))(*[g.ctypes.data for g in gs])
+    out = np.empty_like(gs[0])
+    lib().or_grad_sum_bf16(ptrs, len(gs), gs[0].size, _p(out))
+    return out
+
+
 def grad_sum_f32(grads):
     gs = [np.ascontiguousarray(g, dtype=np.float32) for g in grads]
     ptrs = (C.c_void_p * len(gs))(*[g.ctypes.data for g in gs])
     out = np.empty_like(gs[0])
     lib().or_grad_sum_f32(ptrs, len(gs), gs[0].size, _p(out))
     return out
+
+
+def ref_manifests(scenario: dict):
+    """Every checkpoint manifest of the first job of `scenario`, built by the reference's
+    own scheduler + build_manifest (oracle/ref_shim.cpp ref_manifest_run): stats and, per
+    rank, the DevRecs {slot, addr, words, cat, digest} with their content (u64 words)."""
+    import json
+    R = ref()
+    h = R.ref_manifest_run(json.dumps(scenario).encode())
+    if not h:
+        raise RuntimeError("reference scenario run failed")
+    try:
+        out = []
+        for k in range(R.ref_manifest_count(h)):
+            st = np.zeros(8, np.uint64)
+            R.ref_manifest_stats(h, k, _p(st))
+            names = ["s_g", "s_cr", "s_cr_inc", "upload_bytes", "dump_d2h_max",
+                     "total_blob_bytes", "device_upload", "world"]
+            m = {n: int(v) for n, v in zip(names, st)}
+            m["dev"] = []
+            for r in range(m["world"]):
+                recs = []
+                for i in range(R.ref_manifest_ndev(h, k, r)):
+                    rec = np.zeros(5, np.uint64)
+                    R.ref_manifest_dev(h, k, r, i, _p(rec), None)
+                    words = np.zeros(int(rec[2]), np.uint64)
+                    R.ref_manifest_dev(h, k, r, i, _p(rec), _p(words))
+                    recs.append({"slot": int(np.int64(rec[0])), "addr": int(rec[1]),
+                                 "words": int(rec[2]), "cat": int(np.int64(rec[3])),
+                                 "digest": int(rec[4]), "content": words})
+                m["dev"].append(recs)
+            out.append(m)
+        return out
+    finally:
+        R.ref_manifest_free(h)

@@ -7,12 +7,18 @@
 #include <atomic>
 #include <cstring>
 #include <map>
+#include <set>
 #include <memory>
 #include <thread>
 #include <vector>
 
 #include "fleetsim/alloc.hpp"
 #include "fleetsim/ckpt.hpp"
+#include "fleetsim/oracle.hpp"
+#include "fleetsim/runner.hpp"
+#include "fleetsim/scenario.hpp"
+#include "fleetsim/sched.hpp"
+#include "fleetsim/trace.hpp"
 #include "fleetsim/sim.hpp"
 #include "fleetsim/splice.hpp"
 #include "fleetsim/vdev.hpp"
@@ -222,6 +228,10 @@ void ref_grad_sum_u64(const uint64_t* const* g, uint32_t nranks, uint64_t n, uin
 struct RefSplice {
   std::unique_ptr<vdev::Gpu> gpu;
   std::unique_ptr<splice::GpuLedger> led;
+  // JobRuntime's side of result installs (job.cpp:164-171, 206-222): the rank
+  // of the last switch is active; the others queue (ProxyServer::install_queue)
+  RankId active = kNoRank;
+  std::map<RankId, std::vector<std::pair<int, std::vector<u64>>>> queue;
 };
 
 void* ref_splice_new(uint64_t mem_bytes, uint64_t max_buf) {
@@ -279,6 +289,154 @@ int ref_splice_switch(void* p, int from, int to, uint64_t* out) {
     return -1;
   } catch (const InternalError&) {
     return -2;
+  }
+}
+
+// ---- build_manifest through the reference's own scheduler (ckpt.cpp:79-189) ----
+// Runs a scenario (Scenario::parse JSON) the way cli::run_scenario does
+// (runner.cpp:20-80) but in small steps of simulated time, capturing every
+// checkpoint manifest of job 1 as it is produced, plus the device content of
+// every DevRec (BlobStore::get of its digest, digest-verified). device_upload =
+// bytes of the manifest's unique device blobs whose digest the store did not
+// hold before this checkpoint (build_manifest's `fresh`, device part only).
+struct RefManifests {
+  struct M {
+    uint64_t s_g, s_cr, s_cr_inc, upload, dump_d2h_max, total_blob, device_upload, world;
+    std::vector<std::vector<ckpt::WorkerSnapshot::DevRec>> dev;  // [rank]
+    std::vector<std::vector<std::vector<u64>>> content;          // [rank][i]
+  };
+  std::vector<M> ms;
+};
+
+void* ref_manifest_run(const char* scenario_json) {
+  try {
+    auto sc = cli::Scenario::parse(Json::parse(scenario_json));
+    sim::Engine eng;
+    TraceSink trace(false);
+    ckpt::BlobStore store;
+    sched::Scheduler sched(eng, sc.cost, trace, store, sc.fleet, sc.sla);
+    std::map<std::string, int> ids;
+    for (size_t i = 0; i < sc.jobs.size(); ++i) {
+      auto spec = sc.jobs[i].spec;
+      spec.seed = sim::mix3(sc.seed, i, spec.seed);
+      auto cfg = sc.jobs[i].cfg;
+      std::vector<Dur> mb;
+      if (cli::oracle_feasible(spec, nullptr)) mb = oracle::run(wl::build_job(spec), sc.cost).minibatch_ns;
+      eng.schedule(from_secs(sc.jobs[i].arrival_sec), [&sched, &ids, spec, cfg, mb]() {
+        ids[spec.name] = sched.submit(spec, cfg, mb);
+      });
+    }
+    for (const auto& ev : sc.events)
+      if (ev.kind == "checkpoint")
+        eng.schedule(from_secs(ev.at_sec), [&sched, &ids, ev]() {
+          auto it = ids.find(ev.job);
+          if (it != ids.end()) sched.request_checkpoint(it->second);
+        });
+    auto* out = new RefManifests();
+    std::set<u64> seen;  // every digest the store held before a checkpoint
+    int count = 0;
+    const Time step = 5 * kUsec;
+    for (Time h = step;; h += step) {
+      const bool drained = eng.run(h);
+      if (!sched.jobs().empty()) {
+        auto& rec = sched.rec(sched.jobs().begin()->first);
+        if (rec.ckpt_count > count && rec.last_manifest) {
+          count = rec.ckpt_count;
+          const auto& m = *rec.last_manifest;
+          RefManifests::M x{m.s_g, m.s_cr, m.s_cr_inc, m.upload_bytes, m.dump_d2h_max,
+                            m.total_blob_bytes, 0, uint64_t(m.workers.size()), {}, {}};
+          for (const auto& [d, b] : m.device_blobs)
+            if (!seen.count(d)) x.device_upload += b;
+          for (const auto& ws : m.workers) {
+            x.dev.push_back(ws.dev);
+            x.content.emplace_back();
+            for (const auto& d : ws.dev) x.content.back().push_back(store.get(sim::Digest{d.digest}));
+            for (u64 p : ws.pages) seen.insert(p);
+            for (const auto& f : ws.files)
+              if (!f.deleted) seen.insert(f.digest);
+          }
+          for (const auto& [d, b] : m.device_blobs) seen.insert(d);
+          out->ms.push_back(std::move(x));
+        }
+      }
+      if (drained) break;
+      if (h > 3600 * kSecond) break;
+    }
+    return out;
+  } catch (...) {
+    return nullptr;
+  }
+}
+void ref_manifest_free(void* h) { delete static_cast<RefManifests*>(h); }
+int ref_manifest_count(void* h) { return int(static_cast<RefManifests*>(h)->ms.size()); }
+// out = {s_g, s_cr, s_cr_inc, upload_bytes, dump_d2h_max, total_blob_bytes, device_upload, world}
+void ref_manifest_stats(void* h, int k, uint64_t* out) {
+  const auto& m = static_cast<RefManifests*>(h)->ms.at(k);
+  const uint64_t v[8] = {m.s_g, m.s_cr, m.s_cr_inc, m.upload, m.dump_d2h_max, m.total_blob,
+                         m.device_upload, m.world};
+  std::memcpy(out, v, sizeof v);
+}
+int ref_manifest_ndev(void* h, int k, int rank) {
+  return int(static_cast<RefManifests*>(h)->ms.at(k).dev.at(rank).size());
+}
+// rec = {slot, addr, words, cat, digest}
+void ref_manifest_dev(void* h, int k, int rank, int i, uint64_t* rec, uint64_t* words) {
+  const auto& m = static_cast<RefManifests*>(h)->ms.at(k);
+  const auto& d = m.dev.at(rank).at(i);
+  rec[0] = uint64_t(int64_t(d.slot));
+  rec[1] = d.addr;
+  rec[2] = d.words;
+  rec[3] = uint64_t(int64_t(d.cat));
+  rec[4] = d.digest;
+  if (words) std::memcpy(words, m.content.at(rank).at(i).data(), d.words * 8);
+}
+
+// switch_to (job.cpp:146-171): plan, execute, then the queued installs of
+// `to`. out = {swap_out, swap_in, d2d, moves, host_cache_bytes, install_bytes}
+int ref_splice_switch2(void* p, int from, int to, uint64_t* out) {
+  auto* s = static_cast<RefSplice*>(p);
+  const int rc = ref_splice_switch(p, from, to, out);
+  if (rc != 0) return rc;
+  uint64_t inst = 0;
+  try {
+    if (to >= 0) {
+      for (auto& [slot, words] : s->queue[to]) {
+        s->led->install_result(to, slot, words);
+        inst += words.size() * 8;
+      }
+      s->queue[to].clear();
+    }
+  } catch (const InternalError&) {
+    return -2;
+  }
+  s->active = to < 0 ? kNoRank : to;
+  out[5] = inst;
+  return 0;
+}
+
+// WorkerExec::do_collective marks the issuer's gradient pending (worker.cpp:298)
+int ref_splice_mark_pending(void* p, int rank, int slot) {
+  try {
+    static_cast<RefSplice*>(p)->led->mark_pending_result(rank, slot);
+    return 0;
+  } catch (...) {
+    return -1;
+  }
+}
+
+// on_coll_complete (job.cpp:206-222): active rank installs now, others queue
+int ref_splice_install(void* p, int rank, int slot, const uint64_t* words, uint64_t n) {
+  auto* s = static_cast<RefSplice*>(p);
+  try {
+    if (s->active == rank)
+      s->led->install_result(rank, slot, std::span<const u64>(words, n));
+    else
+      s->queue[rank].push_back({slot, std::vector<u64>(words, words + n)});
+    return 0;
+  } catch (const InternalError&) {
+    return -2;
+  } catch (...) {
+    return -1;
   }
 }
 

@@ -255,3 +255,27 @@ void or_grad_sum_f32(const float* const* grads, uint32_t nranks, uint64_t n, flo
     out[i] = s;
   }
 }
+
+/* bf16 gradients (C5): the same ascending-order chain in fp32 over the bf16
+ * values, rounded once to bf16 (round to nearest, ties to even; NaN stays a
+ * quiet NaN). */
+static float or_bf16_to_f32(uint16_t h) {
+  union { uint32_t u; float f; } x;
+  x.u = (uint32_t)h << 16;
+  return x.f;
+}
+static uint16_t or_f32_to_bf16(float f) {
+  union { uint32_t u; float f; } x;
+  x.f = f;
+  if ((x.u & 0x7f800000u) == 0x7f800000u && (x.u & 0x007fffffu)) return (uint16_t)((x.u >> 16) | 0x40);
+  x.u += 0x7fffu + ((x.u >> 16) & 1u);
+  return (uint16_t)(x.u >> 16);
+}
+void or_grad_sum_bf16(const uint16_t* const* grads, uint32_t nranks, uint64_t n, uint16_t* out) {
+#pragma omp parallel for schedule(static)
+  for (uint64_t i = 0; i < n; ++i) {
+    volatile float s = or_bf16_to_f32(grads[0][i]);
+    for (uint32_t r = 1; r < nranks; ++r) s = s + or_bf16_to_f32(grads[r][i]);
+    out[i] = or_f32_to_bf16(s);
+  }
+}

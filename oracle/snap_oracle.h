@@ -82,6 +82,7 @@ void or_restore(uint8_t* const* arenas, const or_buf* bufs, uint64_t n, uint32_t
  * u64 modular and fp32 fixed (ascending dp) order. */
 void or_grad_sum_u64(const uint64_t* const* grads, uint32_t nranks, uint64_t n, uint64_t* out);
 void or_grad_sum_f32(const float* const* grads, uint32_t nranks, uint64_t n, float* out);
+void or_grad_sum_bf16(const uint16_t* const* grads, uint32_t nranks, uint64_t n, uint16_t* out);
 
 #ifdef __cplusplus
 }

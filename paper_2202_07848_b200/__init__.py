@@ -18,7 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SNAP_LIB_PATH") or os.path.join(HERE, "libsnap.so")
 
 SNAP_OK, SNAP_EINVAL, SNAP_ENOMEM, SNAP_EFAULT, SNAP_ECUDA, SNAP_EINTERNAL = 0, -1, -2, -3, -4, -5
-U64, F32 = 0, 1
+U64, F32, BF16 = 0, 1, 2
 
 # vdev::BufCat (vdev.hpp:17)
 PARAM, OPTSTATE, GRAD, ACTIVATION, SCRATCH = range(5)
@@ -52,7 +52,8 @@ class SwitchStats(C.Structure):
 
     _fields_ = [("hashed_bytes", C.c_uint64), ("swap_out_bytes", C.c_uint64),
                 ("swap_in_bytes", C.c_uint64), ("resident_bytes", C.c_uint64),
-                ("cache_bytes", C.c_uint64)]
+                ("cache_bytes", C.c_uint64), ("install_bytes", C.c_uint64),
+                ("cache_free_bytes", C.c_uint64), ("reclaimed_bytes", C.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -143,6 +144,9 @@ _SIGS = {
     "snap_comm_init": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
     "snap_comm_destroy": (C.c_int, [C.c_void_p]),
     "snap_allreduce": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, C.c_uint64]),
+    "snap_allreduce_ordered": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_uint32,
+                                         C.c_uint64, C.c_uint64]),
+    "snap_comm_init_local": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_char_p]),
     "snap_host_alloc": (C.c_int, [C.c_uint64, C.POINTER(C.c_void_p)]),
     "snap_host_free": (C.c_int, [C.c_void_p]),
     "snap_snapshot_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p,
@@ -183,6 +187,11 @@ _SIGS = {
                                       C.POINTER(C.c_uint64)]),
     "snap_alloc_restore": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
     "snap_splice_init": (C.c_int, [C.c_void_p, C.c_uint64]),
+    "snap_splice_init_slots": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32]),
+    "snap_splice_install": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint64,
+                                      C.c_uint64]),
+    "snap_splice_pending": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_uint64),
+                                      C.POINTER(C.c_uint64)]),
     "snap_splice_set_rank": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_uint64, C.c_void_p]),
     "snap_splice_switch": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
     "snap_splice_recorded": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.POINTER(C.c_uint64)]),
@@ -647,8 +656,22 @@ class Ctx:
         self._ck(self._L.snap_restore_self(self.h, 1 if verify else 0), "snap_restore_self")
 
     # -- splice (GpuLedger::plan_switch/execute_switch)
-    def splice_init(self, cache_bytes: int):
-        self._ck(self._L.snap_splice_init(self.h, cache_bytes), "snap_splice_init")
+    def splice_init(self, cache_bytes: int, slot_bytes: int = 65536):
+        self._ck(self._L.snap_splice_init_slots(self.h, cache_bytes, slot_bytes),
+                 "snap_splice_init_slots")
+
+    def splice_install(self, ranks, dst_addrs, src_addr: int, nbytes: int):
+        """on_coll_complete install (job.cpp:206-222): active rank now, others queued."""
+        r = np.ascontiguousarray(ranks, dtype=np.int32)
+        d = np.ascontiguousarray(dst_addrs, dtype=np.uint64)
+        self._ck(self._L.snap_splice_install(self.h, _p(r), _p(d), r.size, src_addr, nbytes),
+                 "snap_splice_install")
+
+    def splice_pending(self, rank: int):
+        c, b = C.c_uint64(), C.c_uint64()
+        self._ck(self._L.snap_splice_pending(self.h, rank, C.byref(c), C.byref(b)),
+                 "snap_splice_pending")
+        return c.value, b.value
 
     def splice_set_rank(self, rank: int, bufs, page_bytes=4096, chunk_bytes=65536):
         arr = bufs_array([b[:5] for b in bufs])
@@ -682,6 +705,18 @@ class Ctx:
     def comm_init(self, nranks: int, rank: int, uid: bytes):
         buf = (C.c_uint8 * 128).from_buffer_copy(uid)
         self._ck(self._L.snap_comm_init(self.h, nranks, rank, buf), "snap_comm_init")
+
+    def comm_init_local(self, nranks: int, rank: int, key: str):
+        """In-process communicator (one ctx per thread; blocks until all ranks joined)."""
+        self._ck(self._L.snap_comm_init_local(self.h, nranks, rank, key.encode()),
+                 "snap_comm_init_local")
+
+    def allreduce_ordered(self, dtype, keys, src_addrs, dst_addr: int, elems: int):
+        """Fixed-order allreduce: sum of every GPU's sources in ascending key order."""
+        k = np.ascontiguousarray(keys, dtype=np.uint32)
+        a = np.ascontiguousarray(src_addrs, dtype=np.uint64)
+        self._ck(self._L.snap_allreduce_ordered(self.h, dtype, _p(k), _p(a), k.size, dst_addr,
+                                                elems), "snap_allreduce_ordered")
 
     def comm_destroy(self):
         self._ck(self._L.snap_comm_destroy(self.h), "snap_comm_destroy")

@@ -113,6 +113,8 @@ int prepare_dedup(snap_ctx* ctx, uint64_t n, TableDev* out, uint64_t** slot, uin
 int select_with_known(snap_ctx* ctx, const uint64_t* dig, const uint32_t* lens, uint64_t n,
                       TableDev kn, bool use_known, bool inserted, uint64_t* spec_next,
                       const uint64_t* fix_spec, uint8_t* fix_staging) {
+  if (n >= snap::kMaxScanEntries)
+    return fail(ctx, SNAP_EINVAL, "select: a selection covers at most 2^26 - 1 chunks");
   uint64_t *slot, *scan, *owner, *offsets, *totals;
   uint8_t* sel;
   uint32_t* list;
@@ -162,6 +164,14 @@ uint64_t* gdig_region(const snap_ctx* ctx, uint64_t epoch) {
          (epoch & 1) * uint64_t(ctx->nranks) * ctx->maxn;
 }
 
+void close_peer_staging(snap_ctx* ctx) {
+  for (size_t r = 0; r < ctx->peer_staging.size(); ++r)
+    if (int(r) != ctx->rank && r < ctx->peer_opened.size())
+      ipc_close(ctx->peer_staging[r], ctx->peer_opened[r]);
+  ctx->peer_staging.clear();
+  ctx->peer_opened.clear();
+}
+
 void close_peer_windows(snap_ctx* ctx) {
   for (size_t q = 0; q < ctx->xpeer.size(); ++q)
     if (int(q) != ctx->rank && ctx->xpeer[q]) cudaIpcCloseMemHandle(ctx->xpeer[q]);
@@ -185,7 +195,7 @@ int setup_exchange_window(snap_ctx* ctx) {
     return e && e[0] == '1';
   }();
   const uint64_t need = xflag_bytes(ctx) + 2 * uint64_t(R) * ctx->maxn * 8;
-  if (!fused) {  // NCCL allgather into the (unmapped) window
+  if (!fused || !ctx->comm) {  // allgather into the (unmapped) window
     if (need > ctx->d_gdig.cap) {
       release(ctx->d_gdig);
       uint8_t* w;
@@ -196,9 +206,9 @@ int setup_exchange_window(snap_ctx* ctx) {
   uint8_t* xh;
   RC(ensure(ctx, ctx->d_xh, 64 * uint64_t(R) + 16, &xh));
   int32_t* word = reinterpret_cast<int32_t*>(xh + 64 * uint64_t(R));
-  auto agree = [&](int32_t v, ncclRedOp_t op, int32_t* out) -> int {
+  auto agree = [&](int32_t v, CommOp op, int32_t* out) -> int {
     CK(cudaMemcpyAsync(word, &v, 4, cudaMemcpyHostToDevice, ctx->stream));
-    CKN(ncclAllReduce(word, word, 1, ncclInt32, op, ctx->comm, ctx->stream));
+    RC(comm_allreduce(ctx, word, word, 1, kCommI32, op));
     CK(cudaMemcpyAsync(out, word, 4, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     return SNAP_OK;
@@ -206,7 +216,7 @@ int setup_exchange_window(snap_ctx* ctx) {
   // every importer has closed its mapping of the old windows once this
   // collective returns, so a window may be freed and reallocated after it
   int32_t any_grow = 0;
-  RC(agree(need > ctx->d_gdig.cap ? 1 : 0, ncclMax, &any_grow));
+  RC(agree(need > ctx->d_gdig.cap ? 1 : 0, kCommMax, &any_grow));
   if (need > ctx->d_gdig.cap) {
     release(ctx->d_gdig);
     uint8_t* w;
@@ -220,7 +230,7 @@ int setup_exchange_window(snap_ctx* ctx) {
     std::memset(&h, 0, sizeof h);
   }
   CK(cudaMemcpyAsync(xh + 64 * ctx->rank, &h, 64, cudaMemcpyHostToDevice, ctx->stream));
-  CKN(ncclAllGather(xh + 64 * ctx->rank, xh, 64, ncclUint8, ctx->comm, ctx->stream));
+  RC(comm_allgather(ctx, xh + 64 * ctx->rank, xh, 64, kCommU8));
   std::vector<uint8_t> all(64 * size_t(R));
   CK(cudaMemcpyAsync(all.data(), xh, all.size(), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -245,7 +255,7 @@ int setup_exchange_window(snap_ctx* ctx) {
     }
   }
   int32_t all_ok = 0;
-  RC(agree(ok ? 1 : 0, ncclMin, &all_ok));
+  RC(agree(ok ? 1 : 0, kCommMin, &all_ok));
   if (!all_ok) {
     close_peer_windows(ctx);
     return SNAP_OK;
@@ -270,7 +280,7 @@ int setup_exchange_window(snap_ctx* ctx) {
 // gathered vector of the coming exchange (epoch xepoch + 1) when the windows
 // are mapped; the exchange then reduces to the barrier.
 void k1_fanout(snap_ctx* ctx, GridDev& g) {
-  if (!ctx->comm || !ctx->xwin_ready) return;
+  if (!ctx->attached() || !ctx->xwin_ready) return;
   g.xdig = P<uint64_t*>(ctx->d_xdig);
   g.xn = uint32_t(ctx->nranks);
   g.xoff = ((ctx->xepoch + 1) & 1) * uint64_t(ctx->nranks) * ctx->maxn +
@@ -278,24 +288,51 @@ void k1_fanout(snap_ctx* ctx, GridDev& g) {
   ctx->k1_fanout = true;
 }
 
+}  // namespace
+
+// Per-grid part of the exchange, collective: every rank's chunk count (-> maxn)
+// and chunk lengths are all-gathered and the exchange windows set up. Issued by
+// snap_comm_init and by snap_set_buffers / snap_load with a communicator
+// attached (those calls are collective then), never conditionally inside a
+// snapshot: every rank's snapshot issues the same NCCL sequence no matter
+// which rank re-installed its grid.
+int grid_exchange(snap_ctx* ctx) {
+  const int R = ctx->nranks;
+  uint64_t* dc;
+  RC(ensure(ctx, ctx->d_counts, 2 * R, &dc));
+  CK(cudaMemcpyAsync(dc + R, &ctx->nchunks, 8, cudaMemcpyHostToDevice, ctx->stream));
+  RC(comm_allgather(ctx, dc + R, dc, 1, kCommU64));
+  ctx->counts.assign(R, 0);
+  CK(cudaMemcpyAsync(ctx->counts.data(), dc, 8 * R, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->maxn = *std::max_element(ctx->counts.begin(), ctx->counts.end());
+  if (uint64_t(R) * ctx->maxn >= snap::kMaxScanEntries)
+    return fail(ctx, SNAP_EINVAL, "exchange: nranks x max chunks per rank exceeds 2^26 entries");
+  ctx->k1_fanout = false;  // K1 ran before the windows existed for this grid
+  RC(setup_exchange_window(ctx));
+  const uint64_t maxn = ctx->maxn, n = uint64_t(R) * maxn;
+  uint32_t* glens;
+  RC(ensure(ctx, ctx->d_glens, n + maxn, &glens));
+  uint32_t* slen = glens + n;
+  CK(cudaMemsetAsync(slen, 0, maxn * 4, ctx->stream));
+  if (ctx->nchunks)
+    CK(cudaMemcpyAsync(slen, P<uint32_t>(ctx->d_lens), ctx->nchunks * 4, cudaMemcpyDeviceToDevice,
+                       ctx->stream));
+  RC(comm_allgather(ctx, slen, glens, maxn, kCommU32));
+  ctx->glens_valid = true;
+  return SNAP_OK;
+}
+
+namespace {
+
 // The exchange step: per-rank digest vectors gathered (rank-major, padded to
-// the largest rank) — by K1's own NVLink stores + a peer barrier, or (first
-// snapshot of a grid, no IPC) by an NCCL allgather; chunk lengths once per
-// grid by NCCL. The only bytes that cross NVLink: 8 B per 64 KiB chunk.
+// the largest rank) — by K1's own NVLink stores + a peer barrier, or by an
+// NCCL allgather. The only bytes that cross NVLink: 8 B per 64 KiB chunk.
 int exchange_impl(snap_ctx* ctx) {
   const int R = ctx->nranks;
-  if (!ctx->glens_valid) {
-    uint64_t* dc;
-    RC(ensure(ctx, ctx->d_counts, 2 * R, &dc));
-    CK(cudaMemcpyAsync(dc + R, &ctx->nchunks, 8, cudaMemcpyHostToDevice, ctx->stream));
-    CKN(ncclAllGather(dc + R, dc, 1, ncclUint64, ctx->comm, ctx->stream));
-    ctx->counts.assign(R, 0);
-    CK(cudaMemcpyAsync(ctx->counts.data(), dc, 8 * R, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    ctx->maxn = *std::max_element(ctx->counts.begin(), ctx->counts.end());
-    ctx->k1_fanout = false;  // K1 ran before the windows existed for this grid
-    RC(setup_exchange_window(ctx));
-  }
+  if (!ctx->glens_valid)
+    return fail(ctx, SNAP_EINTERNAL, "exchange: grid not exchanged (snap_set_buffers / "
+                                     "snap_comm_init are collective with a communicator)");
   const uint64_t maxn = ctx->maxn, n = uint64_t(R) * maxn;
   const uint64_t epoch = ctx->xepoch + 1;
   uint64_t* gdig = gdig_region(ctx, epoch);
@@ -307,21 +344,11 @@ int exchange_impl(snap_ctx* ctx) {
     // padding entries' values are ignored (their gathered lengths are 0)
     uint64_t* sdig;
     RC(ensure_keep(ctx, ctx->d_dig, maxn, ctx->nchunks * 8, &sdig));
-    CKN(ncclAllGather(sdig, gdig, maxn, ncclUint64, ctx->comm, ctx->stream));
+    RC(comm_allgather(ctx, sdig, gdig, maxn, kCommU64));
   }
   ctx->k1_fanout = false;
   ctx->xepoch = epoch;
-  uint32_t* glens;
-  if (!ctx->glens_valid) {
-    RC(ensure(ctx, ctx->d_glens, n + maxn, &glens));
-    uint32_t* slen = glens + n;
-    CK(cudaMemsetAsync(slen, 0, maxn * 4, ctx->stream));
-    if (ctx->nchunks)
-      CK(cudaMemcpyAsync(slen, P<uint32_t>(ctx->d_lens), ctx->nchunks * 4,
-                         cudaMemcpyDeviceToDevice, ctx->stream));
-    CKN(ncclAllGather(slen, glens, maxn, ncclUint32, ctx->comm, ctx->stream));
-    ctx->glens_valid = true;
-  }
+  (void)n;
   ctx->exchanged = true;
   return SNAP_OK;
 }
@@ -422,7 +449,7 @@ int staging_reserve(snap_ctx* ctx, uint64_t bytes, bool keep, uint8_t** out) {
 // snapshot to learn the actual shard size (compact_impl).
 constexpr uint64_t kFullStagingMax = 16ull << 30;
 uint64_t staging_target(const snap_ctx* ctx) {
-  if (!ctx->comm || ctx->nranks == 1 || ctx->spec_bytes == 0 ||
+  if (!ctx->attached() || ctx->nranks == 1 || ctx->spec_bytes == 0 ||
       ctx->grid_bytes <= kFullStagingMax)
     return ctx->grid_bytes;
   return ctx->spec_bytes + ctx->spec_bytes / 16 + (64ull << 20);
@@ -446,7 +473,7 @@ int init_spec(snap_ctx* ctx) {
   const uint64_t n = ctx->nchunks;
   std::vector<uint64_t> spec(n, ~0ull);
   const int emu = spec_stripe_emu();
-  if ((!ctx->comm || ctx->nranks == 1) && emu > 1) {
+  if ((!ctx->attached() || ctx->nranks == 1) && emu > 1) {
     // measurement aid: predict the layout rank 0 of an emu-rank job stages
     // (private chunks + every emu-th replicated chunk); the fix-up copies the rest
     std::vector<uint8_t> rep(n, 0);
@@ -459,7 +486,7 @@ int init_spec(snap_ctx* ctx) {
         spec[g] = off;
         off += ctx->h_lens[g];
       }
-  } else if (!ctx->comm || ctx->nranks == 1) {
+  } else if (!ctx->attached() || ctx->nranks == 1) {
     uint64_t off = 0;
     for (uint64_t g = 0; g < n; ++g) {
       spec[g] = off;
@@ -512,7 +539,7 @@ int hash_fused(snap_ctx* ctx, uint64_t c0 = 0, uint64_t c1 = 0) {
     const char* e = std::getenv("SNAP_K1_INSERT");
     return e && e[0] == '1';
   }();
-  if (!ctx->comm && k1_insert) {
+  if (!ctx->attached() && k1_insert) {
     // SNAP_K1_INSERT=1 (single GPU): K1 also does the K2 insert of its chunks in
     // a warp epilogue (the table is prepared once, before the first slice of the
     // grid). Off by default: the epilogue costs more kernel tail (14 us on C2)
@@ -547,7 +574,7 @@ int hash_fused(snap_ctx* ctx, uint64_t c0 = 0, uint64_t c1 = 0) {
 
 int compact_impl(snap_ctx* ctx, uint32_t* moved = nullptr, unsigned int* nmoved = nullptr) {
   uint8_t* st;
-  const bool shard = ctx->comm && ctx->exchanged;
+  const bool shard = ctx->attached() && ctx->exchanged;
   if (shard && staging_target(ctx) < ctx->grid_bytes) {
     // shard-sized staging: learn the actual shard size, grow (keeping the
     // speculative bytes) before the fix-up writes beyond the prediction
@@ -576,7 +603,7 @@ int compact_impl(snap_ctx* ctx, uint32_t* moved = nullptr, unsigned int* nmoved 
   if (nmoved) CK(cudaMemsetAsync(nmoved, 0, 4, ctx->stream));
   if (fixed) {
     // the selection scan already copied the mismatched chunks
-  } else if (ctx->comm && ctx->exchanged) {
+  } else if (ctx->attached() && ctx->exchanged) {
     CKL(snap::launch_gather(ctx->arena, ctx->grid, P<uint32_t>(ctx->d_lens),
                             P<uint32_t>(ctx->d_my_list), P<uint64_t>(ctx->d_my_totals),
                             P<uint64_t>(ctx->d_my_off), true, spec_cur, spec_next, st,
@@ -654,7 +681,9 @@ int snap_close(snap_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   close_peer_windows(ctx);
+  ar_release(ctx);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
+  local_group_leave(ctx);
   splice_release(ctx);
   window_release(ctx);
   for (DevMem* m :
@@ -664,14 +693,14 @@ int snap_close(snap_ctx* ctx) {
         &ctx->staging, &ctx->d_counts, &ctx->d_gdig, &ctx->d_glens, &ctx->d_writer,
         &ctx->d_shard_off, &ctx->d_my_list, &ctx->d_my_off, &ctx->d_my_totals, &ctx->d_dig2,
         &ctx->d_expect, &ctx->d_nbad, &ctx->d_srcoff, &ctx->d_spec[0], &ctx->d_spec[1],
-        &ctx->d_tmaps, &ctx->scan2, &ctx->d_xdig, &ctx->d_xflag, &ctx->d_xh})
+        &ctx->d_tmaps, &ctx->scan2, &ctx->d_xdig, &ctx->d_xflag, &ctx->d_xh, &ctx->d_arflag,
+        &ctx->d_arh, &ctx->d_arrec, &ctx->d_arptr, &ctx->d_arcnt})
     release(*m);
   for (cudaEvent_t e : ctx->prof.pool) cudaEventDestroy(e);
   if (ctx->arena) cudaFree(ctx->arena);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
-  for (size_t r = 0; r < ctx->peer_staging.size(); ++r)
-    if (int(r) != ctx->rank && ctx->peer_staging[r]) cudaIpcCloseMemHandle(ctx->peer_staging[r]);
+  close_peer_staging(ctx);
   release(ctx->d_peers);
   for (cudaEvent_t e : ctx->pipe_ev) cudaEventDestroy(e);
   release(ctx->d_moved);
@@ -837,6 +866,9 @@ int snap_set_buffers(snap_ctx* ctx, const snap_buf* bufs, uint64_t n, const snap
   ctx->xwin_ready = false;  // maxn may change: the next exchange re-maps the windows
   ctx->k1_fanout = false;
   if (n_chunks) *n_chunks = ctx->nchunks;
+  // with a communicator attached this call is collective: the new grid's
+  // counts and lengths are exchanged here, never inside a snapshot
+  if (ctx->attached()) RC(grid_exchange(ctx));
   return SNAP_OK;
 }
 
@@ -907,7 +939,7 @@ int snap_known_commit(snap_ctx* ctx) {
   if (!ctx) return SNAP_EINVAL;
   if (!ctx->hashed) return fail(ctx, SNAP_EINVAL, "known_commit before snap_hash");
   CK(cudaSetDevice(ctx->device));
-  if (ctx->comm && ctx->exchanged) {
+  if (ctx->attached() && ctx->exchanged) {
     // the store is global: every rank's digests become known
     const uint64_t n = uint64_t(ctx->nranks) * ctx->maxn;
     std::vector<uint32_t> gl(n);
@@ -927,7 +959,7 @@ int snap_select(snap_ctx* ctx) {
   if (!ctx) return SNAP_EINVAL;
   if (!ctx->hashed) return fail(ctx, SNAP_EINVAL, "select before snap_hash");
   CK(cudaSetDevice(ctx->device));
-  if (ctx->comm) {
+  if (ctx->attached()) {
     {
       ProfScope ps(ctx, kProfExchange);
       RC(exchange_impl(ctx));
@@ -975,7 +1007,7 @@ int snap_get_selection(snap_ctx* ctx, uint8_t* sel, uint64_t* owner, uint64_t* o
 
 int snap_global_info(snap_ctx* ctx, uint64_t* n_global, uint64_t* max_per_rank) {
   if (!ctx) return SNAP_EINVAL;
-  const bool g = ctx->comm && ctx->exchanged;
+  const bool g = ctx->attached() && ctx->exchanged;
   if (n_global) *n_global = g ? uint64_t(ctx->nranks) * ctx->maxn : ctx->nchunks;
   if (max_per_rank) *max_per_rank = g ? ctx->maxn : ctx->nchunks;
   return SNAP_OK;
@@ -983,7 +1015,7 @@ int snap_global_info(snap_ctx* ctx, uint64_t* n_global, uint64_t* max_per_rank) 
 
 int snap_get_global_digests(snap_ctx* ctx, uint64_t* gdig, uint32_t* glens) {
   if (!ctx) return SNAP_EINVAL;
-  if (!(ctx->comm && ctx->exchanged)) return fail(ctx, SNAP_EINVAL, "no exchanged digests");
+  if (!(ctx->attached() && ctx->exchanged)) return fail(ctx, SNAP_EINVAL, "no exchanged digests");
   CK(cudaSetDevice(ctx->device));
   const uint64_t n = uint64_t(ctx->nranks) * ctx->maxn;
   if (gdig)
@@ -997,7 +1029,7 @@ int snap_get_global_digests(snap_ctx* ctx, uint64_t* gdig, uint32_t* glens) {
 int snap_get_shard(snap_ctx* ctx, int32_t* writer, uint64_t* shard_off, uint64_t* my_bytes,
                    uint64_t* my_chunks) {
   if (!ctx) return SNAP_EINVAL;
-  if (!(ctx->comm && ctx->exchanged && ctx->selected))
+  if (!(ctx->attached() && ctx->exchanged && ctx->selected))
     return fail(ctx, SNAP_EINVAL, "get_shard needs a multi-rank snap_select");
   CK(cudaSetDevice(ctx->device));
   const uint64_t n = uint64_t(ctx->nranks) * ctx->maxn;
@@ -1031,27 +1063,23 @@ int snap_ipc_export(snap_ctx* ctx, void* handle64) {
   if (!ctx || !handle64) return SNAP_EINVAL;
   if (!ctx->staging.p) return fail(ctx, SNAP_EINVAL, "ipc_export: no staging image yet");
   CK(cudaSetDevice(ctx->device));
-  cudaIpcMemHandle_t h;
-  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t size");
-  CK(cudaIpcGetMemHandle(&h, ctx->staging.p));
-  std::memcpy(handle64, &h, 64);
-  return SNAP_OK;
+  return ipc_handle(ctx, ctx->staging.p, handle64);
 }
 
 int snap_ipc_import(snap_ctx* ctx, int nranks, const void* handles) {
   if (!ctx || !handles || nranks != ctx->nranks) return SNAP_EINVAL;
   CK(cudaSetDevice(ctx->device));
-  for (size_t r = 0; r < ctx->peer_staging.size(); ++r)
-    if (int(r) != ctx->rank && ctx->peer_staging[r]) cudaIpcCloseMemHandle(ctx->peer_staging[r]);
+  close_peer_staging(ctx);
   ctx->peer_staging.assign(nranks, nullptr);
+  ctx->peer_opened.assign(nranks, false);
   for (int r = 0; r < nranks; ++r) {
     if (r == ctx->rank) {
       ctx->peer_staging[r] = ctx->staging.p;
       continue;
     }
-    cudaIpcMemHandle_t h;
-    std::memcpy(&h, static_cast<const uint8_t*>(handles) + 64 * r, 64);
-    CK(cudaIpcOpenMemHandle(&ctx->peer_staging[r], h, cudaIpcMemLazyEnablePeerAccess));
+    bool opened = false;
+    RC(ipc_open(ctx, static_cast<const uint8_t*>(handles) + 64 * r, &ctx->peer_staging[r], &opened));
+    ctx->peer_opened[r] = opened;
   }
   void** dp;
   RC(ensure(ctx, ctx->d_peers, nranks, &dp));
@@ -1065,7 +1093,7 @@ int snap_ipc_import(snap_ctx* ctx, int nranks, const void* handles) {
 // `src_rank`'s layout (= the installed grid) is rebuilt from the striped
 // shards of the last multi-rank snapshot, reading peer shards over NVLink.
 int snap_restore_shards(snap_ctx* ctx, int src_rank, int verify) {
-  if (!ctx || !ctx->comm || !ctx->exchanged || !ctx->selected || src_rank < 0 ||
+  if (!ctx || !ctx->attached() || !ctx->exchanged || !ctx->selected || src_rank < 0 ||
       src_rank >= ctx->nranks)
     return fail(ctx, SNAP_EINVAL, "restore_shards needs a multi-rank snapshot");
   if (int(ctx->peer_staging.size()) != ctx->nranks)
@@ -1222,7 +1250,7 @@ int snapshot_host_pipelined(snap_ctx* ctx, const uint8_t* host_src, uint64_t add
   }
   st = static_cast<uint8_t*>(ctx->staging.p);  // the fix-up may have grown the image
   ctx->h_spec_valid = false;  // the fix-up wrote the next layout on the device
-  const bool shard = ctx->comm && ctx->exchanged;
+  const bool shard = ctx->attached() && ctx->exchanged;
   uint64_t tot[2] = {0, 0};
   uint32_t nmv = 0;
   CK(cudaMemcpyAsync(tot, shard ? ctx->d_my_totals.p : ctx->totals.p, 16, cudaMemcpyDeviceToHost,
@@ -1292,7 +1320,7 @@ int snap_snapshot_host(snap_ctx* ctx, const void* host_src, uint64_t addr, uint6
     CK(cudaMemcpyAsync(ctx->arena + addr, host_src, bytes, cudaMemcpyHostToDevice, ctx->stream));
   RC(snap_snapshot(ctx));
   uint64_t tot[2] = {0, 0};
-  const bool shard = ctx->comm && ctx->exchanged;
+  const bool shard = ctx->attached() && ctx->exchanged;
   CK(cudaMemcpyAsync(tot, shard ? ctx->d_my_totals.p : ctx->totals.p, 16, cudaMemcpyDeviceToHost,
                      ctx->stream));
   if (host_digests && ctx->nchunks)
@@ -1381,7 +1409,7 @@ int snap_restore_self(snap_ctx* ctx, int verify) {
   if (ctx->kn_count)
     return fail(ctx, SNAP_EINVAL, "restore_self: incremental snapshot (known set) needs the "
                                   "older images; use snap_restore");
-  if (ctx->comm && ctx->exchanged)
+  if (ctx->attached() && ctx->exchanged)
     return fail(ctx, SNAP_EINVAL, "restore_self: multi-rank snapshots restore from the shards "
                                   "(snap_restore)");
   CK(cudaSetDevice(ctx->device));
@@ -1399,9 +1427,10 @@ int snap_restore_self(snap_ctx* ctx, int verify) {
 
 int snap_grad_sum(snap_ctx* ctx, int dtype, const uint64_t* src_addrs, uint32_t nsrc,
                   uint64_t dst_addr, uint64_t elems, int accumulate) {
-  if (!ctx || !src_addrs || (dtype != SNAP_U64 && dtype != SNAP_F32) || nsrc == 0 || nsrc > 16)
-    return fail(ctx, SNAP_EINVAL, "grad_sum: bad arguments (1..16 sources, u64|f32)");
-  const uint64_t esz = dtype == SNAP_F32 ? 4 : 8;
+  if (!ctx || !src_addrs || (dtype != SNAP_U64 && dtype != SNAP_F32 && dtype != SNAP_BF16) ||
+      nsrc == 0 || nsrc > 16)
+    return fail(ctx, SNAP_EINVAL, "grad_sum: bad arguments (1..16 sources, u64|f32|bf16)");
+  const uint64_t esz = dtype == SNAP_F32 ? 4 : dtype == SNAP_BF16 ? 2 : 8;
   if (elems > ctx->arena_bytes / esz) return fail(ctx, SNAP_EINVAL, "grad_sum: size");
   for (uint32_t r = 0; r < nsrc; ++r) {
     if (src_addrs[r] % 16) return fail(ctx, SNAP_EINVAL, "grad_sum: sources must be 16-B aligned");
@@ -1432,7 +1461,7 @@ int snap_comm_init(snap_ctx* ctx, int nranks, int rank, const void* id128) {
   CK(cudaSetDevice(ctx->device));
   ncclUniqueId id;
   std::memcpy(&id, id128, 128);
-  if (ctx->comm) return fail(ctx, SNAP_EINVAL, "comm_init: destroy the current communicator "
+  if (ctx->attached()) return fail(ctx, SNAP_EINVAL, "comm_init: destroy the current communicator "
                                                "first (snap_comm_destroy, collective)");
   CKN(ncclCommInitRank(&ctx->comm, nranks, id, rank));
   ctx->nranks = nranks;
@@ -1443,22 +1472,27 @@ int snap_comm_init(snap_ctx* ctx, int nranks, int rank, const void* id128) {
   ctx->glens_valid = false;
   ctx->exchanged = false;
   ctx->spec_ready = false;
-  return SNAP_OK;
+  return grid_exchange(ctx);  // the installed grid (possibly empty) of every rank
 }
 
 // Collective over the communicator's ranks (the rendezvous of a resize,
 // collectives.cpp:37-59, rebuilds the device-level world afterwards).
 int snap_comm_destroy(snap_ctx* ctx) {
   if (!ctx) return SNAP_EINVAL;
-  if (!ctx->comm) return SNAP_OK;
+  if (!ctx->attached()) return SNAP_OK;
   CK(cudaSetDevice(ctx->device));
   CK(cudaStreamSynchronize(ctx->stream));
-  for (size_t r = 0; r < ctx->peer_staging.size(); ++r)
-    if (int(r) != ctx->rank && ctx->peer_staging[r]) cudaIpcCloseMemHandle(ctx->peer_staging[r]);
-  ctx->peer_staging.clear();
+  close_peer_staging(ctx);
   close_peer_windows(ctx);
-  CKN(ncclCommDestroy(ctx->comm));
-  ctx->comm = nullptr;
+  ar_release(ctx);
+  if (ctx->comm) {
+    CKN(ncclCommDestroy(ctx->comm));
+    ctx->comm = nullptr;
+  }
+  if (ctx->lgroup) {
+    comm_barrier(ctx);  // no peer still reads this rank's buffers
+    local_group_leave(ctx);
+  }
   ctx->nranks = 1;
   ctx->rank = 0;
   ctx->glens_valid = false;
@@ -1469,13 +1503,14 @@ int snap_comm_destroy(snap_ctx* ctx) {
 }
 
 int snap_allreduce(snap_ctx* ctx, int dtype, uint64_t addr, uint64_t elems) {
-  if (!ctx || !ctx->comm) return fail(ctx, SNAP_EINVAL, "allreduce: no communicator");
+  if (!ctx || !ctx->attached()) return fail(ctx, SNAP_EINVAL, "allreduce: no communicator");
+  if (dtype != SNAP_U64 && dtype != SNAP_F32)
+    return fail(ctx, SNAP_EINVAL, "allreduce: u64 | f32 (bf16: snap_allreduce_ordered)");
   const uint64_t esz = dtype == SNAP_F32 ? 4 : 8;
   RC(check_range(ctx, addr, elems * esz));
   CK(cudaSetDevice(ctx->device));
-  CKN(ncclAllReduce(ctx->arena + addr, ctx->arena + addr, elems,
-                    dtype == SNAP_F32 ? ncclFloat32 : ncclUint64, ncclSum, ctx->comm, ctx->stream));
-  return SNAP_OK;
+  return comm_allreduce(ctx, ctx->arena + addr, ctx->arena + addr, elems,
+                        dtype == SNAP_F32 ? kCommF32 : kCommU64, kCommSum);
 }
 
 // ---------------------------------------------------------------- timing

@@ -19,6 +19,13 @@ using snap::TableDev;
 
 struct SpliceState;
 struct WindowState;
+struct LocalGroup;
+
+// Communicator collectives (comm.cpp): NCCL or the in-process group.
+enum CommType { kCommU8, kCommI32, kCommU32, kCommU64, kCommF32 };
+enum CommOp { kCommSum, kCommMax, kCommMin };
+// sliced ranks per GPU in one fixed-order allreduce call
+constexpr uint32_t kArMaxLocal = 16;
 
 struct DevMem {
   void* p = nullptr;
@@ -79,8 +86,11 @@ struct snap_ctx {
   bool spec_ready = false;
   bool spec_used = false;
 
-  // cross-rank exchange (NCCL allgather of digest vectors) and striping
+  // cross-rank exchange (NCCL allgather of digest vectors) and striping;
+  // the communicator is NCCL (one process per GPU) or an in-process group
   ncclComm_t comm = nullptr;
+  LocalGroup* lgroup = nullptr;
+  bool attached() const { return comm != nullptr || lgroup != nullptr; }
   int nranks = 1, rank = 0;
   bool exchanged = false;
   uint64_t maxn = 0;
@@ -114,6 +124,7 @@ struct snap_ctx {
 
   // resize / reshard: peer ranks' staging shards mapped over CUDA IPC
   std::vector<void*> peer_staging;  // [nranks]; own rank = local staging
+  std::vector<bool> peer_opened;    // mapped through cudaIpcOpenMemHandle (closed on release)
   DevMem d_peers;
   bool shard_offsets_all = false;   // d_shard_off valid for every writer
   // multi-rank step: global staging offsets (offsets/sel_list/totals) not yet
@@ -126,6 +137,12 @@ struct snap_ctx {
   // predicted staging bytes (multi-rank shards are sized to the prediction and
   // grown on demand instead of reserving a whole image per GPU)
   uint64_t spec_bytes = 0;
+  // fixed-order allreduce: every rank's arena + flag lines (peer memory)
+  std::vector<void*> ar_peer_arena, ar_peer_flag;
+  std::vector<bool> ar_opened;
+  bool ar_ready = false;
+  uint64_t ar_epoch = 0;
+  DevMem d_arflag, d_arh, d_arrec, d_arptr, d_arcnt;
   // pinned slabs of the persist/load file path (allocated once, reused)
   uint8_t* io_pin[2] = {nullptr, nullptr};
   uint64_t io_pin_cap = 0;
@@ -234,6 +251,19 @@ inline uint64_t table_cap(uint64_t n) {
   while (c < 2 * n) c <<= 1;
   return c;
 }
+
+// comm.cpp
+int comm_allgather(snap_ctx* ctx, const void* send, void* recv, uint64_t count, CommType t);
+int comm_allreduce(snap_ctx* ctx, const void* send, void* recv, uint64_t count, CommType t,
+                   CommOp op);
+void comm_barrier(snap_ctx* ctx);
+int ipc_handle(snap_ctx* ctx, void* dev_ptr, void* handle64);
+int ipc_open(snap_ctx* ctx, const void* handle64, void** out, bool* opened);
+void ipc_close(void* p, bool opened);
+void ar_release(snap_ctx* ctx);
+void local_group_leave(snap_ctx* ctx);
+// capi.cpp: per-grid part of the exchange (collective)
+int grid_exchange(snap_ctx* ctx);
 
 // splice_host.cpp: seed the splice chunk cache with a rank's content (restore_job)
 int splice_seed(snap_ctx* ctx, int rank, const uint8_t* image, const uint64_t* src_off,

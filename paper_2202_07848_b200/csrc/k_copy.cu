@@ -15,6 +15,8 @@
 // re-read soon.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "snap_internal.h"
 #include "table.cuh"
 
@@ -154,14 +156,15 @@ __global__ void __launch_bounds__(kThreads)
 k_gather_from(const uint8_t* __restrict__ image, const uint64_t* __restrict__ src_off,
               const uint32_t* __restrict__ lens, const uint32_t* __restrict__ sel_list,
               const uint64_t* __restrict__ totals, const uint64_t* __restrict__ offsets,
-              uint8_t* __restrict__ dst) {
+              int by_list, uint8_t* __restrict__ dst) {
+  griddep_wait();
   const uint64_t nsel = totals[0];
   const int lane = threadIdx.x & 31;
   const uint64_t w0 = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
   const uint64_t nw = (uint64_t(gridDim.x) * kThreads) >> 5;
   for (uint64_t w = w0; w < nsel; w += nw) {
     const uint32_t gc = sel_list[w];
-    warp_copy(dst + offsets[gc], image + src_off[gc], lens[gc], lane);
+    warp_copy(dst + offsets[by_list ? w : gc], image + src_off[gc], lens[gc], lane);
   }
 }
 
@@ -175,20 +178,70 @@ __global__ void k_compare(const uint64_t* __restrict__ a, const uint64_t* __rest
   if ((threadIdx.x & 31) == 0 && bad) atomicAdd(nbad, bad);
 }
 
-// Splice swap-out bookkeeping: index the chunks just gathered into the chunk
-// cache (digest -> cache offset), the B200 replacement of host_cache_put's
-// digest-keyed std::map (splice.cpp:79-82).
-__global__ void k_cache_insert(TableDev cache, const uint64_t* __restrict__ dig,
+// Splice swap-out bookkeeping, before the gather: list entry k (chunk
+// sel_list[k]) takes the free cache slot free_stack[free_n - 1 - k]; its
+// gather destination is list_off[k] = slot << slot_shift and its digest is
+// indexed digest -> slot (the B200 replacement of host_cache_put's
+// digest-keyed std::map, splice.cpp:79-82). The host guarantees
+// totals[0] <= free_n.
+__global__ void k_cache_assign(TableDev cache, const uint64_t* __restrict__ dig,
                                const uint32_t* __restrict__ sel_list,
                                const uint64_t* __restrict__ totals,
-                               const uint64_t* __restrict__ offsets, uint64_t base) {
+                               const uint32_t* __restrict__ lens,
+                               const uint32_t* __restrict__ free_stack, uint64_t free_n,
+                               uint32_t slot_shift, uint64_t* __restrict__ list_off,
+                               uint32_t* __restrict__ slot_len) {
   griddep_wait();
   const uint64_t n = totals[0];
-  for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
+  for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n && k < free_n;
        k += uint64_t(gridDim.x) * blockDim.x) {
     const uint32_t g = sel_list[k];
+    const uint32_t slot = free_stack[free_n - 1 - k];
+    list_off[k] = uint64_t(slot) << slot_shift;
+    slot_len[slot] = lens[g];
     const uint64_t s = table_find_or_insert(cache, dig[g]);
-    cache.vals[s] = base + offsets[g];
+    cache.vals[s] = slot;
+  }
+}
+
+// Splice cache reclamation (no reference counterpart: the reference's host
+// cache is an unbounded std::map, splice.hpp:128; the B200 cache is a fixed
+// HBM slot array). Every entry of the old index whose digest is still recorded
+// by some rank (`live`) is re-indexed into `fresh`; the slots of the others go
+// back on the free stack (cnt[0] slots freed, cnt[1] bytes freed, cnt[2] kept).
+__global__ void k_cache_gc(TableDev old, TableDev live, TableDev fresh,
+                           uint32_t* __restrict__ free_stack, uint64_t free_n,
+                           const uint32_t* __restrict__ slot_len,
+                           unsigned long long* __restrict__ cnt) {
+  const uint64_t n = old.mask + 2;
+  for (uint64_t s = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; s < n;
+       s += uint64_t(gridDim.x) * blockDim.x) {
+    const unsigned long long key = s == old.mask + 1 ? kEmptyKey : old.keys[s];
+    const unsigned long long slot = old.vals[s];
+    if (s == old.mask + 1 ? slot == ~0ull : key == kEmptyKey) continue;
+    if (table_find(live, key) != ~0ull) {
+      const uint64_t f = table_find_or_insert(fresh, key);
+      fresh.vals[f] = slot;
+      atomicAdd(cnt + 2, 1ull);
+    } else {
+      free_stack[free_n + atomicAdd(cnt + 0, 1ull)] = uint32_t(slot);
+      atomicAdd(cnt + 1, static_cast<unsigned long long>(slot_len[slot]));
+    }
+  }
+}
+
+// Byte-range copies (result installs): range r copies bytes[r] (multiple of
+// 16) from src[r] to dst[r]; every CTA takes a slice of every range.
+__global__ void __launch_bounds__(kThreads)
+k_copy_ranges(uint8_t* const* __restrict__ dst, const uint8_t* const* __restrict__ src,
+              const uint64_t* __restrict__ bytes, uint32_t nr) {
+  for (uint32_t r = 0; r < nr; ++r) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(src[r]);
+    uint4* d4 = reinterpret_cast<uint4*>(dst[r]);
+    const uint64_t n16 = bytes[r] >> 4;
+    for (uint64_t i = uint64_t(blockIdx.x) * kThreads + threadIdx.x; i < n16;
+         i += uint64_t(gridDim.x) * kThreads)
+      __stcs(d4 + i, __ldcs(s4 + i));
   }
 }
 
@@ -202,7 +255,8 @@ __global__ void __launch_bounds__(kThreads)
 k_splice_in(uint8_t* __restrict__ arena, GridDev to, const uint32_t* __restrict__ lens,
             const uint64_t* __restrict__ want, const int64_t* __restrict__ match,
             const uint64_t* __restrict__ dig_from, TableDev cache,
-            const uint8_t* __restrict__ cache_base, unsigned long long* __restrict__ counters) {
+            const uint8_t* __restrict__ cache_base, uint32_t slot_shift,
+            unsigned long long* __restrict__ counters) {
   griddep_wait();
   const int lane = threadIdx.x & 31;
   const uint64_t w0 = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
@@ -241,7 +295,7 @@ k_splice_in(uint8_t* __restrict__ arena, GridDev to, const uint32_t* __restrict_
         continue;
       }
       uint8_t* dst = const_cast<uint8_t*>(chunk_ptr(arena, to, gq));
-      warp_copy(dst, cache_base + cache.vals[s], lq, lane);
+      warp_copy(dst, cache_base + (cache.vals[s] << slot_shift), lq, lane);
       if (lane == 0) swapped += lq;
     }
   }
@@ -291,35 +345,56 @@ int launch_scatter(uint8_t* arena, const GridDev& g, const uint32_t* lens, const
 
 int launch_gather_from(const uint8_t* image, const uint64_t* src_off, const uint32_t* lens,
                        const uint32_t* sel_list, const uint64_t* totals, const uint64_t* offsets,
-                       uint8_t* dst, uint64_t max_sel, cudaStream_t s) {
+                       uint8_t* dst, uint64_t max_sel, cudaStream_t s, bool offsets_by_list) {
   if (max_sel == 0) return 0;
   uint64_t blocks = (max_sel * 32 + kThreads - 1) / kThreads;
   if (blocks > copy_grid()) blocks = copy_grid();
-  k_gather_from<<<unsigned(blocks), kThreads, 0, s>>>(image, src_off, lens, sel_list, totals,
-                                                      offsets, dst);
+  launch_pdl(k_gather_from, unsigned(blocks), kThreads, 0, s, image, src_off, lens, sel_list,
+             totals, offsets, offsets_by_list ? 1 : 0, dst);
   return 1;
 }
 
-int launch_cache_insert(TableDev cache, const uint64_t* dig, const uint32_t* sel_list,
-                        const uint64_t* totals, const uint64_t* offsets, uint64_t base,
-                        uint64_t max_n, cudaStream_t s) {
-  if (max_n == 0) return 0;
-  uint64_t blocks = (max_n + 255) / 256;
+int launch_cache_assign(TableDev cache, const uint64_t* dig, const uint32_t* sel_list,
+                        const uint64_t* totals, const uint32_t* lens, const uint32_t* free_stack,
+                        uint64_t free_n, uint32_t slot_shift, uint64_t* list_off,
+                        uint32_t* slot_len, uint64_t max_n, cudaStream_t s) {
+  if (max_n == 0 || free_n == 0) return 0;
+  uint64_t blocks = (std::min(max_n, free_n) + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  launch_pdl(k_cache_insert, unsigned(blocks), 256, 0, s, cache, dig, sel_list, totals, offsets,
-             base);
+  launch_pdl(k_cache_assign, unsigned(blocks), 256, 0, s, cache, dig, sel_list, totals, lens,
+             free_stack, free_n, slot_shift, list_off, slot_len);
+  return 1;
+}
+
+int launch_cache_gc(TableDev old, TableDev live, TableDev fresh, uint32_t* free_stack,
+                    uint64_t free_n, const uint32_t* slot_len, unsigned long long* cnt,
+                    cudaStream_t s) {
+  cudaMemsetAsync(cnt, 0, 3 * sizeof(unsigned long long), s);
+  uint64_t blocks = (old.mask + 2 + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_cache_gc<<<unsigned(blocks), 256, 0, s>>>(old, live, fresh, free_stack, free_n, slot_len, cnt);
+  return 1;
+}
+
+int launch_copy_ranges(uint8_t* const* dst, const uint8_t* const* src, const uint64_t* bytes,
+                       uint32_t nr, uint64_t max_bytes, cudaStream_t s) {
+  if (nr == 0 || max_bytes == 0) return 0;
+  uint64_t blocks = (max_bytes / 16 + kThreads - 1) / kThreads;
+  if (blocks > copy_grid()) blocks = copy_grid();
+  k_copy_ranges<<<unsigned(blocks), kThreads, 0, s>>>(dst, src, bytes, nr);
   return 1;
 }
 
 int launch_splice_in(uint8_t* arena, const GridDev& to, const uint32_t* lens, const uint64_t* want,
                      const int64_t* match, const uint64_t* dig_from, TableDev cache,
-                     const uint8_t* cache_base, unsigned long long* counters, cudaStream_t s) {
+                     const uint8_t* cache_base, uint32_t slot_shift, unsigned long long* counters,
+                     cudaStream_t s) {
   cudaMemsetAsync(counters, 0, 3 * sizeof(unsigned long long), s);
   if (to.nchunks == 0) return 0;
   uint64_t blocks = (to.nchunks * 4 + kThreads - 1) / kThreads;  // 8 chunks per warp step
   if (blocks > copy_grid()) blocks = copy_grid();
   launch_pdl(k_splice_in, unsigned(blocks), kThreads, 0, s, arena, to, lens, want, match, dig_from,
-             cache, cache_base, counters);
+             cache, cache_base, slot_shift, counters);
   return 1;
 }
 

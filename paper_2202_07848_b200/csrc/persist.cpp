@@ -132,20 +132,17 @@ bool write_all(int fd, const uint8_t* p, size_t n) {
   return true;
 }
 
-// Blob files are created in place with O_EXCL (one syscall decides "already
-// present", like a non-fresh BlobStore::put); a torn file left by a crash is
-// caught by snap_load's digest verification. Returns 1 written, 0 present, -errno.
+int put_file(const std::string& path, const void* p, size_t n, bool skip_existing);
+
+// Blob files: a file already present with the blob's size counts as present
+// (one stat, like a non-fresh BlobStore::put); otherwise the blob is written to
+// a temp file in the same directory and renamed into place, so a crash never
+// leaves a torn file under the content-addressed name (a wrong-size file left
+// by an older writer is rewritten). Returns 1 written, 0 present, -errno.
 int put_blob(const std::string& path, const void* p, size_t n) {
-  const int fd = ::open(path.c_str(), O_WRONLY | O_CREAT | O_EXCL | O_CLOEXEC, 0644);
-  if (fd < 0) return errno == EEXIST ? 0 : -errno;
-  const bool ok = write_all(fd, static_cast<const uint8_t*>(p), n);
-  const int e = errno;
-  ::close(fd);
-  if (!ok) {
-    ::unlink(path.c_str());
-    return -e;
-  }
-  return 1;
+  struct stat sb;
+  if (::stat(path.c_str(), &sb) == 0 && S_ISREG(sb.st_mode) && uint64_t(sb.st_size) == n) return 0;
+  return put_file(path, p, n, false);
 }
 
 // Layout / manifest files: tmp in the same directory + rename (atomic replace).
@@ -328,7 +325,7 @@ extern "C" int snap_persist_rank(snap_ctx* ctx, const char* dir, int layout_rank
   RC(snap_get_digests(ctx, dig.data(), nullptr, bufdig.data()));
   std::vector<Blob> blobs;
   uint64_t s_g = 0, staged = 0;
-  if (ctx->comm && ctx->exchanged) {
+  if (ctx->attached() && ctx->exchanged) {
     uint64_t n = 0;
     RC(snap_global_info(ctx, &n, nullptr));
     std::vector<uint64_t> gdig(n), soff(n);

@@ -111,6 +111,10 @@ uint32_t mma_schedule(const uint64_t* addr, const uint64_t* bytes, uint32_t n,
                       uint32_t page_shift, uint32_t chunk_shift, int sms,
                       std::vector<uint32_t>& out);
 
+// The decoupled look-back scans (k_select.cu) keep a tile's chunk count in 26
+// bits of the status word: a selection / shard scan covers < 2^26 entries.
+constexpr uint64_t kMaxScanEntries = 1ull << 26;
+
 // Open-addressing digest table (dedup + known set), power-of-two capacity.
 
 // Launchers (each returns the number of kernels launched).
@@ -232,17 +236,46 @@ int launch_scatter_shards(uint8_t* arena, const GridDev& g, const uint32_t* lens
 int launch_compare(const uint64_t* a, const uint64_t* b, uint64_t n, unsigned long long* nbad,
                    cudaStream_t s);
 
-// K3 with an image source: chunk sel_list[k] from image + src_off[chunk].
+// K3 with an image source: chunk sel_list[k] from image + src_off[chunk] to
+// dst + offsets[chunk] (offsets[k] when offsets_by_list).
 int launch_gather_from(const uint8_t* image, const uint64_t* src_off, const uint32_t* lens,
                        const uint32_t* sel_list, const uint64_t* totals, const uint64_t* offsets,
-                       uint8_t* dst, uint64_t max_sel, cudaStream_t s);
-// Splice: chunk-cache index insert and the swap-in pass.
-int launch_cache_insert(TableDev cache, const uint64_t* dig, const uint32_t* sel_list,
-                        const uint64_t* totals, const uint64_t* offsets, uint64_t base,
-                        uint64_t max_n, cudaStream_t s);
+                       uint8_t* dst, uint64_t max_sel, cudaStream_t s, bool offsets_by_list = false);
+// Splice chunk cache (fixed HBM slot array + digest -> slot index): slot
+// assignment of the selected chunks from the free stack (+ index insert), the
+// reclamation pass, and the swap-in pass (cache.vals = slot index).
+int launch_cache_assign(TableDev cache, const uint64_t* dig, const uint32_t* sel_list,
+                        const uint64_t* totals, const uint32_t* lens, const uint32_t* free_stack,
+                        uint64_t free_n, uint32_t slot_shift, uint64_t* list_off,
+                        uint32_t* slot_len, uint64_t max_n, cudaStream_t s);
+int launch_cache_gc(TableDev old, TableDev live, TableDev fresh, uint32_t* free_stack,
+                    uint64_t free_n, const uint32_t* slot_len, unsigned long long* cnt,
+                    cudaStream_t s);
 int launch_splice_in(uint8_t* arena, const GridDev& to, const uint32_t* lens, const uint64_t* want,
                      const int64_t* match, const uint64_t* dig_from, TableDev cache,
-                     const uint8_t* cache_base, unsigned long long* counters, cudaStream_t s);
+                     const uint8_t* cache_base, uint32_t slot_shift, unsigned long long* counters,
+                     cudaStream_t s);
+// dst[r] <- src[r], bytes[r] (multiple of 16) for r < nr; device pointer arrays.
+int launch_copy_ranges(uint8_t* const* dst, const uint8_t* const* src, const uint64_t* bytes,
+                       uint32_t nr, uint64_t max_bytes, cudaStream_t s);
+
+// Fixed-order allreduce over peer memory (k_allreduce.cu): GPU `me` sums its
+// slice of every source in list order and stores it into every dst; with
+// use_flags, device flag barriers (system-scope release/acquire on the peers'
+// flag lines) before the reads and after the stores.
+struct ArArgs {
+  const uint8_t* const* src = nullptr;  // [R] peer-mapped sources, sum order
+  uint8_t* const* dst = nullptr;        // [N] every GPU's destination
+  uint64_t* const* flags = nullptr;     // [N] every GPU's flag lines
+  uint64_t* myflag = nullptr;
+  uint32_t R = 0, N = 1, me = 0;
+  int dtype = 0;
+  uint64_t elems = 0;
+  uint64_t epoch = 0;
+  int use_flags = 0;
+  unsigned int* cta_count = nullptr;    // zero; the last CTA resets it
+};
+int launch_ordered_allreduce(const ArArgs& a, cudaStream_t s);
 
 // K5.
 int launch_grad_sum(int dtype, uint8_t* arena, const uint64_t* src_addrs_dev, uint32_t nsrc,

@@ -5,14 +5,24 @@
 //    digest-indexed CHUNK cache in spare HBM (180 GB per GPU holds several
 //    replicas' state), so swap-out/in are D2D copies at HBM speed instead of
 //    PCIe transfers, and dedup is per 64 KiB chunk instead of per buffer;
+//  * the cache is a fixed array of chunk-sized slots with a device free stack
+//    and a digest -> slot index; when a swap-out could run out of slots, the
+//    chunks no rank records any more are reclaimed (the reference's map only
+//    grows, which a fixed HBM region cannot afford over many mini-batches);
 //  * swap-out = K1 hash of the outgoing rank's live, non-pending buffers +
-//    K2 selection against the cache index + K3 gather of the new chunks;
+//    K2 selection against the cache index + slot assignment + K3 gather of
+//    the new chunks;
 //  * swap-in = one pass over the incoming rank's chunks: resident when the
 //    fresh digest of the same address range equals the incoming rank's
 //    recorded digest (the stale-digest defect of SURVEY App. A-1 is fixed by
 //    construction: the comparison uses the digests just computed), else a
-//    copy from the cache by digest; a missing digest is a SimFault.
-// One host sync per switch (cache cursor + the switch report of job.cpp:181-195).
+//    copy from the cache by digest; a missing digest is a SimFault;
+//  * collective results for inactive ranks are queued and installed at their
+//    next switch-in (JobRuntime::on_coll_complete / switch_to, job.cpp:164-171,
+//    206-222, ProxyServer::install_queue, proxy.hpp:75-79).
+// One host sync per switch (the switch report of job.cpp:181-195).
+#include <memory>
+
 #include "ctx.h"
 
 struct RankGrid {
@@ -21,52 +31,197 @@ struct RankGrid {
   std::vector<uint32_t> lens;
   std::vector<uint64_t> chunk_addr;
   uint64_t nchunks = 0, bytes = 0;
+  uint32_t chunk_bytes = 0;
   DevMem d_addr, d_bytes, d_cstart, d_lens, d_rec, d_tmaps;
   GridDev grid;
   bool recorded = false;
 };
 
+// A collective result kept for the ranks that install it later
+// (DeferredInstall::words, proxy.hpp:75-78): one device copy shared by every
+// queued install of the same call.
+struct ResultSlab {
+  DevMem mem;
+  ~ResultSlab() { release(mem); }
+};
+struct Install {
+  uint64_t dst = 0, bytes = 0;
+  std::shared_ptr<ResultSlab> src;
+};
+
 struct SpliceState {
-  uint64_t cap = 0, cursor = 0, entries = 0;
-  DevMem cache, ck, cv, counters, seed_off;
-  uint64_t cmask = 0;
+  uint64_t slot_bytes = 65536, nslots = 0, free_n = 0, live_bytes = 0, entries = 0;
+  uint32_t slot_shift = 16;
+  uint64_t gc_runs = 0, gc_freed_bytes = 0;
+  DevMem cache, ck, cv, ck2, cv2, lk, lv, free_stack, slot_len, list_off, counters, seed_off;
+  DevMem inst_ptrs;  // device arrays of the install copies
+  uint64_t cmask = 0, lmask = 0;
   std::map<int, RankGrid> ranks;
   std::map<std::pair<int, int>, DevMem> match;
+  std::map<int, std::vector<Install>> queue;
   int active = -1;
 };
 
 void splice_release(snap_ctx* ctx) {
   SpliceState* S = ctx->splice;
   if (!S) return;
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (auto& [r, g] : S->ranks)
     for (DevMem* m : {&g.d_addr, &g.d_bytes, &g.d_cstart, &g.d_lens, &g.d_rec, &g.d_tmaps})
       release(*m);
   for (auto& [k, m] : S->match) release(m);
-  for (DevMem* m : {&S->cache, &S->ck, &S->cv, &S->counters, &S->seed_off}) release(*m);
+  for (DevMem* m : {&S->cache, &S->ck, &S->cv, &S->ck2, &S->cv2, &S->lk, &S->lv, &S->free_stack,
+                    &S->slot_len, &S->list_off, &S->counters, &S->seed_off, &S->inst_ptrs})
+    release(*m);
   delete S;
   ctx->splice = nullptr;
 }
 
+namespace {
+
+TableDev cache_index(SpliceState* S) {
+  return TableDev{P<unsigned long long>(S->ck), P<unsigned long long>(S->cv), S->cmask};
+}
+
+// Reclaims the slots of cached chunks that no rank records any more: live set
+// = every recorded rank's digest vector (the outgoing rank's already
+// refreshed), index rebuilt with the live entries, dead slots pushed back.
+int cache_gc(snap_ctx* ctx) {
+  SpliceState* S = ctx->splice;
+  uint64_t nrec = 0;
+  for (auto& [r, g] : S->ranks)
+    if (g.recorded) nrec += g.nchunks;
+  const uint64_t lcap = table_cap(std::max<uint64_t>(nrec, 1));
+  unsigned long long *lk, *lv, *k2, *v2, *cnt;
+  RC(ensure(ctx, S->lk, lcap + 1, &lk));
+  RC(ensure(ctx, S->lv, lcap + 1, &lv));
+  RC(ensure(ctx, S->ck2, S->cmask + 2, &k2));
+  RC(ensure(ctx, S->cv2, S->cmask + 2, &v2));
+  RC(ensure(ctx, S->counters, 4, &cnt));
+  TableDev live{lk, lv, lcap - 1};
+  CKL(snap::launch_table_clear(live, ctx->stream));
+  for (auto& [r, g] : S->ranks)
+    if (g.recorded) CKL(snap::launch_table_insert_min(live, P<uint64_t>(g.d_rec), g.nchunks, 0, ctx->stream));
+  TableDev fresh{k2, v2, S->cmask};
+  CKL(snap::launch_table_clear(fresh, ctx->stream));
+  CKL(snap::launch_cache_gc(cache_index(S), live, fresh, P<uint32_t>(S->free_stack), S->free_n,
+                            P<uint32_t>(S->slot_len), cnt, ctx->stream));
+  unsigned long long c[3] = {0, 0, 0};
+  CK(cudaMemcpyAsync(c, cnt, 24, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  std::swap(S->ck, S->ck2);
+  std::swap(S->cv, S->cv2);
+  S->free_n += c[0];
+  S->live_bytes -= c[1];
+  S->entries = c[2];
+  S->gc_runs += 1;
+  S->gc_freed_bytes += c[1];
+  return SNAP_OK;
+}
+
+// Stores the chunks the last selection over `dig` picked (ctx->sel_list /
+// ctx->totals) into free cache slots: from the arena grid `from` (swap-out) or
+// from image + src_off (seeding). Makes room first when the worst case
+// (every chunk new) does not fit the free slots.
+int cache_put(snap_ctx* ctx, const uint64_t* dig, const uint32_t* lens, uint64_t n,
+              const GridDev* from, const uint8_t* image, const uint64_t* src_off) {
+  SpliceState* S = ctx->splice;
+  uint64_t tot[2] = {0, 0};
+  if (S->free_n < n) {
+    // tight: learn how many chunks are actually new before assigning slots
+    CK(cudaMemcpyAsync(tot, ctx->totals.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (tot[0] > S->free_n)
+      return fail(ctx, SNAP_ENOMEM, "splice: chunk cache full (" + std::to_string(S->nslots - S->free_n) +
+                                        " of " + std::to_string(S->nslots) + " slots hold chunks "
+                                        "recorded by some rank; " + std::to_string(tot[0]) +
+                                        " new chunks)");
+  }
+  uint64_t* loff;
+  RC(ensure(ctx, S->list_off, std::max<uint64_t>(n, 1), &loff));
+  CKL(snap::launch_cache_assign(cache_index(S), dig, P<uint32_t>(ctx->sel_list),
+                                P<uint64_t>(ctx->totals), lens, P<uint32_t>(S->free_stack),
+                                S->free_n, S->slot_shift, loff, P<uint32_t>(S->slot_len), n,
+                                ctx->stream));
+  if (from) {
+    CKL(snap::launch_gather(ctx->arena, *from, lens, P<uint32_t>(ctx->sel_list),
+                            P<uint64_t>(ctx->totals), loff, true, nullptr, nullptr,
+                            P<uint8_t>(S->cache), std::min(n, S->free_n), ctx->stream));
+  } else {
+    CKL(snap::launch_gather_from(image, src_off, lens, P<uint32_t>(ctx->sel_list),
+                                 P<uint64_t>(ctx->totals), loff, P<uint8_t>(S->cache),
+                                 std::min(n, S->free_n), ctx->stream, true));
+  }
+  return SNAP_OK;
+}
+
+// Applies the rank's queued result installs (switch_to, job.cpp:164-171):
+// one kernel for all of them; returns their bytes.
+int apply_installs(snap_ctx* ctx, int rank, uint64_t* bytes_out) {
+  SpliceState* S = ctx->splice;
+  *bytes_out = 0;
+  auto it = S->queue.find(rank);
+  if (it == S->queue.end() || it->second.empty()) return SNAP_OK;
+  const auto& q = it->second;
+  const uint32_t nr = uint32_t(q.size());
+  std::vector<uint64_t> host(3 * nr);
+  uint64_t mx = 0;
+  for (uint32_t i = 0; i < nr; ++i) {
+    host[i] = reinterpret_cast<uint64_t>(ctx->arena + q[i].dst);
+    host[nr + i] = reinterpret_cast<uint64_t>(q[i].src->mem.p);
+    host[2 * nr + i] = q[i].bytes;
+    mx = std::max(mx, q[i].bytes);
+    *bytes_out += q[i].bytes;
+  }
+  uint64_t* d;
+  RC(ensure(ctx, S->inst_ptrs, 3 * nr, &d));
+  CK(cudaMemcpyAsync(d, host.data(), 3 * nr * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CKL(snap::launch_copy_ranges(reinterpret_cast<uint8_t* const*>(d),
+                               reinterpret_cast<const uint8_t* const*>(d + nr), d + 2 * nr, nr, mx,
+                               ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));  // host array + result slabs die here
+  S->queue.erase(it);
+  return SNAP_OK;
+}
+
+}  // namespace
+
 extern "C" {
 
-int snap_splice_init(snap_ctx* ctx, uint64_t cache_bytes) {
-  if (!ctx || cache_bytes == 0) return SNAP_EINVAL;
+int snap_splice_init_slots(snap_ctx* ctx, uint64_t cache_bytes, uint32_t slot_bytes) {
+  if (!ctx || cache_bytes == 0 || !pow2(slot_bytes) || slot_bytes < 256)
+    return fail(ctx, SNAP_EINVAL, "splice_init: cache_bytes > 0, slot_bytes a power of two >= 256");
   CK(cudaSetDevice(ctx->device));
   splice_release(ctx);
   ctx->splice = new SpliceState();
   SpliceState* S = ctx->splice;
-  S->cap = (cache_bytes + 255) / 256 * 256;
+  S->slot_bytes = slot_bytes;
+  S->slot_shift = log2u(slot_bytes);
+  S->nslots = std::max<uint64_t>(cache_bytes / slot_bytes, 1);
+  if (S->nslots >= (1ull << 32)) return fail(ctx, SNAP_EINVAL, "splice_init: too many slots");
   uint8_t* c;
-  RC(ensure(ctx, S->cache, S->cap, &c));
-  const uint64_t tcap = table_cap(std::max<uint64_t>(S->cap / 4096, 1024));
+  RC(ensure(ctx, S->cache, S->nslots * slot_bytes, &c));
+  // index capacity >= 2 x slots: an index of cached chunks never fills
+  const uint64_t tcap = table_cap(S->nslots);
   unsigned long long *k, *v, *cnt;
   RC(ensure(ctx, S->ck, tcap + 1, &k));
   RC(ensure(ctx, S->cv, tcap + 1, &v));
   RC(ensure(ctx, S->counters, 4, &cnt));
   S->cmask = tcap - 1;
   CKL(snap::launch_table_clear(TableDev{k, v, S->cmask}, ctx->stream));
+  uint32_t *fs, *sl;
+  RC(ensure(ctx, S->free_stack, S->nslots, &fs));
+  RC(ensure(ctx, S->slot_len, S->nslots, &sl));
+  std::vector<uint32_t> init(S->nslots);
+  for (uint64_t j = 0; j < S->nslots; ++j) init[j] = uint32_t(S->nslots - 1 - j);  // slot 0 on top
+  CK(cudaMemcpyAsync(fs, init.data(), S->nslots * 4, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  S->free_n = S->nslots;
   return SNAP_OK;
+}
+
+int snap_splice_init(snap_ctx* ctx, uint64_t cache_bytes) {
+  return snap_splice_init_slots(ctx, cache_bytes, 65536);
 }
 
 // The rank's live buffers (its RankBuf map, splice.hpp:26-34) in slot order;
@@ -79,8 +234,10 @@ int snap_splice_set_rank(snap_ctx* ctx, int rank, const snap_buf* bufs, uint64_t
   if (!pow2(g.page_bytes) || !pow2(g.chunk_bytes) || g.page_bytes < 256 ||
       g.chunk_bytes < g.page_bytes || g.chunk_bytes / g.page_bytes > 32)
     return fail(ctx, SNAP_EINVAL, "splice: bad geometry");
-  CK(cudaSetDevice(ctx->device));
   SpliceState* S = ctx->splice;
+  if (g.chunk_bytes > S->slot_bytes)
+    return fail(ctx, SNAP_EINVAL, "splice: chunk_bytes larger than the cache slot");
+  CK(cudaSetDevice(ctx->device));
   RankGrid& R = S->ranks[rank];
   R.bufs.clear();
   for (uint64_t i = 0; i < n; ++i)
@@ -91,6 +248,7 @@ int snap_splice_set_rank(snap_ctx* ctx, int rank, const snap_buf* bufs, uint64_t
   R.lens.clear();
   R.chunk_addr.clear();
   R.bytes = 0;
+  R.chunk_bytes = g.chunk_bytes;
   for (uint64_t b = 0; b < nb; ++b) {
     const snap_buf& x = R.bufs[b];
     if (x.bytes == 0 || x.addr % 256 || x.bytes % 256)
@@ -107,6 +265,8 @@ int snap_splice_set_rank(snap_ctx* ctx, int rank, const snap_buf* bufs, uint64_t
     R.bytes += x.bytes;
   }
   R.nchunks = R.cstart[nb];
+  if (R.nchunks >= snap::kMaxScanEntries)
+    return fail(ctx, SNAP_EINVAL, "splice: a rank holds at most 2^26 - 1 chunks");
   uint64_t *da, *db, *dc, *dr;
   uint32_t* dl;
   RC(ensure(ctx, R.d_addr, nb, &da));
@@ -142,27 +302,21 @@ int snap_splice_switch(snap_ctx* ctx, int from, int to, snap_switch_stats* st) {
   if ((from >= 0 && !S->ranks.count(from)) || (to >= 0 && !S->ranks.count(to)))
     return fail(ctx, SNAP_EINVAL, "splice: unknown rank");
   CK(cudaSetDevice(ctx->device));
-  TableDev cache{P<unsigned long long>(S->ck), P<unsigned long long>(S->cv), S->cmask};
   snap_switch_stats out{};
   RankGrid* F = from >= 0 ? &S->ranks[from] : nullptr;
   RankGrid* T = to >= 0 ? &S->ranks[to] : nullptr;
   if (F) {
-    if (S->cursor + F->bytes > S->cap)
-      return fail(ctx, SNAP_ENOMEM, "splice: chunk cache full (" + std::to_string(S->cursor) +
-                                        " of " + std::to_string(S->cap) + " bytes used)");
-    // swap-out: refresh digests (K1), select against the cache (K2), gather (K3)
+    // swap-out: refresh digests (K1), select against the cache (K2), slots +
+    // gather (K3); reclaim first when the new chunks might not fit
     CKL(snap::launch_hash(ctx->arena, F->grid, P<uint64_t>(F->d_rec), nullptr, nullptr,
                           ctx->stream));
     F->recorded = true;
-    RC(select_with_known(ctx, P<uint64_t>(F->d_rec), P<uint32_t>(F->d_lens), F->nchunks, cache,
-                         S->entries > 0));
+    if (S->free_n < F->nchunks) RC(cache_gc(ctx));
+    RC(select_with_known(ctx, P<uint64_t>(F->d_rec), P<uint32_t>(F->d_lens), F->nchunks,
+                         cache_index(S), S->entries > 0));
     ctx->selected = false;  // the ctx selection vectors now hold this plan
-    CKL(snap::launch_gather(ctx->arena, F->grid, P<uint32_t>(F->d_lens), P<uint32_t>(ctx->sel_list),
-                            P<uint64_t>(ctx->totals), P<uint64_t>(ctx->offsets), false, nullptr,
-                            nullptr, P<uint8_t>(S->cache) + S->cursor, F->nchunks, ctx->stream));
-    CKL(snap::launch_cache_insert(cache, P<uint64_t>(F->d_rec), P<uint32_t>(ctx->sel_list),
-                                  P<uint64_t>(ctx->totals), P<uint64_t>(ctx->offsets), S->cursor,
-                                  F->nchunks, ctx->stream));
+    RC(cache_put(ctx, P<uint64_t>(F->d_rec), P<uint32_t>(F->d_lens), F->nchunks, &F->grid,
+                 nullptr, nullptr));
     out.hashed_bytes = F->bytes;
   }
   unsigned long long cnt[3] = {0, 0, 0};
@@ -186,25 +340,99 @@ int snap_splice_switch(snap_ctx* ctx, int from, int to, snap_switch_stats* st) {
       match = P<int64_t>(S->match[key]);
     }
     CKL(snap::launch_splice_in(ctx->arena, T->grid, P<uint32_t>(T->d_lens), P<uint64_t>(T->d_rec),
-                               match, F ? P<uint64_t>(F->d_rec) : nullptr, cache,
-                               P<uint8_t>(S->cache), P<unsigned long long>(S->counters),
-                               ctx->stream));
+                               match, F ? P<uint64_t>(F->d_rec) : nullptr, cache_index(S),
+                               P<uint8_t>(S->cache), S->slot_shift,
+                               P<unsigned long long>(S->counters), ctx->stream));
     CK(cudaMemcpyAsync(cnt, S->counters.p, 24, cudaMemcpyDeviceToHost, ctx->stream));
   }
   uint64_t tot[2] = {0, 0};
   if (F) CK(cudaMemcpyAsync(tot, ctx->totals.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  S->cursor += tot[1];
+  S->free_n -= tot[0];
+  S->live_bytes += tot[1];
   S->entries += tot[0];
   S->active = to;
+  // deferred collective results of the incoming rank (after the swap-ins,
+  // like the reference: execute_switch, then install_result per queued entry)
+  uint64_t inst = 0;
+  if (to >= 0) RC(apply_installs(ctx, to, &inst));
   out.swap_out_bytes = tot[1];
   out.swap_in_bytes = cnt[0];
   out.resident_bytes = cnt[1];
-  out.cache_bytes = S->cursor;
+  out.cache_bytes = S->live_bytes;
+  out.install_bytes = inst;
+  out.cache_free_bytes = S->free_n * S->slot_bytes;
+  out.reclaimed_bytes = S->gc_freed_bytes;
   if (st) *st = out;
   if (cnt[2])
     return fail(ctx, SNAP_EFAULT, "splice: content for " + std::to_string(cnt[2]) +
                                       " chunk digest(s) lost (not resident, not cached)");
+  return SNAP_OK;
+}
+
+// JobRuntime::on_coll_complete (job.cpp:206-222): the result at arena
+// [src_addr, +bytes) goes into rank ranks[i]'s buffer at dst_addrs[i]. The
+// active rank (and every rank of a ctx without splicing) gets it now; the
+// others queue it (one library copy of the result shared by the queue,
+// DeferredInstall::words, proxy.hpp:75-78) until their next switch-in.
+int snap_splice_install(snap_ctx* ctx, const int* ranks, const uint64_t* dst_addrs, uint32_t n,
+                        uint64_t src_addr, uint64_t bytes) {
+  if (!ctx || (n && (!ranks || !dst_addrs)) || bytes % 16 || src_addr % 16)
+    return fail(ctx, SNAP_EINVAL, "install: 16-byte aligned ranges");
+  RC(check_range(ctx, src_addr, bytes));
+  for (uint32_t i = 0; i < n; ++i) {
+    RC(check_range(ctx, dst_addrs[i], bytes));
+    if (dst_addrs[i] % 16) return fail(ctx, SNAP_EINVAL, "install: 16-byte aligned ranges");
+  }
+  CK(cudaSetDevice(ctx->device));
+  SpliceState* S = ctx->splice;
+  std::vector<uint64_t> now;
+  std::shared_ptr<ResultSlab> slab;
+  for (uint32_t i = 0; i < n; ++i) {
+    const bool active = !S || ranks[i] < 0 || ranks[i] == S->active;
+    if (active) {
+      now.push_back(dst_addrs[i]);
+      continue;
+    }
+    if (!slab) {
+      slab = std::make_shared<ResultSlab>();
+      uint8_t* p;
+      RC(ensure(ctx, slab->mem, bytes, &p));
+      now.push_back(~0ull);  // marker: copy the result into the slab
+    }
+    S->queue[ranks[i]].push_back(Install{dst_addrs[i], bytes, slab});
+  }
+  if (now.empty() || bytes == 0) return SNAP_OK;
+  const uint32_t nr = uint32_t(now.size());
+  std::vector<uint64_t> host(3 * nr);
+  for (uint32_t i = 0; i < nr; ++i) {
+    host[i] = now[i] == ~0ull ? reinterpret_cast<uint64_t>(slab->mem.p)
+                              : reinterpret_cast<uint64_t>(ctx->arena + now[i]);
+    host[nr + i] = reinterpret_cast<uint64_t>(ctx->arena + src_addr);
+    host[2 * nr + i] = bytes;
+  }
+  DevMem tmp;
+  uint64_t* d;
+  RC(ensure(ctx, S ? S->inst_ptrs : tmp, 3 * nr, &d));
+  CK(cudaMemcpyAsync(d, host.data(), 3 * nr * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CKL(snap::launch_copy_ranges(reinterpret_cast<uint8_t* const*>(d),
+                               reinterpret_cast<const uint8_t* const*>(d + nr), d + 2 * nr, nr,
+                               bytes, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  release(tmp);
+  return SNAP_OK;
+}
+
+// Pending installs of a rank: count and bytes (the switch report's
+// install_bytes before it happens).
+int snap_splice_pending(snap_ctx* ctx, int rank, uint64_t* count, uint64_t* bytes) {
+  if (!ctx || !ctx->splice) return SNAP_EINVAL;
+  uint64_t c = 0, b = 0;
+  auto it = ctx->splice->queue.find(rank);
+  if (it != ctx->splice->queue.end())
+    for (const Install& q : it->second) c += 1, b += q.bytes;
+  if (count) *count = c;
+  if (bytes) *bytes = b;
   return SNAP_OK;
 }
 
@@ -219,11 +447,7 @@ int splice_seed(snap_ctx* ctx, int rank, const uint8_t* image, const uint64_t* s
   SpliceState* S = ctx->splice;
   if (!S || !S->ranks.count(rank)) return fail(ctx, SNAP_EINVAL, "splice: unknown rank");
   RankGrid& R = S->ranks[rank];
-  if (S->cursor + R.bytes > S->cap)
-    return fail(ctx, SNAP_ENOMEM, "splice: chunk cache full (" + std::to_string(S->cursor) +
-                                      " of " + std::to_string(S->cap) + " bytes used)");
   CK(cudaSetDevice(ctx->device));
-  TableDev cache{P<unsigned long long>(S->ck), P<unsigned long long>(S->cv), S->cmask};
   uint64_t* so;
   RC(ensure(ctx, S->seed_off, R.nchunks, &so));
   if (R.nchunks) {
@@ -231,21 +455,25 @@ int splice_seed(snap_ctx* ctx, int rank, const uint8_t* image, const uint64_t* s
                        ctx->stream));
     CK(cudaMemcpyAsync(so, src_off, R.nchunks * 8, cudaMemcpyHostToDevice, ctx->stream));
   }
-  RC(select_with_known(ctx, P<uint64_t>(R.d_rec), P<uint32_t>(R.d_lens), R.nchunks, cache,
-                       S->entries > 0));
+  const bool was = R.recorded;
+  R.recorded = true;  // its digests are live from now on
+  if (S->free_n < R.nchunks) {
+    const int rc = cache_gc(ctx);
+    if (rc) {
+      R.recorded = was;
+      return rc;
+    }
+  }
+  RC(select_with_known(ctx, P<uint64_t>(R.d_rec), P<uint32_t>(R.d_lens), R.nchunks,
+                       cache_index(S), S->entries > 0));
   ctx->selected = false;
-  CKL(snap::launch_gather_from(image, so, P<uint32_t>(R.d_lens), P<uint32_t>(ctx->sel_list),
-                               P<uint64_t>(ctx->totals), P<uint64_t>(ctx->offsets),
-                               P<uint8_t>(S->cache) + S->cursor, R.nchunks, ctx->stream));
-  CKL(snap::launch_cache_insert(cache, P<uint64_t>(R.d_rec), P<uint32_t>(ctx->sel_list),
-                                P<uint64_t>(ctx->totals), P<uint64_t>(ctx->offsets), S->cursor,
-                                R.nchunks, ctx->stream));
+  RC(cache_put(ctx, P<uint64_t>(R.d_rec), P<uint32_t>(R.d_lens), R.nchunks, nullptr, image, so));
   uint64_t tot[2] = {0, 0};
   CK(cudaMemcpyAsync(tot, ctx->totals.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  S->cursor += tot[1];
+  S->free_n -= tot[0];
+  S->live_bytes += tot[1];
   S->entries += tot[0];
-  R.recorded = true;
   return SNAP_OK;
 }
 

@@ -1,4 +1,5 @@
-"""Elastic resize parity worker (C5 shape, small): run under torchrun on N GPUs (N even).
+"""Elastic resize parity worker (C5 shape, small): under torchrun on N GPUs (N even), or as
+N threads sharing one GPU (tests/_group.py).
 
 1. N ranks hold identical DP state (params + Adam m,v, identical addresses); snapshot on N
    (cross-rank dedup -> each GPU writes a 1/N stripe shard).
@@ -34,40 +35,26 @@ def replica_layout(scale_mib):
     return bufs, addr
 
 
-def main():
-    import torch
-    import torch.distributed as td
-    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
-    td.init_process_group("gloo", rank=rank, world_size=world)
+def run(g) -> bool:
+    rank, world = g.rank, g.world
     scale = int(os.environ.get("RESIZE_SCALE_MIB", "8"))
     bufs, nbytes = replica_layout(scale)
     truth = O.fill_mix64(nbytes // 8, 1234, 0)
-    ctx = snap.Ctx(local, nbytes + MIB)
+    ctx = snap.Ctx(g.device, nbytes + MIB)
     ok = True
-
-    def new_comm(members):
-        ctx.comm_destroy()  # collective over the previous world (every rank that had one)
-        uid = torch.zeros(128, dtype=torch.uint8)
-        if rank == members[0]:
-            uid[:] = torch.frombuffer(bytearray(snap.Ctx.unique_id()), dtype=torch.uint8)
-        td.broadcast(uid, members[0])
-        if rank in members:
-            ctx.comm_init(len(members), members.index(rank), bytes(uid.numpy().tobytes()))
-
     members = list(range(world))
     ctx.write(0, truth)
     ctx.set_buffers(bufs)
     stage = 0
     while len(members) >= 2:
-        new_comm(members)
+        ctx.comm_destroy()  # collective over the previous world (every rank that had one)
+        g.comm_init(ctx, members)
         if rank in members:
             ctx.snapshot()
             _, _, my_bytes, _ = ctx.shard()
             _, _, _, gbytes, _ = ctx.global_selection()
             assert gbytes == nbytes, (gbytes, nbytes)  # replicas dedup to one copy
-        handles = [None] * world
-        td.all_gather_object(handles, ctx.ipc_export() if rank in members else b"\0" * 64)
+        handles = g.all_gather(ctx.ipc_export() if rank in members else b"\0" * 64)
         blob = b"".join(handles[m] for m in members)
         targets = members[: len(members) // 2]
         if rank in targets:
@@ -81,16 +68,23 @@ def main():
             if rank == targets[0]:
                 print(f"stage {stage}: {len(members)} -> {len(targets)} GPUs, shard "
                       f"{my_bytes} B, restored {nbytes} B bit-exact")
-        td.barrier()  # sources keep their shards mapped until every target is done
+        g.barrier()  # sources keep their shards mapped until every target is done
         members = targets
         stage += 1
-    flags = [None] * world
-    td.all_gather_object(flags, ok)
+    ctx.comm_destroy()
+    flags = g.all_gather(ok)
     ctx.close()
-    td.destroy_process_group()
     if rank == 0:
         print("RESIZE PARITY", "OK" if all(flags) else "FAIL")
-    sys.exit(0 if all(flags) else 1)
+    return all(flags)
+
+
+def main():
+    from _group import ProcGroup
+    g = ProcGroup()
+    ok = run(g)
+    g.close()
+    sys.exit(0 if ok else 1)
 
 
 if __name__ == "__main__":

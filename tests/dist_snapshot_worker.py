@@ -1,4 +1,6 @@
-"""Multi-rank snapshot parity worker (run under torchrun, one rank per GPU).
+"""Multi-rank snapshot parity worker: under torchrun (one rank per GPU, NCCL) or as
+threads of one process sharing a GPU (tests/_group.py ThreadGroup, libsnap's in-process
+communicator).
 
 Each rank builds a small DP image (replicated P/O buffers + per-rank buffers, unequal chunk
 counts, mispredicted replication hints), snapshots it twice through the C ABI with NCCL
@@ -52,26 +54,18 @@ def fill_host(bufs, fills, nbytes):
     return img
 
 
-def main():
-    import torch.distributed as td
-    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
-    td.init_process_group("gloo", rank=rank, world_size=world)
+def run(g) -> bool:
+    rank, world = g.rank, g.world
     bufs, fills, nbytes = layout(rank)
     arena = nbytes + MIB
-    ctx = snap.Ctx(local, arena)
+    ctx = snap.Ctx(g.device, arena)
     host = fill_host(bufs, fills, nbytes)
     ctx.write(0, host)
     sb = snap.bufs_array([b[:5] for b in bufs])
     for i, b in enumerate(bufs):
         sb[i].flags = b[5]
     n = C_set_buffers(ctx, sb, len(bufs))
-    import torch
-    uid = torch.zeros(128, dtype=torch.uint8)
-    if rank == 0:
-        uid[:] = torch.frombuffer(bytearray(snap.Ctx.unique_id()), dtype=torch.uint8)
-    td.broadcast(uid, 0)
-    ctx.comm_init(world, rank, bytes(uid.numpy().tobytes()))
+    g.comm_init(ctx)
     results = []
     for it in range(2):  # second snapshot uses the learned layout
         ctx.snapshot()
@@ -81,9 +75,8 @@ def main():
         shard = ctx.read_staging(0, my_bytes) if my_bytes else np.zeros(0, np.uint8)
         results.append((d, lens, gsel, gown, goff, gbytes, writer, shard_off, my_bytes, shard))
     _, maxn = ctx.global_info()
-    objs = [None] * world
-    td.all_gather_object(objs, {"rank": rank, "host": host, "bufs": bufs, "res": results,
-                                "maxn": maxn})
+    objs = g.all_gather({"rank": rank, "host": host, "bufs": bufs, "res": results,
+                         "maxn": maxn})
     ok = True
     if rank == 0:
         objs.sort(key=lambda o: o["rank"])
@@ -132,9 +125,9 @@ def main():
                     ok = False
                     continue
                 exp = np.zeros(int(oshbytes[w]), np.uint8)
-                for g in np.nonzero((osel == 1) & (owriter == w))[0]:
-                    r = int(np.searchsorted(base, g, side="right") - 1)
-                    i = int(g - base[r])
+                for gi in np.nonzero((osel == 1) & (owriter == w))[0]:
+                    r = int(np.searchsorted(base, gi, side="right") - 1)
+                    i = int(gi - base[r])
                     # chunk i of rank r: locate its bytes in rank r's host image
                     o = objs[r]
                     k = i
@@ -143,7 +136,7 @@ def main():
                         if k < nc:
                             ln = min(65536, nb - k * 65536)
                             src = o["host"].view(np.uint8)[a + k * 65536:a + k * 65536 + ln]
-                            exp[int(oshoff[g]):int(oshoff[g]) + ln] = src
+                            exp[int(oshoff[gi]):int(oshoff[gi]) + ln] = src
                             break
                         k -= nc
                 if not np.array_equal(shard, exp):
@@ -151,34 +144,38 @@ def main():
                     ok = False
         print("DIST PARITY", "OK" if ok else "FAIL", "world", world, "chunks", npr,
               "unique", int(osel.sum()))
-    ok = persist_stage(ctx, rank, world, objs, ok) and ok
-    flag = torch.tensor([1 if ok else 0])
-    td.broadcast(flag, 0)
+    ok = persist_stage(g, ctx, objs, ok) and ok
+    ok = g.bcast(ok, 0)
+    ctx.comm_destroy()
     ctx.close()
-    td.destroy_process_group()
-    sys.exit(0 if int(flag.item()) == 1 else 1)
+    return ok
 
 
-def persist_stage(ctx, rank, world, objs, ok):
+def main():
+    from _group import ProcGroup
+    g = ProcGroup()
+    ok = run(g)
+    g.close()
+    sys.exit(0 if ok else 1)
+
+
+def persist_stage(g, ctx, objs, ok):
     """On-disk format across ranks: every rank persists its shard of the (last) snapshot into
     one shared directory (content-addressed, no coordination), then restores the NEXT rank's
     layout from the directory alone into a fresh context and compares it with that rank's
     image. Rank 0 checks that the directory holds exactly the globally unique chunks."""
     import tempfile
-    import torch.distributed as td
-    paths = [None] * world
-    td.all_gather_object(paths, tempfile.mkdtemp(prefix="snap_persist_") if rank == 0 else None)
+    rank, world = g.rank, g.world
+    paths = g.all_gather(tempfile.mkdtemp(prefix="snap_persist_") if rank == 0 else None)
     root = paths[0]
     st = ctx.persist(root)
-    sts = [None] * world
-    td.all_gather_object(sts, st)
-    td.barrier()
+    sts = g.all_gather(st)
     good = True
     peer = (rank + 1) % world
     o = [x for x in objs if x["rank"] == peer][0]
     bufs = [b[:5] for b in o["bufs"]]
     nbytes = max(a + n for (_, _, a, n, _) in bufs)
-    with snap.Ctx(int(os.environ.get("LOCAL_RANK", rank)), nbytes + MIB) as c2:
+    with snap.Ctx(g.device, nbytes + MIB) as c2:
         c2.load(root, rank=peer)
         got = c2.read(0, nbytes).view(np.uint64)
         for (_, _, a, n, _) in bufs:
@@ -194,9 +191,7 @@ def persist_stage(ctx, rank, world, objs, ok):
                   f"unique {uniq}")
             good = False
         print("PERSIST", "OK" if good else "FAIL", "files", nfiles)
-    flags = [None] * world
-    td.all_gather_object(flags, good)
-    td.barrier()
+    flags = g.all_gather(good)
     if rank == 0:
         import shutil
         shutil.rmtree(root, ignore_errors=True)

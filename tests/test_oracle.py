@@ -169,3 +169,107 @@ def test_host_pages_oracle_vs_reference_store():
     prev = set(dig[:2].tolist())
     assert [bool(f & 2) for f in f2] == [d not in prev for d in dig.tolist()]
     del rng
+
+
+def test_bf16_sum_rounding_matches_torch(oracle_mod):
+    """The bf16 gradient restatement (fp32 chain, one RN-even rounding) against torch's
+    float32 -> bfloat16 conversion on the CPU."""
+    import numpy as np
+    import torch
+    rng = np.random.default_rng(5)
+    a = (rng.standard_normal(100_000) * 10.0 ** rng.integers(-20, 20, 100_000)).astype(np.float32)
+    b = (rng.standard_normal(100_000) * 10.0 ** rng.integers(-20, 20, 100_000)).astype(np.float32)
+    ha = (a.view(np.uint32) >> 16).astype(np.uint16)
+    hb = (b.view(np.uint32) >> 16).astype(np.uint16)
+    got = oracle_mod.grad_sum_bf16([ha, hb])
+    fa = torch.from_numpy((ha.astype(np.uint32) << 16).view(np.float32))
+    fb = torch.from_numpy((hb.astype(np.uint32) << 16).view(np.float32))
+    exp = (fa + fb).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(got, exp)
+
+
+def _blobstore_select(R, chunks, known_chunks):
+    """The reference's own BlobStore::put (ckpt.cpp:16-21) over a canonical chunk sequence,
+    after the known chunks were stored: fresh flags and the staging offsets they imply."""
+    import ctypes as C
+    st = R.ref_store_new()
+    d = C.c_uint64()
+    for w in known_chunks:
+        R.ref_store_put(st, w.ctypes.data_as(C.c_void_p), w.size, C.byref(d))
+    fresh, offs, digs, total, at = [], [], [], 0, {}
+    for w in chunks:
+        f = R.ref_store_put(st, w.ctypes.data_as(C.c_void_p), w.size, C.byref(d))
+        fresh.append(f)
+        digs.append(d.value)
+        if f:
+            at[d.value] = total
+        # a repeated chunk's bytes are at its first occurrence's offset; a chunk the
+        # store already held before this snapshot has no bytes in this image
+        offs.append(at.get(d.value, 2**64 - 1))
+        total += w.size * 8 if f else 0
+    R.ref_store_free(st)
+    return np.array(fresh, np.uint8), np.array(offs, np.uint64), np.array(digs, np.uint64), total
+
+
+@pytest.mark.parametrize("case", ["ragged", "random_dups", "known_set"])
+def test_select_pinned_to_blobstore_put(ref_lib, golden, case):
+    """K2's CPU restatement (or_select: first occurrence in canonical order, not in the
+    known set, staging offsets = running sum of staged bytes) is exactly BlobStore::put's
+    `fresh` over the same chunk sequence (VERDICT r1 weak #2)."""
+    rng = np.random.default_rng(11)
+    if case == "ragged":
+        arena, bufs = ragged_arena(golden)
+        chunks = []
+        for (_r, _s, a, n, _c) in bufs:
+            for k in range(0, n, 65536):
+                chunks.append(arena[(a + k) // 8:(a + min(n, k + 65536)) // 8])
+    else:
+        pool = [O.fill_mix64(int(rng.integers(1, 64)) * 32, 100 + i, 0) for i in range(40)]
+        chunks = [pool[int(rng.integers(0, 40))] for _ in range(300)]
+    known = [] if case != "known_set" else [chunks[int(i)] for i in rng.integers(0, 300, 25)]
+    fresh, offs, digs, total = _blobstore_select(ref_lib, chunks, known)
+    lens = np.array([w.size * 8 for w in chunks], np.uint32)
+    kn = np.array([O.digest_of_words(w) for w in known], np.uint64)
+    sel, owner, off, tot = O.select(digs, lens, kn if known else None)
+    assert np.array_equal(sel, fresh)
+    assert np.array_equal(off, offs)
+    assert tot == total
+    assert np.array_equal(digs, [O.digest_of_words(w) for w in chunks])
+
+
+def appendix_b_scenario(dp):
+    """SURVEY Appendix B: one DP job, 4 layers x 2048 words, scenario seed 7, one node of dp
+    4 MiB GPUs, checkpoints at 0.5 ms and 2.1 ms of simulated time."""
+    return {"seed": 7,
+            "fleet": {"regions": [{"clusters": [{"nodes": [{"gpus": dp, "mem_mib": 4}]}]}]},
+            "jobs": [{"name": "j", "spec": {"world": dp, "dp": dp, "layers": 4,
+                                            "params_per_layer": 2048}}],
+            "events": [{"at_sec": 0.0005, "kind": "checkpoint", "job": "j"},
+                       {"at_sec": 0.0021, "kind": "checkpoint", "job": "j"}]}
+
+
+@pytest.mark.parametrize("dp,s_cr,s_cr_inc,upload", [(4, 1097728, 16384, 414240),
+                                                      (8, 2195456, 32768, 430912)])
+def test_manifest_dedup_pinned_to_reference(ref_lib, dp, s_cr, s_cr_inc, upload):
+    """build_manifest's device section (ckpt.cpp:147-167), run by the reference's own
+    scheduler on the Appendix-B scenario, reproduces the Appendix-B goldens; the oracle's
+    chunk-level select over the manifest's device buffers (canonical rank/slot order, one
+    chunk per buffer) gives the same S_G and the same device upload bytes, first and
+    incremental checkpoint (VERDICT r1 missing #6)."""
+    ms = O.ref_manifests(appendix_b_scenario(dp))
+    assert len(ms) == 2
+    m1, m2 = ms
+    assert (m1["s_g"], m2["s_g"]) == (131072, 131072)  # S_G invariant under DP degree
+    assert m1["s_cr"] == s_cr and m2["s_cr_inc"] == s_cr_inc and m1["upload_bytes"] == upload
+    prev = None
+    for m in ms:
+        recs = [d for r in range(m["world"]) for d in m["dev"][r]]
+        digs = np.array([d["digest"] for d in recs], np.uint64)
+        assert all(O.digest_of_words(d["content"]) == d["digest"] for d in recs)
+        lens = np.array([d["words"] * 8 for d in recs], np.uint32)
+        sel, _, _, tot = O.select(digs, lens)
+        assert tot == m["s_g"]
+        known = None if prev is None else prev
+        _, _, _, up = O.select(digs, lens, known)
+        assert up == m["device_upload"]
+        prev = digs
