@@ -60,6 +60,18 @@ def c2_layout():
     return bufs, replicated, addr - replicated
 
 
+def c2_config(N):
+    """The workload descriptor both arms print (static: identical dicts at the same N)."""
+    bufs, replicated, per_rank = c2_layout()
+    return {"workload": "C2: data-parallel image per rank = 1.5 GiB replicated (bf16 params + "
+                        "fp32 Adam m,v; identical on all ranks) + 0.5 GiB per-rank grads; one "
+                        "rank per GPU; cross-rank dedup + striped compaction at N>1",
+            "image_bytes_per_rank": replicated + per_rank, "chunk_bytes": CHUNK,
+            "page_bytes": PAGE, "chunks_per_rank": sum((b[3] + CHUNK - 1) // CHUNK for b in bufs),
+            "parallelism": f"dp{N} (1 rank/GPU)",
+            "l2": "inputs 2 GiB/GPU > 126 MB L2 (no flush needed)"}
+
+
 def fill_rank(ctx, rank, replicated, per_rank, seed=1):
     ctx.fill_mix64(0, replicated, seed, 0)
     ctx.fill_mix64(replicated, per_rank, seed ^ (rank << 40), replicated // 8)
@@ -85,6 +97,82 @@ def mix64_np(x):
         x = (x ^ (x >> np.uint64(30))) * np.uint64(0xbf58476d1ce4e5b9)
         x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94d049bb133111eb)
     return x ^ (x >> np.uint64(31))
+
+
+FNV_OFFSET, FNV_PRIME = np.uint64(0xCBF29CE484222325), np.uint64(0x100000001B3)
+
+
+def fnv1a_rows(rows: np.ndarray) -> np.ndarray:
+    """64-bit FNV-1a (sim.hpp:55-65) of every row of a uint8 matrix, vectorized over rows
+    (the bench's own restatement for its untimed parity sample; not the test oracle)."""
+    h = np.full(rows.shape[0], FNV_OFFSET, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        for k in range(rows.shape[1]):
+            h ^= rows[:, k].astype(np.uint64)
+            h *= FNV_PRIME
+    return h
+
+
+def chunk_digests_np(chunks: np.ndarray, page=PAGE) -> np.ndarray:
+    """Full 64 KiB chunks (n, 65536) uint8 -> digest_of_words(16 page digests) per chunk."""
+    n = chunks.shape[0]
+    pd = fnv1a_rows(chunks.reshape(n * (chunks.shape[1] // page), page))
+    return fnv1a_rows(pd.reshape(n, -1).view(np.uint8).reshape(n, -1))
+
+
+def parity_block(ctx, dist, bufs, expect_unique, nsample=48):
+    """Untimed correctness evidence of the timed snapshot path at any N: sampled full chunks
+    re-hashed on the host against the GPU digests, the global unique bytes against the
+    workload's closed form, every rank's selection / stripe writers identical, and (N>1)
+    this rank's layout rebuilt from all ranks' shards over peer memory and digest-verified
+    (N=1: from its own staging image)."""
+    import hashlib
+    N = dist.world
+    out = {"comm_ranks": N}
+    d, _ = ctx.digests()
+    starts, g = [], 0
+    for (_r, _s, a, n, _c) in bufs:
+        for k in range(0, n, CHUNK):
+            if n - k >= CHUNK:
+                starts.append((g, a + k))
+            g += 1
+    rng = np.random.default_rng(1234 + dist.rank)
+    pick = [starts[i] for i in sorted(rng.choice(len(starts), size=min(nsample, len(starts)),
+                                                  replace=False))]
+    chunks = np.stack([ctx.read(a, CHUNK) for (_, a) in pick])
+    host = chunk_digests_np(chunks)
+    ok = bool(np.array_equal(host, d[[gi for (gi, _) in pick]]))
+    out["sampled_chunk_digests"] = f"{int(ok) * len(pick)}/{len(pick)} match"
+    if N > 1:
+        _, _, _, g_bytes, _ = ctx.global_selection()
+        writer, _, _, _ = ctx.shard()
+        sel, owner, _, _, _ = ctx.global_selection()
+        hv = hashlib.blake2b(sel.tobytes() + owner.tobytes() + writer.tobytes(),
+                             digest_size=16).hexdigest()
+        agree = len(set(dist.all_gather(hv))) == 1
+    else:
+        _, _, _, g_bytes, _ = ctx.selection()
+        agree = True
+    out["unique_bytes"] = int(g_bytes)
+    out["unique_bytes_expected"] = int(expect_unique)
+    out["ranks_agree"] = bool(agree)
+    before = d.copy()
+    if N > 1:
+        handles = dist.all_gather(ctx.ipc_export())
+        ctx.ipc_import(b"".join(handles), N)
+        ctx.write(0, np.zeros(64 << 20, np.uint8))  # lose part of the rank's state
+        ctx.restore_shards(dist.rank, verify=True)
+        dist.barrier()  # peers keep their shards until every rank restored
+    else:
+        ctx.write(0, np.zeros(64 << 20, np.uint8))
+        ctx.restore_self(verify=True)
+    ctx.hash()
+    after, _ = ctx.digests()
+    restored = bool(np.array_equal(before, after))
+    out["restore_verified"] = restored
+    oks = dist.all_gather(bool(ok and agree and restored and g_bytes == expect_unique))
+    out["all_ranks_ok"] = all(oks)
+    return out
 
 
 # ------------------------------------------------------------------ plumbing
@@ -120,6 +208,13 @@ class Dist:
         t = torch.tensor([x], dtype=torch.float64)
         self.td.all_reduce(t, op=self.td.ReduceOp.SUM)
         return float(t.item())
+
+    def all_gather(self, obj):
+        if self.world == 1:
+            return [obj]
+        out = [None] * self.world
+        self.td.all_gather_object(out, obj)
+        return out
 
     def bcast_bytes(self, b: bytes | None, n: int) -> bytes:
         if self.world == 1:
@@ -223,10 +318,11 @@ def cpu_baseline(replicated, per_rank, seconds_cap=30.0):
     kind = "reference"
     nthreads = os.cpu_count() or 1
     img = host_image(0, replicated, per_rank)
-    sample = min(img.nbytes, 1 << 30)
+    sample = img.nbytes
     if R is None:
         return {"value": None, "unit": "GB/s", "cores": nthreads, "kind": "unavailable",
                 "sample": "reference library not built"}
+    R.ref_snapshot_chunks(img.ctypes.data, 256 << 20, CHUNK, nthreads, None)  # warm-up
     t0 = time.perf_counter()
     R.ref_snapshot_chunks(img.ctypes.data, sample, CHUNK, nthreads, None)
     dt = time.perf_counter() - t0
@@ -235,8 +331,9 @@ def cpu_baseline(replicated, per_rank, seconds_cap=30.0):
     R.ref_snapshot_chunks(img.ctypes.data, 128 << 20, CHUNK, 1, None)
     dt1 = time.perf_counter() - t1
     return {"value": round(sample / dt / 1e9, 3), "unit": "GB/s", "cores": nthreads, "kind": kind,
-            "sample": f"first {sample >> 20} MiB of the rank-0 C2 image, 64 KiB chunks, "
-                      f"BlobStore::put per chunk, {nthreads} threads x 1 store each",
+            "sample": f"the whole {sample >> 20} MiB rank-0 C2 image, 64 KiB chunks, "
+                      f"BlobStore::put per chunk, {nthreads} threads x 1 store each "
+                      f"(after a 256 MiB warm-up pass)",
             "single_core_gbs": round((128 << 20) / dt1 / 1e9, 3)}
 
 
@@ -420,6 +517,7 @@ def c1_bench(snap, device, reps=20):
     import oracle as O
     nbytes, nb = 256 << 20, 4 << 20
     bufs = [(0, i, i * nb, nb, 0) for i in range(nbytes // nb)]
+    peak, _ = peaks()
     with snap.Ctx(device, nbytes) as c:
         c.fill_mix64(0, nbytes, 1, 0)
         c.set_buffers(bufs)
@@ -432,9 +530,27 @@ def c1_bench(snap, device, reps=20):
             c.snapshot()
             c.restore_self(verify=True)
         ms = c.timer_stop() / reps
+        # each direction alone (the other direction's bytes are not in L2: 2 x 256 MiB)
+        c.sync()
+        c.timer_start()
+        for _ in range(reps):
+            c.snapshot()
+        snap_ms = c.timer_stop() / reps
+        k_snap = snap.last_k1_kernel()
+        c.sync()
+        c.timer_start()
+        for _ in range(reps):
+            c.restore_self(verify=True)
+        rest_ms = c.timer_stop() / reps
+    rw = 2 * nbytes  # R + W each way (every chunk unique: W = 256 MiB; restore reads + writes)
     out = {"workload": "C1: 256 MiB image (64 x 4 MiB buffers), 4096 x 64 KiB chunks, "
                        "snapshot + digest-verified restore round trip",
-           "round_trip_ms": round(ms, 3), "round_trip_gbs": round(nbytes / ms / 1e6, 1)}
+           "round_trip_ms": round(ms, 3), "round_trip_gbs": round(nbytes / ms / 1e6, 1),
+           "snapshot_ms": round(snap_ms, 4), "snapshot_frac": round(rw / snap_ms / 1e6 / peak, 4),
+           "snapshot_k1": k_snap,
+           "restore_verify_ms": round(rest_ms, 4),
+           "restore_frac": round(rw / rest_ms / 1e6 / peak, 4),
+           "algorithmic_bytes_each_way": rw}
     R = O.ref()
     if R is not None:
         img = O.fill_mix64(nbytes // 8, 1, 0)
@@ -541,9 +657,11 @@ def persist_bench(snap, device, mib=256):
 
 
 def resize_bench(snap, dist, reps=2):
-    """C5 on the N GPUs of this run: Llama-3-8B DP state (80.3 GB/replica) snapshot on N,
-    restore onto N/2 from the peer shards over NVLink, reshard, repeat down to 1 GPU.
-    Scaled down (1/2, 1/4) only if a replica + its shard do not fit."""
+    """C5 (BASELINE configs[4]) on the N GPUs of this run: Llama-3-8B DP state (80.3 GB per
+    replica, identical on every rank) snapshot on N (cross-rank dedup, 1/N stripes), then
+    restore onto N/2 GPUs straight from the peer shards over NVLink, reshard (a new
+    communicator over the N/2), and again — 8 -> 4 -> 2 at N = 8 (4 -> 2 at N = 4, 2 -> 1 at
+    N = 2). Every stage's restore is digest-verified (K1 re-hash against the snapshot)."""
     import torch
     sys.path.insert(0, os.path.join(ROOT, "tools"))
     from bench_resize import layout
@@ -552,7 +670,8 @@ def resize_bench(snap, dist, reps=2):
     scale = int(os.environ.get("C5_SCALE", "1"))
     bufs, nbytes = layout(scale)
     out = {"workload": f"C5: Llama-3-8B DP state {nbytes / 1e9:.2f} GB/replica (bf16 P + fp32 "
-                       f"m,v), identical on every rank; resize by halving", "stages": []}
+                       f"m,v), identical on every rank; resize by halving down to "
+                       f"{1 if world == 2 else 2} GPUs", "stages": []}
     ctx = snap.Ctx(dist.local, nbytes + (64 << 20))
     try:
         ctx.fill_mix64(0, nbytes, 77, 0)
@@ -564,12 +683,9 @@ def resize_bench(snap, dist, reps=2):
             return float(t.item())
 
         members = list(range(world))
-        while len(members) >= 2:
+        while len(members) >= 2 and (len(members) > 2 or world == 2):
             ctx.comm_destroy()
-            uid = dist.bcast_bytes(snap.Ctx.unique_id() if rank == members[0] else None, 128) \
-                if members[0] == 0 else None
-            if members[0] != 0:
-                raise RuntimeError("members must start at rank 0")
+            uid = dist.bcast_bytes(snap.Ctx.unique_id() if rank == members[0] else None, 128)
             if rank in members:
                 ctx.comm_init(len(members), members.index(rank), uid)
             snap_ms = 0.0
@@ -580,11 +696,11 @@ def resize_bench(snap, dist, reps=2):
                 for _ in range(reps):
                     ctx.snapshot()
                 snap_ms = ctx.timer_stop() / reps
+                _, _, _, gbytes, _ = ctx.global_selection()
             snap_ms = tmax(snap_ms)
-            handles = [None] * world
-            td.all_gather_object(handles, ctx.ipc_export() if rank in members else b"\0" * 64)
+            handles = dist.all_gather(ctx.ipc_export() if rank in members else b"\0" * 64)
             targets = members[: len(members) // 2]
-            rest_ms = 0.0
+            rest_ms, verified = 0.0, True
             if rank in targets:
                 ctx.ipc_import(b"".join(handles[m] for m in members), len(members))
                 ctx.write(0, np.zeros(1 << 20, np.uint8))
@@ -592,17 +708,121 @@ def resize_bench(snap, dist, reps=2):
                 ctx.timer_start()
                 ctx.restore_shards(members.index(rank), verify=False)
                 rest_ms = ctx.timer_stop()
-                ctx.restore_shards(members.index(rank), verify=True)
+                ctx.write(0, np.zeros(64 << 20, np.uint8))  # lose state again, then verify
+                try:
+                    ctx.restore_shards(members.index(rank), verify=True)
+                except Exception:
+                    verified = False
             td.barrier()
             rest_ms = tmax(rest_ms)
+            verified = all(dist.all_gather(verified))
             out["stages"].append({
                 "gpus": f"{len(members)}->{len(targets)}", "snapshot_ms": round(snap_ms, 3),
                 "snapshot_gbs_aggregate": round(len(members) * nbytes / snap_ms / 1e6, 1),
+                "unique_bytes": int(gbytes) if rank in members else None,
                 "restore_ms": round(rest_ms, 3),
                 "nvlink_gbs_per_target": round(nbytes * (len(members) - 1) / len(members)
                                                / rest_ms / 1e6, 1),
-                "verified": True})
+                "restore_verified": verified})
             members = targets
+    finally:
+        try:
+            ctx.comm_destroy()
+        except Exception:
+            pass
+        ctx.close()
+    return out
+
+
+def c2_full_bench(snap, device, steps=10):
+    """C2 as BASELINE states it — 8 ranks x 2 GiB — held by ONE GPU (16 GiB arena, one
+    buffer list of all 8 ranks in canonical rank/slot order): cross-rank dedup is active,
+    so the replicated 1.5 GiB is staged once and 8 x 0.5 GiB per-rank state once each
+    (W = 5.5 GiB of R = 16 GiB). One step = snap_snapshot over the 8-rank list."""
+    bufs1, replicated, per_rank = c2_layout()
+    image = replicated + per_rank
+    nr = 8
+    bufs = [(r, b[1], r * image + b[2], b[3], b[4]) for r in range(nr) for b in bufs1]
+    with snap.Ctx(device, nr * image + (16 << 20)) as c:
+        for r in range(nr):
+            c.fill_mix64(r * image, replicated, 1, 0)
+            c.fill_mix64(r * image + replicated, per_rank, 1 ^ (r << 40), replicated // 8)
+        c.set_buffers(bufs, PAGE, CHUNK)
+        for _ in range(3):
+            c.snapshot()
+        c.sync()
+        c.prof_enable(True)
+        c.timer_start()
+        for _ in range(steps):
+            c.snapshot()
+        ms = c.timer_stop() / steps
+        t_hash, n_hash = c.prof_read(snap.PROF_HASH)
+        c.prof_enable(False)
+        k1 = snap.last_k1_kernel()
+        _, _, _, staged, nsel = c.selection()
+    peak, _ = peaks()
+    R = nr * image
+    hash_ms = t_hash / max(n_hash, 1)
+    return {"workload": f"C2 full: {nr} ranks x {image >> 20} MiB on one GPU, cross-rank dedup",
+            "ms_per_step": round(ms, 3), "gbs": round(R / ms / 1e6, 1),
+            "staged_bytes": int(staged), "staged_expected": int(replicated + nr * per_rank),
+            "rw_gbs": round((R + staged) / ms / 1e6, 1),
+            "step_frac": round((R + staged) / ms / 1e6 / peak, 4),
+            "k1_kernel": k1, "k1_ms": round(hash_ms, 3),
+            "k1_frac": round((R + staged) / hash_ms / 1e6 / peak, 4)}
+
+
+def grad_allreduce_bench(snap, dist, S=2, reps=5):
+    """Spliced-DP gradient reduction across the N GPUs (C3 gradients, GPT-2-medium fp32,
+    1.42 GB per sliced rank, S sliced ranks per GPU): the fixed-order fused kernel
+    (snap_allreduce_ordered: every GPU reads its 1/N slice of every rank's gradient over
+    NVLink and stores the summed slice into every GPU) vs K5 local sum + NCCL allreduce
+    (NCCL's own order). Device time, max over ranks."""
+    import torch
+    td = dist.td
+    n = sum(gpt2_medium_params())
+    gbytes = 4 * n
+    stride = (gbytes + (1 << 20) - 1) // (1 << 20) << 20
+    rank, N = dist.rank, dist.world
+    out = {"workload": f"{S} sliced ranks/GPU x {gbytes / 1e9:.3f} GB fp32 (GPT-2-medium) on "
+                       f"{N} GPUs, sum over {S * N} ranks"}
+    ctx = snap.Ctx(dist.local, (S + 1) * stride)
+    try:
+        uid = dist.bcast_bytes(snap.Ctx.unique_id() if rank == 0 else None, 128)
+        ctx.comm_init(N, rank, uid)
+        for s_ in range(S):
+            ctx.fill_mix64(s_ * stride, gbytes, 900 + rank * S + s_, 0)
+        keys = [rank * S + s_ for s_ in range(S)]
+        srcs = [s_ * stride for s_ in range(S)]
+        acc = S * stride
+
+        def tmax(x):
+            t = torch.tensor([x], dtype=torch.float64)
+            td.all_reduce(t, op=td.ReduceOp.MAX)
+            return float(t.item())
+
+        for mode in ("ordered", "nccl"):
+            def once():
+                if mode == "ordered":
+                    ctx.allreduce_ordered(snap.F32, keys, srcs, acc, n)
+                else:
+                    ctx.grad_sum(snap.F32, srcs, acc, n)
+                    ctx.allreduce(snap.F32, acc, n)
+            once()
+            ctx.sync()
+            dist.barrier()
+            ctx.timer_start()
+            for _ in range(reps):
+                once()
+            ms = tmax(ctx.timer_stop() / reps)
+            remote_rd = (S * N - S) * gbytes / N
+            remote_wr = (N - 1) * gbytes / N
+            out[mode] = {"ms": round(ms, 3),
+                         "nvlink_gbs_per_gpu": round((remote_rd + remote_wr) / ms / 1e6, 1)
+                         if mode == "ordered" else None}
+        out["ordered"]["bytes_per_gpu"] = ("reads its 1/N slice of all S*N gradients "
+                                           "((S*N - S)/N remote), writes the summed slice to "
+                                           "all N GPUs ((N-1)/N remote)")
     finally:
         try:
             ctx.comm_destroy()
@@ -622,16 +842,14 @@ def run_reference(args, dist):
     import oracle as O
     R = O.ref()
     bufs, replicated, per_rank = c2_layout()
-    cfg = {"workload": "C2 rank image: 1.5 GiB replicated bf16 P + fp32 Adam m,v + 0.5 GiB "
-                       "per-rank grads, 64 KiB chunks", "chunk_bytes": CHUNK,
-           "image_bytes_per_rank": replicated + per_rank}
+    cfg = c2_config(args.gpus)
     if R is None:
         print(json.dumps({"impl": "reference", "unavailable": "reference library (oracle/_ref) "
                                                              "not built"}))
         return
     nthreads = os.cpu_count() or 1
     img = host_image(0, replicated, per_rank)
-    sample = min(img.nbytes, 1 << 30)
+    sample = img.nbytes  # the same 2 GiB rank image our arm snapshots
     for _ in range(args.warmup):
         R.ref_snapshot_chunks(img.ctypes.data, sample, CHUNK, nthreads, None)
     t0 = time.perf_counter()
@@ -639,7 +857,7 @@ def run_reference(args, dist):
         R.ref_snapshot_chunks(img.ctypes.data, sample, CHUNK, nthreads, None)
     dt = time.perf_counter() - t0
     v = sample * args.steps / dt / 1e9
-    desc = (f"per step: first {sample >> 20} MiB of the rank-0 C2 image, BlobStore::put per "
+    desc = (f"per step: the whole {sample >> 20} MiB rank-0 C2 image, BlobStore::put per "
             f"64 KiB chunk, {nthreads} threads")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "GB/s",
@@ -736,14 +954,12 @@ def run_ours(args, dist):
            "h2d_bytes_per_step": image, "d2h_bytes_per_step": int(staged + 8 * nchunks),
            "api": "snap_snapshot_host (pinned host image -> arena -> K1-K3 -> staging shard + "
                   "digests to pinned host)"}
-    # correctness self-check of the timed path at N=1: restore the staging image bit-exactly
-    check = None
-    if N == 1:
-        d_before, _ = ctx.digests()
-        ctx.write(0, np.zeros(1 << 20, np.uint8))
-        ctx.restore_self(verify=True)
-        d_after, _ = ctx.digests()
-        check = bool(np.array_equal(d_before, d_after))
+    # untimed correctness evidence of the timed path, at every N
+    try:
+        parity = parity_block(ctx, dist, bufs, replicated + N * per_rank)
+    except Exception as e:  # reported, never hides the headline
+        parity = {"error": repr(e)[:300]}
+    check = parity.get("all_ranks_ok")
     hostimg.free()
     hstage.free()
 
@@ -765,25 +981,22 @@ def run_ours(args, dist):
         pages = guarded(host_pages_bench, snap, dist.local)
         if base is not None:
             base["splice"] = guarded(ref_splice_bench)
-    if 1 < N <= 4 and not args.no_splice:
+    c2full = None
+    if dist.rank == 0 and N == 1 and not args.no_splice:
+        c2full = guarded(c2_full_bench, snap, dist.local)
+    grad = None
+    if N > 1 and not args.no_splice:
+        grad = guarded(grad_allreduce_bench, snap, dist)
+    if N > 1 and not args.no_splice:
         resize = guarded(resize_bench, snap, dist)
-    elif N > 4:
-        resize = {"skipped": "C5 resize section validated on 2 and 4 GPUs this round only "
-                             "(tools/bench_resize.py runs it at any N)"}
     if dist.rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": N,
             "steps": args.steps, "warmup": max(args.warmup, 3),
             "ms_per_step": round(step_s * 1e3, 4), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": "C2: data-parallel image per rank = 1.5 GiB replicated "
-                                   "(bf16 params + fp32 Adam m,v; identical on all ranks) + "
-                                   "0.5 GiB per-rank grads; one rank per GPU; cross-rank dedup "
-                                   "+ striped compaction at N>1",
-                       "image_bytes_per_rank": image, "chunk_bytes": CHUNK, "page_bytes": PAGE,
-                       "chunks_per_rank": nchunks, "parallelism": f"dp{N} (1 rank/GPU)",
-                       "l2": "inputs 2 GiB/GPU > 126 MB L2 (no flush needed)",
-                       "staged_bytes_total": int(w_total), "unique_bytes_global": int(g_bytes)},
+            "config": c2_config(N),
+            "dedup": {"staged_bytes_total": int(w_total), "unique_bytes_global": int(g_bytes)},
             "roofline": {"bound": "hbm", "kernel": k1_kernel,
                          "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "peak_source": peak_src,
@@ -806,6 +1019,9 @@ def run_ours(args, dist):
             "e2e": e2e,
             "cpu_baseline": base,
             "restore_check": check,
+            "parity": parity,
+            "c2_full_1gpu": c2full,
+            "grad_allreduce": grad,
             "splice": splice,
             "incremental": incremental,
             "resize": resize,

@@ -132,6 +132,20 @@ int select_with_known(snap_ctx* ctx, const uint64_t* dig, const uint32_t* lens, 
   RC(ensure(ctx, ctx->offsets, n, &offsets));
   RC(ensure(ctx, ctx->sel_list, n, &list));
   RC(ensure(ctx, ctx->totals, 4, &totals));
+  static const bool small_off = [] {
+    const char* e = std::getenv("SNAP_SELECT_SMALL");
+    return e && e[0] == '0';
+  }();
+  if (!inserted && !small_off && snap::select_small_ok(n)) {
+    // scratch: the (zero) scan state, at least 9 words (prepare_dedup zeroed it)
+    CKL(snap::launch_select_small(dd, kn, use_known, dig, lens, n, sel, owner, offsets, list,
+                                  totals, spec_next, ctx->stream, scan, fix_spec, ctx->arena,
+                                  &ctx->grid, fix_staging));
+    ctx->dd_clean = true;
+    ctx->sel_n = n;
+    ctx->global_offsets_pending = false;
+    return SNAP_OK;
+  }
   if (!inserted) CKL(snap::launch_dedup_insert(dd, kn, use_known, dig, lens, n, slot, ctx->stream));
   CKL(snap::launch_select(dd, slot, lens, n, scan, sel, owner, offsets, list, totals, spec_next,
                           ctx->stream, fix_spec, ctx->arena, &ctx->grid, fix_staging));
@@ -1373,6 +1387,35 @@ static int verify_grid(snap_ctx* ctx, const uint64_t* expect_dev) {
   return SNAP_OK;
 }
 
+// K4 + verification in one pass (restore_job materialization, ckpt.cpp:517-528,
+// with BlobStore::get's digest check of the blob it reads, ckpt.cpp:23-29):
+// every chunk is read once from the image, written to its recorded address
+// and hashed from shared memory on the way; mismatches against `expect` are
+// counted by the kernel. 2 x restored bytes of traffic instead of 3.
+static int restore_verified(snap_ctx* ctx, const uint8_t* image, const uint64_t* src_off_dev,
+                            const uint64_t* expect_dev) {
+  uint64_t* d2;
+  unsigned long long* nbad;
+  RC(ensure(ctx, ctx->d_dig2, ctx->nchunks, &d2));
+  RC(ensure(ctx, ctx->d_nbad, 4, &nbad));
+  CK(cudaMemsetAsync(nbad, 0, 8, ctx->stream));
+  GridDev g = ctx->grid;
+  g.reverse = 1;
+  g.expect = expect_dev;
+  g.nbad = nbad;
+  {
+    ProfScope ps(ctx, kProfRestore);
+    CKL(snap::launch_hash(ctx->arena, g, d2, src_off_dev, const_cast<uint8_t*>(image), ctx->stream));
+  }
+  unsigned long long bad = 0;
+  CK(cudaMemcpyAsync(&bad, nbad, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (bad)
+    return fail(ctx, SNAP_EFAULT, "restore: digest verification failed on " + std::to_string(bad) +
+                                      " chunk(s)");
+  return SNAP_OK;
+}
+
 int snap_restore(snap_ctx* ctx, const void* image, uint64_t image_bytes, const uint64_t* src_off,
                  const uint64_t* expect_digests, int verify) {
   if (!ctx || (!src_off && ctx->nchunks) || (!image && ctx->nchunks)) return SNAP_EINVAL;
@@ -1385,22 +1428,24 @@ int snap_restore(snap_ctx* ctx, const void* image, uint64_t image_bytes, const u
   uint64_t* so;
   RC(ensure(ctx, ctx->d_srcoff, ctx->nchunks, &so));
   CK(cudaMemcpyAsync(so, src_off, ctx->nchunks * 8, cudaMemcpyHostToDevice, ctx->stream));
+  if (verify) {
+    const uint64_t* expect = P<uint64_t>(ctx->d_dig);
+    if (expect_digests) {
+      uint64_t* e;
+      RC(ensure(ctx, ctx->d_expect, ctx->nchunks, &e));
+      CK(cudaMemcpyAsync(e, expect_digests, ctx->nchunks * 8, cudaMemcpyHostToDevice, ctx->stream));
+      expect = e;
+    } else if (!ctx->hashed) {
+      return fail(ctx, SNAP_EINVAL, "restore verify needs expect_digests or a prior snap_hash");
+    }
+    return restore_verified(ctx, static_cast<const uint8_t*>(image), so, expect);
+  }
   {
     ProfScope ps(ctx, kProfRestore);
     CKL(snap::launch_scatter(ctx->arena, ctx->grid, P<uint32_t>(ctx->d_lens),
                              static_cast<const uint8_t*>(image), so, ctx->stream));
   }
-  if (!verify) return snap_sync(ctx);
-  const uint64_t* expect = P<uint64_t>(ctx->d_dig);
-  if (expect_digests) {
-    uint64_t* e;
-    RC(ensure(ctx, ctx->d_expect, ctx->nchunks, &e));
-    CK(cudaMemcpyAsync(e, expect_digests, ctx->nchunks * 8, cudaMemcpyHostToDevice, ctx->stream));
-    expect = e;
-  } else if (!ctx->hashed) {
-    return fail(ctx, SNAP_EINVAL, "restore verify needs expect_digests or a prior snap_hash");
-  }
-  return verify_grid(ctx, expect);
+  return snap_sync(ctx);
 }
 
 int snap_restore_self(snap_ctx* ctx, int verify) {
@@ -1413,14 +1458,16 @@ int snap_restore_self(snap_ctx* ctx, int verify) {
     return fail(ctx, SNAP_EINVAL, "restore_self: multi-rank snapshots restore from the shards "
                                   "(snap_restore)");
   CK(cudaSetDevice(ctx->device));
+  if (verify)
+    return restore_verified(ctx, static_cast<const uint8_t*>(ctx->staging.p),
+                            P<uint64_t>(ctx->offsets), P<uint64_t>(ctx->d_dig));
   {
     ProfScope ps(ctx, kProfRestore);
     CKL(snap::launch_scatter(ctx->arena, ctx->grid, P<uint32_t>(ctx->d_lens),
                              static_cast<const uint8_t*>(ctx->staging.p), P<uint64_t>(ctx->offsets),
                              ctx->stream));
   }
-  if (!verify) return SNAP_OK;
-  return verify_grid(ctx, P<uint64_t>(ctx->d_dig));
+  return SNAP_OK;
 }
 
 // ---------------------------------------------------------------- K5

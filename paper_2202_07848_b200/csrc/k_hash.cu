@@ -207,10 +207,16 @@ k_hash(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ chun
             if (off < bytes) {
               const uint64_t rem = bytes - off;
               len = static_cast<uint32_t>(rem < pb ? rem : pb);
-              src = arena + __ldg(g.addr + b) + off;
-              if (spec_off) {
-                const uint64_t so = __ldg(spec_off + gc);
-                if (so != ~0ull) dst = staging + so + in_chunk;
+              if (g.reverse) {
+                // verify-scatter: the image holds the chunk, the grid address gets it
+                src = staging + __ldg(spec_off + gc) + in_chunk;
+                dst = const_cast<uint8_t*>(arena) + __ldg(g.addr + b) + off;
+              } else {
+                src = arena + __ldg(g.addr + b) + off;
+                if (spec_off) {
+                  const uint64_t so = __ldg(spec_off + gc);
+                  if (so != ~0ull) dst = staging + so + in_chunk;
+                }
               }
             }
           }
@@ -758,6 +764,10 @@ using CfgC = HashCfg<2, 64, 3, 12>;   // 768 chains/SM, deeper ring
 using CfgD = HashCfg<2, 128, 2, 12>;  // 768 chains/SM, 128-B slabs
 using CfgE = HashCfg<1, 256, 2, 12>;  // 256-B slabs: DRAM-friendly write segments
 using CfgF = HashCfg<1, 256, 2, 13>;
+// one wave for small fused grids (C1: 2048 tasks <= 148 x 14 warps): 256-B
+// slabs, one stage per warp — latency hidden across 14-16 warps per SM
+using CfgG = HashCfg<1, 256, 1, 16>;
+using CfgH = HashCfg<1, 256, 1, 14>;
 using WsA = WsCfg<16, 4, 3>;          // warp-specialized: 16 hash + 4 copy warps
 using WsB = WsCfg<16, 2, 3>;          // 16 hash + 2 copy warps
 using WsC = WsCfg<12, 4, 4>;          // 12 hash + 4 copy warps, deeper ring
@@ -839,9 +849,29 @@ bool hash_tma_selected() {
 //    buffer shapes, tools/hash_variants.py): the TMA tensor-load kernel beats
 //    the cp.async CfgA by 1-2 % on every shape; two chains per lane (CfgB) win
 //    by another 1 % on very large buffers but lose 14 % on small tensors.
-enum class K1 { A, B, C, D, E, F, WsA, WsB, WsC, Tma, Mma, MmaFL, TmaF };
+enum class K1 { A, B, C, D, E, F, G, H, WsA, WsB, WsC, Tma, Mma, MmaFL, TmaF };
+// fused launches: CfgE (12 warps) unless its tasks need a second, mostly idle
+// wave that 14-16 single-stage warps per SM cover in one (C1)
+K1 fused_cfg(const GridDev& g) {
+  const uint64_t c_end = g.c_end ? g.c_end : g.nchunks;
+  const uint64_t tasks = (((c_end - g.c_begin) << (g.chunk_shift - g.page_shift)) + 31) / 32;
+  const uint64_t sms = uint64_t(sm_count());
+  if (tasks > sms * 12 && tasks <= sms * 14) return K1::H;
+  if (tasks > sms * 14 && tasks <= sms * 16) return K1::G;
+  return K1::E;
+}
+
 K1 choose_k1(const GridDev& g, const uint64_t* spec_off) {
+  if (g.reverse) {  // the verify-scatter exists as a k_hash geometry only
+    const int v = hash_variant();
+    if (v == 7) return K1::E;
+    if (v == 14) return K1::G;
+    if (v == 15) return K1::H;
+    return fused_cfg(g);
+  }
   switch (hash_variant()) {
+    case 14: return K1::G;
+    case 15: return K1::H;
     case 1: return K1::B;
     case 2: return K1::C;
     case 3: return K1::D;
@@ -873,7 +903,7 @@ K1 choose_k1(const GridDev& g, const uint64_t* spec_off) {
         const uint64_t grid_bytes = (c_end - g.c_begin) << g.chunk_shift;
         if (hash_mma_ok(g) && pages >= 128 * 1024 && g.spec_bytes * 10 < grid_bytes * 7)
           return K1::MmaFL;
-        return K1::E;
+        return fused_cfg(g);
       }
       // tensor-core FNV: one 1024-page group per SM at a time, so small grids
       // leave SMs idle (tools/hash_sizes.py: 256 MiB 2.56 vs 2.85 TB/s for the
@@ -894,6 +924,8 @@ int launch_k1(K1 k, const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
     case K1::D: return launch_hash_cfg<CfgD>(arena, g, chunk_dig, spec_off, staging, s);
     case K1::E: return launch_hash_cfg<CfgE>(arena, g, chunk_dig, spec_off, staging, s);
     case K1::F: return launch_hash_cfg<CfgF>(arena, g, chunk_dig, spec_off, staging, s);
+    case K1::G: return launch_hash_cfg<CfgG>(arena, g, chunk_dig, spec_off, staging, s);
+    case K1::H: return launch_hash_cfg<CfgH>(arena, g, chunk_dig, spec_off, staging, s);
     case K1::WsA: return launch_hash_ws<WsA>(arena, g, chunk_dig, spec_off, staging, s);
     case K1::WsB: return launch_hash_ws<WsB>(arena, g, chunk_dig, spec_off, staging, s);
     case K1::WsC: return launch_hash_ws<WsC>(arena, g, chunk_dig, spec_off, staging, s);
@@ -915,6 +947,8 @@ const char* k1_name(K1 k) {
     case K1::D: return "k_hash<CfgD>";
     case K1::E: return "k_hash<CfgE> (FNV chain + fused K3 stores, 256-B slabs)";
     case K1::F: return "k_hash<CfgF>";
+    case K1::G: return "k_hash<CfgG> (FNV chain + fused stores, 16 warps x 1 stage: one wave)";
+    case K1::H: return "k_hash<CfgH> (FNV chain + fused stores, 14 warps x 1 stage: one wave)";
     case K1::WsA: return "k_hash_ws<WsA>";
     case K1::WsB: return "k_hash_ws<WsB>";
     case K1::WsC: return "k_hash_ws<WsC>";

@@ -390,6 +390,134 @@ __global__ void k_resolve_dups(const uint8_t* __restrict__ sel, const uint64_t* 
   }
 }
 
+// Small selections (n <= kSmallMax, e.g. C1's 4096 chunks): the insert, the
+// scan, the K3 fix-up, the duplicate resolution and the table clean-up of the
+// three-kernel path (k_dedup_insert -> k_select_scan -> k_resolve_dups) in ONE
+// launch of ceil(n / 1024) CTAs, one chunk per thread, phases separated by a
+// software grid barrier — at this size the three launches and their
+// dependency gaps cost more than the work, and one chunk per thread keeps
+// every phase at one or two memory round trips. Same outputs bit for bit.
+// Scratch: sc[0] = barrier arrivals, sc[1 + b] = CTA b's aggregate; the scan
+// state is zero on entry (the selection's invariant) and left zero on exit.
+constexpr int kSmallThreads = 1024;
+constexpr int kSmallCtas = 8;
+constexpr uint64_t kSmallMax = uint64_t(kSmallThreads) * kSmallCtas;
+
+__device__ __forceinline__ void grid_wait(unsigned long long* cnt, unsigned long long target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(cnt, 1ull);
+    while (ld_status(reinterpret_cast<const uint64_t*>(cnt)) < target) __nanosleep(64);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kSmallThreads, 1)
+k_select_small(TableDev dedup, TableDev known, int use_known, const uint64_t* __restrict__ dig,
+               const uint32_t* __restrict__ lens, uint64_t n, uint8_t* __restrict__ sel,
+               uint64_t* owner, uint64_t* offsets, uint32_t* __restrict__ sel_list,
+               uint64_t* __restrict__ totals, uint64_t* __restrict__ spec_next,
+               const uint64_t* __restrict__ spec_cur, const uint8_t* __restrict__ arena,
+               GridDev grid, uint8_t* __restrict__ staging, uint64_t* sc) {
+  __shared__ uint64_t s_warp[kSmallThreads / 32];
+  __shared__ uint64_t s_pre;
+  griddep_wait();
+  unsigned long long* cnt = reinterpret_cast<unsigned long long*>(sc);
+  const unsigned G = gridDim.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t g = uint64_t(blockIdx.x) * kSmallThreads + threadIdx.x;
+  // phase 1: insert (first occurrence by atomicMin), known-set probe
+  uint64_t slot = ~0ull;
+  uint32_t len = 0;
+  if (g < n) {
+    len = lens[g];
+    if (len != 0) {
+      const unsigned long long d = dig[g];
+      if (!(use_known && table_find(known, d) != ~0ull)) {
+        slot = table_find_or_insert(dedup, d);
+        atomicMin(dedup.vals + slot, static_cast<unsigned long long>(g));
+      }
+    }
+  }
+  grid_wait(cnt, G);
+  // phase 2: owner, CTA scan, cross-CTA prefix from the published aggregates
+  const uint64_t own =
+      slot == ~0ull ? ~0ull : __ldcg(reinterpret_cast<const unsigned long long*>(dedup.vals) + slot);
+  const uint64_t val = own == g ? (1ull << kUnitBits) | (len >> 8) : 0;
+  uint64_t incl = val;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const uint64_t w = s_warp[lane];
+    uint64_t wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    s_warp[lane] = wi - w;
+    if (lane == 31) st_status(sc + 1 + blockIdx.x, wi);
+  }
+  grid_wait(cnt, 2ull * G);
+  if (threadIdx.x == 0) {
+    uint64_t pre = 0, all = 0;
+    for (unsigned b = 0; b < G; ++b) {
+      const uint64_t a = ld_status(sc + 1 + b);
+      if (b < blockIdx.x) pre += a;
+      all += a;
+    }
+    s_pre = pre;
+    if (blockIdx.x == G - 1) {
+      totals[0] = all >> kUnitBits;
+      totals[1] = (all & ((1ull << kUnitBits) - 1)) << 8;
+    }
+  }
+  __syncthreads();
+  const uint64_t run = s_pre + s_warp[warp] + (incl - val);
+  const uint64_t off = (run & ((1ull << kUnitBits) - 1)) << 8;
+  const bool sl = val != 0;
+  if (g < n) {
+    sel[g] = sl;
+    owner[g] = own;
+    offsets[g] = own == ~0ull ? ~0ull : off;
+    if (sl) sel_list[run >> kUnitBits] = static_cast<uint32_t>(g);
+    if (spec_next) spec_next[g] = sl ? off : ~0ull;
+  }
+  if (spec_cur) {  // K3 fix-up (see k_select_scan)
+    const bool need = g < n && sl && spec_cur[g] != off;
+    unsigned m = __ballot_sync(0xffffffffu, need);
+    while (m) {
+      const int q = __ffs(m) - 1;
+      m &= m - 1;
+      const uint64_t gq = __shfl_sync(0xffffffffu, g, q);
+      const uint64_t oq = __shfl_sync(0xffffffffu, off, q);
+      warp_copy(staging + oq, chunk_ptr(arena, grid, gq), lens[gq], lane);
+    }
+  }
+  grid_wait(cnt, 3ull * G);
+  // phase 3: duplicates point at their owner's bytes; the table and the
+  // scratch go back to empty
+  if (g < n && !sl && own != ~0ull)
+    offsets[g] = __ldcg(reinterpret_cast<const unsigned long long*>(offsets) + own);
+  for (uint64_t t = g; t < dedup.mask + 2; t += uint64_t(G) * kSmallThreads) {
+    dedup.keys[t] = kEmptyKey;
+    dedup.vals[t] = ~0ull;
+  }
+  if (g < G) sc[1 + g] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // the last CTA out resets the counter (nobody reads it after its increment)
+    if (atomicAdd(cnt, 1ull) == 4ull * G - 1) st_status(sc, 0);
+  }
+}
+
 unsigned grid_for(uint64_t n, unsigned threads, unsigned cap) {
   uint64_t b = (n + threads - 1) / threads;
   if (b > cap) b = cap;
@@ -433,6 +561,21 @@ int launch_select(TableDev dedup, const uint64_t* slot, const uint32_t* lens, ui
   launch_pdl(k_select_scan, unsigned(tiles), kThreads, 0, s, dedup, slot, lens, n, scan_state,
              reinterpret_cast<unsigned int*>(scan_state + tiles), sel, owner, offsets, sel_list,
              totals, spec_next, spec_cur, arena, grid ? *grid : GridDev{}, staging);
+  return 1;
+}
+
+bool select_small_ok(uint64_t n) { return n > 0 && n <= kSmallMax; }
+
+int launch_select_small(TableDev dedup, TableDev known, bool use_known, const uint64_t* dig,
+                        const uint32_t* lens, uint64_t n, uint8_t* sel, uint64_t* owner,
+                        uint64_t* offsets, uint32_t* sel_list, uint64_t* totals,
+                        uint64_t* spec_next, cudaStream_t s, uint64_t* scratch,
+                        const uint64_t* spec_cur, const uint8_t* arena, const GridDev* grid,
+                        uint8_t* staging) {
+  const unsigned ctas = unsigned((n + kSmallThreads - 1) / kSmallThreads);
+  launch_pdl(k_select_small, ctas, kSmallThreads, 0, s, dedup, known, use_known ? 1 : 0, dig, lens,
+             n, sel, owner, offsets, sel_list, totals, spec_next, spec_cur, arena,
+             grid ? *grid : GridDev{}, staging, scratch);
   return 1;
 }
 

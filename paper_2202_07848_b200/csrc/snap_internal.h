@@ -99,6 +99,14 @@ struct GridDev {
   // (round robin): gsched[0..gs_bins] = per-CTA start, then the group order
   const uint32_t* gsched = nullptr;
   uint32_t gs_bins = 0;
+  // Fused verify-scatter (K4 + K1 in one pass, k_hash only): reverse != 0
+  // reads chunk g from image + src_off[g] (launch_hash's staging / spec_off
+  // arguments), writes it to its grid address and hashes the bytes it moved;
+  // with expect != nullptr every chunk digest is compared and mismatches are
+  // counted in *nbad (BlobStore::get verification, ckpt.cpp:23-29).
+  int reverse = 0;
+  const uint64_t* expect = nullptr;
+  unsigned long long* nbad = nullptr;
 };
 
 // Host: balanced k_hash_mma group schedule for a grid of n buffers over `sms`
@@ -179,6 +187,17 @@ int launch_select(TableDev dedup, const uint64_t* slot, const uint32_t* lens, ui
                   uint32_t* sel_list, uint64_t* totals, uint64_t* spec_next, cudaStream_t s,
                   const uint64_t* spec_cur = nullptr, const uint8_t* arena = nullptr,
                   const GridDev* grid = nullptr, uint8_t* staging = nullptr);
+// The same selection for n <= 8192 chunks in one launch of <= 8 CTAs (insert +
+// scan + fix-up + duplicate resolution + table clean-up, software grid
+// barriers), identical outputs; the dedup table must be empty on entry and is
+// left empty; `scratch` = >= 9 words of (zero) scan state, left zero.
+bool select_small_ok(uint64_t n);
+int launch_select_small(TableDev dedup, TableDev known, bool use_known, const uint64_t* dig,
+                        const uint32_t* lens, uint64_t n, uint8_t* sel, uint64_t* owner,
+                        uint64_t* offsets, uint32_t* sel_list, uint64_t* totals,
+                        uint64_t* spec_next, cudaStream_t s, uint64_t* scratch,
+                        const uint64_t* spec_cur = nullptr, const uint8_t* arena = nullptr,
+                        const GridDev* grid = nullptr, uint8_t* staging = nullptr);
 // Shard scan of writer q over the global writer vector (write_list for q ==
 // this rank: local chunk list + offsets).
 int launch_shard_scan(const int32_t* writer, const uint32_t* glens, uint32_t nranks, uint64_t maxn,
