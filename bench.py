@@ -542,6 +542,11 @@ def c1_bench(snap, device, reps=20):
         for _ in range(reps):
             c.restore_self(verify=True)
         rest_ms = c.timer_stop() / reps
+        # opt-in whole-image digest, value-equal to the reference's Gpu::digest
+        c.digest_whole([(0, 0, 0, nbytes, 0)])
+        t = time.perf_counter()
+        whole = int(c.digest_whole([(0, 0, 0, nbytes, 0)])[0])
+        whole_ms = (time.perf_counter() - t) * 1e3
     rw = 2 * nbytes  # R + W each way (every chunk unique: W = 256 MiB; restore reads + writes)
     out = {"workload": "C1: 256 MiB image (64 x 4 MiB buffers), 4096 x 64 KiB chunks, "
                        "snapshot + digest-verified restore round trip",
@@ -550,7 +555,10 @@ def c1_bench(snap, device, reps=20):
            "snapshot_k1": k_snap,
            "restore_verify_ms": round(rest_ms, 4),
            "restore_frac": round(rw / rest_ms / 1e6 / peak, 4),
-           "algorithmic_bytes_each_way": rw}
+           "algorithmic_bytes_each_way": rw,
+           "whole_image_digest": {"ms": round(whole_ms, 2), "value": hex(whole),
+                                  "what": "snap_digest_whole: Gpu::digest value-equal to the "
+                                          "reference (one FNV-1a chain over 256 MiB)"}}
     R = O.ref()
     if R is not None:
         img = O.fill_mix64(nbytes // 8, 1, 0)
@@ -562,6 +570,10 @@ def c1_bench(snap, device, reps=20):
             out[name] = round((time.perf_counter() - t) * 1e3, 1)
             assert rc == 0 and np.array_equal(back, img)
         out["reference_threads"] = th
+        t = time.perf_counter()
+        ref_whole = R.ref_digest_of_words(img.ctypes.data, img.size)
+        out["whole_image_digest"]["reference_ms"] = round((time.perf_counter() - t) * 1e3, 1)
+        out["whole_image_digest"]["equal_to_reference"] = int(ref_whole) == whole
     return out
 
 

@@ -161,6 +161,15 @@ int snap_get_digests(snap_ctx* ctx, uint64_t* chunk_digests, uint32_t* chunk_len
 int snap_digest_ranges(snap_ctx* ctx, const snap_buf* bufs, uint64_t n, const snap_geom* geom,
                        uint64_t* out_buf_digests);
 
+/* Gpu::digest (vdev.cpp:118) VALUE-EQUAL to the reference: digest_of_words
+ * over every byte of each range (one 64-bit FNV-1a chain per range), the
+ * opt-in compatibility path of SURVEY §8(c) — the ledger and snapshot keys use
+ * the parallel chunk-Merkle digest above. The serial chain is split by the
+ * chain's affinity in the state above its low byte: per 64 KiB segment, 256
+ * chains (one per entry low byte) run in parallel, then one table lookup per
+ * segment combines them. Synchronous. */
+int snap_digest_whole(snap_ctx* ctx, const snap_buf* bufs, uint64_t n, uint64_t* out);
+
 /* ----------------------------------------- K2: dedup + dirty (selection) */
 
 /* Known-digest set = the BlobStore's key set (ckpt.hpp:39): chunks whose

@@ -127,6 +127,7 @@ _SIGS = {
     "snap_get_digests": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "snap_digest_ranges": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]),
     "snap_known_clear": (C.c_int, [C.c_void_p]),
+    "snap_digest_whole": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
     "snap_known_add": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
     "snap_known_commit": (C.c_int, [C.c_void_p]),
     "snap_select": (C.c_int, [C.c_void_p]),
@@ -462,6 +463,13 @@ class Ctx:
         return d[:n], lens[:n]
 
     # -- K2
+    def digest_whole(self, bufs):
+        """Gpu::digest value-equal to the reference (one FNV-1a chain per range)."""
+        arr = bufs_array([b[:5] for b in bufs])
+        out = np.zeros(max(len(bufs), 1), np.uint64)
+        self._ck(self._L.snap_digest_whole(self.h, arr, len(bufs), _p(out)), "snap_digest_whole")
+        return out[:len(bufs)]
+
     def known_clear(self):
         self._ck(self._L.snap_known_clear(self.h), "snap_known_clear")
 

@@ -922,6 +922,50 @@ int snap_get_digests(snap_ctx* ctx, uint64_t* chunk_digests, uint32_t* chunk_len
   return SNAP_OK;
 }
 
+// Gpu::digest (vdev.cpp:118), value-equal: digest_of_words over each whole
+// range (the compatibility path; the ledger keys use the chunk-Merkle digest).
+int snap_digest_whole(snap_ctx* ctx, const snap_buf* bufs, uint64_t n, uint64_t* out) {
+  if (!ctx || (n && (!bufs || !out))) return SNAP_EINVAL;
+  if (n == 0) return SNAP_OK;
+  std::vector<uint64_t> host(3 * n + 1);
+  uint64_t* addr = host.data();
+  uint64_t* bytes = addr + n;
+  uint64_t* seg = bytes + n;
+  seg[0] = 0;
+  for (uint64_t b = 0; b < n; ++b) {
+    if (bufs[b].bytes == 0 || bufs[b].addr % 256 || bufs[b].bytes % 256)
+      return fail(ctx, SNAP_EINVAL, "digest_whole: ranges must be non-zero multiples of 256");
+    RC(check_range(ctx, bufs[b].addr, bufs[b].bytes));
+    addr[b] = bufs[b].addr;
+    bytes[b] = bufs[b].bytes;
+    seg[b + 1] = seg[b] + snap::whole_segments(bufs[b].bytes);
+  }
+  const uint64_t nseg = seg[n];
+  CK(cudaSetDevice(ctx->device));
+  DevMem meta, tab, res;
+  auto done = [&](int rc) {
+    release(meta);
+    release(tab);
+    release(res);
+    return rc;
+  };
+  uint64_t *dm, *dt, *dr;
+  int rc = ensure(ctx, meta, host.size(), &dm);
+  if (!rc) rc = ensure(ctx, tab, nseg * 256, &dt);
+  if (!rc) rc = ensure(ctx, res, n, &dr);
+  if (rc) return done(rc);
+  if (cudaMemcpyAsync(dm, host.data(), host.size() * 8, cudaMemcpyHostToDevice, ctx->stream) !=
+      cudaSuccess)
+    return done(fail(ctx, SNAP_ECUDA, "digest_whole: copy"));
+  ctx->launches += snap::launch_whole_digest(ctx->arena, dm, dm + n, dm + 2 * n, uint32_t(n), nseg,
+                                             dt, dr, ctx->stream);
+  const cudaError_t e1 = cudaGetLastError();
+  const cudaError_t e2 = cudaMemcpyAsync(out, dr, n * 8, cudaMemcpyDeviceToHost, ctx->stream);
+  const cudaError_t e3 = cudaStreamSynchronize(ctx->stream);
+  if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess)
+    return done(fail(ctx, SNAP_ECUDA, "digest_whole: kernel"));
+  return done(SNAP_OK);
+}
 
 // ---------------------------------------------------------------- K2
 

@@ -164,6 +164,14 @@ int encode_tensor_maps(const uint8_t* arena, const uint64_t* addr, const uint64_
 // signal in this rank's window (acquire.sys); traps after ~30 s.
 int launch_peer_barrier(uint64_t* const* xflag, const uint64_t* myflag, uint32_t rank, uint32_t n,
                         uint64_t epoch, cudaStream_t s);
+// The reference's whole-buffer digest, value-equal (k_whole.cu): per-segment
+// state tables (64 KiB segments x 256 entry low bytes) then one serial combine
+// per buffer. seg_start[b] = first segment of buffer b (nb + 1 entries), F =
+// nseg * 256 u64 scratch, out[b] = digest_of_words(buffer b).
+uint64_t whole_segments(uint64_t bytes);
+int launch_whole_digest(const uint8_t* arena, const uint64_t* addr, const uint64_t* bytes,
+                        const uint64_t* seg_start, uint32_t nb, uint64_t nseg, uint64_t* F,
+                        uint64_t* out, cudaStream_t s);
 int launch_buf_fold(const GridDev& g, const uint64_t* chunk_dig, uint64_t* buf_dig, cudaStream_t s);
 int launch_fill_mix64(uint64_t* dst, uint64_t nwords, uint64_t seed, uint64_t base, cudaStream_t s);
 int launch_xor_words(uint8_t* arena, const uint64_t* addrs, uint64_t n, uint64_t value,

@@ -25,3 +25,13 @@ with snap.Ctx(0, nbytes) as c:
             best = min(best, c.timer_stop() / 20)
         print(f"{name:18s} {best * 1e3:8.1f} us  frac {2 * nbytes / best / 1e6 / 6558.4:.3f}",
               os.environ.get("SNAP_SELECT_SMALL", ""), flush=True)
+
+with snap.Ctx(0, nbytes) as c:
+    import time
+    c.fill_mix64(0, nbytes, 0, 0)
+    for bl in ([(0, 0, 0, nbytes, 0)], bufs):
+        c.digest_whole(bl)
+        t = time.perf_counter()
+        d = c.digest_whole(bl)
+        print(f"digest_whole {len(bl)} range(s): {(time.perf_counter() - t) * 1e3:.2f} ms",
+              hex(int(d[0])))
