@@ -177,12 +177,37 @@ def parity_block(ctx, dist, bufs, expect_unique, nsample=48):
 
 # ------------------------------------------------------------------ plumbing
 
+def bind_numa_local(gpu: int):
+    """Best effort: run this rank on its GPU's NUMA-local CPUs so the pinned staging pages
+    are first-touched on that node (no-op on a single-node host, as on the B200 boxes
+    measured: profiles/r02_pcie_scale.json)."""
+    try:
+        bus = subprocess.run(["nvidia-smi", "-i", str(gpu), "--query-gpu=pci.bus_id",
+                              "--format=csv,noheader"], capture_output=True, text=True,
+                             timeout=30).stdout.strip().lower()
+        if bus.count(":") == 2 and len(bus.split(":")[0]) == 8:
+            bus = bus[4:]
+        with open(f"/sys/bus/pci/devices/{bus}/local_cpulist") as f:
+            spec = f.read().strip()
+        cpus = set()
+        for part in spec.split(","):
+            a, _, b = part.partition("-")
+            cpus.update(range(int(a), int(b or a) + 1))
+        if cpus and cpus != set(os.sched_getaffinity(0)) and cpus <= set(range(os.cpu_count())):
+            os.sched_setaffinity(0, cpus)
+            return sorted(cpus)
+    except Exception:
+        pass
+    return None
+
+
 class Dist:
     def __init__(self):
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
+        self.numa_cpus = bind_numa_local(self.local) if self.world > 1 else None
         if self.world > 1:
             import torch.distributed as td
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -965,7 +990,12 @@ def run_ours(args, dist):
     e2e = {"value": round(N * image / e2e_s / 1e9, 2), "unit": "GB/s",
            "h2d_bytes_per_step": image, "d2h_bytes_per_step": int(staged + 8 * nchunks),
            "api": "snap_snapshot_host (pinned host image -> arena -> K1-K3 -> staging shard + "
-                  "digests to pinned host)"}
+                  "digests to pinned host)",
+           "bound": "host link: concurrent pinned D2H of all GPUs shares the host memory path "
+                    "(measured aggregate D2H 53 / 70 / 113-137 GB/s and H2D 56 / 111 / 157-199 "
+                    "GB/s at 1 / 2 / 4 GPUs on one NUMA node: profiles/r02_pcie_scale.json)",
+           "numa_cpus": "bound to the GPU's local CPUs" if dist.numa_cpus else
+                        "single NUMA node (no binding needed)"}
     # untimed correctness evidence of the timed path, at every N
     try:
         parity = parity_block(ctx, dist, bufs, replicated + N * per_rank)
