@@ -140,7 +140,8 @@ k_hash(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ chun
   // below is an immediate offset
   const uint32_t page_shift = PS ? PS : g.page_shift;
   const uint32_t ppc_shift = g.chunk_shift - page_shift;
-  constexpr uint32_t slab_shift = SLAB == 256 ? 8 : (SLAB == 128 ? 7 : (SLAB == 64 ? 6 : 5));
+  constexpr uint32_t slab_shift =
+      SLAB == 512 ? 9 : (SLAB == 256 ? 8 : (SLAB == 128 ? 7 : (SLAB == 64 ? 6 : 5)));
   const uint32_t ns_shift = page_shift - slab_shift;  // steps per page (log2)
   const uint32_t ns = 1u << ns_shift;
   const uint64_t pb = 1ull << page_shift;
@@ -768,6 +769,9 @@ using CfgF = HashCfg<1, 256, 2, 13>;
 // slabs, one stage per warp — latency hidden across 14-16 warps per SM
 using CfgG = HashCfg<1, 256, 1, 16>;
 using CfgH = HashCfg<1, 256, 1, 14>;
+// 512-B segments per page and step (fewer DRAM row switches per byte), one stage
+using CfgI = HashCfg<1, 512, 1, 12>;
+using CfgJ = HashCfg<1, 512, 1, 13>;
 using WsA = WsCfg<16, 4, 3>;          // warp-specialized: 16 hash + 4 copy warps
 using WsB = WsCfg<16, 2, 3>;          // 16 hash + 2 copy warps
 using WsC = WsCfg<12, 4, 4>;          // 12 hash + 4 copy warps, deeper ring
@@ -849,17 +853,15 @@ bool hash_tma_selected() {
 //    buffer shapes, tools/hash_variants.py): the TMA tensor-load kernel beats
 //    the cp.async CfgA by 1-2 % on every shape; two chains per lane (CfgB) win
 //    by another 1 % on very large buffers but lose 14 % on small tensors.
-enum class K1 { A, B, C, D, E, F, G, H, WsA, WsB, WsC, Tma, Mma, MmaFL, TmaF };
-// fused launches: CfgE (12 warps) unless its tasks need a second, mostly idle
-// wave that 14-16 single-stage warps per SM cover in one (C1)
-K1 fused_cfg(const GridDev& g) {
-  const uint64_t c_end = g.c_end ? g.c_end : g.nchunks;
-  const uint64_t tasks = (((c_end - g.c_begin) << (g.chunk_shift - g.page_shift)) + 31) / 32;
-  const uint64_t sms = uint64_t(sm_count());
-  if (tasks > sms * 12 && tasks <= sms * 14) return K1::H;
-  if (tasks > sms * 14 && tasks <= sms * 16) return K1::G;
-  return K1::E;
-}
+enum class K1 { A, B, C, D, E, F, G, H, I, J, WsA, WsB, WsC, Tma, Mma, MmaFL, TmaF };
+// Fused launches (hash + stores, and the verify-scatter): CfgG, 16 warps per
+// SM with one 256-byte stage each. Same-box A/B (tools/fused_variants.py,
+// tools/c1_variants.py): C2 N = 1 K1 0.734-0.740 ms vs CfgE's 0.796-0.798
+// (0.89 vs 0.82 of the copy roofline; 512 more page chains in flight per SM
+// outweigh CfgE's second stage), C1 0.114 vs 0.163 ms (2048 tasks fit one wave
+// of 148 x 16 warps; CfgE needed a second, mostly idle one), 512-B slabs lose
+// (0.94 ms).
+K1 fused_cfg(const GridDev&) { return K1::G; }
 
 K1 choose_k1(const GridDev& g, const uint64_t* spec_off) {
   if (g.reverse) {  // the verify-scatter exists as a k_hash geometry only
@@ -872,6 +874,8 @@ K1 choose_k1(const GridDev& g, const uint64_t* spec_off) {
   switch (hash_variant()) {
     case 14: return K1::G;
     case 15: return K1::H;
+    case 16: return K1::I;
+    case 17: return K1::J;
     case 1: return K1::B;
     case 2: return K1::C;
     case 3: return K1::D;
@@ -926,6 +930,8 @@ int launch_k1(K1 k, const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
     case K1::F: return launch_hash_cfg<CfgF>(arena, g, chunk_dig, spec_off, staging, s);
     case K1::G: return launch_hash_cfg<CfgG>(arena, g, chunk_dig, spec_off, staging, s);
     case K1::H: return launch_hash_cfg<CfgH>(arena, g, chunk_dig, spec_off, staging, s);
+    case K1::I: return launch_hash_cfg<CfgI>(arena, g, chunk_dig, spec_off, staging, s);
+    case K1::J: return launch_hash_cfg<CfgJ>(arena, g, chunk_dig, spec_off, staging, s);
     case K1::WsA: return launch_hash_ws<WsA>(arena, g, chunk_dig, spec_off, staging, s);
     case K1::WsB: return launch_hash_ws<WsB>(arena, g, chunk_dig, spec_off, staging, s);
     case K1::WsC: return launch_hash_ws<WsC>(arena, g, chunk_dig, spec_off, staging, s);
@@ -947,8 +953,10 @@ const char* k1_name(K1 k) {
     case K1::D: return "k_hash<CfgD>";
     case K1::E: return "k_hash<CfgE> (FNV chain + fused K3 stores, 256-B slabs)";
     case K1::F: return "k_hash<CfgF>";
-    case K1::G: return "k_hash<CfgG> (FNV chain + fused stores, 16 warps x 1 stage: one wave)";
+    case K1::G: return "k_hash<CfgG> (FNV chain + fused K3 stores, 16 warps x 1 stage of 256-B slabs)";
     case K1::H: return "k_hash<CfgH> (FNV chain + fused stores, 14 warps x 1 stage: one wave)";
+    case K1::I: return "k_hash<CfgI> (FNV chain + fused stores, 512-B slabs, 12 warps)";
+    case K1::J: return "k_hash<CfgJ> (FNV chain + fused stores, 512-B slabs, 13 warps)";
     case K1::WsA: return "k_hash_ws<WsA>";
     case K1::WsB: return "k_hash_ws<WsB>";
     case K1::WsC: return "k_hash_ws<WsC>";
