@@ -838,10 +838,13 @@ def grad_allreduce_bench(snap, dist, S=2, reps=5):
             td.all_reduce(t, op=td.ReduceOp.MAX)
             return float(t.item())
 
-        for mode in ("ordered", "nccl"):
+        for mode in ("ordered", "ordered_hier", "nccl"):
             def once():
                 if mode == "ordered":
                     ctx.allreduce_ordered(snap.F32, keys, srcs, acc, n)
+                elif mode == "ordered_hier":  # K5 partial per GPU, then GPU order
+                    ctx.grad_sum(snap.F32, srcs, acc, n)
+                    ctx.allreduce_ordered(snap.F32, [rank], [acc], acc, n)
                 else:
                     ctx.grad_sum(snap.F32, srcs, acc, n)
                     ctx.allreduce(snap.F32, acc, n)
@@ -852,14 +855,23 @@ def grad_allreduce_bench(snap, dist, S=2, reps=5):
             for _ in range(reps):
                 once()
             ms = tmax(ctx.timer_stop() / reps)
-            remote_rd = (S * N - S) * gbytes / N
-            remote_wr = (N - 1) * gbytes / N
+            # bytes each GPU moves per direction over NVLink: its remote reads come in
+            # and the peers' stores of their slices come in; mirror image going out
+            srcs_per_gpu = S if mode == "ordered" else 1
+            per_dir = ((srcs_per_gpu * N - srcs_per_gpu) + (N - 1)) * gbytes / N
+            if mode == "nccl":  # ring allreduce of the K5 partial: 2 (N-1)/N of it
+                per_dir = 2 * (N - 1) * gbytes / N
             out[mode] = {"ms": round(ms, 3),
-                         "nvlink_gbs_per_gpu": round((remote_rd + remote_wr) / ms / 1e6, 1)
-                         if mode == "ordered" else None}
-        out["ordered"]["bytes_per_gpu"] = ("reads its 1/N slice of all S*N gradients "
-                                           "((S*N - S)/N remote), writes the summed slice to "
-                                           "all N GPUs ((N-1)/N remote)")
+                         "nvlink_bytes_per_direction": int(per_dir),
+                         "nvlink_gbs_per_direction": round(per_dir / ms / 1e6, 1),
+                         "link_frac": round(per_dir / ms / 1e6 / 900.0, 3)}
+        out["ordered"]["what"] = ("strict dp order: each GPU reads its 1/N slice of all S*N "
+                                  "gradients and writes the summed slice to all N GPUs, one "
+                                  "kernel; bit-identical to a CPU left-to-right sum")
+        out["ordered_hier"]["what"] = ("K5 left-to-right sum of the GPU's S ranks, then the "
+                                       "fused kernel over one partial per GPU in GPU order")
+        out["nccl"]["what"] = "K5 partial + ncclAllReduce (NCCL's order; not bit-reproducible)"
+        out["link_peak"] = "900 GB/s per direction per GPU (NVLink 5, 18 links)"
     finally:
         try:
             ctx.comm_destroy()
