@@ -501,8 +501,27 @@ int init_spec(snap_ctx* ctx) {
         off += ctx->h_lens[g];
       }
   } else if (!ctx->attached() || ctx->nranks == 1) {
+    // one GPU: every chunk staged in canonical order, except (several ranks in
+    // one buffer list, e.g. C2 held by one GPU) the chunks of a buffer hinted
+    // replicated whose slot the lowest rank also holds with the same size —
+    // predicted to be that rank's duplicates
+    std::vector<uint8_t> dup(n, 0);
+    if (!ctx->bufs.empty()) {
+      uint32_t r0 = ctx->bufs[0].rank;
+      for (const snap_buf& b : ctx->bufs) r0 = std::min(r0, b.rank);
+      std::map<int32_t, uint64_t> first;  // slot -> bytes in the lowest rank
+      for (const snap_buf& b : ctx->bufs)
+        if (b.rank == r0) first[b.slot] = b.bytes;
+      for (size_t b = 0; b < ctx->bufs.size(); ++b) {
+        const snap_buf& x = ctx->bufs[b];
+        auto it = first.find(x.slot);
+        if (x.rank != r0 && replicated_hint(x) && it != first.end() && it->second == x.bytes)
+          for (uint64_t g = ctx->h_cstart[b]; g < ctx->h_cstart[b + 1]; ++g) dup[g] = 1;
+      }
+    }
     uint64_t off = 0;
     for (uint64_t g = 0; g < n; ++g) {
+      if (dup[g]) continue;
       spec[g] = off;
       off += ctx->h_lens[g];
     }
