@@ -690,6 +690,16 @@ class Ctx:
         self._ck(self._L.snap_splice_set_rank(self.h, rank, arr, len(bufs), C.byref(g)),
                  "snap_splice_set_rank")
 
+    def splice_recorded(self, rank: int) -> np.ndarray:
+        """The rank's recorded chunk digests (its last switch-out), buffer/chunk order."""
+        n = C.c_uint64()
+        self._ck(self._L.snap_splice_recorded(self.h, rank, None, C.byref(n)),
+                 "snap_splice_recorded")
+        out = np.zeros(max(n.value, 1), np.uint64)
+        self._ck(self._L.snap_splice_recorded(self.h, rank, _p(out), C.byref(n)),
+                 "snap_splice_recorded")
+        return out[:n.value]
+
     def splice_switch(self, frm: int, to: int) -> dict:
         st = SwitchStats()
         self._ck(self._L.snap_splice_switch(self.h, frm, to, C.byref(st)), "snap_splice_switch")

@@ -266,3 +266,20 @@ def test_splice_install_immediate_without_splicing(snap):
         ctx.splice_install([0, -1], [1 * MIB, 2 * MIB], 0, 65536)
         assert np.array_equal(ctx.read(1 * MIB, 65536), src.view(np.uint8))
         assert np.array_equal(ctx.read(2 * MIB, 65536), src.view(np.uint8))
+
+
+def test_splice_recorded_digests_in_buffer_order(snap):
+    """The splice grid hashes chunk-aligned buffers first (tensor-core task regularity);
+    snap_splice_recorded still reports the digests in the caller's buffer/chunk order."""
+    lay = rank_layout()
+    with snap.Ctx(0, 16 * MIB) as ctx:
+        ctx.splice_init(32 * MIB)
+        ctx.fill_mix64(0, 8 * MIB, 23, 0)
+        ctx.splice_set_rank(0, lay)
+        ctx.splice_set_rank(1, lay)
+        ctx.splice_switch(0, 1)
+        got = ctx.splice_recorded(0)
+        host = ctx.read(0, 8 * MIB)
+        live = [b[:5] for b in lay if not b[5] & 4]
+        exp, _, _ = O.hash_chunks([host], live)
+        assert np.array_equal(got, exp)
