@@ -25,6 +25,9 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "snap_internal.h"
 
 namespace snap {
@@ -136,7 +139,7 @@ __device__ __forceinline__ void scalar_elem(const ArArgs& a, uint64_t i) {
   }
 }
 
-template <int DT>
+template <int DT, int U>
 __global__ void __launch_bounds__(kThreads)
 k_ordered_allreduce(ArArgs a, uint64_t v0, uint64_t v1, uint64_t t0, uint64_t t1) {
   if (a.use_flags) {
@@ -148,26 +151,40 @@ k_ordered_allreduce(ArArgs a, uint64_t v0, uint64_t v1, uint64_t t0, uint64_t t1
       for (uint32_t q = 0; q < a.N; ++q) wait_flag(a.myflag + q * kFlag, a.epoch);
     __syncthreads();
   }
+  // U vectors per thread and iteration (i, i + stride/U, ...): U x kBatch
+  // independent 16-byte loads in flight per thread over NVLink
   const uint64_t stride = uint64_t(gridDim.x) * kThreads;
-  for (uint64_t i = v0 + uint64_t(blockIdx.x) * kThreads + threadIdx.x; i < v1; i += stride) {
-    Acc<DT> acc;
-    uint4 x[kBatch];
+  const uint64_t span = v1 - v0, per = (span + U - 1) / U;
+  for (uint64_t j = uint64_t(blockIdx.x) * kThreads + threadIdx.x; j < per; j += stride) {
+    Acc<DT> acc[U];
+    uint4 x[U][kBatch];
     for (uint32_t r0 = 0; r0 < a.R; r0 += kBatch) {
       const uint32_t nb = min(uint32_t(kBatch), a.R - r0);
 #pragma unroll
-      for (int b = 0; b < kBatch; ++b)
-        if (b < int(nb)) x[b] = __ldcs(reinterpret_cast<const uint4*>(a.src[r0 + b]) + i);
+      for (int u = 0; u < U; ++u) {
+        const uint64_t i = v0 + j + uint64_t(u) * per;
 #pragma unroll
-      for (int b = 0; b < kBatch; ++b) {
-        if (b >= int(nb)) break;
-        if (r0 + b == 0)
-          acc.init(x[b]);
-        else
-          acc.add(x[b]);
+        for (int b = 0; b < kBatch; ++b)
+          if (b < int(nb) && i < v1) x[u][b] = __ldcs(reinterpret_cast<const uint4*>(a.src[r0 + b]) + i);
       }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b) {
+          if (b >= int(nb)) break;
+          if (r0 + b == 0)
+            acc[u].init(x[u][b]);
+          else
+            acc[u].add(x[u][b]);
+        }
     }
-    const uint4 o = acc.out();
-    for (uint32_t q = 0; q < a.N; ++q) __stcs(reinterpret_cast<uint4*>(a.dst[q]) + i, o);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = v0 + j + uint64_t(u) * per;
+      if (i >= v1) continue;
+      const uint4 o = acc[u].out();
+      for (uint32_t q = 0; q < a.N; ++q) __stcs(reinterpret_cast<uint4*>(a.dst[q]) + i, o);
+    }
   }
   for (uint64_t i = t0 + uint64_t(blockIdx.x) * kThreads + threadIdx.x; i < t1; i += stride)
     scalar_elem<DT>(a, i);
@@ -197,13 +214,33 @@ int launch_ordered_allreduce(const ArArgs& a, cudaStream_t s) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  uint64_t blocks = (v1 - v0 + kThreads - 1) / kThreads;
-  blocks = std::max<uint64_t>(1, std::min<uint64_t>(blocks, uint64_t(sms) * 4));
+  // tuning knobs (A/B on the box): SNAP_AR_CTAS per SM, SNAP_AR_UNROLL 1 | 2 | 4
+  static const int cps = [] {
+    const char* e = getenv("SNAP_AR_CTAS");
+    return e && atoi(e) > 0 ? atoi(e) : 4;
+  }();
+  static const int unroll = [] {
+    const char* e = getenv("SNAP_AR_UNROLL");
+    const int v = e ? atoi(e) : 1;
+    return v == 2 || v == 4 ? v : 1;
+  }();
+  uint64_t blocks = (v1 - v0 + uint64_t(kThreads) * unroll - 1) / (uint64_t(kThreads) * unroll);
+  blocks = std::max<uint64_t>(1, std::min<uint64_t>(blocks, uint64_t(sms) * cps));
+#define SNAP_AR_LAUNCH(DT)                                                                       \
+  do {                                                                                          \
+    if (unroll == 4)                                                                            \
+      k_ordered_allreduce<DT, 4><<<unsigned(blocks), kThreads, 0, s>>>(a, v0, v1, t0, t1);      \
+    else if (unroll == 2)                                                                       \
+      k_ordered_allreduce<DT, 2><<<unsigned(blocks), kThreads, 0, s>>>(a, v0, v1, t0, t1);      \
+    else                                                                                        \
+      k_ordered_allreduce<DT, 1><<<unsigned(blocks), kThreads, 0, s>>>(a, v0, v1, t0, t1);      \
+  } while (0)
   switch (a.dtype) {
-    case SNAP_U64: k_ordered_allreduce<SNAP_U64><<<unsigned(blocks), kThreads, 0, s>>>(a, v0, v1, t0, t1); break;
-    case SNAP_F32: k_ordered_allreduce<SNAP_F32><<<unsigned(blocks), kThreads, 0, s>>>(a, v0, v1, t0, t1); break;
-    default: k_ordered_allreduce<SNAP_BF16><<<unsigned(blocks), kThreads, 0, s>>>(a, v0, v1, t0, t1); break;
+    case SNAP_U64: SNAP_AR_LAUNCH(SNAP_U64); break;
+    case SNAP_F32: SNAP_AR_LAUNCH(SNAP_F32); break;
+    default: SNAP_AR_LAUNCH(SNAP_BF16); break;
   }
+#undef SNAP_AR_LAUNCH
   return 1;
 }
 

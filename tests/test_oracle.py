@@ -273,3 +273,12 @@ def test_manifest_dedup_pinned_to_reference(ref_lib, dp, s_cr, s_cr_inc, upload)
         _, _, _, up = O.select(digs, lens, known)
         assert up == m["device_upload"]
         prev = digs
+
+
+def test_bench_parity_fnv_restatement(c1_golden):
+    """bench.py's untimed parity block re-hashes sampled chunks with its own numpy FNV-1a;
+    that restatement equals the reference goldens (C1 chunk 0 and 1, Merkle mode)."""
+    import bench
+    img = O.fill_mix64(2 * 65536 // 8).view(np.uint8).reshape(2, 65536)
+    d = bench.chunk_digests_np(img)
+    assert np.array_equal(d, c1_golden["merkle"][:2])
