@@ -1,0 +1,96 @@
+"""K2 selection on both GPU paths against the oracle: the one-launch small selection
+(n <= 8192 chunks) and the three-kernel look-back path (n > 8192), with duplicates, a
+known set and the size boundaries of both; the fused verify-scatter restore on ragged
+layouts and several geometries; K5 in bf16."""
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("nchunks", [1, 31, 1023, 1024, 1025, 4096, 8191, 8192, 8193, 20000])
+def test_selection_paths_vs_oracle(snap, nchunks):
+    rng = np.random.default_rng(nchunks)
+    chunk = 4096  # page == chunk: one 4 KiB chunk per slot, cheap to build many
+    pool = 64 + nchunks // 3
+    nbytes = (pool + nchunks) * chunk
+    with snap.Ctx(0, nbytes) as c:
+        c.fill_mix64(0, pool * chunk, 7 + nchunks, 0)
+        # chunk k of the grid = a copy of pool[perm[k]] (many duplicates)
+        src = rng.integers(0, pool, nchunks)
+        host = c.read(0, pool * chunk)
+        img = np.concatenate([host[int(s) * chunk:(int(s) + 1) * chunk] for s in src])
+        c.write(pool * chunk, img)
+        bufs = [(0, 0, pool * chunk, nchunks * chunk, 1)]
+        c.set_buffers(bufs, chunk, chunk)
+        known = []
+        for rnd in range(2):
+            c.snapshot()
+            d, lens = c.digests()
+            sel, owner, off, tot, nsel = c.selection()
+            osel, oown, ooff, otot = O.select(d, lens, np.array(known, np.uint64) if known else None)
+            assert np.array_equal(sel, osel) and np.array_equal(owner, oown)
+            assert np.array_equal(off, ooff) and tot == otot
+            staged = c.read_staging(0, tot) if tot else np.zeros(0, np.uint8)
+            exp = np.concatenate([img[g * chunk:(g + 1) * chunk] for g in np.nonzero(osel)[0]]) \
+                if otot else np.zeros(0, np.uint8)
+            assert np.array_equal(staged, exp)
+            known = [int(x) for x in d[rng.integers(0, nchunks, max(1, nchunks // 4))]]
+            c.known_clear()
+            c.known_add(np.array(known, np.uint64))
+
+
+@pytest.mark.parametrize("geom", [(4096, 65536), (256, 4096), (1024, 32768), (65536, 65536)])
+def test_verify_scatter_ragged(snap, geom):
+    """snap_restore / snap_restore_self with verification = one pass that scatters and
+    hashes; bit-exact content, and a corrupted image chunk is caught by digest."""
+    rng = np.random.default_rng(geom[0])
+    arena = 24 << 20
+    with snap.Ctx(0, arena) as c:
+        c.fill_mix64(0, arena, 3, 0)
+        bufs, addr = [], 0
+        while True:
+            nb = int(rng.integers(1, 900)) * 256
+            if addr + nb > arena // 2:
+                break
+            bufs.append((0, len(bufs), addr, nb, int(rng.integers(0, 4))))
+            addr += nb + int(rng.integers(0, 4)) * 256
+        host = c.read(0, arena)
+        c.set_buffers(bufs, *geom)
+        c.snapshot()
+        c.write(0, np.zeros(arena // 2, np.uint8))
+        c.restore_self(verify=True)
+        back = c.read(0, arena)
+        for (_r, _s, a, n, _c) in bufs:
+            assert np.array_equal(back[a:a + n], host[a:a + n])
+        # snap_restore from a host-provided image: flip one byte -> SimFault
+        _, _, off, tot, _ = c.selection()
+        d, _ = c.digests()
+        img = c.read_staging(0, tot)
+        dev = c.arena_ptr() + arena // 2
+        c.write(arena // 2, img)
+        c.restore(dev, tot, off, expect=d, verify=True)
+        img[int(rng.integers(0, tot))] ^= 0x5A
+        c.write(arena // 2, img)
+        with pytest.raises(snap.SnapError) as e:
+            c.restore(dev, tot, off, expect=d, verify=True)
+        assert e.value.code == snap.SNAP_EFAULT
+
+
+def test_grad_sum_bf16(snap, ctx):
+    rng = np.random.default_rng(21)
+    n = 1_000_005
+    gs = [((rng.standard_normal(n) * 10.0 ** rng.integers(-8, 8, n)).astype(np.float32)
+           .view(np.uint32) >> 16).astype(np.uint16) for _ in range(4)]
+    stride = (2 * n + 255) // 256 * 256
+    for r, g in enumerate(gs):
+        ctx.write(r * stride, g)
+    ctx.grad_sum(snap.BF16, [r * stride for r in range(4)], 5 * stride, n)
+    got = ctx.read(5 * stride, 2 * n).view(np.uint16)
+    assert np.array_equal(got, O.grad_sum_bf16(gs))
+    # accumulate: dst (bf16) is the first addend of a new chain
+    ctx.grad_sum(snap.BF16, [r * stride for r in range(2)], 5 * stride, n, accumulate=True)
+    got2 = ctx.read(5 * stride, 2 * n).view(np.uint16)
+    assert np.array_equal(got2, O.grad_sum_bf16([O.grad_sum_bf16(gs), gs[0], gs[1]]))
