@@ -444,6 +444,40 @@ def splice_bench(snap, device, nranks=4):
                              "swap_out_bytes": int(sts[-1]["swap_out_bytes"]),
                              "swap_in_bytes": int(sts[-1]["swap_in_bytes"])}
         out["swap_ms_divergent"] = sweep
+        # DP training churn: every mini-batch m each rank applies the same optimizer update
+        # (5 % of the P/O chunks change) before it yields; 200 switches = 50 mini-batches of
+        # new versions (10.6 GB) through 3 replicas of cache, so dead versions must be
+        # reclaimed (bounded HBM cache, splice_host.cpp)
+        churn, ms_list = [], []
+        upd_rng = np.random.default_rng(7)
+        updates = {}
+        # identical replicas again (the divergent sweep left the ranks different): one
+        # untimed cycle records every rank's state from the same bytes
+        c.fill_mix64(0, sbytes, 5, 0)
+        for _ in range(nranks):
+            c.splice_switch(active, (active + 1) % nranks)
+            c.fill_mix64(0, sbytes, 5, 0)
+            active = (active + 1) % nranks
+        for k in range(200):
+            frm, to, mb = active, (active + 1) % nranks, k // nranks
+            if mb not in updates:
+                updates[mb] = upd_rng.choice(nck, size=int(0.05 * nck), replace=False)
+            c.xor_words(updates[mb].astype(np.uint64) * 65536, 0x7000 + mb)
+            ms, wall, st = timed_switch(frm, to)
+            ms_list.append(ms)
+            churn.append(st)
+            active = to
+        out["churn"] = {"switches": len(ms_list), "update_fraction": 0.05,
+                        "swap_ms_median": round(float(np.median(ms_list)), 4),
+                        "swap_ms_max": round(float(np.max(ms_list)), 4),
+                        "cache_capacity_bytes": 3 * sbytes,
+                        "cache_bytes_end": int(churn[-1]["cache_bytes"]),
+                        "reclaimed_bytes": int(churn[-1]["reclaimed_bytes"]),
+                        "swap_out_bytes_total": int(sum(x["swap_out_bytes"] for x in churn)),
+                        "swap_ms_p90": round(float(np.percentile(ms_list, 90)), 4),
+                        "switches_that_reclaimed": int(sum(
+                            1 for a, b in zip(churn, churn[1:])
+                            if b["reclaimed_bytes"] > a["reclaimed_bytes"]))}
         # K5: fixed-order fp32 sum of the 4 ranks' gradients into the accumulator
         n = gbytes // 4
         srcs = [gregion + r * gbytes for r in range(nranks)]

@@ -121,16 +121,19 @@ int cache_gc(snap_ctx* ctx) {
 
 // Stores the chunks the last selection over `dig` picked (ctx->sel_list /
 // ctx->totals) into free cache slots: from the arena grid `from` (swap-out) or
-// from image + src_off (seeding). Makes room first when the worst case
-// (every chunk new) does not fit the free slots.
+// from image + src_off (seeding). When the worst case (every chunk new) does
+// not fit the free slots, the actual count is read back (one sync) and the
+// cache is reclaimed only if the new chunks really do not fit. Reclaiming
+// after the selection is safe: every digest the selection just looked up is
+// recorded by the rank being stored, so none of them is dead.
 int cache_put(snap_ctx* ctx, const uint64_t* dig, const uint32_t* lens, uint64_t n,
               const GridDev* from, const uint8_t* image, const uint64_t* src_off) {
   SpliceState* S = ctx->splice;
   uint64_t tot[2] = {0, 0};
   if (S->free_n < n) {
-    // tight: learn how many chunks are actually new before assigning slots
     CK(cudaMemcpyAsync(tot, ctx->totals.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    if (tot[0] > S->free_n) RC(cache_gc(ctx));
     if (tot[0] > S->free_n)
       return fail(ctx, SNAP_ENOMEM, "splice: chunk cache full (" + std::to_string(S->nslots - S->free_n) +
                                         " of " + std::to_string(S->nslots) + " slots hold chunks "
@@ -311,7 +314,6 @@ int snap_splice_switch(snap_ctx* ctx, int from, int to, snap_switch_stats* st) {
     CKL(snap::launch_hash(ctx->arena, F->grid, P<uint64_t>(F->d_rec), nullptr, nullptr,
                           ctx->stream));
     F->recorded = true;
-    if (S->free_n < F->nchunks) RC(cache_gc(ctx));
     RC(select_with_known(ctx, P<uint64_t>(F->d_rec), P<uint32_t>(F->d_lens), F->nchunks,
                          cache_index(S), S->entries > 0));
     ctx->selected = false;  // the ctx selection vectors now hold this plan
@@ -455,15 +457,7 @@ int splice_seed(snap_ctx* ctx, int rank, const uint8_t* image, const uint64_t* s
                        ctx->stream));
     CK(cudaMemcpyAsync(so, src_off, R.nchunks * 8, cudaMemcpyHostToDevice, ctx->stream));
   }
-  const bool was = R.recorded;
   R.recorded = true;  // its digests are live from now on
-  if (S->free_n < R.nchunks) {
-    const int rc = cache_gc(ctx);
-    if (rc) {
-      R.recorded = was;
-      return rc;
-    }
-  }
   RC(select_with_known(ctx, P<uint64_t>(R.d_rec), P<uint32_t>(R.d_lens), R.nchunks,
                        cache_index(S), S->entries > 0));
   ctx->selected = false;
