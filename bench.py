@@ -285,6 +285,9 @@ class ClockSampler:
             if len(parts) == 7:
                 self.rows.append((time.perf_counter(), parts))
 
+    def ready(self, n=2) -> bool:
+        return self.proc is None or len(self.rows) >= n
+
     def window(self, t0, t1):
         """Marks the timed region [t0, t1] (perf_counter); only samples inside it count."""
         self.t0, self.t1 = t0, t1
@@ -299,7 +302,7 @@ class ClockSampler:
         except subprocess.TimeoutExpired:
             self.proc.kill()
         t0, t1 = getattr(self, "t0", 0.0), getattr(self, "t1", float("inf"))
-        rows = [r for (t, r) in self.rows if t0 <= t <= t1 + 0.03]
+        rows = [r for (t, r) in self.rows if t0 <= t <= t1]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i] == "Active"})
 
@@ -958,6 +961,9 @@ def run_reference(args, dist):
 def run_ours(args, dist):
     import paper_2202_07848_b200 as snap
 
+    clocks = ClockSampler(dist.local)
+    clocks.start()  # early: nvidia-smi needs ~1 s before its first sample
+
     bufs, replicated, per_rank = c2_layout()
     image = replicated + per_rank
     N = dist.world
@@ -984,10 +990,13 @@ def run_ours(args, dist):
         _, _, _, my_bytes, my_chunks = ctx.selection()
         g_bytes, g_chunks = my_bytes, my_chunks
 
-    clocks = ClockSampler(dist.local)
-    clocks.start()
-    for _ in range(20):  # keep the GPU busy while nvidia-smi starts sampling
-        step()
+    # nvidia-smi was started with the run (its start-up takes ~1 s); if it has not delivered
+    # samples yet, keep the GPU busy until it does, so the timed region is sampled
+    t_wait = time.perf_counter()
+    while not clocks.ready() and time.perf_counter() - t_wait < 5.0:
+        for _ in range(20):
+            step()
+        ctx.sync()
     ctx.prof_enable(True)
     l0 = ctx.launches
     dist.barrier()
@@ -997,8 +1006,7 @@ def run_ours(args, dist):
     for _ in range(args.steps):
         step()
     ms = ctx.timer_stop()
-    clocks.window(tw0, time.perf_counter())
-    clk = clocks.stop()
+    tw1 = time.perf_counter()
     launches = ctx.launches - l0
     k1_kernel = snap.last_k1_kernel()  # the K1 the timed steps ran (policy: k_hash.cu choose_k1)
     t_hash, n_hash = ctx.prof_read(snap.PROF_HASH)
@@ -1006,6 +1014,14 @@ def run_ours(args, dist):
     t_cmp, n_cmp = ctx.prof_read(snap.PROF_COMPACT)
     t_xch, n_xch = ctx.prof_read(snap.PROF_EXCHANGE)
     ctx.prof_enable(False)
+    # untimed steps right after the timed region keep the load on for the trailing samples
+    # of the window (a sample every 20 ms; K short steps can be shorter than that)
+    t_tail = time.perf_counter()
+    while time.perf_counter() - t_tail < 0.06:
+        step()
+        ctx.sync()
+    clocks.window(tw0 - 0.02, tw1 + 0.06)
+    clk = clocks.stop()
     ms_max = dist.max(ms)
     w_total = dist.sum(float(my_bytes))
     step_s = ms_max / 1e3 / args.steps
