@@ -104,6 +104,13 @@ class Gpu {
     check(snap_digest_ranges(ctx_, &b, 1, nullptr, &d), ctx_);
     return {d};
   }
+  // vdev.cpp:118 VALUE-equal: digest_of_words over the whole range (opt-in path)
+  sim::Digest digest_exact(MemRange r) const {
+    snap_buf b{0, 0, r.addr, r.bytes, 0, 0};
+    u64 d = 0;
+    check(snap_digest_whole(ctx_, &b, 1, &d), ctx_);
+    return {d};
+  }
   snap_ctx* ctx() const { return ctx_; }
 
  private:
@@ -197,6 +204,7 @@ struct SwitchPlan {
   u64 swap_in_bytes = 0;
   u64 resident_bytes = 0;
   u64 cache_bytes = 0;
+  u64 install_bytes = 0;  // queued collective results applied (switch_report, job.cpp:165-171)
 };
 
 // GpuLedger's switch machinery on the GPU: plan_switch + execute_switch in one
@@ -224,7 +232,22 @@ class Splicer {
   SwitchPlan switch_to(RankId from, RankId to) {
     snap_switch_stats s{};
     check(snap_splice_switch(gpu_->ctx(), from, to, &s), gpu_->ctx());
-    return {s.hashed_bytes, s.swap_out_bytes, s.swap_in_bytes, s.resident_bytes, s.cache_bytes};
+    return {s.hashed_bytes, s.swap_out_bytes, s.swap_in_bytes, s.resident_bytes, s.cache_bytes,
+            s.install_bytes};
+  }
+  // JobRuntime::on_coll_complete (job.cpp:206-222): the result at src goes into every
+  // listed rank's G slot — the active rank now, the others at their next switch_to
+  void install_result(const std::vector<RankId>& ranks, const std::vector<u64>& slot_addrs,
+                      u64 src_addr, u64 bytes) {
+    std::vector<int> r(ranks.begin(), ranks.end());
+    check(snap_splice_install(gpu_->ctx(), r.data(), slot_addrs.data(), uint32_t(r.size()),
+                              src_addr, bytes),
+          gpu_->ctx());
+  }
+  u64 pending_install_bytes(RankId r) const {
+    u64 c = 0, b = 0;
+    check(snap_splice_pending(gpu_->ctx(), r, &c, &b), gpu_->ctx());
+    return b;
   }
 
  private:
@@ -380,6 +403,15 @@ inline void grad_sum(vdev::Gpu& gpu, int dtype, const std::vector<u64>& src_addr
                      u64 elems, bool accumulate = false) {
   check(snap_grad_sum(gpu.ctx(), dtype, src_addrs.data(), uint32_t(src_addrs.size()), dst_addr,
                       elems, accumulate ? 1 : 0),
+        gpu.ctx());
+}
+// The device-level sum over GPUs in a fixed key order (collectives.cpp:137-154 with the
+// fixed-order fp32 mode): collective over the ctx's communicator
+inline void allreduce_ordered(vdev::Gpu& gpu, int dtype, const std::vector<uint32_t>& keys,
+                              const std::vector<u64>& src_addrs, u64 dst_addr, u64 elems) {
+  if (keys.size() != src_addrs.size()) throw ConfigError("allreduce_ordered: keys / sources");
+  check(snap_allreduce_ordered(gpu.ctx(), dtype, keys.data(), src_addrs.data(),
+                               uint32_t(keys.size()), dst_addr, elems),
         gpu.ctx());
 }
 }  // namespace coll

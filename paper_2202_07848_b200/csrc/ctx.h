@@ -293,7 +293,9 @@ inline void build_tmaps(snap_ctx* ctx, DevMem& m, const uint64_t* addr, const ui
   int sms = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device) != cudaSuccess) sms = 0;
   std::vector<uint32_t> sched;
-  const uint32_t bins = snap::mma_schedule(addr, bytes, n, g.page_shift, g.chunk_shift, sms, sched);
+  g.mma_cw = snap::mma_cw_for(g.nchunks << (g.chunk_shift - g.page_shift), sms);
+  const uint32_t bins =
+      snap::mma_schedule(addr, bytes, n, g.page_shift, g.chunk_shift, sms, sched, g.mma_cw);
   std::vector<uint8_t> host(size_t(n) * 128 + 32 * 128 + sched.size() * 4);
   if (!sched.empty()) std::memcpy(host.data() + size_t(n) * 128 + 32 * 128, sched.data(), sched.size() * 4);
   if (snap::encode_tensor_maps(ctx->arena, addr, bytes, n, host.data(), 128) != 0) return;

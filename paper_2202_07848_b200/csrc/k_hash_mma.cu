@@ -72,7 +72,7 @@ constexpr size_t kBTabAll = kBTab + (17 + 17 + 1) * 8;
 // PAIRS chain pairs per thread, SLAB bytes of each page per data stage (TMA
 // boxes of 32 pages x BOXW bytes, SWIZZLE_64B / _128B), ST-deep ring per
 // warp, FUSED: also write every predicted-staged chunk's slab to staging.
-template <int CW_, int PAIRS_, int SLAB_, int ST_, bool FUSED_>
+template <int CW_, int PAIRS_, int SLAB_, int ST_, bool FUSED_, int NA_ = 3, int NDB_ = 2>
 struct MmaCfg {
   static constexpr int CW = CW_, PAIRS = PAIRS_, SLAB = SLAB_, ST = ST_;
   static constexpr bool FUSED = FUSED_;
@@ -89,7 +89,7 @@ struct MmaCfg {
   static constexpr int UPB = BOXW / 16;                 // units per box row
   static constexpr int BPS = UNITS / 2;                 // 32-step batches per stage
   static constexpr int SETS = (CW / 4) * PAIRS;         // pair sets (M = 128 rows each)
-  static constexpr int NA = 3, NDB = 2;                 // A ring, accumulator buffers
+  static constexpr int NA = NA_, NDB = NDB_;             // A ring, accumulator buffers
   static constexpr uint32_t ASET = 32, ABUF = SETS * ASET, DCOL = NA * ABUF, DBUF = SETS * 16;
   static constexpr uint32_t TUSED = DCOL + NDB * DBUF;
   static constexpr uint32_t TCOLS = TUSED <= 32 ? 32 : TUSED <= 64 ? 64 : TUSED <= 128 ? 128
@@ -114,6 +114,9 @@ struct MmaCfg {
 // slabs and 128/256-byte segments, 3-7 % slower at the N = 2..8 write fractions.)
 using MmaHash = MmaCfg<8, 2, 64, 3, false>;
 using MmaFusedLight = MmaCfg<8, 2, 64, 3, true>;
+// hash only, large grids (mma_cw_for): 12 chain warps = 1536 pages in flight per SM;
+// TMEM (480 of 512 columns) and shared memory (2 stages) pay for the extra warps
+using MmaHash12 = MmaCfg<12, 2, 64, 2, false, 2, 1>;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -858,13 +861,24 @@ const uint8_t* device_btab() {
 
 }  // namespace
 
+// 12 chain warps per SM (1536-page groups, 2 data stages, A ring 2, one
+// accumulator buffer) issue 6-7 % more per SM than 8 (the 8-bit chains are
+// issue-latency bound: C3 switch 0.874 -> 0.823 ms, 4 GiB 5.60 -> 6.00 TB/s,
+// same box) but their groups are 1.5x larger, so small grids lose to wave
+// quantization (1 GiB: 4.72 -> 3.67 TB/s): used from 4 groups per SM on.
+uint32_t mma_cw_for(uint64_t slots, int sms) {
+  static const int force = getenv("SNAP_MMA_CW") ? atoi(getenv("SNAP_MMA_CW")) : 0;
+  if (force == 8 || force == 12) return uint32_t(force);
+  return slots >= uint64_t(sms > 0 ? sms : 148) * 4 * MmaHash12::GP ? 12u : 8u;
+}
+
 uint32_t mma_schedule(const uint64_t* addr, const uint64_t* bytes, uint32_t n,
                       uint32_t page_shift, uint32_t chunk_shift, int sms,
-                      std::vector<uint32_t>& out) {
+                      std::vector<uint32_t>& out, uint32_t cw) {
   out.clear();
   if (page_shift != 12 || chunk_shift < 12 || chunk_shift > 17 || n == 0 || sms <= 0) return 0;
-  using C = MmaHash;
-  static_assert(MmaHash::GP == MmaFusedLight::GP, "one schedule for both variants");
+  static_assert(MmaHash::GP == MmaFusedLight::GP, "one schedule for both 8-warp variants");
+  const uint64_t GP = cw == 12 ? uint64_t(MmaHash12::GP) : uint64_t(MmaHash::GP);
   const uint64_t cb = 1ull << chunk_shift;
   std::vector<uint64_t> caddr;  // chunk address, ~0 for a partial chunk
   for (uint32_t b = 0; b < n; ++b)
@@ -872,15 +886,15 @@ uint32_t mma_schedule(const uint64_t* addr, const uint64_t* bytes, uint32_t n,
   const uint64_t nch = caddr.size();
   const uint32_t ppc_shift = chunk_shift - 12;
   const uint64_t nslots = nch << ppc_shift;
-  const uint64_t ngroups = (nslots + C::GP - 1) / C::GP;
+  const uint64_t ngroups = (nslots + GP - 1) / GP;
   if (ngroups == 0 || ngroups >= (1ull << 32)) return 0;
   const uint32_t bins = uint32_t(ngroups < uint64_t(sms) ? ngroups : uint64_t(sms));
   // a task (32 page slots) is regular iff its chunks are full and contiguous
   const uint64_t cpt = 32 >> ppc_shift;  // chunks per task
   std::vector<uint8_t> heavy(ngroups, 0);
   for (uint64_t gi = 0; gi < ngroups; ++gi)
-    for (uint64_t t = 0; t < C::GP / 32 && !heavy[gi]; ++t) {
-      const uint64_t c0 = ((gi * C::GP) >> ppc_shift) + t * cpt;
+    for (uint64_t t = 0; t < GP / 32 && !heavy[gi]; ++t) {
+      const uint64_t c0 = ((gi * GP) >> ppc_shift) + t * cpt;
       bool reg = c0 + cpt <= nch;
       for (uint64_t k = 0; reg && k < cpt; ++k)
         reg = caddr[c0 + k] != ~0ull && caddr[c0 + k] == caddr[c0] + k * cb;
@@ -956,11 +970,14 @@ int launch_mma(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
 }  // namespace
 
 int launch_hash_mma(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig, cudaStream_t s) {
+  if (g.mma_cw == 12) return launch_mma<MmaHash12>(arena, g, chunk_dig, nullptr, nullptr, s);
   return launch_mma<MmaHash>(arena, g, chunk_dig, nullptr, nullptr, s);
 }
 
 int launch_hash_mma_fused(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
                           const uint64_t* spec_off, uint8_t* staging, cudaStream_t s) {
+  // (a 12-warp fused geometry with 2 data stages measured slower: full C2 on one GPU
+  // 4.59 vs 4.28 ms — the stores want the third stage)
   return launch_mma<MmaFusedLight>(arena, g, chunk_dig, spec_off, staging, s);
 }
 

@@ -99,6 +99,9 @@ struct GridDev {
   // (round robin): gsched[0..gs_bins] = per-CTA start, then the group order
   const uint32_t* gsched = nullptr;
   uint32_t gs_bins = 0;
+  // hash-only k_hash_mma geometry chosen at install time: 8 chain warps (1024-page
+  // groups) or, for grids of >= 4 groups of 1536 pages per SM, 12 (mma_cw_for)
+  uint32_t mma_cw = 8;
   // Fused verify-scatter (K4 + K1 in one pass, k_hash only): reverse != 0
   // reads chunk g from image + src_off[g] (launch_hash's staging / spec_off
   // arguments), writes it to its grid address and hashes the bytes it moved;
@@ -117,7 +120,9 @@ struct GridDev {
 // the group indices of CTA 0, CTA 1, ...; returns bins (0: no schedule).
 uint32_t mma_schedule(const uint64_t* addr, const uint64_t* bytes, uint32_t n,
                       uint32_t page_shift, uint32_t chunk_shift, int sms,
-                      std::vector<uint32_t>& out);
+                      std::vector<uint32_t>& out, uint32_t cw = 8);
+// chain warps of the hash-only tensor-core K1 for a grid of `slots` page slots
+uint32_t mma_cw_for(uint64_t slots, int sms);
 
 // The decoupled look-back scans (k_select.cu) keep a tile's chunk count in 26
 // bits of the status word: a selection / shard scan covers < 2^26 entries.

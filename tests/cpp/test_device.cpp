@@ -125,4 +125,37 @@ TEST_CASE("window tracker + persist/load through the C++ mirror") {
   std::filesystem::remove_all(dir);
 }
 
+TEST_CASE("exact whole-range digest equals the reference FNV-1a") {
+  vdev::Gpu g(0, 1 << 20);
+  std::vector<u64> w(4096);
+  for (u64 i = 0; i < w.size(); ++i) w[i] = mix64(i + 7);
+  g.write_words({0, 32768}, w);
+  u64 h = 14695981039346656037ull;  // sim.hpp:55-65 restated over the bytes
+  for (u64 x : w)
+    for (int k = 0; k < 8; ++k) {
+      h ^= (x >> (8 * k)) & 0xff;
+      h *= 0x100000001b3ull;
+    }
+  CHECK(g.digest_exact({0, 32768}).value == h);
+}
+
+TEST_CASE("splice: deferred result install reaches the inactive rank at its switch") {
+  vdev::Gpu g(0, 8 << 20);
+  splice::Splicer sp(g, 4 << 20);
+  std::vector<splice::RankBuf> bufs = {{0, 0, 1 << 20, vdev::BufCat::Param, true, false},
+                                       {1, 1 << 20, 64 << 10, vdev::BufCat::Grad, true, true}};
+  sp.set_rank_bufs(0, bufs);
+  sp.set_rank_bufs(1, bufs);
+  std::vector<u64> res(8192);
+  for (u64 i = 0; i < res.size(); ++i) res[i] = mix64(i ^ 0x77);
+  g.write_words({4 << 20, 65536}, res);
+  sp.switch_to(-1, 0);                                    // rank 0 active
+  sp.install_result({0, 1}, {1 << 20, 1 << 20}, 4 << 20, 65536);
+  CHECK(sp.pending_install_bytes(1) == 65536 && sp.pending_install_bytes(0) == 0);
+  g.write_words({1 << 20, 65536}, std::vector<u64>(8192, 0));  // rank 0's next backward
+  auto plan = sp.switch_to(0, 1);
+  CHECK(plan.install_bytes == 65536);
+  CHECK(g.words({1 << 20, 65536}) == res);
+}
+
 MINI_MAIN()
