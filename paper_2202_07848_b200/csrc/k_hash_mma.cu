@@ -114,9 +114,12 @@ struct MmaCfg {
 // slabs and 128/256-byte segments, 3-7 % slower at the N = 2..8 write fractions.)
 using MmaHash = MmaCfg<8, 2, 64, 3, false>;
 using MmaFusedLight = MmaCfg<8, 2, 64, 3, true>;
-// hash only, large grids (mma_cw_for): 12 chain warps = 1536 pages in flight per SM;
-// TMEM (480 of 512 columns) and shared memory (2 stages) pay for the extra warps
+// 12 chain warps = 1536 pages in flight per SM; TMEM (480 of 512 columns) and
+// shared memory (2 stages) pay for the extra warps (forced only, SNAP_MMA_CW=12)
 using MmaHash12 = MmaCfg<12, 2, 64, 2, false, 2, 1>;
+// default (mma_cw_for): 16 chain warps x 1 chain pair, same 1024-page groups
+using MmaHash16 = MmaCfg<16, 1, 64, 3, false, 3, 2>;
+using MmaFused16 = MmaCfg<16, 1, 64, 3, true, 3, 2>;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -861,15 +864,18 @@ const uint8_t* device_btab() {
 
 }  // namespace
 
-// 12 chain warps per SM (1536-page groups, 2 data stages, A ring 2, one
-// accumulator buffer) issue 6-7 % more per SM than 8 (the 8-bit chains are
-// issue-latency bound: C3 switch 0.874 -> 0.823 ms, 4 GiB 5.60 -> 6.00 TB/s,
-// same box) but their groups are 1.5x larger, so small grids lose to wave
-// quantization (1 GiB: 4.72 -> 3.67 TB/s): used from 4 groups per SM on.
+// Chain warps per SM of the hash-only kernel. The 8-bit chains are issue-latency
+// bound (ncu: tensor pipe 8 % active, 2.25 warps per scheduler with 8 warps x 2 chain
+// pairs), so more warps with fewer pairs each win: 16 x 1 pair (same 1024-page groups,
+// 94 registers) on the same box: C3 switch 0.877 -> 0.813 ms, 1 GiB 4.72 -> 5.02 TB/s,
+// 4 GiB 5.59 -> 6.00 TB/s; 12 x 2 pairs (1536-page groups, 2 stages) ties at 4 GiB but
+// loses below ~3.5 GiB to wave quantization. SNAP_MMA_CW=8|12|16 forces one (A/B).
 uint32_t mma_cw_for(uint64_t slots, int sms) {
   static const int force = getenv("SNAP_MMA_CW") ? atoi(getenv("SNAP_MMA_CW")) : 0;
-  if (force == 8 || force == 12) return uint32_t(force);
-  return slots >= uint64_t(sms > 0 ? sms : 148) * 4 * MmaHash12::GP ? 12u : 8u;
+  if (force == 8 || force == 12 || force == 16) return uint32_t(force);
+  (void)slots;
+  (void)sms;
+  return 16;
 }
 
 uint32_t mma_schedule(const uint64_t* addr, const uint64_t* bytes, uint32_t n,
@@ -878,7 +884,8 @@ uint32_t mma_schedule(const uint64_t* addr, const uint64_t* bytes, uint32_t n,
   out.clear();
   if (page_shift != 12 || chunk_shift < 12 || chunk_shift > 17 || n == 0 || sms <= 0) return 0;
   static_assert(MmaHash::GP == MmaFusedLight::GP, "one schedule for both 8-warp variants");
-  const uint64_t GP = cw == 12 ? uint64_t(MmaHash12::GP) : uint64_t(MmaHash::GP);
+  const uint64_t GP = cw == 12 ? uint64_t(MmaHash12::GP)
+                    : cw == 16 ? uint64_t(MmaHash16::GP) : uint64_t(MmaHash::GP);
   const uint64_t cb = 1ull << chunk_shift;
   std::vector<uint64_t> caddr;  // chunk address, ~0 for a partial chunk
   for (uint32_t b = 0; b < n; ++b)
@@ -971,14 +978,19 @@ int launch_mma(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
 
 int launch_hash_mma(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig, cudaStream_t s) {
   if (g.mma_cw == 12) return launch_mma<MmaHash12>(arena, g, chunk_dig, nullptr, nullptr, s);
+  if (g.mma_cw == 16) return launch_mma<MmaHash16>(arena, g, chunk_dig, nullptr, nullptr, s);
   return launch_mma<MmaHash>(arena, g, chunk_dig, nullptr, nullptr, s);
 }
 
 int launch_hash_mma_fused(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
                           const uint64_t* spec_off, uint8_t* staging, cudaStream_t s) {
-  // (a 12-warp fused geometry with 2 data stages measured slower: full C2 on one GPU
-  // 4.59 vs 4.28 ms — the stores want the third stage)
-  return launch_mma<MmaFusedLight>(arena, g, chunk_dig, spec_off, staging, s);
+  // fused: 16 chain warps x 1 pair, 3 stages (same-box A/B: full C2 on one GPU 4.28 ->
+  // 4.10 ms; rank 0's layout at N = 2 / 4 / 8: K1 0.871 / 0.777 / 0.750 -> 0.858 /
+  // 0.741 / 0.703 ms; a 12 x 2 geometry with 2 stages was slower, 4.59 ms).
+  // SNAP_MMA_FUSED_CW=8 forces the round-1 geometry.
+  static const int fcw = getenv("SNAP_MMA_FUSED_CW") ? atoi(getenv("SNAP_MMA_FUSED_CW")) : 16;
+  if (fcw == 8) return launch_mma<MmaFusedLight>(arena, g, chunk_dig, spec_off, staging, s);
+  return launch_mma<MmaFused16>(arena, g, chunk_dig, spec_off, staging, s);
 }
 
 }  // namespace snap

@@ -171,25 +171,27 @@ def test_scheduled_groups_mma(mma):
             assert bad.size == 0, f"rep {rep}: {bad.size} chunk digests differ, first {bad[:5]}"
 
 
-def test_mma_12_warp_geometry_whole_suite():
-    """The 12-chain-warp geometry (chosen for grids of >= 4 x 148 groups of 1536 pages) on
-    every layout of this file, forced through SNAP_MMA_CW=12 in a child process (the
-    setting is read once per process); plus one grid large enough to pick it by itself."""
+@pytest.mark.parametrize("cw", ["8", "12"])
+def test_mma_other_geometries_whole_suite(cw):
+    """The default tensor-core geometry is 16 chain warps x 1 pair (hash-only and fused);
+    the 8 x 2 (round-1) and 12 x 2 geometries stay selectable for A/B runs. Every layout
+    of this file through them, forced in a child process (read once per process)."""
     import os
     import subprocess
     import sys
     if os.environ.get("SNAP_MMA_CW"):
-        pytest.skip("already the forced run")
+        pytest.skip("already a forced run")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", __file__, "-k", "not 12_warp"],
-                       env=dict(os.environ, SNAP_MMA_CW="12"), capture_output=True, text=True,
-                       timeout=600, cwd=root)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", __file__, "-k",
+                        "not other_geometries"],
+                       env=dict(os.environ, SNAP_MMA_CW=cw, SNAP_MMA_FUSED_CW="8"),
+                       capture_output=True, text=True, timeout=600, cwd=root)
     print(r.stdout[-2000:], r.stderr[-2000:])
     assert r.returncode == 0
 
 
-def test_mma_default_picks_12_warps_on_large_grids(snap):
-    nbytes = 4 << 30  # 1 M pages >= 4 x 148 x 1536: the 12-warp geometry by policy
+def test_mma_large_grid(snap):
+    nbytes = 4 << 30  # 1 M pages, 1024 groups
     bufs = [(0, i, i * (32 << 20), 32 << 20, i % 2) for i in range(nbytes // (32 << 20))]
     with snap.Ctx(0, nbytes) as c:
         c.fill_mix64(0, nbytes, 1234, 0)
