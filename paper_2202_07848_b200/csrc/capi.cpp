@@ -1600,8 +1600,9 @@ int snap_comm_destroy(snap_ctx* ctx) {
     ctx->comm = nullptr;
   }
   if (ctx->lgroup) {
-    comm_barrier(ctx);  // no peer still reads this rank's buffers
+    const bool ok = comm_barrier(ctx);  // no peer still reads this rank's buffers
     local_group_leave(ctx);
+    if (!ok) return fail(ctx, SNAP_EINTERNAL, "comm_destroy: a peer rank never arrived");
   }
   ctx->nranks = 1;
   ctx->rank = 0;

@@ -12,6 +12,7 @@
 //    host barrier; "IPC" handles of the same process resolve to the exporting
 //    ctx's device pointer through a process-wide registry.
 // Every collective is issued in the same order by every rank (snap.h).
+#include <chrono>
 #include <condition_variable>
 #include <cstdlib>
 #include <memory>
@@ -29,18 +30,39 @@ struct LocalGroup {
   std::vector<const void*> ptrs;
   std::vector<int> devices;
 
-  void barrier() {
+  bool broken = false;
+
+  // false when a peer never arrived within the timeout (it failed before this
+  // collective): the group is then broken for every member, like a NCCL error
+  bool barrier() {
     std::unique_lock<std::mutex> lk(m);
+    if (broken) return false;
     const uint64_t g = gen;
     if (++arrived == n) {
       arrived = 0;
       ++gen;
       cv.notify_all();
-    } else {
-      cv.wait(lk, [&] { return gen != g; });
+      return true;
     }
+    static const long secs = [] {
+      const char* e = std::getenv("SNAP_LOCAL_TIMEOUT_S");
+      return e && std::atol(e) > 0 ? std::atol(e) : 120L;
+    }();
+    if (!cv.wait_for(lk, std::chrono::seconds(secs), [&] { return gen != g || broken; }) || broken) {
+      broken = true;
+      cv.notify_all();
+      return false;
+    }
+    return true;
   }
 };
+
+#define BARRIER(G)                                                                     \
+  do {                                                                                 \
+    if (!(G)->barrier())                                                               \
+      return fail(ctx, SNAP_EINTERNAL, "in-process communicator: a peer rank did not " \
+                                       "reach this collective (it failed or diverged)"); \
+  } while (0)
 
 namespace {
 
@@ -136,14 +158,14 @@ int comm_allgather(snap_ctx* ctx, const void* send, void* recv, uint64_t count, 
   if (!G) return fail(ctx, SNAP_EINTERNAL, "allgather without a communicator");
   CK(cudaStreamSynchronize(ctx->stream));
   G->ptrs[ctx->rank] = send;
-  G->barrier();
+  BARRIER(G);
   for (int q = 0; q < G->n; ++q) {
     uint8_t* dst = static_cast<uint8_t*>(recv) + q * bytes;
     if (dst != G->ptrs[q] && bytes)
       CK(cudaMemcpyAsync(dst, G->ptrs[q], bytes, cudaMemcpyDefault, ctx->stream));
   }
   CK(cudaStreamSynchronize(ctx->stream));
-  G->barrier();  // no rank reuses its send buffer before every peer copied it
+  BARRIER(G);  // no rank reuses its send buffer before every peer copied it
   return SNAP_OK;
 }
 
@@ -159,7 +181,7 @@ int comm_allreduce(snap_ctx* ctx, const void* send, void* recv, uint64_t count, 
   const uint64_t bytes = count * type_size(t);
   CK(cudaStreamSynchronize(ctx->stream));
   G->ptrs[ctx->rank] = send;
-  G->barrier();
+  BARRIER(G);
   // every rank reduces all contributions in rank order (the same bits everywhere)
   std::vector<uint8_t> acc(bytes), x(bytes);
   for (int q = 0; q < G->n; ++q) {
@@ -173,15 +195,13 @@ int comm_allreduce(snap_ctx* ctx, const void* send, void* recv, uint64_t count, 
       case kCommU8: reduce_into(acc.data(), x.data(), count, op); break;
     }
   }
-  G->barrier();  // every rank has read every send buffer
+  BARRIER(G);  // every rank has read every send buffer
   CK(cudaMemcpyAsync(recv, acc.data(), bytes, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return SNAP_OK;
 }
 
-void comm_barrier(snap_ctx* ctx) {
-  if (ctx->lgroup) ctx->lgroup->barrier();
-}
+bool comm_barrier(snap_ctx* ctx) { return ctx->lgroup ? ctx->lgroup->barrier() : true; }
 
 // Releases the peer mappings of the fixed-order allreduce.
 void ar_release(snap_ctx* ctx) {
@@ -285,8 +305,11 @@ int snap_comm_init_local(snap_ctx* ctx, int nranks, int rank, const char* key) {
     G->devices[rank] = ctx->device;
     if (G->refs == nranks) g_groups.erase(key);  // complete: the key can be reused
   }
-  G->barrier();  // every member joined
   ctx->lgroup = G;
+  if (!G->barrier()) {  // every member joined
+    local_group_leave(ctx);
+    return fail(ctx, SNAP_EINTERNAL, "comm_init_local: not every rank joined");
+  }
   ctx->nranks = nranks;
   ctx->rank = rank;
   ctx->xepoch = 0;
@@ -383,10 +406,10 @@ int snap_allreduce_ordered(snap_ctx* ctx, int dtype, const uint32_t* keys, const
     // device flag barrier (a spinning kernel could starve a peer's kernel)
     CK(cudaMemsetAsync(cnt, 0, 4, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    ctx->lgroup->barrier();  // every rank's sources are final
+    BARRIER(ctx->lgroup);  // every rank's sources are final
     CKL(snap::launch_ordered_allreduce(a, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    ctx->lgroup->barrier();  // every slice is in every dst
+    BARRIER(ctx->lgroup);  // every slice is in every dst
     return SNAP_OK;
   }
   if (epoch == 1) CK(cudaMemsetAsync(cnt, 0, 4, ctx->stream));

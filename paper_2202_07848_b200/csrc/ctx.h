@@ -256,7 +256,7 @@ inline uint64_t table_cap(uint64_t n) {
 int comm_allgather(snap_ctx* ctx, const void* send, void* recv, uint64_t count, CommType t);
 int comm_allreduce(snap_ctx* ctx, const void* send, void* recv, uint64_t count, CommType t,
                    CommOp op);
-void comm_barrier(snap_ctx* ctx);
+bool comm_barrier(snap_ctx* ctx);
 int ipc_handle(snap_ctx* ctx, void* dev_ptr, void* handle64);
 int ipc_open(snap_ctx* ctx, const void* handle64, void** out, bool* opened);
 void ipc_close(void* p, bool opened);

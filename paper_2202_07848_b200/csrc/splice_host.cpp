@@ -413,15 +413,17 @@ int snap_splice_install(snap_ctx* ctx, const int* ranks, const uint64_t* dst_add
     host[nr + i] = reinterpret_cast<uint64_t>(ctx->arena + src_addr);
     host[2 * nr + i] = bytes;
   }
-  DevMem tmp;
+  struct Scratch {  // pointer arrays of a ctx without splicing, freed on every path
+    DevMem m;
+    ~Scratch() { release(m); }
+  } tmp;
   uint64_t* d;
-  RC(ensure(ctx, S ? S->inst_ptrs : tmp, 3 * nr, &d));
+  RC(ensure(ctx, S ? S->inst_ptrs : tmp.m, 3 * nr, &d));
   CK(cudaMemcpyAsync(d, host.data(), 3 * nr * 8, cudaMemcpyHostToDevice, ctx->stream));
   CKL(snap::launch_copy_ranges(reinterpret_cast<uint8_t* const*>(d),
                                reinterpret_cast<const uint8_t* const*>(d + nr), d + 2 * nr, nr,
                                bytes, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  release(tmp);
   return SNAP_OK;
 }
 
