@@ -95,3 +95,28 @@ def test_manifest_threads(snap, manifests):
         return ok
 
     assert all(run_threads(world, run))
+
+
+def test_manifest_through_integration_glue(snap, manifests):
+    """The maintainer-facing glue (integration/fleetsim_snap.hpp), compiled against the
+    reference's headers into oracle/_ref/libfleetsim_glue.so: at every checkpoint of the
+    reference scheduler, restore_job's materialization of the manifest onto a snap_ctx
+    (one verified scatter pass) and build_manifest's device section through libsnap
+    give the reference's S_G and device upload bytes."""
+    import ctypes as C
+    import json
+    import os
+    path = os.path.join(os.path.dirname(O.__file__), "_ref", "libfleetsim_glue.so")
+    if not os.path.exists(path):
+        pytest.skip("glue library not built")
+    L = C.CDLL(path)
+    L.glue_manifest_run.restype = C.c_int
+    L.glue_manifest_run.argtypes = [C.c_char_p, C.c_int, C.c_void_p, C.c_int]
+    out = np.zeros(4 * 4, np.uint64)
+    n = L.glue_manifest_run(json.dumps(scenario(manifests[0]["world"])).encode(), 0,
+                            out.ctypes.data, 4)
+    assert n == 2
+    rows = out.reshape(4, 4)[:n]
+    assert rows[0][0] == 131072 and rows[0][2] == rows[0][0], rows      # S_G
+    assert rows[1][2] == rows[1][1] == manifests[1]["device_upload"], rows  # upload
+    assert (rows[:, 3] == 1).all(), "restore through the glue failed verification"
