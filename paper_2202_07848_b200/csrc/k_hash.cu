@@ -912,7 +912,7 @@ K1 choose_k1(const GridDev& g, const uint64_t* spec_off) {
       // tensor-core FNV: one 1024-page group per SM at a time, so small grids
       // leave SMs idle (tools/hash_sizes.py: 256 MiB 2.56 vs 2.85 TB/s for the
       // TMA kernel, 384 MiB 3.75 vs 2.29, 512 MiB+ 4.8-6.0 vs 3.0-3.6)
-      if (hash_mma_ok(g) && pages >= 80 * 1024) return K1::Mma;
+      if (hash_mma_ok(g) && (pages >= 80 * 1024 || g.mma_cw == 81)) return K1::Mma;
       if (g.nbufs && (g.nchunks << g.chunk_shift) / g.nbufs >= (64ull << 20)) return K1::B;
       return hash_tma_ok(g) ? K1::Tma : K1::A;
     }

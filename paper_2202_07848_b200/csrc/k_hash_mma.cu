@@ -120,6 +120,9 @@ using MmaHash12 = MmaCfg<12, 2, 64, 2, false, 2, 1>;
 // default (mma_cw_for): 16 chain warps x 1 chain pair, same 1024-page groups
 using MmaHash16 = MmaCfg<16, 1, 64, 3, false, 3, 2>;
 using MmaFused16 = MmaCfg<16, 1, 64, 3, true, 3, 2>;
+// small hash-only grids (mma_cw_for): 512-page groups (8 chain warps x 1 pair)
+using MmaHash8x1 = MmaCfg<8, 1, 64, 3, false, 3, 2>;
+using MmaFused8x1 = MmaCfg<8, 1, 64, 3, true, 3, 2>;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -870,12 +873,14 @@ const uint8_t* device_btab() {
 // 94 registers) on the same box: C3 switch 0.877 -> 0.813 ms, 1 GiB 4.72 -> 5.02 TB/s,
 // 4 GiB 5.59 -> 6.00 TB/s; 12 x 2 pairs (1536-page groups, 2 stages) ties at 4 GiB but
 // loses below ~3.5 GiB to wave quantization. SNAP_MMA_CW=8|12|16 forces one (A/B).
+// Grids of at most one 512-page group per SM (<= ~296 MiB) run 8 chain warps x 1
+// pair (81): twice the groups of the 1024-page geometries, so every SM gets work
+// (hash-only, same box: 16 MiB 190 -> 221 GB/s, 64 MiB 755 -> 878, 256 MiB 2850 ->
+// 3312 vs the TMA FNV kernel; from 384 MiB on 16 x 1 wins: 3684 vs 2603).
 uint32_t mma_cw_for(uint64_t slots, int sms) {
   static const int force = getenv("SNAP_MMA_CW") ? atoi(getenv("SNAP_MMA_CW")) : 0;
-  if (force == 8 || force == 12 || force == 16) return uint32_t(force);
-  (void)slots;
-  (void)sms;
-  return 16;
+  if (force == 8 || force == 12 || force == 16 || force == 81) return uint32_t(force);
+  return slots <= uint64_t(sms > 0 ? sms : 148) * uint64_t(MmaHash8x1::GP) ? 81u : 16u;
 }
 
 uint32_t mma_schedule(const uint64_t* addr, const uint64_t* bytes, uint32_t n,
@@ -885,7 +890,8 @@ uint32_t mma_schedule(const uint64_t* addr, const uint64_t* bytes, uint32_t n,
   if (page_shift != 12 || chunk_shift < 12 || chunk_shift > 17 || n == 0 || sms <= 0) return 0;
   static_assert(MmaHash::GP == MmaFusedLight::GP, "one schedule for both 8-warp variants");
   const uint64_t GP = cw == 12 ? uint64_t(MmaHash12::GP)
-                    : cw == 16 ? uint64_t(MmaHash16::GP) : uint64_t(MmaHash::GP);
+                    : cw == 16 ? uint64_t(MmaHash16::GP)
+                    : cw == 81 ? uint64_t(MmaHash8x1::GP) : uint64_t(MmaHash::GP);
   const uint64_t cb = 1ull << chunk_shift;
   std::vector<uint64_t> caddr;  // chunk address, ~0 for a partial chunk
   for (uint32_t b = 0; b < n; ++b)
@@ -979,6 +985,7 @@ int launch_mma(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
 int launch_hash_mma(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig, cudaStream_t s) {
   if (g.mma_cw == 12) return launch_mma<MmaHash12>(arena, g, chunk_dig, nullptr, nullptr, s);
   if (g.mma_cw == 16) return launch_mma<MmaHash16>(arena, g, chunk_dig, nullptr, nullptr, s);
+  if (g.mma_cw == 81) return launch_mma<MmaHash8x1>(arena, g, chunk_dig, nullptr, nullptr, s);
   return launch_mma<MmaHash>(arena, g, chunk_dig, nullptr, nullptr, s);
 }
 
@@ -990,6 +997,7 @@ int launch_hash_mma_fused(const uint8_t* arena, const GridDev& g, uint64_t* chun
   // SNAP_MMA_FUSED_CW=8 forces the round-1 geometry.
   static const int fcw = getenv("SNAP_MMA_FUSED_CW") ? atoi(getenv("SNAP_MMA_FUSED_CW")) : 16;
   if (fcw == 8) return launch_mma<MmaFusedLight>(arena, g, chunk_dig, spec_off, staging, s);
+  if (fcw == 81) return launch_mma<MmaFused8x1>(arena, g, chunk_dig, spec_off, staging, s);
   return launch_mma<MmaFused16>(arena, g, chunk_dig, spec_off, staging, s);
 }
 
