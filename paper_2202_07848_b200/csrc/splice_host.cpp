@@ -212,6 +212,10 @@ int snap_splice_init_slots(snap_ctx* ctx, uint64_t cache_bytes, uint32_t slot_by
   RC(ensure(ctx, S->counters, 4, &cnt));
   S->cmask = tcap - 1;
   CKL(snap::launch_table_clear(TableDev{k, v, S->cmask}, ctx->stream));
+  // the reclamation's second index, allocated now: no cudaMalloc inside a switch
+  unsigned long long *k2, *v2;
+  RC(ensure(ctx, S->ck2, tcap + 1, &k2));
+  RC(ensure(ctx, S->cv2, tcap + 1, &v2));
   uint32_t *fs, *sl;
   RC(ensure(ctx, S->free_stack, S->nslots, &fs));
   RC(ensure(ctx, S->slot_len, S->nslots, &sl));
@@ -285,6 +289,13 @@ int snap_splice_set_rank(snap_ctx* ctx, int rank, const snap_buf* bufs, uint64_t
   R.grid = GridDev{da, db, dc, uint32_t(nb), R.nchunks, log2u(g.page_bytes), log2u(g.chunk_bytes)};
   build_tmaps(ctx, R.d_tmaps, addr.data(), bytes.data(), uint32_t(nb), R.grid);
   R.recorded = false;
+  // the reclamation's live-digest table covers every rank's chunks: sized here, not in a switch
+  uint64_t total = 0;
+  for (auto& [q, gq] : S->ranks) total += gq.nchunks;
+  const uint64_t lcap = table_cap(std::max<uint64_t>(total, 1));
+  unsigned long long *lk, *lv;
+  RC(ensure(ctx, S->lk, lcap + 1, &lk));
+  RC(ensure(ctx, S->lv, lcap + 1, &lv));
   for (auto it = S->match.begin(); it != S->match.end();) {
     if (it->first.first == rank || it->first.second == rank) {
       release(it->second);
