@@ -845,14 +845,15 @@ bool hash_tma_selected() {
 
 // The K1 kernel a launch uses (SNAP_HASH_VARIANT / snap_set_k1_variant force
 // one; the default is the fastest measured per shape):
-//  * fused hash + speculative stores: CfgE — 256-B slabs keep the mixed
-//    read/write DRAM pattern at ~6 TB/s (128-B segments cap it at ~5.2,
-//    tools/micro/pattern_bw2.cu);
-//  * hash only, >= 320 MiB: the tensor-core FNV kernel (k_hash_mma.cu);
-//  * hash only, smaller grids (alternating same-box A/B over the C2 / C3 / C4
-//    buffer shapes, tools/hash_variants.py): the TMA tensor-load kernel beats
-//    the cp.async CfgA by 1-2 % on every shape; two chains per lane (CfgB) win
-//    by another 1 % on very large buffers but lose 14 % on small tensors.
+//  * fused hash + speculative stores, most of the grid staged, and the
+//    verify-scatter: CfgG (below) — 256-B slabs keep the mixed read/write DRAM
+//    pattern at ~6 TB/s (128-B segments cap it at ~5.2, tools/micro/pattern_bw2.cu);
+//  * fused, less than 70 % of a >= 512 MiB grid staged: the tensor-core kernel
+//    with fused stores;
+//  * hash only, grids with tensor maps: the tensor-core FNV kernel (k_hash_mma.cu:
+//    16 chain warps, or 8 in 512-page groups for grids of <= one group per SM);
+//  * hash only without tensor maps (forced cp.async variants, 64 MiB+ buffers):
+//    CfgB / CfgA (tools/hash_variants.py).
 enum class K1 { A, B, C, D, E, F, G, H, I, J, WsA, WsB, WsC, Tma, Mma, MmaFL, TmaF };
 // Fused launches (hash + stores, and the verify-scatter): CfgG, 16 warps per
 // SM with one 256-byte stage each. Same-box A/B (tools/fused_variants.py,
@@ -896,13 +897,13 @@ K1 choose_k1(const GridDev& g, const uint64_t* spec_off) {
       const uint64_t c_end = g.c_end ? g.c_end : g.nchunks;
       const uint64_t pages = (c_end - g.c_begin) << (g.chunk_shift - g.page_shift);
       // fused hash + speculative stores. Most chunks staged (single GPU, first
-      // snapshot): CfgE — the mixed read/write DRAM stream bounds the pass and
-      // its 256-B segments win (0.79 vs 0.83-0.96 ms on C2). Few staged
+      // snapshot): CfgG — the mixed read/write DRAM stream bounds the pass
+      // (0.74 ms on C2 vs 0.94 for the tensor-core kernel). Few staged
       // (multi-GPU striping: rank r writes its private state + 1/N of the
-      // replicated state): the hash dominates -> tensor-core FNV with the
-      // stores fused (hash-only geometry, 64-B segments). Same-box A/B at the
-      // N = 2 / 4 / 8 write fraction of C2 (tools/stripe_emu.py): 0.755 /
-      // 0.712 / 0.686 ms vs CfgE 0.817 / 0.792 / 0.788.
+      // replicated state; several ranks in one buffer list): the hash dominates
+      // -> tensor-core FNV with the stores fused (64-B segments). Same-box A/B
+      // at the N = 2 / 4 / 8 write fraction of C2 (tools/stripe_emu.py, 16
+      // chain warps): 0.858 / 0.741 / 0.703 ms vs CfgG ~0.84 / 0.83 / 0.82.
       if (spec_off) {
         const uint64_t grid_bytes = (c_end - g.c_begin) << g.chunk_shift;
         if (hash_mma_ok(g) && pages >= 128 * 1024 && g.spec_bytes * 10 < grid_bytes * 7)
