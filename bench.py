@@ -604,6 +604,15 @@ def c1_bench(snap, device, reps=20):
         for _ in range(reps):
             c.restore_self(verify=True)
         rest_ms = c.timer_stop() / reps
+        # kernel-level: the event windows of the K1 of a snapshot and of the verify-scatter
+        c.prof_enable(True)
+        for _ in range(reps):
+            c.snapshot()
+            c.restore_self(verify=True)
+        k1_t, k1_n = c.prof_read(snap.PROF_HASH)
+        rs_t, rs_n = c.prof_read(snap.PROF_RESTORE)
+        c.prof_enable(False)
+        k1_ms, rs_ms = k1_t / max(k1_n, 1), rs_t / max(rs_n, 1)
         # opt-in whole-image digest, value-equal to the reference's Gpu::digest
         c.digest_whole([(0, 0, 0, nbytes, 0)])
         t = time.perf_counter()
@@ -617,6 +626,12 @@ def c1_bench(snap, device, reps=20):
            "snapshot_k1": k_snap,
            "restore_verify_ms": round(rest_ms, 4),
            "restore_frac": round(rw / rest_ms / 1e6 / peak, 4),
+           "kernels": {"snapshot_k1_ms": round(k1_ms, 4),
+                       "snapshot_k1_frac": round(rw / k1_ms / 1e6 / peak, 4),
+                       "verify_scatter_ms": round(rs_ms, 4),
+                       "verify_scatter_frac": round(rw / rs_ms / 1e6 / peak, 4),
+                       "note": "per-call times above add K2/K3 (snapshot) and the host "
+                               "read-back of the verification verdict (restore)"},
            "algorithmic_bytes_each_way": rw,
            "whole_image_digest": {"ms": round(whole_ms, 2), "value": hex(whole),
                                   "what": "snap_digest_whole: Gpu::digest value-equal to the "
