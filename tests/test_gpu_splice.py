@@ -283,3 +283,26 @@ def test_splice_recorded_digests_in_buffer_order(snap):
         live = [b[:5] for b in lay if not b[5] & 4]
         exp, _, _ = O.hash_chunks([host], live)
         assert np.array_equal(got, exp)
+
+
+def test_splice_slot_geometry(snap):
+    """The chunk cache's slot size bounds the chunk size (64 KiB chunks do not fit 4 KiB
+    slots); small slots with small chunks switch correctly (4 KiB chunks, 4 KiB slots)."""
+    lay = rank_layout()
+    with snap.Ctx(0, 16 * MIB) as ctx:
+        ctx.splice_init(8 * MIB, slot_bytes=4096)
+        with pytest.raises(snap.SnapError) as e:
+            ctx.splice_set_rank(0, lay)  # default 64 KiB chunks
+        assert e.value.code == snap.SNAP_EINVAL
+        ctx.fill_mix64(0, 8 * MIB, 41, 0)
+        ctx.splice_set_rank(0, lay, page_bytes=4096, chunk_bytes=4096)
+        ctx.splice_set_rank(1, lay, page_bytes=4096, chunk_bytes=4096)
+        before = ctx.read(0, 6 * MIB)
+        ctx.splice_switch(0, 1)
+        ctx.fill_mix64(0, 6 * MIB, 42, 0)  # rank 1's different P/O
+        st = ctx.splice_switch(1, 0)
+        after = ctx.read(0, 6 * MIB)
+        for (_, s, a, n, c, f) in lay:
+            if not f & 4:
+                assert np.array_equal(after[a:a + n], before[a:a + n])
+        assert st["swap_in_bytes"] > 0
