@@ -1007,8 +1007,13 @@ def run_ours(args, dist):
 
     # nvidia-smi was started with the run (its start-up takes ~1 s); if it has not delivered
     # samples yet, keep the GPU busy until it does, so the timed region is sampled
+    # (collective at N > 1: every rank runs the same number of snapshots, so the decision
+    # to stop waiting is taken together)
     t_wait = time.perf_counter()
-    while not clocks.ready() and time.perf_counter() - t_wait < 5.0:
+    while True:
+        waiting = not clocks.ready() and time.perf_counter() - t_wait < 5.0
+        if dist.max(1.0 if waiting else 0.0) == 0.0:
+            break
         for _ in range(20):
             step()
         ctx.sync()
@@ -1023,16 +1028,16 @@ def run_ours(args, dist):
     tw1 = time.perf_counter()
     launches = ctx.launches - l0
     k1_kernel = snap.last_k1_kernel()  # the K1 the timed steps ran (policy: k_hash.cu choose_k1)
-    # per-kernel-class event windows over the same number of steps, run right after the
-    # timed region (events between kernels cost the step its PDL overlap, so the timed
-    # region runs without them); they also keep the load on for the trailing clock samples
+    # per-kernel-class event windows over as many steps (at least 60 ms of them, which
+    # also keeps the load on for the trailing clock samples), run right after the timed
+    # region: events between kernels cost the step its PDL overlap, so the timed region
+    # runs without them. The count is derived from the max over ranks (snapshots are
+    # collective at N > 1: every rank must run the same number)
+    ms_all = dist.max(ms)
+    n_tail = max(args.steps, int(0.06 / max(ms_all / 1e3 / args.steps, 1e-6)) + 1)
     ctx.prof_enable(True)
-    t_tail = time.perf_counter()
-    for _ in range(args.steps):
+    for _ in range(n_tail):
         step()
-    while time.perf_counter() - t_tail < 0.06:
-        step()
-        ctx.sync()
     t_hash, n_hash = ctx.prof_read(snap.PROF_HASH)
     t_sel, n_sel = ctx.prof_read(snap.PROF_SELECT)
     t_cmp, n_cmp = ctx.prof_read(snap.PROF_COMPACT)
@@ -1040,7 +1045,7 @@ def run_ours(args, dist):
     ctx.prof_enable(False)
     clocks.window(tw0 - 0.02, tw1 + 0.06)
     clk = clocks.stop()
-    ms_max = dist.max(ms)
+    ms_max = ms_all
     w_total = dist.sum(float(my_bytes))
     step_s = ms_max / 1e3 / args.steps
     value = N * image / step_s / 1e9
