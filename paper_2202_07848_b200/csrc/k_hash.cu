@@ -901,12 +901,13 @@ K1 choose_k1(const GridDev& g, const uint64_t* spec_off) {
       // (0.74 ms on C2 vs 0.94 for the tensor-core kernel). Few staged
       // (multi-GPU striping: rank r writes its private state + 1/N of the
       // replicated state; several ranks in one buffer list): the hash dominates
-      // -> tensor-core FNV with the stores fused (64-B segments). Same-box A/B
-      // at the N = 2 / 4 / 8 write fraction of C2 (tools/stripe_emu.py, 16
-      // chain warps): 0.858 / 0.741 / 0.703 ms vs CfgG ~0.84 / 0.83 / 0.82.
+      // -> tensor-core FNV with the stores fused (64-B segments) below 55 %
+      // staged. Real 2-GPU runs of C2 (62 % staged): CfgG K1 0.670 ms vs 0.695
+      // (6106-6123 vs 5890-5922 GB/s); at the N = 4 / 8 write fractions (44 / 38 %)
+      // the tensor-core kernel wins (tools/stripe_emu.py: 0.741 / 0.703 vs ~0.83).
       if (spec_off) {
         const uint64_t grid_bytes = (c_end - g.c_begin) << g.chunk_shift;
-        if (hash_mma_ok(g) && pages >= 128 * 1024 && g.spec_bytes * 10 < grid_bytes * 7)
+        if (hash_mma_ok(g) && pages >= 128 * 1024 && g.spec_bytes * 100 < grid_bytes * 55)
           return K1::MmaFL;
         return fused_cfg(g);
       }
