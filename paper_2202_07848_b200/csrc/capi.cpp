@@ -136,6 +136,20 @@ int select_with_known(snap_ctx* ctx, const uint64_t* dig, const uint32_t* lens, 
     const char* e = std::getenv("SNAP_SELECT_SMALL");
     return e && e[0] == '0';
   }();
+  static const bool cta_off = [] {
+    const char* e = std::getenv("SNAP_SELECT_CTA");
+    return e && e[0] == '0';
+  }();
+  if (!inserted && !small_off && !cta_off && snap::select_cta_ok(n)) {
+    // the table and scan state prepare_dedup guarantees clean stay untouched
+    CKL(snap::launch_select_cta(kn, use_known, dig, lens, n, sel, owner, offsets, list, totals,
+                                spec_next, ctx->stream, fix_spec, ctx->arena, &ctx->grid,
+                                fix_staging));
+    ctx->dd_clean = true;
+    ctx->sel_n = n;
+    ctx->global_offsets_pending = false;
+    return SNAP_OK;
+  }
   if (!inserted && !small_off && snap::select_small_ok(n)) {
     // scratch: the (zero) scan state, at least 9 words (prepare_dedup zeroed it)
     CKL(snap::launch_select_small(dd, kn, use_known, dig, lens, n, sel, owner, offsets, list,
@@ -727,7 +741,7 @@ int snap_close(snap_ctx* ctx) {
         &ctx->d_shard_off, &ctx->d_my_list, &ctx->d_my_off, &ctx->d_my_totals, &ctx->d_dig2,
         &ctx->d_expect, &ctx->d_nbad, &ctx->d_srcoff, &ctx->d_spec[0], &ctx->d_spec[1],
         &ctx->d_tmaps, &ctx->scan2, &ctx->d_xdig, &ctx->d_xflag, &ctx->d_xh, &ctx->d_arflag,
-        &ctx->d_arh, &ctx->d_arrec, &ctx->d_arptr, &ctx->d_arcnt})
+        &ctx->d_arh, &ctx->d_arrec, &ctx->d_arptr, &ctx->d_arcnt, &ctx->d_vbad})
     release(*m);
   for (cudaEvent_t e : ctx->prof.pool) cudaEventDestroy(e);
   if (ctx->arena) cudaFree(ctx->arena);
@@ -739,6 +753,7 @@ int snap_close(snap_ctx* ctx) {
   release(ctx->d_moved);
   for (uint8_t* q : ctx->io_pin)
     if (q) cudaFreeHost(q);
+  if (ctx->h_badflag) cudaFreeHost(ctx->h_badflag);
   if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
   if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -1460,23 +1475,35 @@ static int restore_verified(snap_ctx* ctx, const uint8_t* image, const uint64_t*
   uint64_t* d2;
   unsigned long long* nbad;
   RC(ensure(ctx, ctx->d_dig2, ctx->nchunks, &d2));
-  RC(ensure(ctx, ctx->d_nbad, 4, &nbad));
-  CK(cudaMemsetAsync(nbad, 0, 8, ctx->stream));
+  const bool fresh = ctx->d_vbad.p == nullptr;
+  RC(ensure(ctx, ctx->d_vbad, 4, &nbad));
+  if (!ctx->h_badflag) {
+    // the mismatch flag lives in mapped pinned memory: the success path is one
+    // kernel and a stream synchronize (no memset, no read-back copy)
+    void* hp = nullptr;
+    CK(cudaHostAlloc(&hp, 64, cudaHostAllocMapped | cudaHostAllocPortable));
+    ctx->h_badflag = static_cast<unsigned int*>(hp);
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->d_badflag), hp, 0));
+  }
+  // the counter stays zero between calls (reset below after a mismatch)
+  if (fresh) CK(cudaMemsetAsync(nbad, 0, 8, ctx->stream));
+  *reinterpret_cast<volatile unsigned int*>(ctx->h_badflag) = 0;
   GridDev g = ctx->grid;
   g.reverse = 1;
   g.expect = expect_dev;
   g.nbad = nbad;
+  g.bad_flag = ctx->d_badflag;
   {
     ProfScope ps(ctx, kProfRestore);
     CKL(snap::launch_hash(ctx->arena, g, d2, src_off_dev, const_cast<uint8_t*>(image), ctx->stream));
   }
-  unsigned long long bad = 0;
-  CK(cudaMemcpyAsync(&bad, nbad, 8, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  if (bad)
-    return fail(ctx, SNAP_EFAULT, "restore: digest verification failed on " + std::to_string(bad) +
-                                      " chunk(s)");
-  return SNAP_OK;
+  if (*reinterpret_cast<volatile unsigned int*>(ctx->h_badflag) == 0) return SNAP_OK;
+  unsigned long long bad = 0;
+  CK(cudaMemcpy(&bad, nbad, 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemset(nbad, 0, 8));
+  return fail(ctx, SNAP_EFAULT, "restore: digest verification failed on " + std::to_string(bad) +
+                                    " chunk(s)");
 }
 
 int snap_restore(snap_ctx* ctx, const void* image, uint64_t image_bytes, const uint64_t* src_off,

@@ -108,6 +108,11 @@ struct snap_ctx {
 
   // verify / restore scratch
   DevMem d_dig2, d_expect, d_nbad, d_srcoff;
+  // verified restore: set to 1 by any CTA that sees a digest mismatch (mapped
+  // pinned host word; the success path needs no memset and no read-back copy)
+  unsigned int* h_badflag = nullptr;
+  unsigned int* d_badflag = nullptr;
+  DevMem d_vbad;  // its mismatch counter, zero between calls
 
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   Prof prof;

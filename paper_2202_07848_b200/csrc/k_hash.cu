@@ -151,6 +151,9 @@ k_hash(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ chun
   const uint64_t ntasks = (nslots + NP - 1) / NP;
   const uint64_t gw = uint64_t(blockIdx.x) * C::kWarps + warp;
   const uint64_t nw = uint64_t(gridDim.x) * C::kWarps;
+  // launched with PDL: the CTAs become resident while the previous kernel of
+  // the stream (e.g. the last snapshot's selection) drains; wait for it here
+  griddep_wait();
   if (gw >= ntasks) return;
   const uint64_t my_tasks = (ntasks - gw + nw - 1) / nw;
   const uint64_t nsteps = my_tasks << ns_shift;
@@ -772,6 +775,11 @@ using CfgH = HashCfg<1, 256, 1, 14>;
 // 512-B segments per page and step (fewer DRAM row switches per byte), one stage
 using CfgI = HashCfg<1, 512, 1, 12>;
 using CfgJ = HashCfg<1, 512, 1, 13>;
+// fewer warps, each overlapping its own next slab with the hash of the current
+// one (experimental: small fused grids)
+using CfgK = HashCfg<1, 256, 2, 8>;
+using CfgL = HashCfg<1, 256, 3, 8>;
+using CfgM = HashCfg<1, 256, 2, 10>;
 using WsA = WsCfg<16, 4, 3>;          // warp-specialized: 16 hash + 4 copy warps
 using WsB = WsCfg<16, 2, 3>;          // 16 hash + 2 copy warps
 using WsC = WsCfg<12, 4, 4>;          // 12 hash + 4 copy warps, deeper ring
@@ -813,14 +821,14 @@ int launch_hash_cfg(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
   // the reference's 4 KiB page (strides become immediates) and the default
   // 64 KiB chunk (static chunk split of the speculative stores)
   if (g.page_shift == 12 && g.chunk_shift == 16)
-    k_hash<C, 12, 16><<<unsigned(blocks), C::kWarps * 32, C::kSmem, s>>>(arena, g, chunk_dig,
-                                                                         spec_off, staging);
+    launch_pdl(k_hash<C, 12, 16>, unsigned(blocks), C::kWarps * 32, C::kSmem, s, arena, g,
+               chunk_dig, spec_off, staging);
   else if (g.page_shift == 12)
-    k_hash<C, 12, 0><<<unsigned(blocks), C::kWarps * 32, C::kSmem, s>>>(arena, g, chunk_dig,
-                                                                        spec_off, staging);
+    launch_pdl(k_hash<C, 12, 0>, unsigned(blocks), C::kWarps * 32, C::kSmem, s, arena, g,
+               chunk_dig, spec_off, staging);
   else
-    k_hash<C, 0, 0><<<unsigned(blocks), C::kWarps * 32, C::kSmem, s>>>(arena, g, chunk_dig,
-                                                                       spec_off, staging);
+    launch_pdl(k_hash<C, 0, 0>, unsigned(blocks), C::kWarps * 32, C::kSmem, s, arena, g,
+               chunk_dig, spec_off, staging);
   return 1;
 }
 
@@ -854,7 +862,7 @@ bool hash_tma_selected() {
 //    16 chain warps, or 8 in 512-page groups for grids of <= one group per SM);
 //  * hash only without tensor maps (forced cp.async variants, 64 MiB+ buffers):
 //    CfgB / CfgA (tools/hash_variants.py).
-enum class K1 { A, B, C, D, E, F, G, H, I, J, WsA, WsB, WsC, Tma, Mma, MmaFL, TmaF };
+enum class K1 { A, B, C, D, E, F, G, H, I, J, K, L, M, WsA, WsB, WsC, Tma, Mma, MmaFL, TmaF };
 // Fused launches (hash + stores, and the verify-scatter): CfgG, 16 warps per
 // SM with one 256-byte stage each. Same-box A/B (tools/fused_variants.py,
 // tools/c1_variants.py): C2 N = 1 K1 0.734-0.740 ms vs CfgE's 0.796-0.798
@@ -870,6 +878,9 @@ K1 choose_k1(const GridDev& g, const uint64_t* spec_off) {
     if (v == 7) return K1::E;
     if (v == 14) return K1::G;
     if (v == 15) return K1::H;
+    if (v == 18) return K1::K;
+    if (v == 19) return K1::L;
+    if (v == 20) return K1::M;
     return fused_cfg(g);
   }
   switch (hash_variant()) {
@@ -877,6 +888,9 @@ K1 choose_k1(const GridDev& g, const uint64_t* spec_off) {
     case 15: return K1::H;
     case 16: return K1::I;
     case 17: return K1::J;
+    case 18: return K1::K;
+    case 19: return K1::L;
+    case 20: return K1::M;
     case 1: return K1::B;
     case 2: return K1::C;
     case 3: return K1::D;
@@ -934,6 +948,9 @@ int launch_k1(K1 k, const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
     case K1::H: return launch_hash_cfg<CfgH>(arena, g, chunk_dig, spec_off, staging, s);
     case K1::I: return launch_hash_cfg<CfgI>(arena, g, chunk_dig, spec_off, staging, s);
     case K1::J: return launch_hash_cfg<CfgJ>(arena, g, chunk_dig, spec_off, staging, s);
+    case K1::K: return launch_hash_cfg<CfgK>(arena, g, chunk_dig, spec_off, staging, s);
+    case K1::L: return launch_hash_cfg<CfgL>(arena, g, chunk_dig, spec_off, staging, s);
+    case K1::M: return launch_hash_cfg<CfgM>(arena, g, chunk_dig, spec_off, staging, s);
     case K1::WsA: return launch_hash_ws<WsA>(arena, g, chunk_dig, spec_off, staging, s);
     case K1::WsB: return launch_hash_ws<WsB>(arena, g, chunk_dig, spec_off, staging, s);
     case K1::WsC: return launch_hash_ws<WsC>(arena, g, chunk_dig, spec_off, staging, s);
@@ -959,6 +976,9 @@ const char* k1_name(K1 k) {
     case K1::H: return "k_hash<CfgH> (FNV chain + fused stores, 14 warps x 1 stage: one wave)";
     case K1::I: return "k_hash<CfgI> (FNV chain + fused stores, 512-B slabs, 12 warps)";
     case K1::J: return "k_hash<CfgJ> (FNV chain + fused stores, 512-B slabs, 13 warps)";
+    case K1::K: return "k_hash<CfgK> (FNV chain + fused stores, 8 warps x 2 stages)";
+    case K1::L: return "k_hash<CfgL> (FNV chain + fused stores, 8 warps x 3 stages)";
+    case K1::M: return "k_hash<CfgM> (FNV chain + fused stores, 10 warps x 2 stages)";
     case K1::WsA: return "k_hash_ws<WsA>";
     case K1::WsB: return "k_hash_ws<WsB>";
     case K1::WsC: return "k_hash_ws<WsC>";

@@ -518,6 +518,175 @@ k_select_small(TableDev dedup, TableDev known, int use_known, const uint64_t* __
   }
 }
 
+// Selections of at most 4096 chunks (C1): the whole K2 in ONE CTA with the
+// first-occurrence table in shared memory — no global atomics, no grid
+// barriers, nothing to clean up afterwards (the global dedup table and scan
+// state are not touched). 1024 threads; chunk g = j * 1024 + t (j < 4) so every
+// global load and store is coalesced (one SM's load/store path is the limit
+// here), the scan runs as 4 block scans with a carry. Same outputs bit for bit
+// as k_select_small / the three-kernel path.
+constexpr int kCtaThreads = 1024;
+constexpr int kCtaItems = 4;
+constexpr uint32_t kCtaMax = kCtaThreads * kCtaItems;
+constexpr uint32_t kCtaTab = 2 * kCtaMax;  // slots (load <= 1/2) + 1 for kEmptyKey
+constexpr size_t kCtaSmem = size_t(kCtaTab + 1) * 8 + size_t(kCtaMax) * 8 + size_t(kCtaTab + 1) * 4;
+
+__global__ void __launch_bounds__(kCtaThreads, 1)
+k_select_cta(TableDev known, int use_known, const uint64_t* __restrict__ dig,
+             const uint32_t* __restrict__ lens, uint32_t n, uint8_t* __restrict__ sel,
+             uint64_t* __restrict__ owner, uint64_t* __restrict__ offsets,
+             uint32_t* __restrict__ sel_list, uint64_t* __restrict__ totals,
+             uint64_t* __restrict__ spec_next, const uint64_t* __restrict__ spec_cur,
+             const uint8_t* __restrict__ arena, GridDev grid, uint8_t* __restrict__ staging) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem);
+  uint64_t* s_off = reinterpret_cast<uint64_t*>(smem + size_t(kCtaTab + 1) * 8);
+  uint32_t* vals = reinterpret_cast<uint32_t*>(smem + size_t(kCtaTab + 1 + kCtaMax) * 8);
+  __shared__ uint64_t s_warp[kCtaThreads / 32];
+  __shared__ uint64_t s_tot;
+  __shared__ uint32_t s_nfix;
+  __shared__ uint32_t s_fix[256];
+  const uint32_t t = threadIdx.x;
+  const int lane = t & 31, warp = t >> 5;
+  for (uint32_t i = t; i <= kCtaTab; i += kCtaThreads) {
+    keys[i] = kEmptyKey;
+    vals[i] = 0xffffffffu;
+  }
+  if (t == 0) s_nfix = 0;
+  griddep_wait();
+  // the next kernel of the stream (the next snapshot's K1) may become resident
+  // now; it waits for this grid's completion itself
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  uint32_t len[kCtaItems];
+  unsigned long long d[kCtaItems];
+  uint64_t sc[kCtaItems];
+#pragma unroll
+  for (int j = 0; j < kCtaItems; ++j) {
+    const uint32_t g = j * kCtaThreads + t;
+    len[j] = g < n ? __ldcg(lens + g) : 0;
+    d[j] = g < n ? __ldcg(reinterpret_cast<const unsigned long long*>(dig) + g) : 0;
+    sc[j] = (spec_cur && g < n) ? __ldg(spec_cur + g) : 0;
+  }
+  bool cand[kCtaItems];
+#pragma unroll
+  for (int j = 0; j < kCtaItems; ++j)
+    cand[j] = len[j] != 0 && !(use_known && table_find(known, d[j]) != ~0ull);
+  __syncthreads();  // table initialised
+  // insert: the thread whose CAS claims the slot stores its index; the others
+  // with the same digest (duplicates, rare) take the minimum after a barrier.
+  // The kEmptyKey digest has its own slot and always goes through atomicMin.
+  uint32_t slot[kCtaItems];
+  uint32_t dup = 0;
+#pragma unroll
+  for (int j = 0; j < kCtaItems; ++j) {
+    slot[j] = 0xffffffffu;
+    if (!cand[j]) continue;
+    uint32_t h;
+    if (d[j] == kEmptyKey) {
+      h = kCtaTab;
+      dup |= 1u << j;
+    } else {
+      h = uint32_t(tmix64(d[j])) & (kCtaTab - 1);
+      for (;;) {
+        const unsigned long long prev = atomicCAS(keys + h, kEmptyKey, d[j]);
+        if (prev == kEmptyKey) {
+          vals[h] = j * kCtaThreads + t;
+          break;
+        }
+        if (prev == d[j]) {
+          dup |= 1u << j;
+          break;
+        }
+        h = (h + 1) & (kCtaTab - 1);
+      }
+    }
+    slot[j] = h;
+  }
+  if (__syncthreads_or(dup != 0)) {
+#pragma unroll
+    for (int j = 0; j < kCtaItems; ++j)
+      if (dup >> j & 1) atomicMin(vals + slot[j], j * kCtaThreads + t);
+    __syncthreads();
+  }
+  uint64_t carry = 0;
+  uint64_t own[kCtaItems];
+  bool sl[kCtaItems];
+#pragma unroll
+  for (int j = 0; j < kCtaItems; ++j) {
+    const uint32_t g = j * kCtaThreads + t;
+    own[j] = slot[j] == 0xffffffffu ? ~0ull : uint64_t(vals[slot[j]]);
+    sl[j] = own[j] == g;
+    const uint64_t val = sl[j] ? (1ull << kUnitBits) | (len[j] >> 8) : 0;
+    uint64_t incl = val;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const uint64_t w = s_warp[lane];
+      uint64_t wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += y;
+      }
+      s_warp[lane] = wi - w;
+      if (lane == 31) s_tot = wi;
+    }
+    __syncthreads();
+    const uint64_t run = carry + s_warp[warp] + incl - val;
+    carry += s_tot;
+    if (g < n) {
+      const uint64_t off = (run & ((1ull << kUnitBits) - 1)) << 8;
+      sel[g] = sl[j];
+      owner[g] = own[j];
+      if (sl[j]) {
+        offsets[g] = off;
+        s_off[g] = off;
+        sel_list[run >> kUnitBits] = g;
+        if (spec_cur && sc[j] != off) {
+          // K3 fix-up: the speculative K1 store put this chunk elsewhere
+          const uint32_t q = atomicAdd(&s_nfix, 1u);
+          if (q < 256) s_fix[q] = g;
+        }
+      } else if (own[j] == ~0ull) {
+        offsets[g] = ~0ull;
+      }
+      if (spec_next) spec_next[g] = sl[j] ? off : ~0ull;
+    }
+    __syncthreads();  // s_warp / s_tot reused
+  }
+  if (t == 0) {
+    totals[0] = carry >> kUnitBits;
+    totals[1] = (carry & ((1ull << kUnitBits) - 1)) << 8;
+  }
+  // duplicates point at their owner's bytes
+#pragma unroll
+  for (int j = 0; j < kCtaItems; ++j) {
+    const uint32_t g = j * kCtaThreads + t;
+    if (g < n && !sl[j] && own[j] != ~0ull) offsets[g] = s_off[own[j]];
+  }
+  const uint32_t nfix = s_nfix;
+  if (spec_cur && nfix) {
+    if (nfix <= 256) {
+      for (uint32_t q = warp; q < nfix; q += kCtaThreads / 32) {
+        const uint32_t g = s_fix[q];
+        warp_copy(staging + s_off[g], chunk_ptr(arena, grid, g), lens[g], lane);
+      }
+    } else {
+      // many mispredictions (the layout changed): every selected chunk whose
+      // speculative offset differs, one warp per chunk
+      for (uint32_t g = warp; g < n; g += kCtaThreads / 32) {
+        if (__ldcg(sel + g) && __ldg(spec_cur + g) != s_off[g])
+          warp_copy(staging + s_off[g], chunk_ptr(arena, grid, g), lens[g], lane);
+      }
+    }
+  }
+}
+
 unsigned grid_for(uint64_t n, unsigned threads, unsigned cap) {
   uint64_t b = (n + threads - 1) / threads;
   if (b > cap) b = cap;
@@ -565,6 +734,22 @@ int launch_select(TableDev dedup, const uint64_t* slot, const uint32_t* lens, ui
 }
 
 bool select_small_ok(uint64_t n) { return n > 0 && n <= kSmallMax; }
+bool select_cta_ok(uint64_t n) { return n > 0 && n <= kCtaMax; }
+
+int launch_select_cta(TableDev known, bool use_known, const uint64_t* dig, const uint32_t* lens,
+                      uint64_t n, uint8_t* sel, uint64_t* owner, uint64_t* offsets,
+                      uint32_t* sel_list, uint64_t* totals, uint64_t* spec_next, cudaStream_t s,
+                      const uint64_t* spec_cur, const uint8_t* arena, const GridDev* grid,
+                      uint8_t* staging) {
+  static uint64_t attr = 0;
+  once_per_device(attr, [] {
+    cudaFuncSetAttribute(k_select_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCtaSmem));
+  });
+  launch_pdl(k_select_cta, 1, kCtaThreads, kCtaSmem, s, known, use_known ? 1 : 0, dig, lens,
+             uint32_t(n), sel, owner, offsets, sel_list, totals, spec_next, spec_cur, arena,
+             grid ? *grid : GridDev{}, staging);
+  return 1;
+}
 
 int launch_select_small(TableDev dedup, TableDev known, bool use_known, const uint64_t* dig,
                         const uint32_t* lens, uint64_t n, uint8_t* sel, uint64_t* owner,

@@ -49,7 +49,10 @@ __device__ __forceinline__ uint64_t table_find(TableDev t, unsigned long long k)
 __device__ __forceinline__ void k1_store_digest(const GridDev& g, uint64_t chunk, uint64_t d,
                                                 uint64_t* chunk_dig) {
   chunk_dig[chunk] = d;
-  if (g.expect != nullptr && g.expect[chunk] != d) atomicAdd(g.nbad, 1ull);
+  if (g.expect != nullptr && g.expect[chunk] != d) {
+    atomicAdd(g.nbad, 1ull);
+    if (g.bad_flag) *reinterpret_cast<volatile unsigned int*>(g.bad_flag) = 1u;
+  }
   if (g.xdig != nullptr)
     for (uint32_t q = 0; q < g.xn; ++q) g.xdig[q][g.xoff + chunk] = d;
 }

@@ -77,6 +77,12 @@ def test_verify_scatter_ragged(snap, geom):
         with pytest.raises(snap.SnapError) as e:
             c.restore(dev, tot, off, expect=d, verify=True)
         assert e.value.code == snap.SNAP_EFAULT
+        assert "1 chunk(s)" in str(e.value)
+        # the mismatch state is reset: the intact image verifies again, twice
+        img[:] = c.read_staging(0, tot)
+        c.write(arena // 2, img)
+        c.restore(dev, tot, off, expect=d, verify=True)
+        c.restore_self(verify=True)
 
 
 def test_grad_sum_bf16(snap, ctx):
