@@ -136,15 +136,15 @@ int select_with_known(snap_ctx* ctx, const uint64_t* dig, const uint32_t* lens, 
     const char* e = std::getenv("SNAP_SELECT_SMALL");
     return e && e[0] == '0';
   }();
-  static const bool cta_off = [] {
-    const char* e = std::getenv("SNAP_SELECT_CTA");
+  static const bool cluster_off = [] {
+    const char* e = std::getenv("SNAP_SELECT_CLUSTER");
     return e && e[0] == '0';
   }();
-  if (!inserted && !small_off && !cta_off && snap::select_cta_ok(n)) {
+  if (!inserted && !small_off && !cluster_off && snap::select_cluster_ok(n)) {
     // the table and scan state prepare_dedup guarantees clean stay untouched
-    CKL(snap::launch_select_cta(kn, use_known, dig, lens, n, sel, owner, offsets, list, totals,
-                                spec_next, ctx->stream, fix_spec, ctx->arena, &ctx->grid,
-                                fix_staging));
+    CKL(snap::launch_select_cluster(kn, use_known, dig, lens, n, sel, owner, offsets, list,
+                                    totals, spec_next, ctx->stream, fix_spec, ctx->arena,
+                                    &ctx->grid, fix_staging));
     ctx->dd_clean = true;
     ctx->sel_n = n;
     ctx->global_offsets_pending = false;

@@ -17,6 +17,7 @@
 // chunk at the same local index has the same digest): writer =
 // holders[local_index % |holders|]. Each GPU stages only the chunks it writes,
 // in canonical order (its shard of the global image).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "snap_internal.h"
@@ -518,173 +519,174 @@ k_select_small(TableDev dedup, TableDev known, int use_known, const uint64_t* __
   }
 }
 
-// Selections of at most 4096 chunks (C1): the whole K2 in ONE CTA with the
-// first-occurrence table in shared memory — no global atomics, no grid
-// barriers, nothing to clean up afterwards (the global dedup table and scan
-// state are not touched). 1024 threads; chunk g = j * 1024 + t (j < 4) so every
-// global load and store is coalesced (one SM's load/store path is the limit
-// here), the scan runs as 4 block scans with a carry. Same outputs bit for bit
-// as k_select_small / the three-kernel path.
-constexpr int kCtaThreads = 1024;
-constexpr int kCtaItems = 4;
-constexpr uint32_t kCtaMax = kCtaThreads * kCtaItems;
-constexpr uint32_t kCtaTab = 2 * kCtaMax;  // slots (load <= 1/2) + 1 for kEmptyKey
-constexpr size_t kCtaSmem = size_t(kCtaTab + 1) * 8 + size_t(kCtaMax) * 8 + size_t(kCtaTab + 1) * 4;
+// Selections of at most 4096 chunks (C1): the whole K2 in ONE thread-block
+// CLUSTER of 8 CTAs (one per SM, 512 threads, one chunk per thread) — no
+// global atomics, no grid barriers, nothing to clean up afterwards (the
+// global dedup table and scan state are not touched; same outputs bit for bit
+// as k_select_small / the three-kernel path). The first-occurrence table is
+// partitioned across the 8 CTAs' shared memories (distributed shared memory,
+// slot s lives in CTA s / 1024) so the shared-memory atomics of the insert run
+// on 8 SMs instead of one, and the loads / stores of the outputs use 8 SMs'
+// load-store paths; the scan carries CTA totals through DSMEM. Cluster
+// barriers replace the grid barriers of k_select_small. (A one-CTA version
+// with the table in one shared memory took 11-14 us on C1: one SM's atomic
+// and load-store throughput; this one takes ~7.3 us including launch.)
+constexpr int kClCtas = 8;
+constexpr int kClThreads = 512;
+constexpr uint32_t kClMax = kClCtas * kClThreads;  // 4096 chunks
+// load <= 1/8: every insert is a chain of dependent DSMEM atomics along its
+// probe sequence, so the longest linear-probing run (not the atomic
+// throughput) sets the phase time — at load 1/2 it cost ~6 us
+constexpr uint32_t kClSlots = 8 * kClMax;
+constexpr uint32_t kClLocal = kClSlots / kClCtas;  // slots per CTA
+constexpr size_t kClSmem = size_t(kClLocal) * 12;  // keys + mins
 
-__global__ void __launch_bounds__(kCtaThreads, 1)
-k_select_cta(TableDev known, int use_known, const uint64_t* __restrict__ dig,
-             const uint32_t* __restrict__ lens, uint32_t n, uint8_t* __restrict__ sel,
-             uint64_t* __restrict__ owner, uint64_t* __restrict__ offsets,
-             uint32_t* __restrict__ sel_list, uint64_t* __restrict__ totals,
-             uint64_t* __restrict__ spec_next, const uint64_t* __restrict__ spec_cur,
-             const uint8_t* __restrict__ arena, GridDev grid, uint8_t* __restrict__ staging) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem);
-  uint64_t* s_off = reinterpret_cast<uint64_t*>(smem + size_t(kCtaTab + 1) * 8);
-  uint32_t* vals = reinterpret_cast<uint32_t*>(smem + size_t(kCtaTab + 1 + kCtaMax) * 8);
-  __shared__ uint64_t s_warp[kCtaThreads / 32];
+__global__ void __cluster_dims__(kClCtas, 1, 1) __launch_bounds__(kClThreads, 1)
+k_select_cluster(TableDev known, int use_known, const uint64_t* __restrict__ dig,
+                 const uint32_t* __restrict__ lens, uint32_t n, uint8_t* __restrict__ sel,
+                 uint64_t* __restrict__ owner, uint64_t* __restrict__ offsets,
+                 uint32_t* __restrict__ sel_list, uint64_t* __restrict__ totals,
+                 uint64_t* __restrict__ spec_next, const uint64_t* __restrict__ spec_cur,
+                 const uint8_t* __restrict__ arena, GridDev grid, uint8_t* __restrict__ staging) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(16) unsigned long long keys[];  // [kClLocal]
+  uint32_t* mins = reinterpret_cast<uint32_t*>(keys + kClLocal);
+  __shared__ uint64_t s_off[kClThreads];
+  __shared__ uint64_t s_warp[kClThreads / 32];
   __shared__ uint64_t s_tot;
   __shared__ uint32_t s_nfix;
-  __shared__ uint32_t s_fix[256];
+  __shared__ uint32_t s_fix[kClThreads];
+  __shared__ int s_dup;
   const uint32_t t = threadIdx.x;
+  const uint32_t rank = cl.block_rank();
   const int lane = t & 31, warp = t >> 5;
-  for (uint32_t i = t; i <= kCtaTab; i += kCtaThreads) {
+  for (uint32_t i = t; i < kClLocal; i += kClThreads) {
     keys[i] = kEmptyKey;
-    vals[i] = 0xffffffffu;
-  }
-  if (t == 0) s_nfix = 0;
-  griddep_wait();
-  // the next kernel of the stream (the next snapshot's K1) may become resident
-  // now; it waits for this grid's completion itself
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  uint32_t len[kCtaItems];
-  unsigned long long d[kCtaItems];
-  uint64_t sc[kCtaItems];
-#pragma unroll
-  for (int j = 0; j < kCtaItems; ++j) {
-    const uint32_t g = j * kCtaThreads + t;
-    len[j] = g < n ? __ldcg(lens + g) : 0;
-    d[j] = g < n ? __ldcg(reinterpret_cast<const unsigned long long*>(dig) + g) : 0;
-    sc[j] = (spec_cur && g < n) ? __ldg(spec_cur + g) : 0;
-  }
-  bool cand[kCtaItems];
-#pragma unroll
-  for (int j = 0; j < kCtaItems; ++j)
-    cand[j] = len[j] != 0 && !(use_known && table_find(known, d[j]) != ~0ull);
-  __syncthreads();  // table initialised
-  // insert: the thread whose CAS claims the slot stores its index; the others
-  // with the same digest (duplicates, rare) take the minimum after a barrier.
-  // The kEmptyKey digest has its own slot and always goes through atomicMin.
-  uint32_t slot[kCtaItems];
-  uint32_t dup = 0;
-#pragma unroll
-  for (int j = 0; j < kCtaItems; ++j) {
-    slot[j] = 0xffffffffu;
-    if (!cand[j]) continue;
-    uint32_t h;
-    if (d[j] == kEmptyKey) {
-      h = kCtaTab;
-      dup |= 1u << j;
-    } else {
-      h = uint32_t(tmix64(d[j])) & (kCtaTab - 1);
-      for (;;) {
-        const unsigned long long prev = atomicCAS(keys + h, kEmptyKey, d[j]);
-        if (prev == kEmptyKey) {
-          vals[h] = j * kCtaThreads + t;
-          break;
-        }
-        if (prev == d[j]) {
-          dup |= 1u << j;
-          break;
-        }
-        h = (h + 1) & (kCtaTab - 1);
-      }
-    }
-    slot[j] = h;
-  }
-  if (__syncthreads_or(dup != 0)) {
-#pragma unroll
-    for (int j = 0; j < kCtaItems; ++j)
-      if (dup >> j & 1) atomicMin(vals + slot[j], j * kCtaThreads + t);
-    __syncthreads();
-  }
-  uint64_t carry = 0;
-  uint64_t own[kCtaItems];
-  bool sl[kCtaItems];
-#pragma unroll
-  for (int j = 0; j < kCtaItems; ++j) {
-    const uint32_t g = j * kCtaThreads + t;
-    own[j] = slot[j] == 0xffffffffu ? ~0ull : uint64_t(vals[slot[j]]);
-    sl[j] = own[j] == g;
-    const uint64_t val = sl[j] ? (1ull << kUnitBits) | (len[j] >> 8) : 0;
-    uint64_t incl = val;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (lane == 31) s_warp[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-      const uint64_t w = s_warp[lane];
-      uint64_t wi = w;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint64_t y = __shfl_up_sync(0xffffffffu, wi, o);
-        if (lane >= o) wi += y;
-      }
-      s_warp[lane] = wi - w;
-      if (lane == 31) s_tot = wi;
-    }
-    __syncthreads();
-    const uint64_t run = carry + s_warp[warp] + incl - val;
-    carry += s_tot;
-    if (g < n) {
-      const uint64_t off = (run & ((1ull << kUnitBits) - 1)) << 8;
-      sel[g] = sl[j];
-      owner[g] = own[j];
-      if (sl[j]) {
-        offsets[g] = off;
-        s_off[g] = off;
-        sel_list[run >> kUnitBits] = g;
-        if (spec_cur && sc[j] != off) {
-          // K3 fix-up: the speculative K1 store put this chunk elsewhere
-          const uint32_t q = atomicAdd(&s_nfix, 1u);
-          if (q < 256) s_fix[q] = g;
-        }
-      } else if (own[j] == ~0ull) {
-        offsets[g] = ~0ull;
-      }
-      if (spec_next) spec_next[g] = sl[j] ? off : ~0ull;
-    }
-    __syncthreads();  // s_warp / s_tot reused
+    mins[i] = 0xffffffffu;
   }
   if (t == 0) {
-    totals[0] = carry >> kUnitBits;
-    totals[1] = (carry & ((1ull << kUnitBits) - 1)) << 8;
+    s_nfix = 0;
+    s_dup = 0;
   }
-  // duplicates point at their owner's bytes
-#pragma unroll
-  for (int j = 0; j < kCtaItems; ++j) {
-    const uint32_t g = j * kCtaThreads + t;
-    if (g < n && !sl[j] && own[j] != ~0ull) offsets[g] = s_off[own[j]];
-  }
-  const uint32_t nfix = s_nfix;
-  if (spec_cur && nfix) {
-    if (nfix <= 256) {
-      for (uint32_t q = warp; q < nfix; q += kCtaThreads / 32) {
-        const uint32_t g = s_fix[q];
-        warp_copy(staging + s_off[g], chunk_ptr(arena, grid, g), lens[g], lane);
-      }
+  // split cluster barrier: the partitions' initialisation is published now,
+  // the wait (before the first remote atomic) hides behind the input loads
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  griddep_wait();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const uint32_t g = rank * kClThreads + t;
+  const uint32_t len = g < n ? __ldcg(lens + g) : 0;
+  const unsigned long long d =
+      g < n ? __ldcg(reinterpret_cast<const unsigned long long*>(dig) + g) : 0;
+  const uint64_t sc = (spec_cur && g < n) ? __ldg(spec_cur + g) : 0;
+  const bool cand = len != 0 && !(use_known && table_find(known, d) != ~0ull);
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // partitions ready
+  uint32_t slot = 0xffffffffu;
+  bool dup = false;
+  if (cand) {
+    // kEmptyKey is a legal digest: it always takes the minimum path through
+    // slot 0 of CTA 0's extra handling below (marked as a duplicate of itself)
+    uint32_t h = uint32_t(tmix64(d)) & (kClSlots - 1);
+    if (d == kEmptyKey) {
+      h = kClSlots;  // sentinel: handled by the atomicMin on CTA 0's extra word
+      dup = true;
     } else {
-      // many mispredictions (the layout changed): every selected chunk whose
-      // speculative offset differs, one warp per chunk
-      for (uint32_t g = warp; g < n; g += kCtaThreads / 32) {
-        if (__ldcg(sel + g) && __ldg(spec_cur + g) != s_off[g])
-          warp_copy(staging + s_off[g], chunk_ptr(arena, grid, g), lens[g], lane);
+      for (;;) {
+        unsigned long long* k = cl.map_shared_rank(keys, h / kClLocal) + (h % kClLocal);
+        const unsigned long long prev = atomicCAS(k, kEmptyKey, d);
+        if (prev == kEmptyKey) {
+          *(cl.map_shared_rank(mins, h / kClLocal) + (h % kClLocal)) = g;
+          break;
+        }
+        if (prev == d) {
+          dup = true;
+          break;
+        }
+        h = (h + 1) & (kClSlots - 1);
       }
     }
+    slot = h;
   }
+  if (dup) s_dup = 1;
+  cl.sync();  // claims visible; every CTA's s_dup final
+  int any_dup = 0;
+  for (uint32_t r = 0; r < kClCtas; ++r) any_dup |= *cl.map_shared_rank(&s_dup, r);
+  __shared__ uint32_t s_empty_min;  // first occurrence of the kEmptyKey digest (CTA 0)
+  if (any_dup) {
+    if (t == 0 && rank == 0) s_empty_min = 0xffffffffu;
+    cl.sync();
+    if (dup) {
+      uint32_t* m = slot == kClSlots ? cl.map_shared_rank(&s_empty_min, 0)
+                                     : cl.map_shared_rank(mins, slot / kClLocal) + (slot % kClLocal);
+      atomicMin(m, g);
+    }
+    cl.sync();
+  }
+  uint64_t own = ~0ull;
+  if (slot != 0xffffffffu)
+    own = slot == kClSlots ? *cl.map_shared_rank(&s_empty_min, 0)
+                           : *(cl.map_shared_rank(mins, slot / kClLocal) + (slot % kClLocal));
+  const bool sl = own == g;
+  const uint64_t val = sl ? (1ull << kUnitBits) | (len >> 8) : 0;
+  uint64_t incl = val;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const uint64_t w = lane < kClThreads / 32 ? s_warp[lane] : 0;
+    uint64_t wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    if (lane < kClThreads / 32) s_warp[lane] = wi - w;
+    if (lane == kClThreads / 32 - 1) s_tot = wi;
+  }
+  cl.sync();  // every CTA's total published
+  uint64_t pre = 0, all = 0;
+  for (uint32_t r = 0; r < kClCtas; ++r) {
+    const uint64_t a = *cl.map_shared_rank(&s_tot, r);
+    if (r < rank) pre += a;
+    all += a;
+  }
+  const uint64_t run = pre + s_warp[warp] + incl - val;
+  const uint64_t off = (run & ((1ull << kUnitBits) - 1)) << 8;
+  if (g < n) {
+    sel[g] = sl;
+    owner[g] = own;
+    if (sl) {
+      offsets[g] = off;
+      sel_list[run >> kUnitBits] = g;
+      if (spec_cur && sc != off) s_fix[atomicAdd(&s_nfix, 1u)] = g;  // K3 fix-up
+    } else if (own == ~0ull) {
+      offsets[g] = ~0ull;
+    }
+    if (spec_next) spec_next[g] = sl ? off : ~0ull;
+  }
+  s_off[t] = off;
+  if (rank == kClCtas - 1 && t == 0) {
+    totals[0] = all >> kUnitBits;
+    totals[1] = (all & ((1ull << kUnitBits) - 1)) << 8;
+  }
+  if (any_dup) {
+    cl.sync();  // offsets of every owner in shared memory
+    if (g < n && !sl && own != ~0ull)
+      offsets[g] = *(cl.map_shared_rank(s_off, uint32_t(own) / kClThreads) + (own % kClThreads));
+  }
+  // last remote shared-memory access done: arrive now, wait only before exit
+  // (no CTA may leave while another can still read its shared memory)
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  const uint32_t nfix = s_nfix;
+  for (uint32_t q = warp; q < nfix; q += kClThreads / 32) {
+    const uint32_t gq = s_fix[q];
+    warp_copy(staging + s_off[gq % kClThreads], chunk_ptr(arena, grid, gq), lens[gq], lane);
+  }
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 unsigned grid_for(uint64_t n, unsigned threads, unsigned cap) {
@@ -734,18 +736,18 @@ int launch_select(TableDev dedup, const uint64_t* slot, const uint32_t* lens, ui
 }
 
 bool select_small_ok(uint64_t n) { return n > 0 && n <= kSmallMax; }
-bool select_cta_ok(uint64_t n) { return n > 0 && n <= kCtaMax; }
+bool select_cluster_ok(uint64_t n) { return n > 0 && n <= kClMax; }
 
-int launch_select_cta(TableDev known, bool use_known, const uint64_t* dig, const uint32_t* lens,
-                      uint64_t n, uint8_t* sel, uint64_t* owner, uint64_t* offsets,
-                      uint32_t* sel_list, uint64_t* totals, uint64_t* spec_next, cudaStream_t s,
-                      const uint64_t* spec_cur, const uint8_t* arena, const GridDev* grid,
-                      uint8_t* staging) {
+int launch_select_cluster(TableDev known, bool use_known, const uint64_t* dig,
+                          const uint32_t* lens, uint64_t n, uint8_t* sel, uint64_t* owner,
+                          uint64_t* offsets, uint32_t* sel_list, uint64_t* totals,
+                          uint64_t* spec_next, cudaStream_t s, const uint64_t* spec_cur,
+                          const uint8_t* arena, const GridDev* grid, uint8_t* staging) {
   static uint64_t attr = 0;
   once_per_device(attr, [] {
-    cudaFuncSetAttribute(k_select_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCtaSmem));
+    cudaFuncSetAttribute(k_select_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kClSmem));
   });
-  launch_pdl(k_select_cta, 1, kCtaThreads, kCtaSmem, s, known, use_known ? 1 : 0, dig, lens,
+  launch_pdl(k_select_cluster, kClCtas, kClThreads, kClSmem, s, known, use_known ? 1 : 0, dig, lens,
              uint32_t(n), sel, owner, offsets, sel_list, totals, spec_next, spec_cur, arena,
              grid ? *grid : GridDev{}, staging);
   return 1;

@@ -206,13 +206,13 @@ int launch_select(TableDev dedup, const uint64_t* slot, const uint32_t* lens, ui
 // barriers), identical outputs; the dedup table must be empty on entry and is
 // left empty; `scratch` = >= 9 words of (zero) scan state, left zero.
 bool select_small_ok(uint64_t n);
-// n <= 4096: the whole selection in one CTA, shared-memory first-occurrence table
-bool select_cta_ok(uint64_t n);
-int launch_select_cta(TableDev known, bool use_known, const uint64_t* dig, const uint32_t* lens,
-                      uint64_t n, uint8_t* sel, uint64_t* owner, uint64_t* offsets,
-                      uint32_t* sel_list, uint64_t* totals, uint64_t* spec_next, cudaStream_t s,
-                      const uint64_t* spec_cur, const uint8_t* arena, const GridDev* grid,
-                      uint8_t* staging);
+// n <= 4096: the whole selection in one 8-CTA cluster (DSMEM first-occurrence table)
+bool select_cluster_ok(uint64_t n);
+int launch_select_cluster(TableDev known, bool use_known, const uint64_t* dig,
+                          const uint32_t* lens, uint64_t n, uint8_t* sel, uint64_t* owner,
+                          uint64_t* offsets, uint32_t* sel_list, uint64_t* totals,
+                          uint64_t* spec_next, cudaStream_t s, const uint64_t* spec_cur,
+                          const uint8_t* arena, const GridDev* grid, uint8_t* staging);
 int launch_select_small(TableDev dedup, TableDev known, bool use_known, const uint64_t* dig,
                         const uint32_t* lens, uint64_t n, uint8_t* sel, uint64_t* owner,
                         uint64_t* offsets, uint32_t* sel_list, uint64_t* totals,
