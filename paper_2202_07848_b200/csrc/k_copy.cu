@@ -251,6 +251,24 @@ k_copy_ranges(uint8_t* const* __restrict__ dst, const uint8_t* const* __restrict
 // the same address range equals the incoming rank's recorded digest;
 // otherwise its bytes come from the device chunk cache by digest. A digest
 // missing from the cache is counted (content lost -> SimFault on the host).
+// End of a splice switch: the swap-in counters and the selection totals go
+// to mapped pinned host memory in one tiny launch (no device memset, no
+// pageable read-backs), and the counters are re-armed for the next switch.
+__global__ void k_splice_report(unsigned long long* counters, const uint64_t* totals,
+                                unsigned long long* host) {
+  griddep_wait();
+  if (threadIdx.x == 0) {
+    volatile unsigned long long* h = host;
+    for (int i = 0; i < 3; ++i) {
+      h[i] = counters[i];
+      counters[i] = 0;
+    }
+    h[3] = totals ? totals[0] : 0;
+    h[4] = totals ? totals[1] : 0;
+    __threadfence_system();
+  }
+}
+
 __global__ void __launch_bounds__(kThreads)
 k_splice_in(uint8_t* __restrict__ arena, GridDev to, const uint32_t* __restrict__ lens,
             const uint64_t* __restrict__ want, const int64_t* __restrict__ match,
@@ -389,12 +407,18 @@ int launch_splice_in(uint8_t* arena, const GridDev& to, const uint32_t* lens, co
                      const int64_t* match, const uint64_t* dig_from, TableDev cache,
                      const uint8_t* cache_base, uint32_t slot_shift, unsigned long long* counters,
                      cudaStream_t s) {
-  cudaMemsetAsync(counters, 0, 3 * sizeof(unsigned long long), s);
+  // counters are zero on entry (zeroed at init, re-armed by k_splice_report)
   if (to.nchunks == 0) return 0;
   uint64_t blocks = (to.nchunks * 4 + kThreads - 1) / kThreads;  // 8 chunks per warp step
   if (blocks > copy_grid()) blocks = copy_grid();
   launch_pdl(k_splice_in, unsigned(blocks), kThreads, 0, s, arena, to, lens, want, match, dig_from,
              cache, cache_base, slot_shift, counters);
+  return 1;
+}
+
+int launch_splice_report(unsigned long long* counters, const uint64_t* totals,
+                         unsigned long long* host, cudaStream_t s) {
+  launch_pdl(k_splice_report, 1, 32, 0, s, counters, totals, host);
   return 1;
 }
 

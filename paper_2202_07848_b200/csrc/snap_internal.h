@@ -291,6 +291,10 @@ int launch_cache_assign(TableDev cache, const uint64_t* dig, const uint32_t* sel
 int launch_cache_gc(TableDev old, TableDev live, TableDev fresh, uint32_t* free_stack,
                     uint64_t free_n, const uint32_t* slot_len, unsigned long long* cnt,
                     cudaStream_t s);
+// copies counters[0..2] (re-arming them to zero) and totals[0..1] (or zeros) to
+// the mapped host words host[0..4]
+int launch_splice_report(unsigned long long* counters, const uint64_t* totals,
+                         unsigned long long* host, cudaStream_t s);
 int launch_splice_in(uint8_t* arena, const GridDev& to, const uint32_t* lens, const uint64_t* want,
                      const int64_t* match, const uint64_t* dig_from, TableDev cache,
                      const uint8_t* cache_base, uint32_t slot_shift, unsigned long long* counters,

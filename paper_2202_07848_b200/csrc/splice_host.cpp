@@ -55,6 +55,11 @@ struct SpliceState {
   uint64_t gc_runs = 0, gc_freed_bytes = 0;
   DevMem cache, ck, cv, ck2, cv2, lk, lv, free_stack, slot_len, list_off, counters, seed_off;
   DevMem inst_ptrs;  // device arrays of the install copies
+  // swap-in counters (zero between switches) and their mapped host report:
+  // [swap-in bytes, resident bytes, lost, selected chunks, selected bytes]
+  DevMem sin_cnt;
+  unsigned long long* h_rep = nullptr;
+  unsigned long long* d_rep = nullptr;
   uint64_t cmask = 0, lmask = 0;
   std::map<int, RankGrid> ranks;
   std::map<std::pair<int, int>, DevMem> match;
@@ -71,8 +76,10 @@ void splice_release(snap_ctx* ctx) {
       release(*m);
   for (auto& [k, m] : S->match) release(m);
   for (DevMem* m : {&S->cache, &S->ck, &S->cv, &S->ck2, &S->cv2, &S->lk, &S->lv, &S->free_stack,
-                    &S->slot_len, &S->list_off, &S->counters, &S->seed_off, &S->inst_ptrs})
+                    &S->slot_len, &S->list_off, &S->counters, &S->seed_off, &S->inst_ptrs,
+                    &S->sin_cnt})
     release(*m);
+  if (S->h_rep) cudaFreeHost(S->h_rep);
   delete S;
   ctx->splice = nullptr;
 }
@@ -210,6 +217,15 @@ int snap_splice_init_slots(snap_ctx* ctx, uint64_t cache_bytes, uint32_t slot_by
   RC(ensure(ctx, S->ck, tcap + 1, &k));
   RC(ensure(ctx, S->cv, tcap + 1, &v));
   RC(ensure(ctx, S->counters, 4, &cnt));
+  unsigned long long* sin;
+  RC(ensure(ctx, S->sin_cnt, 4, &sin));
+  CK(cudaMemsetAsync(sin, 0, 32, ctx->stream));
+  {
+    void* hp = nullptr;
+    CK(cudaHostAlloc(&hp, 64, cudaHostAllocMapped | cudaHostAllocPortable));
+    S->h_rep = static_cast<unsigned long long*>(hp);
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&S->d_rep), hp, 0));
+  }
   S->cmask = tcap - 1;
   CKL(snap::launch_table_clear(TableDev{k, v, S->cmask}, ctx->stream));
   // the reclamation's second index, allocated now: no cudaMalloc inside a switch
@@ -332,7 +348,6 @@ int snap_splice_switch(snap_ctx* ctx, int from, int to, snap_switch_stats* st) {
                  nullptr, nullptr));
     out.hashed_bytes = F->bytes;
   }
-  unsigned long long cnt[3] = {0, 0, 0};
   if (T && T->recorded) {
     const int64_t* match = nullptr;
     if (F) {
@@ -355,12 +370,14 @@ int snap_splice_switch(snap_ctx* ctx, int from, int to, snap_switch_stats* st) {
     CKL(snap::launch_splice_in(ctx->arena, T->grid, P<uint32_t>(T->d_lens), P<uint64_t>(T->d_rec),
                                match, F ? P<uint64_t>(F->d_rec) : nullptr, cache_index(S),
                                P<uint8_t>(S->cache), S->slot_shift,
-                               P<unsigned long long>(S->counters), ctx->stream));
-    CK(cudaMemcpyAsync(cnt, S->counters.p, 24, cudaMemcpyDeviceToHost, ctx->stream));
+                               P<unsigned long long>(S->sin_cnt), ctx->stream));
   }
-  uint64_t tot[2] = {0, 0};
-  if (F) CK(cudaMemcpyAsync(tot, ctx->totals.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
+  CKL(snap::launch_splice_report(P<unsigned long long>(S->sin_cnt),
+                                 F ? P<uint64_t>(ctx->totals) : nullptr, S->d_rep, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  const volatile unsigned long long* rep = S->h_rep;
+  const unsigned long long cnt[3] = {rep[0], rep[1], rep[2]};
+  const uint64_t tot[2] = {rep[3], rep[4]};
   S->free_n -= tot[0];
   S->live_bytes += tot[1];
   S->entries += tot[0];
