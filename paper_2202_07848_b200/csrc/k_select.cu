@@ -22,6 +22,7 @@
 
 #include "snap_internal.h"
 #include <algorithm>
+#include <cstdlib>
 
 #include "table.cuh"
 
@@ -519,172 +520,214 @@ k_select_small(TableDev dedup, TableDev known, int use_known, const uint64_t* __
   }
 }
 
-// Selections of at most 4096 chunks (C1): the whole K2 in ONE thread-block
-// CLUSTER of 8 CTAs (one per SM, 512 threads, one chunk per thread) — no
-// global atomics, no grid barriers, nothing to clean up afterwards (the
-// global dedup table and scan state are not touched; same outputs bit for bit
-// as k_select_small / the three-kernel path). The first-occurrence table is
-// partitioned across the 8 CTAs' shared memories (distributed shared memory,
-// slot s lives in CTA s / 1024) so the shared-memory atomics of the insert run
-// on 8 SMs instead of one, and the loads / stores of the outputs use 8 SMs'
-// load-store paths; the scan carries CTA totals through DSMEM. Cluster
-// barriers replace the grid barriers of k_select_small. (A one-CTA version
-// with the table in one shared memory took 11-14 us on C1: one SM's atomic
-// and load-store throughput; this one takes ~7.3 us including launch.)
-constexpr int kClCtas = 8;
-constexpr int kClThreads = 512;
-constexpr uint32_t kClMax = kClCtas * kClThreads;  // 4096 chunks
-// load <= 1/8: every insert is a chain of dependent DSMEM atomics along its
-// probe sequence, so the longest linear-probing run (not the atomic
-// throughput) sets the phase time — at load 1/2 it cost ~6 us
-constexpr uint32_t kClSlots = 8 * kClMax;
-constexpr uint32_t kClLocal = kClSlots / kClCtas;  // slots per CTA
-constexpr size_t kClSmem = size_t(kClLocal) * 12;  // keys + mins
+// Selections of up to 4096 chunks (C1): the whole K2 in ONE thread-block
+// CLUSTER (one CTA per SM) — no global
+// atomics, no grid barriers, nothing to clean up afterwards (the global dedup
+// table and scan state are not touched; same outputs bit for bit as
+// k_select_small / the three-kernel path). The first-occurrence table is
+// partitioned across the CTAs' shared memories (distributed shared memory:
+// slot s lives in CTA s / LOCAL), so the inserts' shared-memory atomics and
+// the outputs' loads / stores spread over CTAS SMs; the scan carries CTA
+// totals through DSMEM, and cluster barriers replace grid barriers. Table load
+// <= 1/4: an insert is a chain of dependent DSMEM atomics along its probe
+// sequence, so the longest linear-probing run, not the atomic throughput, sets
+// the phase time (at load 1/2 the 4096-chunk insert took ~6 us, at 1/8 ~1 us).
+// Chunk g = rank * THREADS * ITEMS + j * THREADS + t: coalesced. (A one-CTA
+// version with the table in one shared memory took 11-14 us on C1 — one SM's
+// atomic and load-store throughput — against ~7.3 us for 8 CTAs.)
+template <int CTAS, int THREADS, int ITEMS, uint32_t LOCAL>
+struct ClCfg {
+  static constexpr uint32_t kPer = uint32_t(THREADS) * ITEMS;  // chunks per CTA
+  static constexpr uint32_t kMax = uint32_t(CTAS) * kPer;
+  static constexpr uint32_t kSlots = uint32_t(CTAS) * LOCAL;
+  static constexpr size_t kSmem = size_t(LOCAL) * 12 + size_t(kPer) * 4;  // keys, mins, fix list
+  static_assert((kSlots & (kSlots - 1)) == 0 && kSlots >= 4 * kMax, "table load <= 1/4");
+};
+// n <= 4096, load 1/8. (Measured and dropped: 16 CTAs x 1024 threads x 4
+// chunks at load 1/4 for n <= 65536 — 26.7 us on C3's 64970 chunks and 30 us
+// on a C2 rank's 32960 against 12 / 22.5 us for the three-kernel path: four
+// dependent probe chains per thread in sequence.)
+using ClSmall = ClCfg<8, 512, 1, 4096>;
 
-__global__ void __cluster_dims__(kClCtas, 1, 1) __launch_bounds__(kClThreads, 1)
+template <int CTAS, int THREADS, int ITEMS, uint32_t LOCAL>
+__global__ void __launch_bounds__(THREADS, 1)
 k_select_cluster(TableDev known, int use_known, const uint64_t* __restrict__ dig,
                  const uint32_t* __restrict__ lens, uint32_t n, uint8_t* __restrict__ sel,
                  uint64_t* __restrict__ owner, uint64_t* __restrict__ offsets,
                  uint32_t* __restrict__ sel_list, uint64_t* __restrict__ totals,
                  uint64_t* __restrict__ spec_next, const uint64_t* __restrict__ spec_cur,
                  const uint8_t* __restrict__ arena, GridDev grid, uint8_t* __restrict__ staging) {
+  using C = ClCfg<CTAS, THREADS, ITEMS, LOCAL>;
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
-  extern __shared__ __align__(16) unsigned long long keys[];  // [kClLocal]
-  uint32_t* mins = reinterpret_cast<uint32_t*>(keys + kClLocal);
-  __shared__ uint64_t s_off[kClThreads];
-  __shared__ uint64_t s_warp[kClThreads / 32];
+  extern __shared__ __align__(16) unsigned long long keys[];  // [LOCAL]
+  uint32_t* mins = reinterpret_cast<uint32_t*>(keys + LOCAL);
+  uint32_t* s_fix = mins + LOCAL;                             // [kPer]
+  __shared__ uint64_t s_warp[THREADS / 32];
   __shared__ uint64_t s_tot;
   __shared__ uint32_t s_nfix;
-  __shared__ uint32_t s_fix[kClThreads];
+  __shared__ uint32_t s_empty_min;  // first occurrence of the kEmptyKey digest (CTA 0)
   __shared__ int s_dup;
   const uint32_t t = threadIdx.x;
   const uint32_t rank = cl.block_rank();
   const int lane = t & 31, warp = t >> 5;
-  for (uint32_t i = t; i < kClLocal; i += kClThreads) {
+  for (uint32_t i = t; i < LOCAL; i += THREADS) {
     keys[i] = kEmptyKey;
     mins[i] = 0xffffffffu;
   }
   if (t == 0) {
     s_nfix = 0;
     s_dup = 0;
+    s_empty_min = 0xffffffffu;
   }
   // split cluster barrier: the partitions' initialisation is published now,
   // the wait (before the first remote atomic) hides behind the input loads
   asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   griddep_wait();
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  const uint32_t g = rank * kClThreads + t;
-  const uint32_t len = g < n ? __ldcg(lens + g) : 0;
-  const unsigned long long d =
-      g < n ? __ldcg(reinterpret_cast<const unsigned long long*>(dig) + g) : 0;
-  const uint64_t sc = (spec_cur && g < n) ? __ldg(spec_cur + g) : 0;
-  const bool cand = len != 0 && !(use_known && table_find(known, d) != ~0ull);
+  uint32_t len[ITEMS];
+  unsigned long long d[ITEMS];
+  uint64_t sc[ITEMS];
+  bool cand[ITEMS];
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    const uint32_t g = rank * C::kPer + j * THREADS + t;
+    len[j] = g < n ? __ldcg(lens + g) : 0;
+    d[j] = g < n ? __ldcg(reinterpret_cast<const unsigned long long*>(dig) + g) : 0;
+    sc[j] = (spec_cur && g < n) ? __ldg(spec_cur + g) : 0;
+  }
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j)
+    cand[j] = len[j] != 0 && !(use_known && table_find(known, d[j]) != ~0ull);
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // partitions ready
-  uint32_t slot = 0xffffffffu;
-  bool dup = false;
-  if (cand) {
-    // kEmptyKey is a legal digest: it always takes the minimum path through
-    // slot 0 of CTA 0's extra handling below (marked as a duplicate of itself)
-    uint32_t h = uint32_t(tmix64(d)) & (kClSlots - 1);
-    if (d == kEmptyKey) {
-      h = kClSlots;  // sentinel: handled by the atomicMin on CTA 0's extra word
-      dup = true;
-    } else {
-      for (;;) {
-        unsigned long long* k = cl.map_shared_rank(keys, h / kClLocal) + (h % kClLocal);
-        const unsigned long long prev = atomicCAS(k, kEmptyKey, d);
-        if (prev == kEmptyKey) {
-          *(cl.map_shared_rank(mins, h / kClLocal) + (h % kClLocal)) = g;
-          break;
-        }
-        if (prev == d) {
-          dup = true;
-          break;
-        }
-        h = (h + 1) & (kClSlots - 1);
-      }
+  // insert: a CAS claims a free slot (the claimer stores its index), an equal
+  // key makes the chunk a duplicate (rare), resolved by atomicMin below
+  uint32_t slot[ITEMS];
+  uint32_t dup = 0;
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    slot[j] = 0xffffffffu;
+    if (!cand[j]) continue;
+    const uint32_t g = rank * C::kPer + j * THREADS + t;
+    if (d[j] == kEmptyKey) {  // a legal digest: its own word in CTA 0
+      slot[j] = C::kSlots;
+      dup |= 1u << j;
+      continue;
     }
-    slot = h;
+    uint32_t h = uint32_t(tmix64(d[j])) & (C::kSlots - 1);
+    for (;;) {
+      unsigned long long* k = cl.map_shared_rank(keys, h / LOCAL) + (h % LOCAL);
+      const unsigned long long prev = atomicCAS(k, kEmptyKey, d[j]);
+      if (prev == kEmptyKey) {
+        *(cl.map_shared_rank(mins, h / LOCAL) + (h % LOCAL)) = g;
+        break;
+      }
+      if (prev == d[j]) {
+        dup |= 1u << j;
+        break;
+      }
+      h = (h + 1) & (C::kSlots - 1);
+    }
+    slot[j] = h;
   }
   if (dup) s_dup = 1;
   cl.sync();  // claims visible; every CTA's s_dup final
   int any_dup = 0;
-  for (uint32_t r = 0; r < kClCtas; ++r) any_dup |= *cl.map_shared_rank(&s_dup, r);
-  __shared__ uint32_t s_empty_min;  // first occurrence of the kEmptyKey digest (CTA 0)
+  for (uint32_t r = 0; r < CTAS; ++r) any_dup |= *cl.map_shared_rank(&s_dup, r);
   if (any_dup) {
-    if (t == 0 && rank == 0) s_empty_min = 0xffffffffu;
-    cl.sync();
-    if (dup) {
-      uint32_t* m = slot == kClSlots ? cl.map_shared_rank(&s_empty_min, 0)
-                                     : cl.map_shared_rank(mins, slot / kClLocal) + (slot % kClLocal);
-      atomicMin(m, g);
-    }
-    cl.sync();
-  }
-  uint64_t own = ~0ull;
-  if (slot != 0xffffffffu)
-    own = slot == kClSlots ? *cl.map_shared_rank(&s_empty_min, 0)
-                           : *(cl.map_shared_rank(mins, slot / kClLocal) + (slot % kClLocal));
-  const bool sl = own == g;
-  const uint64_t val = sl ? (1ull << kUnitBits) | (len >> 8) : 0;
-  uint64_t incl = val;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
+    for (int j = 0; j < ITEMS; ++j)
+      if (dup >> j & 1) {
+        const uint32_t g = rank * C::kPer + j * THREADS + t;
+        uint32_t* m = slot[j] == C::kSlots
+                          ? cl.map_shared_rank(&s_empty_min, 0)
+                          : cl.map_shared_rank(mins, slot[j] / LOCAL) + (slot[j] % LOCAL);
+        atomicMin(m, g);
+      }
+    cl.sync();
   }
-  if (lane == 31) s_warp[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    const uint64_t w = lane < kClThreads / 32 ? s_warp[lane] : 0;
-    uint64_t wi = w;
+  // owners, then the CTA-local scan (ITEMS block scans with a carry)
+  uint64_t own[ITEMS], run[ITEMS];
+  bool sl[ITEMS];
+  uint64_t carry = 0;
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    const uint32_t g = rank * C::kPer + j * THREADS + t;
+    own[j] = slot[j] == 0xffffffffu ? ~0ull
+             : slot[j] == C::kSlots
+                 ? uint64_t(*cl.map_shared_rank(&s_empty_min, 0))
+                 : uint64_t(*(cl.map_shared_rank(mins, slot[j] / LOCAL) + (slot[j] % LOCAL)));
+    sl[j] = own[j] == g;
+    const uint64_t val = sl[j] ? (1ull << kUnitBits) | (len[j] >> 8) : 0;
+    uint64_t incl = val;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const uint64_t y = __shfl_up_sync(0xffffffffu, wi, o);
-      if (lane >= o) wi += y;
+      const uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
     }
-    if (lane < kClThreads / 32) s_warp[lane] = wi - w;
-    if (lane == kClThreads / 32 - 1) s_tot = wi;
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const uint64_t w = lane < THREADS / 32 ? s_warp[lane] : 0;
+      uint64_t wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += y;
+      }
+      if (lane < THREADS / 32) s_warp[lane] = wi - w;
+      if (lane == THREADS / 32 - 1) s_tot = wi;
+    }
+    __syncthreads();
+    run[j] = carry + s_warp[warp] + incl - val;
+    carry += s_tot;
+    __syncthreads();  // s_warp / s_tot reused
   }
+  if (t == 0) s_tot = carry;
   cl.sync();  // every CTA's total published
   uint64_t pre = 0, all = 0;
-  for (uint32_t r = 0; r < kClCtas; ++r) {
+  for (uint32_t r = 0; r < CTAS; ++r) {
     const uint64_t a = *cl.map_shared_rank(&s_tot, r);
     if (r < rank) pre += a;
     all += a;
   }
-  const uint64_t run = pre + s_warp[warp] + incl - val;
-  const uint64_t off = (run & ((1ull << kUnitBits) - 1)) << 8;
-  if (g < n) {
-    sel[g] = sl;
-    owner[g] = own;
-    if (sl) {
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    const uint32_t g = rank * C::kPer + j * THREADS + t;
+    if (g >= n) continue;
+    const uint64_t r = pre + run[j];
+    const uint64_t off = (r & ((1ull << kUnitBits) - 1)) << 8;
+    sel[g] = sl[j];
+    owner[g] = own[j];
+    if (sl[j]) {
       offsets[g] = off;
-      sel_list[run >> kUnitBits] = g;
-      if (spec_cur && sc != off) s_fix[atomicAdd(&s_nfix, 1u)] = g;  // K3 fix-up
-    } else if (own == ~0ull) {
+      sel_list[r >> kUnitBits] = g;
+      if (spec_cur && sc[j] != off) s_fix[atomicAdd(&s_nfix, 1u)] = g;  // K3 fix-up
+    } else if (own[j] == ~0ull) {
       offsets[g] = ~0ull;
     }
-    if (spec_next) spec_next[g] = sl ? off : ~0ull;
+    if (spec_next) spec_next[g] = sl[j] ? off : ~0ull;
   }
-  s_off[t] = off;
-  if (rank == kClCtas - 1 && t == 0) {
+  if (rank == CTAS - 1 && t == 0) {
     totals[0] = all >> kUnitBits;
     totals[1] = (all & ((1ull << kUnitBits) - 1)) << 8;
   }
   if (any_dup) {
-    cl.sync();  // offsets of every owner in shared memory
-    if (g < n && !sl && own != ~0ull)
-      offsets[g] = *(cl.map_shared_rank(s_off, uint32_t(own) / kClThreads) + (own % kClThreads));
+    cl.sync();  // the owners' offsets (global, written above) visible cluster-wide
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+      const uint32_t g = rank * C::kPer + j * THREADS + t;
+      if (g < n && !sl[j] && own[j] != ~0ull) offsets[g] = __ldcg(offsets + own[j]);
+    }
   }
   // last remote shared-memory access done: arrive now, wait only before exit
   // (no CTA may leave while another can still read its shared memory)
   asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  __syncthreads();  // this CTA's fix-up list and offsets complete
   const uint32_t nfix = s_nfix;
-  for (uint32_t q = warp; q < nfix; q += kClThreads / 32) {
+  for (uint32_t q = warp; q < nfix; q += THREADS / 32) {
     const uint32_t gq = s_fix[q];
-    warp_copy(staging + s_off[gq % kClThreads], chunk_ptr(arena, grid, gq), lens[gq], lane);
+    warp_copy(staging + __ldcg(offsets + gq), chunk_ptr(arena, grid, gq), lens[gq], lane);
   }
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -736,20 +779,63 @@ int launch_select(TableDev dedup, const uint64_t* slot, const uint32_t* lens, ui
 }
 
 bool select_small_ok(uint64_t n) { return n > 0 && n <= kSmallMax; }
-bool select_cluster_ok(uint64_t n) { return n > 0 && n <= kClMax; }
+// the 16-CTA cluster needs 16 free SMs of one GPC (non-portable size):
+// checked once per device, else the larger selections keep the other paths
+template <class C, int CTAS, int THREADS, int ITEMS, uint32_t LOCAL>
+bool cluster_fits() {
+  static uint64_t done = 0;
+  static int ok[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  once_per_device(done, [&] {
+    auto k = k_select_cluster<CTAS, THREADS, ITEMS, LOCAL>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem));
+    if (CTAS > 8) cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = CTAS;
+    cfg.blockDim = THREADS;
+    cfg.dynamicSmemBytes = C::kSmem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CTAS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    const cudaError_t e = cudaOccupancyMaxActiveClusters(&nc, k, &cfg);
+    if (e != cudaSuccess) cudaGetLastError();
+    if (dev >= 0 && dev < 64) ok[dev] = e == cudaSuccess && nc > 0;
+  });
+  return dev >= 0 && dev < 64 && ok[dev];
+}
+
+bool select_cluster_ok(uint64_t n) {
+  return n > 0 && n <= ClSmall::kMax && cluster_fits<ClSmall, 8, 512, 1, 4096>();
+}
 
 int launch_select_cluster(TableDev known, bool use_known, const uint64_t* dig,
                           const uint32_t* lens, uint64_t n, uint8_t* sel, uint64_t* owner,
                           uint64_t* offsets, uint32_t* sel_list, uint64_t* totals,
                           uint64_t* spec_next, cudaStream_t s, const uint64_t* spec_cur,
                           const uint8_t* arena, const GridDev* grid, uint8_t* staging) {
-  static uint64_t attr = 0;
-  once_per_device(attr, [] {
-    cudaFuncSetAttribute(k_select_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kClSmem));
-  });
-  launch_pdl(k_select_cluster, kClCtas, kClThreads, kClSmem, s, known, use_known ? 1 : 0, dig, lens,
-             uint32_t(n), sel, owner, offsets, sel_list, totals, spec_next, spec_cur, arena,
-             grid ? *grid : GridDev{}, staging);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = 8;
+  cfg.blockDim = 512;
+  cfg.dynamicSmemBytes = ClSmall::kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 8;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  cudaLaunchKernelEx(&cfg, k_select_cluster<8, 512, 1, 4096>, known, use_known ? 1 : 0, dig, lens,
+                     uint32_t(n), sel, owner, offsets, sel_list, totals, spec_next, spec_cur,
+                     arena, grid ? *grid : GridDev{}, staging);
   return 1;
 }
 

@@ -1,6 +1,7 @@
-"""K2 selection on both GPU paths against the oracle: the one-launch small selection
-(n <= 8192 chunks) and the three-kernel look-back path (n > 8192), with duplicates, a
-known set and the size boundaries of both; the fused verify-scatter restore on ragged
+"""K2 selection on every GPU path against the oracle: the 8-CTA cluster selection
+(n <= 4096 chunks), the one-launch small selection (n <= 8192) and the three-kernel
+look-back path beyond,
+with duplicates, a known set and the size boundaries; the fused verify-scatter restore on ragged
 layouts and several geometries; K5 in bf16."""
 import numpy as np
 import pytest
@@ -10,7 +11,8 @@ import oracle as O
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("nchunks", [1, 31, 1023, 1024, 1025, 4096, 8191, 8192, 8193, 20000])
+@pytest.mark.parametrize("nchunks", [1, 31, 1023, 1024, 1025, 4096, 4097, 8191, 8192, 8193, 20000,
+                                     65536, 65537])
 def test_selection_paths_vs_oracle(snap, nchunks):
     rng = np.random.default_rng(nchunks)
     chunk = 4096  # page == chunk: one 4 KiB chunk per slot, cheap to build many
