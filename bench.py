@@ -618,7 +618,28 @@ def c1_bench(snap, device, reps=20):
         t = time.perf_counter()
         whole = int(c.digest_whole([(0, 0, 0, nbytes, 0)])[0])
         whole_ms = (time.perf_counter() - t) * 1e3
+        # SURVEY 8(d) duplicate-heavy variant: chunk c = chunk (c mod 1024) -> W = 64 MiB
+        quarter = nbytes // 4
+        head = c.read(0, quarter)
+        for k in range(1, 4):
+            c.write(k * quarter, head)
+        for _ in range(3):
+            c.snapshot()
+            c.restore_self(verify=True)
+        _, _, _, dup_staged, dup_nsel = c.selection()
+        c.sync()
+        c.timer_start()
+        for _ in range(reps):
+            c.snapshot()
+        dup_snap_ms = c.timer_stop() / reps
+        c.sync()
+        c.timer_start()
+        for _ in range(reps):
+            c.restore_self(verify=True)
+        dup_rest_ms = c.timer_stop() / reps
+        dup_ok = bool(np.array_equal(c.read(3 * quarter, 1 << 20), head[: 1 << 20]))
     rw = 2 * nbytes  # R + W each way (every chunk unique: W = 256 MiB; restore reads + writes)
+    dup_rw = nbytes + int(dup_staged)
     out = {"workload": "C1: 256 MiB image (64 x 4 MiB buffers), 4096 x 64 KiB chunks, "
                        "snapshot + digest-verified restore round trip",
            "round_trip_ms": round(ms, 3), "round_trip_gbs": round(nbytes / ms / 1e6, 1),
@@ -633,6 +654,15 @@ def c1_bench(snap, device, reps=20):
                        "note": "per-call times above add K2/K3 (snapshot) and the host "
                                "read-back of the verification verdict (restore)"},
            "algorithmic_bytes_each_way": rw,
+           "duplicate_heavy": {"what": "SURVEY 8(d) variant: chunk c = chunk (c mod 1024), "
+                                       "1024 unique chunks staged",
+                               "staged_bytes": int(dup_staged), "staged_chunks": int(dup_nsel),
+                               "snapshot_ms": round(dup_snap_ms, 4),
+                               "snapshot_frac": round(dup_rw / dup_snap_ms / 1e6 / peak, 4),
+                               "restore_verify_ms": round(dup_rest_ms, 4),
+                               "restore_frac": round(rw / dup_rest_ms / 1e6 / peak, 4),
+                               "restored_content_ok": dup_ok,
+                               "algorithmic_bytes": {"snapshot": dup_rw, "restore": rw}},
            "whole_image_digest": {"ms": round(whole_ms, 2), "value": hex(whole),
                                   "what": "snap_digest_whole: Gpu::digest value-equal to the "
                                           "reference (one FNV-1a chain over 256 MiB)"}}
