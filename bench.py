@@ -1168,7 +1168,8 @@ def run_ours(args, dist):
                          "frac": round(achieved / peak, 4), "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": int(k_bytes),
                          "algorithmic_bytes": "R (image bytes hashed) + W (shard bytes staged)",
-                         "traffic": traffic_for("k_hash" if k1_kernel.startswith("k_hash<")
+                         "traffic": traffic_for(("k_hash" if N == 1 else f"k_hash N={N}")
+                                                if k1_kernel.startswith("k_hash<")
                                                 else f"{k1_kernel.split(' (')[0]} N={N}")},
             "step_hbm": {"rw_bytes_per_gpu": int(image + my_bytes),
                          "rw_gbs_per_gpu": round((image + my_bytes) / step_s / 1e9, 1),
