@@ -426,6 +426,14 @@ def splice_bench(snap, device, nranks=4):
         res = [timed_switch(r % nranks, (r + 1) % nranks) for r in range(8)]
         out["swap_ms_identical"] = round(float(np.median([x[0] for x in res])), 4)
         out["swap_wall_ms_identical"] = round(float(np.median([x[1] for x in res])), 4)
+        # the switch's GPU span alone (first launch .. report kernel, SNAP_PROF_SWITCH):
+        # the per-call figures above add the caller's launch latency and host return
+        c.prof_enable(True)
+        for r in range(8):
+            c.splice_switch(r % nranks, (r + 1) % nranks)
+        t_sw, n_sw = c.prof_read(snap.PROF_SWITCH)
+        c.prof_enable(False)
+        out["swap_gpu_ms_identical"] = round(t_sw / max(n_sw, 1), 4)
         st = res[-1][2]
         out["identical_switch"] = {k: int(v) for k, v in st.items()}
         out["digest_gbs"] = round(st["hashed_bytes"] / (out["swap_ms_identical"] / 1e3) / 1e9, 1)

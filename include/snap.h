@@ -457,13 +457,14 @@ int snap_splice_load(snap_ctx* ctx, const char* dir, int layout_rank, int splice
 int snap_timer_start(snap_ctx* ctx);
 int snap_timer_stop(snap_ctx* ctx, float* ms);
 /* Per-kernel-class CUDA events on the ctx stream (live roofline evidence):
- * kind 0 hash, 1 select, 2 compact, 3 restore, 4 grad, 5 exchange. */
+ * kind 0 hash, 1 select, 2 compact, 3 restore, 4 grad, 5 exchange, 6 splice switch. */
 #define SNAP_PROF_HASH 0
 #define SNAP_PROF_SELECT 1
 #define SNAP_PROF_COMPACT 2
 #define SNAP_PROF_RESTORE 3
 #define SNAP_PROF_GRAD 4
 #define SNAP_PROF_EXCHANGE 5
+#define SNAP_PROF_SWITCH 6 /* a whole snap_splice_switch: first launch .. last kernel */
 int snap_prof_enable(snap_ctx* ctx, int on);
 int snap_prof_read(snap_ctx* ctx, int kind, float* total_ms, uint64_t* count);
 

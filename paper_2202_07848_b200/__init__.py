@@ -279,7 +279,7 @@ def layout_carve(mem_bytes, max_buffer_bytes, slack_fraction):
     return tuple(out)
 
 
-PROF_HASH, PROF_SELECT, PROF_COMPACT, PROF_RESTORE, PROF_GRAD, PROF_EXCHANGE = range(6)
+PROF_HASH, PROF_SELECT, PROF_COMPACT, PROF_RESTORE, PROF_GRAD, PROF_EXCHANGE, PROF_SWITCH = range(7)
 
 
 class BidiAllocator:

@@ -12,40 +12,6 @@ void window_release(snap_ctx* ctx);
 
 namespace {
 
-// ---- profiler ----
-enum { kProfHash = 0, kProfSelect, kProfCompact, kProfRestore, kProfGrad, kProfExchange, kProfN };
-
-cudaEvent_t prof_event(snap_ctx* ctx) {
-  Prof& p = ctx->prof;
-  if (p.used == p.pool.size()) {
-    cudaEvent_t e;
-    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
-    p.pool.push_back(e);
-  }
-  return p.pool[p.used++];
-}
-
-struct ProfScope {
-  snap_ctx* ctx;
-  int kind;
-  cudaEvent_t a = nullptr;
-  ProfScope(snap_ctx* c, int k) : ctx(c), kind(k) {
-    if (ctx->prof.on) {
-      a = prof_event(ctx);
-      if (a) cudaEventRecord(a, ctx->stream);
-    }
-  }
-  ~ProfScope() {
-    if (a) {
-      cudaEvent_t b = prof_event(ctx);
-      if (b) {
-        cudaEventRecord(b, ctx->stream);
-        ctx->prof.marks.push_back({kind, {a, b}});
-      }
-    }
-  }
-};
-
 int ensure_known(snap_ctx* ctx, uint64_t extra) {
   // grows (and rebuilds) the known-set table to keep load <= 1/2
   const uint64_t need = ctx->kn_count + extra;

@@ -327,3 +327,37 @@ inline int check_range(snap_ctx* ctx, uint64_t addr, uint64_t bytes) {
   return SNAP_OK;
 }
 
+// ---- profiler ----
+// kinds of snap_prof_read (SNAP_PROF_* in snap.h); kProfSwitch = one whole splice switch
+enum { kProfHash = 0, kProfSelect, kProfCompact, kProfRestore, kProfGrad, kProfExchange, kProfSwitch, kProfN };
+
+inline cudaEvent_t prof_event(snap_ctx* ctx) {
+  Prof& p = ctx->prof;
+  if (p.used == p.pool.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    p.pool.push_back(e);
+  }
+  return p.pool[p.used++];
+}
+
+struct ProfScope {
+  snap_ctx* ctx;
+  int kind;
+  cudaEvent_t a = nullptr;
+  ProfScope(snap_ctx* c, int k) : ctx(c), kind(k) {
+    if (ctx->prof.on) {
+      a = prof_event(ctx);
+      if (a) cudaEventRecord(a, ctx->stream);
+    }
+  }
+  ~ProfScope() {
+    if (a) {
+      cudaEvent_t b = prof_event(ctx);
+      if (b) {
+        cudaEventRecord(b, ctx->stream);
+        ctx->prof.marks.push_back({kind, {a, b}});
+      }
+    }
+  }
+};

@@ -335,6 +335,12 @@ int snap_splice_switch(snap_ctx* ctx, int from, int to, snap_switch_stats* st) {
   snap_switch_stats out{};
   RankGrid* F = from >= 0 ? &S->ranks[from] : nullptr;
   RankGrid* T = to >= 0 ? &S->ranks[to] : nullptr;
+  // SNAP_PROF_SWITCH: the switch's GPU span, first launch to the report kernel
+  auto* span = new ProfScope(ctx, kProfSwitch);
+  struct SpanEnd {
+    ProfScope*& p;
+    ~SpanEnd() { delete p; }
+  } span_end{span};
   if (F) {
     // swap-out: refresh digests (K1), select against the cache (K2), slots +
     // gather (K3); reclaim first when the new chunks might not fit
@@ -374,6 +380,8 @@ int snap_splice_switch(snap_ctx* ctx, int from, int to, snap_switch_stats* st) {
   }
   CKL(snap::launch_splice_report(P<unsigned long long>(S->sin_cnt),
                                  F ? P<uint64_t>(ctx->totals) : nullptr, S->d_rep, ctx->stream));
+  delete span;  // end event before the host waits
+  span = nullptr;
   CK(cudaStreamSynchronize(ctx->stream));
   const volatile unsigned long long* rep = S->h_rep;
   const unsigned long long cnt[3] = {rep[0], rep[1], rep[2]};
