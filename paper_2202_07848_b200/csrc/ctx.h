@@ -111,6 +111,11 @@ struct snap_ctx {
   // verified restore: set to 1 by any CTA that sees a digest mismatch (mapped
   // pinned host word; the success path needs no memset and no read-back copy)
   unsigned int* h_badflag = nullptr;
+  // the verified restore's launch as an instantiated CUDA graph, reused while its
+  // parameters (grid, image, offsets, digests) stay the same
+  cudaGraphExec_t rv_exec = nullptr;
+  std::vector<uint8_t> rv_key;
+  int rv_launches = 0;
   unsigned int* d_badflag = nullptr;
   DevMem d_vbad;  // its mismatch counter, zero between calls
 
