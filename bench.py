@@ -578,6 +578,34 @@ def incremental_bench(snap, device, gib=32, reps=3):
             "bound": "hbm (hash-only K1 on the tensor cores: 8-bit FNV chain + int8 MMA, k_hash_mma)"}
 
 
+def timeline_steps(ctx, step, dist, path, steps=3):
+    """Dev hook (SNAP_BENCH_TIMELINE=path): rank 0 records every kernel / copy of `steps`
+    snapshot steps with CUPTI (torch.profiler) and writes start, duration and the idle gap
+    before each; the other ranks run the same collective steps unprofiled."""
+    dist.barrier()
+    ctx.sync()
+    if dist.rank != 0:
+        for _ in range(steps):
+            step()
+        ctx.sync()
+        return
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for _ in range(steps):
+            step()
+        ctx.sync()
+    evs = sorted((e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA),
+                 key=lambda e: e.time_range.start)
+    with open(path, "w") as f:
+        prev, t0 = None, evs[0].time_range.start if evs else 0
+        for e in evs:
+            s, t = e.time_range.start, e.time_range.end
+            gap = "" if prev is None else f"gap {s - prev:8.2f}"
+            f.write(f"{s - t0:10.2f} {t - s:9.2f} us {gap:14s} {e.name[:100]}\n")
+            prev = t if prev is None else max(prev, t)
+
+
 def c1_bench(snap, device, reps=20):
     """C1 (BASELINE configs[0], the reference's CPU-runnable case): a 256 MiB single-rank
     image (64 x 4 MiB buffers, words = mix64(1 ^ i)), 64 KiB chunks, snapshot + restore
@@ -1065,6 +1093,8 @@ def run_ours(args, dist):
     ms = ctx.timer_stop()
     tw1 = time.perf_counter()
     launches = ctx.launches - l0
+    if os.environ.get("SNAP_BENCH_TIMELINE"):  # dev hook: CUPTI timeline of 3 steps, rank 0
+        timeline_steps(ctx, step, dist, os.environ["SNAP_BENCH_TIMELINE"])
     k1_kernel = snap.last_k1_kernel()  # the K1 the timed steps ran (policy: k_hash.cu choose_k1)
     # per-kernel-class event windows over as many steps (at least 60 ms of them, which
     # also keeps the load on for the trailing clock samples), run right after the timed
