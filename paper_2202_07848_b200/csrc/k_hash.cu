@@ -856,7 +856,7 @@ bool hash_tma_selected() {
 //  * fused hash + speculative stores, most of the grid staged, and the
 //    verify-scatter: CfgG (below) — 256-B slabs keep the mixed read/write DRAM
 //    pattern at ~6 TB/s (128-B segments cap it at ~5.2, tools/micro/pattern_bw2.cu);
-//  * fused, less than 70 % of a >= 512 MiB grid staged: the tensor-core kernel
+//  * fused, less than 55 % of a >= 512 MiB grid staged: the tensor-core kernel
 //    with fused stores;
 //  * hash only, grids with tensor maps: the tensor-core FNV kernel (k_hash_mma.cu:
 //    16 chain warps, or 8 in 512-page groups for grids of <= one group per SM);

@@ -108,7 +108,7 @@ struct MmaCfg {
 // hash only: 1024 pages in flight per SM (2 chain pairs per thread, 2 warps
 // per SM sub-partition) for latency hiding; 64-byte slabs keep 3 stages in
 // shared memory. Fused, few chunks staged (multi-GPU striping, the default
-// when the predicted staging is < 70 % of the grid): the same geometry, each
+// when the predicted staging is < 55 % of the grid): the same geometry, each
 // stage's staged slabs written right after it is hashed (64-byte segments,
 // full prefetch depth). (Measured and dropped: 8 warps x 1 pair with 128-byte
 // slabs and 128/256-byte segments, 3-7 % slower at the N = 2..8 write fractions.)
