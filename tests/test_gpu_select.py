@@ -102,3 +102,78 @@ def test_grad_sum_bf16(snap, ctx):
     ctx.grad_sum(snap.BF16, [r * stride for r in range(2)], 5 * stride, n, accumulate=True)
     got2 = ctx.read(5 * stride, 2 * n).view(np.uint16)
     assert np.array_equal(got2, O.grad_sum_bf16([O.grad_sum_bf16(gs), gs[0], gs[1]]))
+
+
+def test_selection_fuzz_small_ragged(snap):
+    """Random ragged layouts of <= 4096 chunks (the 8-CTA cluster selection), duplicate
+    chunks across buffers, and random known sets; every round checked against the oracle,
+    the staged image against the selected chunks' bytes."""
+    rng = np.random.default_rng(77)
+    arena = 48 << 20
+    with snap.Ctx(0, arena) as c:
+        c.fill_mix64(0, arena, 5, 0)
+        for rnd in range(12):
+            geom = [(4096, 65536), (256, 4096), (1024, 16384)][rnd % 3]
+            bufs, addr = [], 0
+            while len(bufs) < 200:
+                nb = int(rng.integers(1, 6 * geom[1] // 256)) * 256
+                if addr + nb > arena // 2:
+                    break
+                bufs.append((0, len(bufs), addr, nb, int(rng.integers(0, 4))))
+                addr += nb + int(rng.integers(0, 3)) * 256
+            # duplicate some buffers' leading chunks into others
+            host = c.read(0, arena // 2)
+            for _ in range(20):
+                a, b = rng.integers(0, len(bufs), 2)
+                n = min(bufs[a][3], bufs[b][3]) // geom[1] * geom[1]
+                if n:
+                    host[bufs[b][2]:bufs[b][2] + n] = host[bufs[a][2]:bufs[a][2] + n]
+            c.write(0, host)
+            n = c.set_buffers(bufs, *geom)
+            assert n <= 4096
+            c.known_clear()
+            known = None
+            if rnd % 2:
+                c.snapshot()
+                d0, _ = c.digests()
+                known = d0[rng.integers(0, n, max(1, n // 3))]
+                c.known_add(known)
+            c.snapshot()
+            d, lens = c.digests()
+            sel, owner, off, tot, _ = c.selection()
+            osel, oown, ooff, otot = O.select(d, lens, known)
+            assert np.array_equal(sel, osel) and np.array_equal(owner, oown), rnd
+            assert np.array_equal(off, ooff) and tot == otot, rnd
+            if otot:
+                # each selected chunk's bytes at its offset
+                img = c.read_staging(0, tot)
+                starts = np.concatenate([[0], np.cumsum(
+                    [(b[3] + geom[1] - 1) // geom[1] for b in bufs])])
+                for gi in np.nonzero(osel)[0][:64]:
+                    bi = int(np.searchsorted(starts, gi, side="right") - 1)
+                    k = int(gi - starts[bi])
+                    a0 = bufs[bi][2] + k * geom[1]
+                    ln = int(lens[gi])
+                    assert np.array_equal(img[int(ooff[gi]):int(ooff[gi]) + ln],
+                                          host[a0:a0 + ln]), (rnd, gi)
+
+
+def test_restore_graph_follows_layout_changes(snap):
+    """The verified restore replays a cached CUDA graph while the layout is unchanged; a new
+    layout must never be served by a stale graph (a corrupted image behind a replayed graph:
+    test_verify_scatter_ragged)."""
+    rng = np.random.default_rng(5)
+    arena = 16 << 20
+    with snap.Ctx(0, arena) as c:
+        for rnd in range(6):
+            c.fill_mix64(0, arena // 2, 100 + rnd, 0)
+            nb = int(rng.integers(64, 512)) * 1024
+            bufs = [(0, i, i * nb, nb, 0) for i in range((arena // 2) // nb)]
+            c.set_buffers(bufs)
+            host = c.read(0, arena // 2)
+            c.snapshot()
+            for _ in range(3):  # replays
+                c.write(0, np.zeros(arena // 2, np.uint8))
+                c.restore_self(verify=True)
+                assert np.array_equal(c.read(0, arena // 2)[:len(bufs) * nb],
+                                      host[:len(bufs) * nb]), rnd
