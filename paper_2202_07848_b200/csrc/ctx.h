@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -56,7 +57,7 @@ struct snap_ctx {
   uint64_t grid_bytes = 0;
   std::vector<uint64_t> h_cstart;
   std::vector<uint32_t> h_lens;
-  DevMem d_addr, d_bytes, d_cstart, d_lens, d_dig, d_bufdig;
+  DevMem d_addr, d_bytes, d_cstart, d_lens, d_dig, d_bufdig, d_chunk_buf;
   GridDev grid;
   bool hashed = false;
 
@@ -256,6 +257,24 @@ inline uint32_t log2u(uint64_t x) {
   while ((1ull << s) < x) ++s;
   return s;
 }
+// GridDev::chunk_buf of a grid: buffer index of every chunk, uploaded on the ctx
+// stream (the caller synchronizes before `host` goes away)
+inline int upload_chunk_buf(snap_ctx* ctx, DevMem& m, const std::vector<uint64_t>& cstart,
+                            std::vector<uint32_t>& host, const uint32_t** out) {
+  static const bool off = std::getenv("SNAP_CHUNK_BUF") && std::getenv("SNAP_CHUNK_BUF")[0] == '0';
+  *out = nullptr;
+  if (off) return SNAP_OK;  // A/B: the binary search over cstart
+  const uint64_t nb = cstart.size() - 1, n = cstart[nb];
+  host.resize(n);
+  for (uint64_t b = 0; b < nb; ++b)
+    for (uint64_t c = cstart[b]; c < cstart[b + 1]; ++c) host[c] = uint32_t(b);
+  uint32_t* d;
+  RC(ensure(ctx, m, std::max<uint64_t>(n, 1), &d));
+  if (n) CK(cudaMemcpyAsync(d, host.data(), n * 4, cudaMemcpyHostToDevice, ctx->stream));
+  *out = d;
+  return SNAP_OK;
+}
+
 inline uint64_t table_cap(uint64_t n) {
   uint64_t c = 1024;
   while (c < 2 * n) c <<= 1;

@@ -27,6 +27,7 @@ constexpr int kThreads = 512;
 constexpr int kUnroll = 8;
 
 __device__ __forceinline__ uint32_t find_buf(const GridDev& g, uint64_t gc) {
+  if (g.chunk_buf) return __ldg(g.chunk_buf + gc);
   uint32_t lo = 0, hi = g.nbufs;
   while (hi - lo > 1) {
     uint32_t mid = (lo + hi) >> 1;

@@ -78,6 +78,7 @@ __device__ __forceinline__ void fnv_word(uint32_t& lo, uint32_t& hi, uint32_t w)
 
 // Last buffer b with cstart[b] <= gc (cstart has nbufs + 1 entries).
 __device__ __forceinline__ uint32_t find_buf(const GridDev& g, uint64_t gc) {
+  if (g.chunk_buf) return __ldg(g.chunk_buf + gc);
   uint32_t lo = 0, hi = g.nbufs;
   while (hi - lo > 1) {
     uint32_t mid = (lo + hi) >> 1;

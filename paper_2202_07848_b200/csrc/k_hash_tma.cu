@@ -87,6 +87,7 @@ __device__ __forceinline__ void fnv_word(uint32_t& lo, uint32_t& hi, uint32_t w)
   fnv_step(lo, hi, w >> 24);
 }
 __device__ __forceinline__ uint32_t find_buf(const GridDev& g, uint64_t gc) {
+  if (g.chunk_buf) return __ldg(g.chunk_buf + gc);
   uint32_t lo = 0, hi = g.nbufs;
   while (hi - lo > 1) {
     uint32_t mid = (lo + hi) >> 1;

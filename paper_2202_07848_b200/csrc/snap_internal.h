@@ -67,6 +67,10 @@ struct GridDev {
   uint64_t nchunks = 0;
   uint32_t page_shift = 12;
   uint32_t chunk_shift = 16;
+  // [nchunks] buffer index of every chunk (built with the grid): one load
+  // instead of a binary search over cstart at every task start (~log2(nbufs)
+  // dependent L2 round trips); nullptr: the search
+  const uint32_t* chunk_buf = nullptr;
   // K1 hashes chunks [c_begin, c_end) (c_end == 0: all); lets the host-buffer
   // snapshot hash each slab as soon as its H2D copy lands
   uint64_t c_begin = 0;
