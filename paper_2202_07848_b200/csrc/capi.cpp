@@ -700,7 +700,7 @@ int snap_close(snap_ctx* ctx) {
   splice_release(ctx);
   window_release(ctx);
   for (DevMem* m :
-       {&ctx->d_addr, &ctx->d_bytes, &ctx->d_cstart, &ctx->d_lens, &ctx->d_dig, &ctx->d_bufdig, &ctx->d_chunk_buf,
+       {&ctx->d_addr, &ctx->d_bytes, &ctx->d_cstart, &ctx->d_lens, &ctx->d_dig, &ctx->d_bufdig, &ctx->d_chunk_buf, &ctx->d_chunk_addr,
         &ctx->dd_keys, &ctx->dd_vals, &ctx->dd_slot, &ctx->kn_keys, &ctx->kn_vals, &ctx->kn_list,
         &ctx->scan, &ctx->sel, &ctx->owner, &ctx->offsets, &ctx->sel_list, &ctx->totals,
         &ctx->staging, &ctx->d_counts, &ctx->d_gdig, &ctx->d_glens, &ctx->d_writer,
@@ -861,8 +861,11 @@ int snap_set_buffers(snap_ctx* ctx, const snap_buf* bufs, uint64_t n, const snap
   CK(cudaMemcpyAsync(dc, cstart.data(), (n + 1) * 8, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(dl, lens.data(), lens.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
   std::vector<uint32_t> cbuf;
+  std::vector<uint64_t> caddr;
   const uint32_t* dcb = nullptr;
-  RC(upload_chunk_buf(ctx, ctx->d_chunk_buf, cstart, cbuf, &dcb));
+  const uint64_t* dca = nullptr;
+  RC(upload_chunk_buf(ctx, ctx->d_chunk_buf, ctx->d_chunk_addr, cstart, addr.data(),
+                      log2u(g.chunk_bytes), cbuf, caddr, &dcb, &dca));
   CK(cudaStreamSynchronize(ctx->stream));  // host vectors die here
   ctx->bufs.assign(bufs, bufs + n);
   ctx->geom = g;
@@ -871,7 +874,7 @@ int snap_set_buffers(snap_ctx* ctx, const snap_buf* bufs, uint64_t n, const snap
   ctx->h_cstart = std::move(cstart);
   ctx->h_lens = std::move(lens);
   ctx->grid = GridDev{da, db, dc, static_cast<uint32_t>(n), ctx->nchunks, log2u(g.page_bytes),
-                      log2u(g.chunk_bytes), dcb};
+                      log2u(g.chunk_bytes), dcb, dca, dca ? dl : nullptr};
   build_tmaps(ctx, ctx->d_tmaps, addr.data(), bytes.data(), static_cast<uint32_t>(n), ctx->grid);
   ctx->hashed = false;
   ctx->selected = false;

@@ -57,7 +57,7 @@ struct snap_ctx {
   uint64_t grid_bytes = 0;
   std::vector<uint64_t> h_cstart;
   std::vector<uint32_t> h_lens;
-  DevMem d_addr, d_bytes, d_cstart, d_lens, d_dig, d_bufdig, d_chunk_buf;
+  DevMem d_addr, d_bytes, d_cstart, d_lens, d_dig, d_bufdig, d_chunk_buf, d_chunk_addr;
   GridDev grid;
   bool hashed = false;
 
@@ -259,19 +259,36 @@ inline uint32_t log2u(uint64_t x) {
 }
 // GridDev::chunk_buf of a grid: buffer index of every chunk, uploaded on the ctx
 // stream (the caller synchronizes before `host` goes away)
-inline int upload_chunk_buf(snap_ctx* ctx, DevMem& m, const std::vector<uint64_t>& cstart,
-                            std::vector<uint32_t>& host, const uint32_t** out) {
+// GridDev::chunk_buf / chunk_addr of a grid (buffer index and arena offset of every
+// chunk), uploaded on the ctx stream (the caller synchronizes before `host` and
+// `haddr` go away). SNAP_CHUNK_BUF=0 (A/B): neither, the kernels search cstart.
+inline int upload_chunk_buf(snap_ctx* ctx, DevMem& m, DevMem& ma,
+                            const std::vector<uint64_t>& cstart, const uint64_t* buf_addr,
+                            uint32_t chunk_shift, std::vector<uint32_t>& host,
+                            std::vector<uint64_t>& haddr, const uint32_t** out,
+                            const uint64_t** out_addr) {
   static const bool off = std::getenv("SNAP_CHUNK_BUF") && std::getenv("SNAP_CHUNK_BUF")[0] == '0';
   *out = nullptr;
-  if (off) return SNAP_OK;  // A/B: the binary search over cstart
+  *out_addr = nullptr;
+  if (off) return SNAP_OK;
   const uint64_t nb = cstart.size() - 1, n = cstart[nb];
   host.resize(n);
+  haddr.resize(n);
   for (uint64_t b = 0; b < nb; ++b)
-    for (uint64_t c = cstart[b]; c < cstart[b + 1]; ++c) host[c] = uint32_t(b);
+    for (uint64_t c = cstart[b]; c < cstart[b + 1]; ++c) {
+      host[c] = uint32_t(b);
+      haddr[c] = buf_addr[b] + ((c - cstart[b]) << chunk_shift);
+    }
   uint32_t* d;
+  uint64_t* da;
   RC(ensure(ctx, m, std::max<uint64_t>(n, 1), &d));
-  if (n) CK(cudaMemcpyAsync(d, host.data(), n * 4, cudaMemcpyHostToDevice, ctx->stream));
+  RC(ensure(ctx, ma, std::max<uint64_t>(n, 1), &da));
+  if (n) {
+    CK(cudaMemcpyAsync(d, host.data(), n * 4, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(da, haddr.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  }
   *out = d;
+  *out_addr = da;
   return SNAP_OK;
 }
 

@@ -38,6 +38,7 @@ __device__ __forceinline__ uint32_t find_buf(const GridDev& g, uint64_t gc) {
 
 __device__ __forceinline__ const uint8_t* chunk_ptr(const uint8_t* arena, const GridDev& g,
                                                     uint64_t gc) {
+  if (g.chunk_addr) return arena + __ldg(g.chunk_addr + gc);
   const uint32_t b = find_buf(g, gc);
   return arena + __ldg(g.addr + b) + ((gc - __ldg(g.cstart + b)) << g.chunk_shift);
 }

@@ -204,20 +204,19 @@ k_hash(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ chun
           uint8_t* dst = nullptr;
           uint32_t len = 0;
           if (gc < c_end) {
-            const uint32_t b = find_buf(g, gc);
-            const uint64_t k = gc - __ldg(g.cstart + b);
+            uint64_t ca;
+            uint32_t clen;
+            chunk_loc(g, gc, ca, clen);
             const uint64_t in_chunk = (slot & ((1u << ppc_shift) - 1)) << page_shift;
-            const uint64_t off = (k << g.chunk_shift) + in_chunk;
-            const uint64_t bytes = __ldg(g.bytes + b);
-            if (off < bytes) {
-              const uint64_t rem = bytes - off;
+            if (in_chunk < clen) {
+              const uint64_t rem = clen - in_chunk;
               len = static_cast<uint32_t>(rem < pb ? rem : pb);
               if (g.reverse) {
                 // verify-scatter: the image holds the chunk, the grid address gets it
                 src = staging + __ldg(spec_off + gc) + in_chunk;
-                dst = const_cast<uint8_t*>(arena) + __ldg(g.addr + b) + off;
+                dst = const_cast<uint8_t*>(arena) + ca + in_chunk;
               } else {
-                src = arena + __ldg(g.addr + b) + off;
+                src = arena + ca + in_chunk;
                 if (spec_off) {
                   const uint64_t so = __ldg(spec_off + gc);
                   if (so != ~0ull) dst = staging + so + in_chunk;

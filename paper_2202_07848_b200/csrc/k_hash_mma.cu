@@ -458,15 +458,14 @@ k_hash_mma(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ 
       if (rel < nslots) {
         const uint64_t slot = slot_base + rel;
         const uint64_t gc = slot >> ppc_shift;
-        b = find_buf(g, gc);
-        const uint64_t k = gc - __ldg(g.cstart + b);
-        const uint64_t off = (k << g.chunk_shift) + ((slot & ((1u << ppc_shift) - 1)) << 12);
-        const uint64_t bytes = __ldg(g.bytes + b);
-        if (off < bytes) {
-          const uint64_t rem = bytes - off;
+        uint64_t ca;
+        uint32_t clen;
+        chunk_loc(g, gc, ca, clen);
+        const uint64_t in_chunk = (slot & ((1u << ppc_shift) - 1)) << 12;
+        if (in_chunk < clen) {
+          const uint64_t rem = clen - in_chunk;
           len = static_cast<uint32_t>(rem < 4096 ? rem : 4096);
-          src = arena + __ldg(g.addr + b) + off;
-          row = static_cast<uint32_t>(off >> 12);
+          src = arena + ca + in_chunk;
           gcout = gc;
         }
       }

@@ -32,6 +32,7 @@ namespace {
 // chunk address and warp copy (as in k_copy.cu) for the fix-up fused into the scan
 __device__ __forceinline__ const uint8_t* chunk_ptr(const uint8_t* arena, const GridDev& g,
                                                     uint64_t gc) {
+  if (g.chunk_addr) return arena + __ldg(g.chunk_addr + gc);
   if (g.chunk_buf) {
     const uint32_t b = __ldg(g.chunk_buf + gc);
     return arena + __ldg(g.addr + b) + ((gc - __ldg(g.cstart + b)) << g.chunk_shift);

@@ -71,6 +71,10 @@ struct GridDev {
   // instead of a binary search over cstart at every task start (~log2(nbufs)
   // dependent L2 round trips); nullptr: the search
   const uint32_t* chunk_buf = nullptr;
+  // [nchunks] arena offset and byte length of every chunk (with chunk_buf): a
+  // task's page descriptors in one round of independent loads
+  const uint64_t* chunk_addr = nullptr;
+  const uint32_t* chunk_len = nullptr;
   // K1 hashes chunks [c_begin, c_end) (c_end == 0: all); lets the host-buffer
   // snapshot hash each slab as soon as its H2D copy lands
   uint64_t c_begin = 0;

@@ -32,7 +32,7 @@ struct RankGrid {
   std::vector<uint64_t> chunk_addr;
   uint64_t nchunks = 0, bytes = 0;
   uint32_t chunk_bytes = 0;
-  DevMem d_addr, d_bytes, d_cstart, d_lens, d_rec, d_tmaps, d_chunk_buf;
+  DevMem d_addr, d_bytes, d_cstart, d_lens, d_rec, d_tmaps, d_chunk_buf, d_chunk_addr;
   GridDev grid;
   bool recorded = false;
 };
@@ -73,7 +73,7 @@ void splice_release(snap_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (auto& [r, g] : S->ranks)
     for (DevMem* m : {&g.d_addr, &g.d_bytes, &g.d_cstart, &g.d_lens, &g.d_rec, &g.d_tmaps,
-                      &g.d_chunk_buf})
+                      &g.d_chunk_buf, &g.d_chunk_addr})
       release(*m);
   for (auto& [k, m] : S->match) release(m);
   for (DevMem* m : {&S->cache, &S->ck, &S->cv, &S->ck2, &S->cv2, &S->lk, &S->lv, &S->free_stack,
@@ -303,11 +303,14 @@ int snap_splice_set_rank(snap_ctx* ctx, int rank, const snap_buf* bufs, uint64_t
   CK(cudaMemcpyAsync(dc, R.cstart.data(), (nb + 1) * 8, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(dl, R.lens.data(), R.nchunks * 4, cudaMemcpyHostToDevice, ctx->stream));
   std::vector<uint32_t> cbuf;
+  std::vector<uint64_t> caddr;
   const uint32_t* dcb = nullptr;
-  RC(upload_chunk_buf(ctx, R.d_chunk_buf, R.cstart, cbuf, &dcb));
+  const uint64_t* dca = nullptr;
+  RC(upload_chunk_buf(ctx, R.d_chunk_buf, R.d_chunk_addr, R.cstart, addr.data(),
+                      log2u(g.chunk_bytes), cbuf, caddr, &dcb, &dca));
   CK(cudaStreamSynchronize(ctx->stream));
   R.grid = GridDev{da, db, dc, uint32_t(nb), R.nchunks, log2u(g.page_bytes), log2u(g.chunk_bytes),
-                   dcb};
+                   dcb, dca, dca ? dl : nullptr};
   build_tmaps(ctx, R.d_tmaps, addr.data(), bytes.data(), uint32_t(nb), R.grid);
   R.recorded = false;
   // the reclamation's live-digest table covers every rank's chunks: sized here, not in a switch

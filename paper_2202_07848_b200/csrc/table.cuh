@@ -44,6 +44,32 @@ __device__ __forceinline__ uint64_t table_find(TableDev t, unsigned long long k)
   }
 }
 
+// Arena offset and byte length of chunk gc: the grid's per-chunk maps when it
+// carries them (one round of independent loads), else the buffer search.
+__device__ __forceinline__ void chunk_loc(const GridDev& g, uint64_t gc, uint64_t& addr,
+                                          uint32_t& len) {
+  if (g.chunk_addr) {
+    addr = __ldg(g.chunk_addr + gc);
+    len = __ldg(g.chunk_len + gc);
+    return;
+  }
+  uint32_t b;
+  if (g.chunk_buf) {
+    b = __ldg(g.chunk_buf + gc);
+  } else {
+    uint32_t lo = 0, hi = g.nbufs;
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (__ldg(g.cstart + mid) <= gc) lo = mid; else hi = mid;
+    }
+    b = lo;
+  }
+  const uint64_t off = (gc - __ldg(g.cstart + b)) << g.chunk_shift;
+  const uint64_t rem = __ldg(g.bytes + b) - off;
+  addr = __ldg(g.addr + b) + off;
+  len = static_cast<uint32_t>(rem < (1ull << g.chunk_shift) ? rem : (1ull << g.chunk_shift));
+}
+
 // K1: store one finished chunk digest locally and, with the fused exchange, into
 // every rank's gathered vector (8-byte NVLink stores, fire and forget).
 __device__ __forceinline__ void k1_store_digest(const GridDev& g, uint64_t chunk, uint64_t d,
