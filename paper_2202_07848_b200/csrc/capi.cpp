@@ -1461,7 +1461,9 @@ static int restore_verified(snap_ctx* ctx, const uint8_t* image, const uint64_t*
   // the counter stays zero between calls (reset below after a mismatch)
   if (fresh) CK(cudaMemsetAsync(nbad, 0, 8, ctx->stream));
   *reinterpret_cast<volatile unsigned int*>(ctx->h_badflag) = 0;
-  GridDev g = ctx->grid;
+  // byte copy (padding included): the graph cache below keys on the bytes of g
+  GridDev g;
+  std::memcpy(static_cast<void*>(&g), &ctx->grid, sizeof(GridDev));
   g.reverse = 1;
   g.expect = expect_dev;
   g.nbad = nbad;
