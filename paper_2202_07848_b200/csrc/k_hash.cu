@@ -183,6 +183,28 @@ k_hash(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ chun
   const uint32_t wshift = two_chunks ? ppc_shift : 31;
   uint32_t ist = 0, cst = 0;  // stage of the next issue / of the step being consumed
 
+  // next task's chunk descriptors (arena offset, length, staging offset), loaded one
+  // step before the task starts so the loads overlap the current step's hash
+  uint64_t pf_ca[CH], pf_so[CH];
+  uint32_t pf_clen[CH];
+  uint64_t pf_i = ~0ull;
+  auto prefetch = [&](uint64_t i) {
+    if (!g.chunk_addr) return;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const uint64_t gc = (slot_base + (gw + i * nw) * NP + c * 32 + lane) >> ppc_shift;
+      pf_ca[c] = 0;
+      pf_clen[c] = 0;
+      pf_so[c] = ~0ull;
+      if (gc < c_end) {
+        pf_ca[c] = __ldg(g.chunk_addr + gc);
+        pf_clen[c] = __ldg(g.chunk_len + gc);
+        if (spec_off) pf_so[c] = __ldg(spec_off + gc);
+      }
+    }
+    pf_i = i;
+  };
+
   auto issue = [&](uint64_t p) {
     const uint32_t st = ist;
     ist = ist + 1 == ST ? 0 : ist + 1;
@@ -204,23 +226,27 @@ k_hash(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ chun
           uint8_t* dst = nullptr;
           uint32_t len = 0;
           if (gc < c_end) {
-            uint64_t ca;
+            uint64_t ca, so = ~0ull;
             uint32_t clen;
-            chunk_loc(g, gc, ca, clen);
+            if (pf_i == i) {
+              ca = pf_ca[c];
+              clen = pf_clen[c];
+              so = pf_so[c];
+            } else {
+              chunk_loc(g, gc, ca, clen);
+              if (spec_off) so = __ldg(spec_off + gc);
+            }
             const uint64_t in_chunk = (slot & ((1u << ppc_shift) - 1)) << page_shift;
             if (in_chunk < clen) {
               const uint64_t rem = clen - in_chunk;
               len = static_cast<uint32_t>(rem < pb ? rem : pb);
               if (g.reverse) {
                 // verify-scatter: the image holds the chunk, the grid address gets it
-                src = staging + __ldg(spec_off + gc) + in_chunk;
+                src = staging + so + in_chunk;
                 dst = const_cast<uint8_t*>(arena) + ca + in_chunk;
               } else {
                 src = arena + ca + in_chunk;
-                if (spec_off) {
-                  const uint64_t so = __ldg(spec_off + gc);
-                  if (so != ~0ull) dst = staging + so + in_chunk;
-                }
+                if (so != ~0ull) dst = staging + so + in_chunk;
               }
             }
           }
@@ -326,6 +352,7 @@ k_hash(const uint8_t* __restrict__ arena, GridDev g, uint64_t* __restrict__ chun
   for (int c = 0; c < CH; ++c) lo[c] = hi[c] = mylen[c] = 0;
   for (uint64_t t = 0; t < nsteps; ++t) {
     issue(t + ST - 1);
+    if (((t + ST) & (ns - 1)) == 0 && t + ST < nsteps) prefetch((t + ST) >> ns_shift);
     cp_wait<ST - 1>();
     __syncwarp();
     const uint64_t i = t >> ns_shift;
