@@ -548,15 +548,34 @@ int hash_fused(snap_ctx* ctx, uint64_t c0 = 0, uint64_t c1 = 0) {
   GridDev g = ctx->grid;
   g.c_begin = c0;
   g.c_end = c1;
-  static const bool k1_insert = [] {
+  const bool spec = ctx->kn_count == 0;
+  uint8_t* st = nullptr;
+  const uint64_t* so = nullptr;
+  if (spec) {
+    if (!ctx->spec_ready || spec_stripe_emu() > 1) RC(init_spec(ctx));
+    RC(staging_reserve(ctx, staging_target(ctx), true, &st));
+    g.spec_bytes = ctx->spec_bytes;
+    so = P<uint64_t>(ctx->d_spec[ctx->spec_cur]);
+  }
+  static const int k1_insert_env = [] {
     const char* e = std::getenv("SNAP_K1_INSERT");
-    return e && e[0] == '1';
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
   }();
-  if (!ctx->attached() && k1_insert) {
-    // SNAP_K1_INSERT=1 (single GPU): K1 also does the K2 insert of its chunks in
-    // a warp epilogue (the table is prepared once, before the first slice of the
-    // grid). Off by default: the epilogue costs more kernel tail (14 us on C2)
-    // than the standalone insert kernel (8 us).
+  // Single GPU, grids above the cluster selection's 4096 chunks, K1 kernels with
+  // the insert epilogue (the FNV-chain k_hash family): K1 also does the K2 insert
+  // of its chunks (the table is prepared once, before the first slice of the
+  // grid). Same-box A/B on C2 N=1 with the final K1: 2933-2938 vs 2921-2926 GB/s
+  // (the standalone insert kernel's 7.5 us after K1 goes; in round 1, before the
+  // descriptor maps, the epilogue cost more than it saved). The tensor-core K1
+  // would run the insert as a separate, non-PDL range kernel: slower than the
+  // standalone insert (full C2 on one GPU 4.08 vs 4.11 ms), so not there.
+  // SNAP_K1_INSERT=0 / 1 forces it off / on.
+  if (c0 == 0)
+    ctx->k1_insert_now =
+        !ctx->attached() &&
+        (k1_insert_env >= 0 ? k1_insert_env == 1
+                            : !snap::select_cluster_ok(ctx->nchunks) && snap::k1_epilogue_insert(g, so));
+  if (ctx->k1_insert_now) {
     if (c0 == 0) {
       uint64_t *slot, *scan;
       RC(prepare_dedup(ctx, ctx->nchunks, &g.dd, &slot, &scan));
@@ -570,18 +589,8 @@ int hash_fused(snap_ctx* ctx, uint64_t c0 = 0, uint64_t c1 = 0) {
     ctx->k1_inserted = true;
   }
   k1_fanout(ctx, g);
-  if (ctx->kn_count > 0) {
-    CKL(snap::launch_hash(ctx->arena, g, P<uint64_t>(ctx->d_dig), nullptr, nullptr, ctx->stream));
-    ctx->spec_used = false;
-    return SNAP_OK;
-  }
-  if (!ctx->spec_ready || spec_stripe_emu() > 1) RC(init_spec(ctx));
-  uint8_t* st;
-  RC(staging_reserve(ctx, staging_target(ctx), true, &st));
-  g.spec_bytes = ctx->spec_bytes;
-  CKL(snap::launch_hash(ctx->arena, g, P<uint64_t>(ctx->d_dig),
-                        P<uint64_t>(ctx->d_spec[ctx->spec_cur]), st, ctx->stream));
-  ctx->spec_used = true;
+  CKL(snap::launch_hash(ctx->arena, g, P<uint64_t>(ctx->d_dig), so, st, ctx->stream));
+  ctx->spec_used = spec;
   return SNAP_OK;
 }
 

@@ -112,6 +112,7 @@ struct snap_ctx {
   // verified restore: set to 1 by any CTA that sees a digest mismatch (mapped
   // pinned host word; the success path needs no memset and no read-back copy)
   unsigned int* h_badflag = nullptr;
+  bool k1_insert_now = false;  // this snapshot's K1 does the K2 insert (hash_fused)
   // the verified restore's launch as an instantiated CUDA graph, reused while its
   // parameters (grid, image, offsets, digests) stay the same
   cudaGraphExec_t rv_exec = nullptr;

@@ -1038,6 +1038,12 @@ int launch_hash(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
 
 const char* last_k1_name() { return g_last_k1; }
 
+bool k1_epilogue_insert(const GridDev& g, const uint64_t* spec_off) {
+  const K1 k = choose_k1(g, spec_off);
+  return !(k == K1::WsA || k == K1::WsB || k == K1::WsC || k == K1::Tma || k == K1::Mma ||
+           k == K1::MmaFL || k == K1::TmaF);
+}
+
 int launch_buf_fold(const GridDev& g, const uint64_t* chunk_dig, uint64_t* buf_dig,
                     cudaStream_t s) {
   if (g.nbufs == 0) return 0;

@@ -142,6 +142,9 @@ constexpr uint64_t kMaxScanEntries = 1ull << 26;
 // Launchers (each returns the number of kernels launched).
 // K1; with spec_off != nullptr also the fused speculative K3 (TMA bulk stores
 // of every chunk whose spec_off[chunk] != ~0 to staging + spec_off[chunk]).
+// whether the K1 launch_hash would pick for (g, spec_off) does the K2 insert in its
+// epilogue (the FNV-chain k_hash family) rather than in a separate range kernel
+bool k1_epilogue_insert(const GridDev& g, const uint64_t* spec_off);
 int launch_hash(const uint8_t* arena, const GridDev& g, uint64_t* chunk_dig,
                 const uint64_t* spec_off, uint8_t* staging, cudaStream_t s);
 // K1 hash-only through TMA tensor loads (needs grid tensor maps, 4 KiB pages).
