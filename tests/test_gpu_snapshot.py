@@ -233,20 +233,22 @@ def test_fused_speculation_learns_and_recovers(snap, ctx, golden):
     check(host)
 
 
-@pytest.mark.parametrize("variant", [-1, 11, 12, 13])
-def test_snapshot_host_pipelined(snap, variant):
+@pytest.mark.parametrize("variant,chunk", [(-1, 65536), (11, 65536), (12, 65536), (13, 65536),
+                                           (-1, 16384)])
+def test_snapshot_host_pipelined(snap, variant, chunk):
     """snap_snapshot_host (pinned host image -> arena -> K1..K3 -> staging to host), slab
     pipelined: staging image == oracle compaction, through mispredicted, learned and
     incremental layouts, and through the non-pipelined fallback (unsorted buffers).
-    variant 11/12: the tensor-core K1 kernels on every slab (grid slices c_begin..c_end)."""
+    variant 11/12: the tensor-core K1 kernels on every slab (grid slices c_begin..c_end).
+    16 KiB chunks: 10240 chunks, so K1 also does the K2 insert, slab by slab."""
     snap.set_k1_variant(variant)
     try:
-        _host_pipelined(snap)
+        _host_pipelined(snap, chunk)
     finally:
         snap.set_k1_variant(-1)
 
 
-def _host_pipelined(snap):
+def _host_pipelined(snap, chunk=65536):
     nbytes = 160 << 20
     img = O.fill_mix64(nbytes // 8, 21, 0)
     # buffers spanning several 64 MiB slabs, a duplicate (mispredicted speculation)
@@ -258,11 +260,11 @@ def _host_pipelined(snap):
     pin.array[:] = img.view(np.uint8)
     out = snap.PinnedHost(nbytes)
     with snap.Ctx(0, nbytes) as c:
-        c.set_buffers(bufs)
+        c.set_buffers(bufs, 4096, chunk)
         dig = np.zeros(c.nchunks, np.uint64)
-        od, olens, _ = O.hash_chunks([img], bufs)
+        od, olens, _ = O.hash_chunks([img], bufs, 4096, chunk)
         osel, oown, ooff, otot = O.select(od, olens)
-        exp = O.compact([img], bufs, 65536, osel, ooff, otot)
+        exp = O.compact([img], bufs, chunk, osel, ooff, otot)
         for it in range(2):
             staged = c.snapshot_host(pin.ptr, 0, nbytes, out.ptr, nbytes, dig)
             assert staged == otot and np.array_equal(dig, od), it
@@ -270,23 +272,23 @@ def _host_pipelined(snap):
         # incremental: 3 dirty chunks against the committed store
         c.known_commit()
         host2 = img.copy()
-        host2[[3 * 8192, 700 * 8192, 1900 * 8192]] ^= np.uint64(0xABCD)
+        host2[[3 * 8192, 700 * 8192, 1900 * 8192]] ^= np.uint64(0xABCD)  # 3 chunks at any chunk size
         pin.array[:] = host2.view(np.uint8)
         staged = c.snapshot_host(pin.ptr, 0, nbytes, out.ptr, nbytes, dig)
-        d2, l2, _ = O.hash_chunks([host2], bufs)
+        d2, l2, _ = O.hash_chunks([host2], bufs, 4096, chunk)
         s2, _, o2, t2 = O.select(d2, l2, known=od)
-        assert staged == t2 == 3 * 65536
-        assert np.array_equal(out.array[:staged], O.compact([host2], bufs, 65536, s2, o2, t2))
+        assert staged == t2 == 3 * chunk
+        assert np.array_equal(out.array[:staged], O.compact([host2], bufs, chunk, s2, o2, t2))
     # unsorted buffer order -> sequential fallback, same result
     bufs_u = [bufs[1], bufs[0], bufs[2]]
     with snap.Ctx(0, nbytes) as c:
         pin.array[:] = img.view(np.uint8)
-        c.set_buffers(bufs_u)
+        c.set_buffers(bufs_u, 4096, chunk)
         dig = np.zeros(c.nchunks, np.uint64)
         staged = c.snapshot_host(pin.ptr, 0, nbytes, out.ptr, nbytes, dig)
-        od, olens, _ = O.hash_chunks([img], bufs_u)
+        od, olens, _ = O.hash_chunks([img], bufs_u, 4096, chunk)
         osel, oown, ooff, otot = O.select(od, olens)
         assert staged == otot
-        assert np.array_equal(out.array[:staged], O.compact([img], bufs_u, 65536, osel, ooff, otot))
+        assert np.array_equal(out.array[:staged], O.compact([img], bufs_u, chunk, osel, ooff, otot))
     pin.free()
     out.free()
